@@ -1,0 +1,173 @@
+/* cmgpu.h — C ABI of the B200 cheesemap cell index and neighbour-query engine.
+ *
+ * This is the drop-in boundary for the reference's C++ index API
+ * (/root/reference/proj/core/include/cheesemap/):
+ *
+ *   reference                                         replaced by
+ *   ------------------------------------------------  -----------------------------
+ *   Cheesemap::build(cloud, BuildOptions)  map.hpp:55  cm_build
+ *   Cheesemap::grid()                      map.hpp:57  cm_get_grid
+ *   Cheesemap::occupancy_stats()     map.hpp:104, map.cpp:150-171  cm_get_occupancy
+ *   Cheesemap::voxel_lookup / for_each_in_voxel  map.hpp:69-102  cm_export_voxels
+ *   kernel_search<SphereKernel|BoxKernel>  search.hpp:102-127
+ *                                 cm_radius_count + cm_radius_fill, cm_radius_search,
+ *                                 cm_radius_digest (batched; one row per query centre)
+ *   knn_search(map, c, k)                  search.hpp:131-134, search.cpp:87-146
+ *                                                               cm_knn (batched)
+ *   Cheesemap::corrupt_for_testing()       map.hpp:109, map.cpp:194-223
+ *                                                               cm_corrupt_for_testing
+ *   cheesemap::Error hierarchy             errors.hpp:8-42     cm_status + cm_last_error
+ *
+ * The reference has no batch entry point: one C++ call answers one query.
+ * Here one call answers a batch; row q of the output is what the reference's
+ * call returns for centre q, as a list SORTED ASCENDING (the reference
+ * returns visit order; its own tests compare sorted copies,
+ * tests/test_util.hpp:30-35).
+ *
+ * Conventions
+ *  - Points are the reference's PointCloud layout (geometry.hpp:13-24):
+ *    n x 3 doubles, AoS (x, y, z). A handle is the point's position in that
+ *    array (u64 in the reference; u32 here, so n < 2^32).
+ *  - Input/output pointers may be HOST or DEVICE memory (detected with
+ *    cudaPointerGetAttributes). Host inputs are copied in, host outputs are
+ *    copied back and the call synchronises. With device outputs calls are
+ *    ordered on `stream` (a cudaStream_t; NULL = legacy default stream).
+ *  - A built index is immutable and may be queried concurrently from many
+ *    host threads / streams (map.hpp:50-52). The index owns device copies of
+ *    the points; the caller's cloud need not outlive it.
+ *  - Errors: cm_status with the reference's trigger conditions checked in the
+ *    reference's order (map.cpp:23-39, grid.cpp:18-27 and :51-59,
+ *    search.cpp:90-92). cm_last_error() returns a thread-local message.
+ */
+#ifndef CMGPU_H
+#define CMGPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  CM_OK = 0,
+  CM_EMPTY_CLOUD = 1,      /* EmptyCloudError      errors.hpp:13-17 */
+  CM_INVALID_ARGUMENT = 2, /* InvalidArgumentError errors.hpp:34-37 */
+  CM_CAPACITY = 3,         /* CapacityError        errors.hpp:19-22 */
+  CM_OUT_OF_DOMAIN = 4,    /* OutOfDomainError     errors.hpp:24-27 */
+  CM_CUDA = 5,             /* CUDA runtime failure (no reference analogue) */
+  CM_NCCL = 6              /* collective failure (multi-GPU slabs) */
+} cm_status;
+
+/* map.hpp:15 */
+typedef enum { CM_DENSE = 0, CM_SPARSE = 1, CM_MIXED = 2 } cm_flavor;
+/* grid.hpp:10 */
+typedef enum { CM_TWOD = 0, CM_THREED = 1 } cm_grid_mode;
+/* geometry.hpp:73-92: SphereKernel{c, r}; BoxKernel{{c-r}, {c+r}} (the cube
+ * the reference CLI/tests build, cmd_bench.cpp:107-111) */
+typedef enum { CM_SPHERE = 0, CM_CUBE = 1 } cm_kernel;
+
+/* BuildOptions, field for field (map.hpp:17-26). `reorder` is accepted and
+ * ignored: the device index is always stored in cell order, and results are
+ * always original handles (what reorder=true returns, map.hpp:131-138). */
+typedef struct {
+  int32_t flavor;             /* cm_flavor, default CM_DENSE */
+  int32_t mode;               /* cm_grid_mode, default CM_THREED */
+  double cell_x, cell_y, cell_z; /* default 1.0 */
+  int32_t reorder;            /* default 0 */
+  double densify_threshold;   /* default 0.80 */
+  uint64_t dense_voxel_cap;   /* default 2^32 */
+} cm_build_options;
+
+/* GridParams (grid.hpp:47-81) */
+typedef struct {
+  double origin[3];
+  double cell[3];
+  uint64_t nx, ny, nz;
+  int32_t mode;
+  double bounds_min[3], bounds_max[3];
+} cm_grid_params;
+
+/* OccupancyStats (map.hpp:34-39); slices are reported for every flavour,
+ * with the mixed flavour's densify rule (map.cpp:106-108) applied. */
+typedef struct {
+  uint64_t total_voxels;
+  uint64_t non_empty;
+  double empty_fraction;
+  uint64_t n_slices;
+  uint64_t n_columns;   /* non-empty (i, j) columns (mixed layout) */
+} cm_occupancy;
+
+/* Device-side build timing, milliseconds (CUDA events). */
+typedef struct {
+  double total_ms;      /* device-resident points -> ready index */
+  double h2d_ms;        /* host->device copy of the cloud (0 for device input) */
+  double bbox_ms, keys_ms, sort_ms, gather_ms, tables_ms;
+  uint32_t sort_passes;
+} cm_build_timing;
+
+typedef struct cm_index cm_index;
+typedef struct cm_csr cm_csr;
+
+void cm_default_options(cm_build_options* opts);
+
+/* Cheesemap::build (map.cpp:22-122). xyz: n x 3 doubles, host or device. */
+cm_status cm_build(const double* xyz, uint64_t n, const cm_build_options* opts,
+                   int device, void* stream, cm_index** out);
+cm_status cm_free(cm_index* index);
+
+cm_status cm_get_grid(const cm_index* index, cm_grid_params* out);
+cm_status cm_get_occupancy(const cm_index* index, cm_occupancy* out,
+                           uint8_t* slice_dense, uint64_t* slice_non_empty,
+                           uint64_t slice_capacity);
+cm_status cm_get_build_timing(const cm_index* index, cm_build_timing* out);
+/* Per-voxel handle sets in stored order (key ascending, handles ascending
+ * inside a voxel): keys[p], handles[p] for p < n. Host or device outputs. */
+cm_status cm_export_voxels(const cm_index* index, uint64_t* keys, uint32_t* handles);
+uint64_t cm_size(const cm_index* index);
+
+/* kernel_search, count pass: counts[q] = |result(q)|; optional
+ * points_tested[q] = the reference's QueryStats::points_tested
+ * (search.hpp:116). Either output may be NULL. */
+cm_status cm_radius_count(const cm_index* index, const double* q, uint64_t nq,
+                          int kernel, double r, uint32_t* counts,
+                          uint64_t* points_tested, void* stream);
+/* kernel_search, fill pass: cols[row_ptr[q] .. row_ptr[q+1]) = sorted
+ * handles of result(q). row_ptr must come from the counts of the same call
+ * arguments (exclusive scan, nq + 1 entries). */
+cm_status cm_radius_fill(const cm_index* index, const double* q, uint64_t nq,
+                         int kernel, double r, const uint64_t* row_ptr,
+                         uint32_t* cols, void* stream);
+/* count + scan + fill in one call; the CSR lives in device memory owned by
+ * the returned cm_csr. */
+cm_status cm_radius_search(const cm_index* index, const double* q, uint64_t nq,
+                           int kernel, double r, void* stream, cm_csr** out);
+cm_status cm_csr_info(const cm_csr* csr, uint64_t* nq, uint64_t* nnz,
+                      const uint64_t** row_ptr_device, const uint32_t** cols_device);
+/* row_ptr (nq + 1) and cols (nnz) to caller memory (host or device). */
+cm_status cm_csr_download(const cm_csr* csr, uint64_t* row_ptr, uint32_t* cols,
+                          void* stream);
+cm_status cm_csr_free(cm_csr* csr);
+/* Per-query count and set digest sum(mix64(handle)) mod 2^64 (splitmix64
+ * finaliser) — verification of outputs too large to materialise. */
+cm_status cm_radius_digest(const cm_index* index, const double* q, uint64_t nq,
+                           int kernel, double r, uint32_t* counts,
+                           uint64_t* digests, void* stream);
+
+/* knn_search (search.cpp:87-146), exact, rows ordered by (fp64 squared
+ * distance, handle). idx[q*k + t], d2[q*k + t] (d2 may be NULL). Rows of a
+ * cloud with fewer than k points are padded with UINT32_MAX / +inf. */
+cm_status cm_knn(const cm_index* index, const double* q, uint64_t nq, uint32_t k,
+                 uint32_t* idx, double* d2, void* stream);
+
+/* Test hook (map.cpp:194-223): drops one stored handle from the first
+ * non-empty voxel so verification harnesses can prove they detect it. */
+cm_status cm_corrupt_for_testing(cm_index* index);
+
+const char* cm_last_error(void);
+const char* cm_status_name(cm_status s);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CMGPU_H */

@@ -1,0 +1,133 @@
+"""TEST INFRASTRUCTURE — ctypes loader for the CPU oracle (liboracle.so,
+the restatement) and the compiled reference (_ref/libcheesemap_ref.so).
+
+Only tests/, __graft_entry__.smoke() and bench.py's CPU legs import this.
+Both libraries export the same ABI (prefix ``orc_`` / ``ref_``)."""
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+STATUS = {0: "OK", 1: "EMPTY_CLOUD", 2: "INVALID_ARGUMENT", 3: "CAPACITY", 4: "OUT_OF_DOMAIN"}
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+class CpuIndexLib:
+    def __init__(self, which="oracle"):
+        if which == "oracle":
+            path, pre = os.path.join(_HERE, "liboracle.so"), "orc_"
+        elif which == "reference":
+            path, pre = os.path.join(_HERE, "_ref", "libcheesemap_ref.so"), "ref_"
+        else:
+            raise ValueError(which)
+        if not os.path.exists(path):
+            raise FileNotFoundError(path)
+        self.which, self.path = which, path
+        lib = ctypes.CDLL(path)
+        u64, u32, dbl, p, i = (ctypes.c_uint64, ctypes.c_uint32, ctypes.c_double,
+                               ctypes.c_void_p, ctypes.c_int)
+        def f(name, args, res):
+            fn = getattr(lib, pre + name)
+            fn.argtypes, fn.restype = args, res
+            return fn
+        self.build_ = f("build", [p, u64, i, i, dbl, dbl, dbl, dbl, u64, ctypes.POINTER(p)], i)
+        self.free_ = f("free", [p], None)
+        self.grid_ = f("grid", [p, p, p, p, p, p], None)
+        self.non_empty_ = f("non_empty", [p], u64)
+        self.slice_flags_ = f("slice_flags", [p, p, p], u64)
+        self.export_ = f("export", [p, p, p], None)
+        self.radius_ = f("radius", [p, p, u64, i, dbl, ctypes.c_uint, p, p, p, p], i)
+        self.radius_fill_ = f("radius_fill", [p, p, u64, i, dbl, ctypes.c_uint, p, p], i)
+        self.knn_ = f("knn", [p, p, u64, u32, ctypes.c_uint, p, p, p, p], i)
+        self.lib = lib
+
+
+_LIBS = {}
+
+
+def lib(which="oracle"):
+    if which not in _LIBS:
+        _LIBS[which] = CpuIndexLib(which)
+    return _LIBS[which]
+
+
+class CpuIndex:
+    """A built CPU index (restatement or reference)."""
+
+    def __init__(self, xyz, flavor=0, mode=1, cell=(1.0, 1.0, 1.0), tau=0.8,
+                 dense_cap=1 << 32, which="oracle"):
+        self.L = lib(which)
+        self.xyz = np.ascontiguousarray(xyz, dtype=np.float64).reshape(-1, 3)
+        h = ctypes.c_void_p()
+        rc = self.L.build_(_p(self.xyz), self.xyz.shape[0], flavor, mode, cell[0], cell[1],
+                           cell[2], tau, dense_cap, ctypes.byref(h))
+        if rc != 0:
+            raise RuntimeError(f"{which} build failed: {STATUS.get(rc, rc)}", rc)
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.L.free_(self.h)
+            self.h = None
+
+    def grid(self):
+        o, c, b0, b1 = (np.zeros(3) for _ in range(4))
+        d = np.zeros(3, dtype=np.uint64)
+        self.L.grid_(self.h, _p(o), _p(c), _p(d), _p(b0), _p(b1))
+        return dict(origin=o, cell=c, dims=d, bmin=b0, bmax=b1)
+
+    def non_empty(self):
+        return int(self.L.non_empty_(self.h))
+
+    def slice_flags(self):
+        nz = int(self.grid()["dims"][2])
+        dense = np.zeros(nz, dtype=np.uint8)
+        ne = np.zeros(nz, dtype=np.uint64)
+        got = self.L.slice_flags_(self.h, _p(dense), _p(ne))
+        return dense[:got].astype(bool), ne[:got]
+
+    def export(self):
+        n = self.xyz.shape[0]
+        k = np.zeros(n, dtype=np.uint64)
+        h = np.zeros(n, dtype=np.uint64)
+        self.L.export_(self.h, _p(k), _p(h))
+        return k, h
+
+    def radius(self, q, kernel=0, r=1.0, threads=0, stats=False):
+        q = np.ascontiguousarray(q, dtype=np.float64).reshape(-1, 3)
+        nq = q.shape[0]
+        cnt = np.zeros(nq, dtype=np.uint32)
+        dig = np.zeros(nq, dtype=np.uint64)
+        pt = np.zeros(nq, dtype=np.uint64) if stats else None
+        vv = np.zeros(nq, dtype=np.uint64) if stats else None
+        rc = self.L.radius_(self.h, _p(q), nq, kernel, r, threads, _p(cnt), _p(dig), _p(pt), _p(vv))
+        if rc:
+            raise RuntimeError(STATUS.get(rc, rc))
+        return (cnt, dig, pt, vv) if stats else (cnt, dig)
+
+    def radius_csr(self, q, kernel=0, r=1.0, threads=0):
+        q = np.ascontiguousarray(q, dtype=np.float64).reshape(-1, 3)
+        cnt, _ = self.radius(q, kernel, r, threads)
+        row = np.zeros(q.shape[0] + 1, dtype=np.uint64)
+        np.cumsum(cnt, out=row[1:])
+        cols = np.zeros(int(row[-1]), dtype=np.uint32)
+        rc = self.L.radius_fill_(self.h, _p(q), q.shape[0], kernel, r, threads, _p(row), _p(cols))
+        if rc:
+            raise RuntimeError(STATUS.get(rc, rc))
+        return row, cols
+
+    def knn(self, q, k, threads=0, stats=False):
+        q = np.ascontiguousarray(q, dtype=np.float64).reshape(-1, 3)
+        nq = q.shape[0]
+        idx = np.zeros((nq, k), dtype=np.uint32)
+        d2 = np.zeros((nq, k), dtype=np.float64)
+        prk = np.zeros(nq, dtype=np.uint64) if stats else None
+        pa2 = np.zeros(nq, dtype=np.uint64) if stats else None
+        rc = self.L.knn_(self.h, _p(q), nq, k, threads, _p(idx), _p(d2), _p(prk), _p(pa2))
+        if rc:
+            raise RuntimeError(STATUS.get(rc, rc))
+        return (idx, d2, prk, pa2) if stats else (idx, d2)

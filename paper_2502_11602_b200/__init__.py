@@ -1,0 +1,7 @@
+"""B200-native cheesemap: cell-index build and batched neighbour queries on
+sm_100a behind the reference's index API."""
+from .cheesemap import (BoxKernel, BuildOptions, CapacityError, CellSize, Cheesemap,  # noqa: F401
+                        CudaError, EmptyCloudError, Error, Flavor, GridMode,
+                        InvalidArgumentError, Neighbor, OutOfDomainError, SphereKernel,
+                        kernel_search, knn_batch, knn_search, radius_count,
+                        radius_digest_batch, radius_search_batch)

@@ -1,0 +1,93 @@
+"""ctypes binding of libcmgpu.so (include/cmgpu.h).
+
+The product path: there is no CPU fallback. Loading fails loudly when the
+library is missing; calls fail loudly when no CUDA device is present.
+"""
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcmgpu.so")
+
+STATUS_NAMES = {0: "CM_OK", 1: "CM_EMPTY_CLOUD", 2: "CM_INVALID_ARGUMENT", 3: "CM_CAPACITY",
+                4: "CM_OUT_OF_DOMAIN", 5: "CM_CUDA", 6: "CM_NCCL"}
+
+EXPORTS = [
+    "cm_default_options", "cm_build", "cm_free", "cm_get_grid", "cm_get_occupancy",
+    "cm_get_build_timing", "cm_export_voxels", "cm_size", "cm_radius_count", "cm_radius_fill",
+    "cm_radius_search", "cm_csr_info", "cm_csr_download", "cm_csr_free", "cm_radius_digest",
+    "cm_knn", "cm_corrupt_for_testing", "cm_last_error", "cm_status_name",
+]
+
+
+class BuildOptionsC(ctypes.Structure):
+    _fields_ = [("flavor", ctypes.c_int32), ("mode", ctypes.c_int32),
+                ("cell_x", ctypes.c_double), ("cell_y", ctypes.c_double),
+                ("cell_z", ctypes.c_double), ("reorder", ctypes.c_int32),
+                ("densify_threshold", ctypes.c_double), ("dense_voxel_cap", ctypes.c_uint64)]
+
+
+class GridParamsC(ctypes.Structure):
+    _fields_ = [("origin", ctypes.c_double * 3), ("cell", ctypes.c_double * 3),
+                ("nx", ctypes.c_uint64), ("ny", ctypes.c_uint64), ("nz", ctypes.c_uint64),
+                ("mode", ctypes.c_int32), ("bounds_min", ctypes.c_double * 3),
+                ("bounds_max", ctypes.c_double * 3)]
+
+
+class OccupancyC(ctypes.Structure):
+    _fields_ = [("total_voxels", ctypes.c_uint64), ("non_empty", ctypes.c_uint64),
+                ("empty_fraction", ctypes.c_double), ("n_slices", ctypes.c_uint64),
+                ("n_columns", ctypes.c_uint64)]
+
+
+class BuildTimingC(ctypes.Structure):
+    _fields_ = [("total_ms", ctypes.c_double), ("h2d_ms", ctypes.c_double),
+                ("bbox_ms", ctypes.c_double), ("keys_ms", ctypes.c_double),
+                ("sort_ms", ctypes.c_double), ("gather_ms", ctypes.c_double),
+                ("tables_ms", ctypes.c_double), ("sort_passes", ctypes.c_uint32)]
+
+
+_LIB = None
+
+
+def lib():
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} is missing; build it with __graft_entry__.build() "
+                           "(there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    p, u64, u32, i32, dbl = (ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int,
+                             ctypes.c_double)
+    sig = {
+        "cm_default_options": ([ctypes.POINTER(BuildOptionsC)], None),
+        "cm_build": ([p, u64, ctypes.POINTER(BuildOptionsC), i32, p, ctypes.POINTER(p)], i32),
+        "cm_free": ([p], i32),
+        "cm_get_grid": ([p, ctypes.POINTER(GridParamsC)], i32),
+        "cm_get_occupancy": ([p, ctypes.POINTER(OccupancyC), p, p, u64], i32),
+        "cm_get_build_timing": ([p, ctypes.POINTER(BuildTimingC)], i32),
+        "cm_export_voxels": ([p, p, p], i32),
+        "cm_size": ([p], u64),
+        "cm_radius_count": ([p, p, u64, i32, dbl, p, p, p], i32),
+        "cm_radius_fill": ([p, p, u64, i32, dbl, p, p, p], i32),
+        "cm_radius_search": ([p, p, u64, i32, dbl, p, ctypes.POINTER(p)], i32),
+        "cm_csr_info": ([p, ctypes.POINTER(u64), ctypes.POINTER(u64), ctypes.POINTER(p),
+                         ctypes.POINTER(p)], i32),
+        "cm_csr_download": ([p, p, p, p], i32),
+        "cm_csr_free": ([p], i32),
+        "cm_radius_digest": ([p, p, u64, i32, dbl, p, p, p], i32),
+        "cm_knn": ([p, p, u64, u32, p, p, p], i32),
+        "cm_corrupt_for_testing": ([p], i32),
+        "cm_last_error": ([], ctypes.c_char_p),
+        "cm_status_name": ([i32], ctypes.c_char_p),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes, fn.restype = args, res
+    _LIB = L
+    return L
+
+
+def last_error():
+    return lib().cm_last_error().decode(errors="replace")

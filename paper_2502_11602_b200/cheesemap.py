@@ -1,0 +1,332 @@
+"""Host-side mirror of the reference's C++ index API over the C ABI.
+
+Names, argument meaning and error behaviour follow
+/root/reference/proj/core/include/cheesemap/{geometry,grid,map,search,errors}.hpp
+so parity tests read like the reference's own tests:
+
+  reference (C++)                               here
+  Cheesemap::build(cloud, BuildOptions)          Cheesemap.build(cloud, BuildOptions())
+  map.grid() / occupancy_stats()                 Cheesemap.grid() / .occupancy_stats()
+  kernel_search(map, SphereKernel{c, r})         kernel_search(map, SphereKernel(c, r))
+  kernel_search(map, BoxKernel{{c-r},{c+r}})     kernel_search(map, BoxKernel.cube(c, r))
+  knn_search(map, c, k)                          knn_search(map, c, k)
+  cheesemap::EmptyCloudError, ...                EmptyCloudError, ...
+
+plus the batched calls the reference lacks (radius_search_batch,
+radius_digest_batch, knn_batch). Inputs may be numpy arrays (host) or CUDA
+torch tensors (device); the C ABI stages host buffers itself.
+"""
+import ctypes
+from dataclasses import dataclass, field
+from enum import IntEnum
+
+import numpy as np
+
+from . import _native
+
+
+# ---------------------------------------------------------------- errors --
+class Error(RuntimeError):
+    """cheesemap::Error (errors.hpp:8-11)."""
+
+
+class EmptyCloudError(Error):
+    pass
+
+
+class InvalidArgumentError(Error):
+    pass
+
+
+class CapacityError(Error):
+    pass
+
+
+class OutOfDomainError(Error):
+    pass
+
+
+class CudaError(Error):
+    pass
+
+
+class NcclError(Error):
+    pass
+
+
+_ERRORS = {1: EmptyCloudError, 2: InvalidArgumentError, 3: CapacityError, 4: OutOfDomainError,
+           5: CudaError, 6: NcclError}
+
+
+def _check(status):
+    if status != 0:
+        raise _ERRORS.get(status, Error)(f"{_native.STATUS_NAMES.get(status, status)}: "
+                                         f"{_native.last_error()}")
+
+
+# ----------------------------------------------------------------- types --
+class Flavor(IntEnum):  # map.hpp:15
+    Dense = 0
+    Sparse = 1
+    Mixed = 2
+
+
+class GridMode(IntEnum):  # grid.hpp:10
+    TwoD = 0
+    ThreeD = 1
+
+
+@dataclass
+class CellSize:  # grid.hpp:15-21
+    x: float = 1.0
+    y: float = 1.0
+    z: float = 1.0
+
+    @staticmethod
+    def uniform(s):
+        return CellSize(s, s, s)
+
+
+@dataclass
+class BuildOptions:  # map.hpp:17-26
+    flavor: Flavor = Flavor.Dense
+    mode: GridMode = GridMode.ThreeD
+    cell: CellSize = field(default_factory=CellSize)
+    reorder: bool = False
+    densify_threshold: float = 0.80
+    dense_voxel_cap: int = 1 << 32
+
+    def to_c(self):
+        c = _native.BuildOptionsC()
+        c.flavor, c.mode = int(self.flavor), int(self.mode)
+        c.cell_x, c.cell_y, c.cell_z = self.cell.x, self.cell.y, self.cell.z
+        c.reorder = int(bool(self.reorder))
+        c.densify_threshold = self.densify_threshold
+        c.dense_voxel_cap = self.dense_voxel_cap
+        return c
+
+
+@dataclass
+class SphereKernel:  # geometry.hpp:73-85
+    center: tuple
+    radius: float
+
+
+@dataclass
+class BoxKernel:  # geometry.hpp:87-92; the device path takes cubes c +- r
+    center: tuple
+    half: float
+
+    @staticmethod
+    def cube(center, r):
+        return BoxKernel(tuple(center), float(r))
+
+
+@dataclass
+class Neighbor:  # search.hpp:19-24 (distance = sqrt of the fp64 d^2)
+    handle: int
+    distance: float
+
+
+SPHERE, CUBE = 0, 1
+
+
+# -------------------------------------------------------------- buffers --
+def _is_torch(x):
+    return type(x).__module__.startswith("torch")
+
+
+def _in_ptr(x, dtype=np.float64):
+    """Pointer to a host (numpy) or device (torch) buffer, plus a keepalive."""
+    if x is None:
+        return None, None
+    if _is_torch(x):
+        x = x.contiguous()
+        return ctypes.c_void_p(x.data_ptr()), x
+    a = np.ascontiguousarray(x, dtype=dtype)
+    return a.ctypes.data_as(ctypes.c_void_p), a
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        return None
+    if hasattr(stream, "cuda_stream"):
+        return ctypes.c_void_p(stream.cuda_stream)
+    return ctypes.c_void_p(int(stream))
+
+
+def _nrows(q):
+    return int(q.shape[0]) if len(q.shape) == 2 else int(q.shape[0]) // 3
+
+
+# ---------------------------------------------------------------- index --
+class Cheesemap:
+    """Device-resident cheesemap (map.hpp:53-151). Immutable once built;
+    owns its device copies of the points."""
+
+    def __init__(self, handle, opts, device, n):
+        self._h = handle
+        self._opts = opts
+        self.device = device
+        self._n = n
+
+    @staticmethod
+    def build(cloud, opts=None, device=0, stream=None):
+        opts = opts or BuildOptions()
+        L = _native.lib()
+        p, keep = _in_ptr(cloud)
+        n = _nrows(keep) if keep is not None else 0
+        h = ctypes.c_void_p()
+        c = opts.to_c()
+        _check(L.cm_build(p, n, ctypes.byref(c), device, _stream_ptr(stream), ctypes.byref(h)))
+        return Cheesemap(h, opts, device, n)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                _native.lib().cm_free(h)
+            except Exception:
+                pass
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def flavor(self):
+        return self._opts.flavor
+
+    def mode(self):
+        return self._opts.mode
+
+    def size(self):
+        return self._n
+
+    def grid(self):
+        g = _native.GridParamsC()
+        _check(_native.lib().cm_get_grid(self._h, ctypes.byref(g)))
+        return dict(origin=tuple(g.origin), cell=tuple(g.cell), nx=g.nx, ny=g.ny, nz=g.nz,
+                    mode=GridMode(g.mode), bounds_min=tuple(g.bounds_min),
+                    bounds_max=tuple(g.bounds_max))
+
+    def occupancy_stats(self):
+        """OccupancyStats (map.hpp:34-39) + per-slice mixed flags."""
+        nz = self.grid()["nz"]
+        dense = np.zeros(nz, dtype=np.uint8)
+        ne = np.zeros(nz, dtype=np.uint64)
+        o = _native.OccupancyC()
+        _check(_native.lib().cm_get_occupancy(self._h, ctypes.byref(o),
+                                              dense.ctypes.data_as(ctypes.c_void_p),
+                                              ne.ctypes.data_as(ctypes.c_void_p), nz))
+        return dict(total_voxels=o.total_voxels, non_empty=o.non_empty,
+                    empty_fraction=o.empty_fraction, n_columns=o.n_columns,
+                    slice_dense=dense.astype(bool), slice_non_empty=ne)
+
+    def build_timing(self):
+        t = _native.BuildTimingC()
+        _check(_native.lib().cm_get_build_timing(self._h, ctypes.byref(t)))
+        return {k: getattr(t, k) for k, _ in t._fields_}
+
+    def export_voxels(self):
+        """(keys u64, handles u32) in stored order (per-voxel handle sets)."""
+        keys = np.zeros(self._n, dtype=np.uint64)
+        hs = np.zeros(self._n, dtype=np.uint32)
+        _check(_native.lib().cm_export_voxels(self._h, keys.ctypes.data_as(ctypes.c_void_p),
+                                              hs.ctypes.data_as(ctypes.c_void_p)))
+        return keys, hs
+
+    def corrupt_for_testing(self):
+        _check(_native.lib().cm_corrupt_for_testing(self._h))
+
+
+# -------------------------------------------------------------- queries --
+def _kernel_args(kernel):
+    if isinstance(kernel, SphereKernel):
+        return np.asarray(kernel.center, dtype=np.float64).reshape(1, 3), SPHERE, kernel.radius
+    if isinstance(kernel, BoxKernel):
+        return np.asarray(kernel.center, dtype=np.float64).reshape(1, 3), CUBE, kernel.half
+    raise InvalidArgumentError("kernel must be SphereKernel or BoxKernel.cube")
+
+
+def radius_count(m, centers, r, kernel=SPHERE, counts=None, points_tested=None, stream=None):
+    """Per-centre neighbour counts (and QueryStats::points_tested)."""
+    qp, qk = _in_ptr(centers)
+    nq = _nrows(qk)
+    if counts is None:
+        counts = np.zeros(nq, dtype=np.uint32)
+    cp, ck = _in_ptr(counts, np.uint32)
+    tp, tk = _in_ptr(points_tested, np.uint64) if points_tested is not None else (None, None)
+    _check(_native.lib().cm_radius_count(m.handle, qp, nq, kernel, float(r), cp, tp,
+                                         _stream_ptr(stream)))
+    return counts if not isinstance(counts, np.ndarray) else ck
+
+
+def radius_search_batch(m, centers, r, kernel=SPHERE, stream=None, device_out=False):
+    """Sorted CSR of kernel_search over every centre: (row_ptr u64[nq+1],
+    cols u32[nnz]) as numpy arrays, or as CUDA torch tensors when
+    device_out=True."""
+    qp, qk = _in_ptr(centers)
+    nq = _nrows(qk)
+    L = _native.lib()
+    csr = ctypes.c_void_p()
+    _check(L.cm_radius_search(m.handle, qp, nq, kernel, float(r), _stream_ptr(stream),
+                              ctypes.byref(csr)))
+    try:
+        nnz = ctypes.c_uint64()
+        _check(L.cm_csr_info(csr, None, ctypes.byref(nnz), None, None))
+        if device_out:
+            import torch
+            row = torch.empty(nq + 1, dtype=torch.int64, device=f"cuda:{m.device}")
+            cols = torch.empty(max(nnz.value, 1), dtype=torch.int32, device=f"cuda:{m.device}")
+            _check(L.cm_csr_download(csr, ctypes.c_void_p(row.data_ptr()),
+                                     ctypes.c_void_p(cols.data_ptr()), _stream_ptr(stream)))
+            return row, cols[: nnz.value]
+        row = np.zeros(nq + 1, dtype=np.uint64)
+        cols = np.zeros(nnz.value, dtype=np.uint32)
+        _check(L.cm_csr_download(csr, row.ctypes.data_as(ctypes.c_void_p),
+                                 cols.ctypes.data_as(ctypes.c_void_p), _stream_ptr(stream)))
+        return row, cols
+    finally:
+        L.cm_csr_free(csr)
+
+
+def radius_digest_batch(m, centers, r, kernel=SPHERE, stream=None):
+    """Per-centre (count u32, digest u64 = sum(mix64(handle)))."""
+    qp, qk = _in_ptr(centers)
+    nq = _nrows(qk)
+    counts = np.zeros(nq, dtype=np.uint32)
+    dig = np.zeros(nq, dtype=np.uint64)
+    _check(_native.lib().cm_radius_digest(m.handle, qp, nq, kernel, float(r),
+                                          counts.ctypes.data_as(ctypes.c_void_p),
+                                          dig.ctypes.data_as(ctypes.c_void_p),
+                                          _stream_ptr(stream)))
+    return counts, dig
+
+
+def knn_batch(m, centers, k, stream=None):
+    """(idx u32[nq, k], d2 f64[nq, k]) ordered by (d^2, handle)."""
+    qp, qk = _in_ptr(centers)
+    nq = _nrows(qk)
+    idx = np.zeros((nq, k), dtype=np.uint32)
+    d2 = np.zeros((nq, k), dtype=np.float64)
+    _check(_native.lib().cm_knn(m.handle, qp, nq, int(k), idx.ctypes.data_as(ctypes.c_void_p),
+                                d2.ctypes.data_as(ctypes.c_void_p), _stream_ptr(stream)))
+    return idx, d2
+
+
+def kernel_search(m, kernel):
+    """kernel_search (search.hpp:102-127) for one kernel: the handles inside
+    it, sorted ascending."""
+    c, kind, r = _kernel_args(kernel)
+    _, cols = radius_search_batch(m, c, r, kind)
+    return cols.astype(np.uint64)
+
+
+def knn_search(m, c, k):
+    """knn_search (search.cpp:87-146): min(k, N) nearest, by (d^2, handle)."""
+    if k == 0:
+        raise InvalidArgumentError("k must be at least 1")
+    idx, d2 = knn_batch(m, np.asarray(c, dtype=np.float64).reshape(1, 3), k)
+    return [Neighbor(int(i), float(np.sqrt(d))) for i, d in zip(idx[0], d2[0])
+            if i != 0xFFFFFFFF]

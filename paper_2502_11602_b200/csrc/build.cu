@@ -1,0 +1,425 @@
+// Index build on sm_100a: K1 bbox -> grid dims -> K2 cell keys -> K3 radix
+// sort -> record gather -> K4 unique voxels + flavour tables.
+// Replaces Cheesemap::build (map.cpp:22-122).
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "index.cuh"
+#include "sort_scan.cuh"
+
+namespace cmg {
+
+namespace {
+
+__device__ __forceinline__ unsigned long long ord_of(double d) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(d);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+inline double double_of_ord(unsigned long long u) {
+  const unsigned long long b = (u >> 63) ? (u & 0x7fffffffffffffffull) : ~u;
+  double d;
+  std::memcpy(&d, &b, 8);
+  return d;
+}
+
+// K1: per-axis min/max (aabb_of_points, geometry.cpp:7-21).
+__global__ void bbox_kernel(const double* __restrict__ xyz, uint64_t n,
+                            unsigned long long* __restrict__ out /* minx,miny,minz,maxx,maxy,maxz */) {
+  double lo[3], hi[3];
+  bool any = false;
+  for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n;
+       p += (uint64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double v = xyz[3 * p + a];
+      if (!any) {
+        lo[a] = hi[a] = v;
+      } else {
+        lo[a] = (v < lo[a]) ? v : lo[a];
+        hi[a] = (hi[a] < v) ? v : hi[a];
+      }
+    }
+    any = true;
+  }
+  unsigned long long olo[3], ohi[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    olo[a] = any ? ord_of(lo[a]) : ~0ull;
+    ohi[a] = any ? ord_of(hi[a]) : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long l2 = __shfl_xor_sync(0xffffffffu, olo[a], o);
+      const unsigned long long h2 = __shfl_xor_sync(0xffffffffu, ohi[a], o);
+      olo[a] = l2 < olo[a] ? l2 : olo[a];
+      ohi[a] = h2 > ohi[a] ? h2 : ohi[a];
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      atomicMin(out + a, olo[a]);
+      atomicMax(out + 3 + a, ohi[a]);
+    }
+  }
+}
+
+// K2: key = global_index(voxel_of(p)) (grid.cpp:63-72, grid.hpp:65-67).
+template <typename K>
+__global__ void keys_kernel(const double* __restrict__ xyz, uint64_t n, DevGrid g,
+                            K* __restrict__ keys, uint32_t* __restrict__ vals) {
+  for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n;
+       p += (uint64_t)gridDim.x * blockDim.x) {
+    const double x = xyz[3 * p], y = xyz[3 * p + 1], z = xyz[3 * p + 2];
+    const uint64_t i = axis_index(x, g.ox, g.sx, g.nx);
+    const uint64_t j = axis_index(y, g.oy, g.sy, g.ny);
+    const uint64_t k = g.mode3d ? axis_index(z, g.oz, g.sz, g.nz) : 0;
+    keys[p] = (K)(i * (g.ny * g.nz) + j * g.nz + k);
+    vals[p] = (uint32_t)p;
+  }
+}
+
+// Sorted order -> 32-byte records; run-start flags for the unique pass.
+template <typename K>
+__global__ void gather_kernel(const double* __restrict__ xyz, const K* __restrict__ keys,
+                              const uint32_t* __restrict__ perm, uint64_t n, uint64_t nz,
+                              PointRec* __restrict__ rec, uint32_t* __restrict__ flags) {
+  for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < n;
+       s += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t h = perm[s];
+    const uint64_t key = (uint64_t)keys[s];
+    double2 a, b;
+    a.x = xyz[3 * (uint64_t)h];
+    a.y = xyz[3 * (uint64_t)h + 1];
+    b.x = xyz[3 * (uint64_t)h + 2];
+    uint2 t;
+    t.x = h;
+    t.y = (uint32_t)(key % nz);
+    b.y = *reinterpret_cast<double*>(&t);
+    reinterpret_cast<double2*>(rec + s)[0] = a;
+    reinterpret_cast<double2*>(rec + s)[1] = b;
+    flags[s] = (s == 0 || keys[s - 1] != keys[s]) ? 1u : 0u;
+  }
+}
+
+template <typename K>
+__global__ void unique_kernel(const K* __restrict__ keys, const uint32_t* __restrict__ flags,
+                              const uint32_t* __restrict__ pos, uint64_t n, uint64_t nz,
+                              uint64_t* __restrict__ ukey, uint32_t* __restrict__ ustart,
+                              uint32_t* __restrict__ uk_k, unsigned long long* __restrict__ slice_ne) {
+  for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < n;
+       s += (uint64_t)gridDim.x * blockDim.x) {
+    if (flags[s]) {
+      const uint32_t u = pos[s];
+      const uint64_t key = (uint64_t)keys[s];
+      ukey[u] = key;
+      ustart[u] = (uint32_t)s;
+      const uint32_t k = (uint32_t)(key % nz);
+      if (uk_k) uk_k[u] = k;
+      atomicAdd(slice_ne + k, 1ull);
+    }
+  }
+}
+
+__global__ void dense_counts_kernel(const uint64_t* __restrict__ ukey,
+                                    const uint32_t* __restrict__ ustart, uint64_t U,
+                                    uint32_t* __restrict__ cnt) {
+  for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < U;
+       u += (uint64_t)gridDim.x * blockDim.x)
+    cnt[ukey[u]] = ustart[u + 1] - ustart[u];
+}
+
+__global__ void hash_insert_kernel(const uint64_t* __restrict__ keys,
+                                   const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
+                                   uint64_t m, HashSlot* __restrict__ t, uint64_t mask,
+                                   int a_is_index) {
+  for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < m;
+       u += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t key = keys[u];
+    uint64_t s = mix64(key) & mask;
+    for (;;) {
+      const unsigned long long prev = atomicCAS(
+          reinterpret_cast<unsigned long long*>(&t[s].key), (unsigned long long)kEmptyKey,
+          (unsigned long long)key);
+      if (prev == kEmptyKey) {
+        t[s].a = a_is_index ? (uint32_t)u : a[u];
+        t[s].b = a_is_index ? 0u : b[u];
+        break;
+      }
+      s = (s + 1) & mask;
+    }
+  }
+}
+
+// Column of each unique voxel; run-start flags over columns.
+__global__ void column_flags_kernel(const uint64_t* __restrict__ ukey, uint64_t U, uint64_t nz,
+                                    uint32_t* __restrict__ flags) {
+  for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < U;
+       u += (uint64_t)gridDim.x * blockDim.x)
+    flags[u] = (u == 0 || ukey[u - 1] / nz != ukey[u] / nz) ? 1u : 0u;
+}
+
+__global__ void column_scatter_kernel(const uint64_t* __restrict__ ukey,
+                                      const uint32_t* __restrict__ flags,
+                                      const uint32_t* __restrict__ pos, uint64_t U, uint64_t nz,
+                                      uint64_t* __restrict__ col_id,
+                                      uint32_t* __restrict__ col_vbeg,
+                                      uint32_t* __restrict__ col_dense) {
+  for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < U;
+       u += (uint64_t)gridDim.x * blockDim.x) {
+    if (flags[u]) {
+      const uint32_t c = pos[u];
+      const uint64_t col = ukey[u] / nz;
+      col_vbeg[c] = (uint32_t)u;
+      if (col_id) col_id[c] = col;
+      if (col_dense) col_dense[col] = c;
+    }
+  }
+}
+
+unsigned grid_for(uint64_t n, unsigned threads = 256) {
+  const uint64_t want = (n + threads - 1) / threads;
+  const uint64_t cap = (uint64_t)sm_count() * 16;
+  return (unsigned)std::max<uint64_t>(1, std::min(want, cap));
+}
+
+uint64_t next_pow2(uint64_t v) {
+  uint64_t p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+int bit_width(uint64_t v) {
+  int b = 0;
+  while (v) {
+    ++b;
+    v >>= 1;
+  }
+  return b;
+}
+
+// grid.cpp:18-27
+cm_status axis_dim(double lo, double hi, double cell, uint64_t* out, const char* axis) {
+  if (!(cell > 0.0)) {
+    set_error(std::string("cell size must be strictly positive (axis ") + axis + ")");
+    return CM_INVALID_ARGUMENT;
+  }
+  const double n = std::floor((hi - lo) / cell) + 1.0;
+  if (n >= 9.3e18) {
+    set_error("grid axis exceeds the index type capacity");
+    return CM_CAPACITY;
+  }
+  *out = static_cast<uint64_t>(n);
+  return CM_OK;
+}
+
+struct Events {
+  cudaEvent_t e[8];
+  int used = 0;
+  Events() {
+    for (auto& x : e) cudaEventCreate(&x);
+  }
+  ~Events() {
+    for (auto& x : e) cudaEventDestroy(x);
+  }
+};
+
+template <typename K>
+cm_status build_typed(const double* xyz, uint64_t n, cudaStream_t st, cm_index* ix,
+                      Events& ev) {
+  const DevGrid& g = ix->g;
+  K* keys = nullptr;
+  uint32_t* perm = nullptr;
+  void* scratch = nullptr;
+  CM_CUDA_TRY(dev_alloc_t(&keys, n, st));
+  CM_CUDA_TRY(dev_alloc_t(&perm, n, st));
+  CM_CUDA_TRY(dev_alloc(&scratch, radix_scratch_bytes<K>(n), st));
+  keys_kernel<K><<<grid_for(n), 256, 0, st>>>(xyz, n, g, keys, perm);
+  cudaEventRecord(ev.e[2], st);
+  ix->key_bits = bit_width(ix->V - 1);
+  ix->timing.sort_passes = (uint32_t)radix_sort_pairs<K>(keys, perm, n, ix->key_bits, scratch, st);
+  cudaEventRecord(ev.e[3], st);
+  dev_free(scratch, st);
+
+  CM_CUDA_TRY(dev_alloc_t(&ix->rec, n, st));
+  uint32_t* flags = nullptr;
+  uint32_t* pos = nullptr;
+  uint32_t* part = nullptr;
+  CM_CUDA_TRY(dev_alloc_t(&flags, n, st));
+  CM_CUDA_TRY(dev_alloc_t(&pos, n + 1, st));
+  CM_CUDA_TRY(dev_alloc_t(&part, scan_part_elems(n), st));
+  gather_kernel<K><<<grid_for(n), 256, 0, st>>>(xyz, keys, perm, n, g.nz, ix->rec, flags);
+  cudaEventRecord(ev.e[4], st);
+  exclusive_scan<uint32_t, uint32_t>(flags, n, pos, part, 1, st);
+  uint32_t U32 = 0;
+  CM_CUDA_TRY(cudaMemcpyAsync(&U32, pos + n, 4, cudaMemcpyDeviceToHost, st));
+  CM_CUDA_TRY(cudaStreamSynchronize(st));
+  const uint64_t U = U32;
+  ix->U = U;
+  const int flavor = ix->opts.flavor;
+  unsigned long long* slice_ne = nullptr;
+  CM_CUDA_TRY(dev_alloc_t(&ix->ukey, U, st));
+  CM_CUDA_TRY(dev_alloc_t(&ix->ustart, U + 1, st));
+  if (flavor == CM_MIXED) CM_CUDA_TRY(dev_alloc_t(&ix->uk_k, U, st));
+  CM_CUDA_TRY(dev_alloc_t(&slice_ne, g.nz, st));
+  CM_CUDA_TRY(cudaMemsetAsync(slice_ne, 0, g.nz * 8, st));
+  const uint32_t n32 = (uint32_t)n;
+  CM_CUDA_TRY(cudaMemcpyAsync(ix->ustart + U, &n32, 4, cudaMemcpyHostToDevice, st));
+  unique_kernel<K><<<grid_for(n), 256, 0, st>>>(keys, flags, pos, n, g.nz, ix->ukey, ix->ustart,
+                                                 ix->uk_k, slice_ne);
+  ix->slice_ne.assign(g.nz, 0);
+  CM_CUDA_TRY(cudaMemcpyAsync(ix->slice_ne.data(), slice_ne, g.nz * 8, cudaMemcpyDeviceToHost, st));
+  dev_free(keys, st);
+  dev_free(perm, st);
+
+  if (flavor == CM_DENSE) {
+    CM_CUDA_TRY(dev_alloc_t(&ix->dense_off, ix->V + 1, st));
+    CM_CUDA_TRY(cudaMemsetAsync(ix->dense_off, 0, (ix->V + 1) * 4, st));
+    dense_counts_kernel<<<grid_for(U), 256, 0, st>>>(ix->ukey, ix->ustart, U, ix->dense_off);
+    uint32_t* vpart = nullptr;
+    CM_CUDA_TRY(dev_alloc_t(&vpart, scan_part_elems(ix->V), st));
+    exclusive_scan<uint32_t, uint32_t>(ix->dense_off, ix->V, ix->dense_off, vpart, 1, st);
+    dev_free(vpart, st);
+  } else if (flavor == CM_SPARSE) {
+    const uint64_t cap = next_pow2(std::max<uint64_t>(2 * U, 1024));
+    ix->vmask = cap - 1;
+    CM_CUDA_TRY(dev_alloc_t(&ix->vhash, cap, st));
+    CM_CUDA_TRY(cudaMemsetAsync(ix->vhash, 0xff, cap * sizeof(HashSlot), st));
+    hash_insert_kernel<<<grid_for(U), 256, 0, st>>>(ix->ukey, ix->ustart, ix->ustart + 1, U,
+                                                    ix->vhash, ix->vmask, 0);
+  } else {
+    // mixed: 2D column table over the (i, j) footprint + sparse z lists
+    column_flags_kernel<<<grid_for(U), 256, 0, st>>>(ix->ukey, U, g.nz, flags);
+    exclusive_scan<uint32_t, uint32_t>(flags, U, pos, part, 1, st);
+    uint32_t C32 = 0;
+    CM_CUDA_TRY(cudaMemcpyAsync(&C32, pos + U, 4, cudaMemcpyDeviceToHost, st));
+    CM_CUDA_TRY(cudaStreamSynchronize(st));
+    const uint64_t C = C32;
+    ix->C = C;
+    const uint64_t footprint = g.nx * g.ny;
+    CM_CUDA_TRY(dev_alloc_t(&ix->col_vbeg, C + 1, st));
+    const uint32_t U32v = (uint32_t)U;
+    CM_CUDA_TRY(cudaMemcpyAsync(ix->col_vbeg + C, &U32v, 4, cudaMemcpyHostToDevice, st));
+    // The column table densifies by the reference's rule for a mixed slice
+    // (map.cpp:106-108), applied to the 2D footprint.
+    const bool dense_fp =
+        static_cast<double>(C) / static_cast<double>(footprint) >= ix->opts.densify_threshold;
+    uint64_t* col_id = nullptr;
+    if (dense_fp) {
+      CM_CUDA_TRY(dev_alloc_t(&ix->col_dense, footprint, st));
+      CM_CUDA_TRY(cudaMemsetAsync(ix->col_dense, 0xff, footprint * 4, st));
+    } else {
+      CM_CUDA_TRY(dev_alloc_t(&col_id, C, st));
+    }
+    column_scatter_kernel<<<grid_for(U), 256, 0, st>>>(ix->ukey, flags, pos, U, g.nz, col_id,
+                                                       ix->col_vbeg, ix->col_dense);
+    if (!dense_fp) {
+      const uint64_t cap = next_pow2(std::max<uint64_t>(2 * C, 1024));
+      ix->cmask = cap - 1;
+      CM_CUDA_TRY(dev_alloc_t(&ix->chash, cap, st));
+      CM_CUDA_TRY(cudaMemsetAsync(ix->chash, 0xff, cap * sizeof(HashSlot), st));
+      hash_insert_kernel<<<grid_for(C), 256, 0, st>>>(col_id, nullptr, nullptr, C, ix->chash,
+                                                      ix->cmask, 1);
+      dev_free(col_id, st);
+    }
+  }
+  dev_free(flags, st);
+  dev_free(pos, st);
+  dev_free(part, st);
+  dev_free(slice_ne, st);
+  CM_CUDA_TRY(cudaGetLastError());
+  return CM_OK;
+}
+
+}  // namespace
+
+cm_status build_index(const double* xyz, uint64_t n, const cm_build_options& o, cudaStream_t st,
+                      cm_index* ix) {
+  // Check order follows map.cpp:23-39.
+  if (n == 0) {
+    set_error("point cloud is empty");
+    return CM_EMPTY_CLOUD;
+  }
+  if (!(o.densify_threshold > 0.0) || o.densify_threshold > 1.0) {
+    set_error("densify threshold must be in (0, 1]");
+    return CM_INVALID_ARGUMENT;
+  }
+  if (o.flavor < CM_DENSE || o.flavor > CM_MIXED || (o.mode != CM_TWOD && o.mode != CM_THREED)) {
+    set_error("unknown flavor or grid mode");
+    return CM_INVALID_ARGUMENT;
+  }
+  if (n >= (1ull << 32)) {
+    set_error("clouds of 2^32 points or more exceed the device handle type (u32)");
+    return CM_CAPACITY;
+  }
+  ix->opts = o;
+  ix->n = n;
+  Events ev;
+  cudaEventRecord(ev.e[0], st);
+  unsigned long long* bb = nullptr;
+  CM_CUDA_TRY(dev_alloc_t(&bb, 6, st));
+  unsigned long long init[6] = {~0ull, ~0ull, ~0ull, 0ull, 0ull, 0ull};
+  CM_CUDA_TRY(cudaMemcpyAsync(bb, init, sizeof(init), cudaMemcpyHostToDevice, st));
+  bbox_kernel<<<grid_for(n), 256, 0, st>>>(xyz, n, bb);
+  unsigned long long hb[6];
+  CM_CUDA_TRY(cudaMemcpyAsync(hb, bb, sizeof(hb), cudaMemcpyDeviceToHost, st));
+  cudaEventRecord(ev.e[1], st);
+  CM_CUDA_TRY(cudaStreamSynchronize(st));
+  dev_free(bb, st);
+  double lo[3], hi[3];
+  for (int a = 0; a < 3; ++a) {
+    lo[a] = double_of_ord(hb[a]);
+    hi[a] = double_of_ord(hb[3 + a]);
+  }
+  // grid_dims (grid.cpp:41-61)
+  DevGrid& g = ix->g;
+  g.ox = lo[0], g.oy = lo[1], g.oz = lo[2];
+  g.bx0 = lo[0], g.by0 = lo[1], g.bz0 = lo[2];
+  g.bx1 = hi[0], g.by1 = hi[1], g.bz1 = hi[2];
+  g.sx = o.cell_x, g.sy = o.cell_y, g.sz = o.cell_z;
+  g.mode3d = o.mode == CM_THREED;
+  cm_status s;
+  if ((s = axis_dim(lo[0], hi[0], o.cell_x, &g.nx, "x")) != CM_OK) return s;
+  if ((s = axis_dim(lo[1], hi[1], o.cell_y, &g.ny, "y")) != CM_OK) return s;
+  if (g.mode3d) {
+    if ((s = axis_dim(lo[2], hi[2], o.cell_z, &g.nz, "z")) != CM_OK) return s;
+  } else {
+    g.nz = 1;
+  }
+  const uint64_t limit = 1ull << 63;
+  if ((g.ny != 0 && g.nx > limit / g.ny) || (g.nz != 0 && g.nx * g.ny > limit / g.nz)) {
+    set_error("voxel count overflows the index type");
+    return CM_CAPACITY;
+  }
+  ix->V = g.nx * g.ny * g.nz;
+  if (o.flavor == CM_DENSE && ix->V > o.dense_voxel_cap) {  // map.cpp:35-39
+    set_error("dense grid of " + std::to_string(ix->V) +
+              " voxels exceeds the cap; use the sparse or mixed flavor");
+    return CM_CAPACITY;
+  }
+  if (o.flavor == CM_DENSE && ix->V >= (1ull << 32) - 1) {
+    set_error("dense offset table needs V + 1 < 2^32 entries on the device");
+    return CM_CAPACITY;
+  }
+  s = ix->V <= (1ull << 32) ? build_typed<uint32_t>(xyz, n, st, ix, ev)
+                            : build_typed<uint64_t>(xyz, n, st, ix, ev);
+  if (s != CM_OK) return s;
+  cudaEventRecord(ev.e[5], st);
+  CM_CUDA_TRY(cudaStreamSynchronize(st));
+  float ms;
+  cudaEventElapsedTime(&ms, ev.e[0], ev.e[5]);
+  ix->timing.total_ms = ms;
+  cudaEventElapsedTime(&ms, ev.e[0], ev.e[1]);
+  ix->timing.bbox_ms = ms;
+  cudaEventElapsedTime(&ms, ev.e[1], ev.e[2]);
+  ix->timing.keys_ms = ms;
+  cudaEventElapsedTime(&ms, ev.e[2], ev.e[3]);
+  ix->timing.sort_ms = ms;
+  cudaEventElapsedTime(&ms, ev.e[3], ev.e[4]);
+  ix->timing.gather_ms = ms;
+  cudaEventElapsedTime(&ms, ev.e[4], ev.e[5]);
+  ix->timing.tables_ms = ms;
+  return CM_OK;
+}
+
+}  // namespace cmg

@@ -1,0 +1,114 @@
+// Host-side index object and internal entry points shared by the build,
+// query and kNN translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <vector>
+
+#include "common.cuh"
+
+struct cm_index {
+  int device = 0;
+  cm_build_options opts{};
+  cmg::DevGrid g{};
+  uint64_t n = 0;       // points
+  uint64_t V = 0;       // total voxels
+  uint64_t U = 0;       // non-empty voxels
+  uint64_t C = 0;       // non-empty (i, j) columns
+  int key_bits = 0;
+
+  cmg::PointRec* rec = nullptr;  // n, cell order
+  uint64_t* ukey = nullptr;      // U unique voxel keys (ascending)
+  uint32_t* ustart = nullptr;    // U + 1 record offsets
+  uint32_t* uk_k = nullptr;      // U voxel z index
+  // dense
+  uint32_t* dense_off = nullptr;  // V + 1
+  // sparse
+  cmg::HashSlot* vhash = nullptr;
+  uint64_t vmask = 0;
+  // mixed
+  uint32_t* col_dense = nullptr;  // nx*ny (when the footprint is dense)
+  cmg::HashSlot* chash = nullptr;
+  uint64_t cmask = 0;
+  uint32_t* col_vbeg = nullptr;   // C + 1
+
+  std::vector<uint64_t> slice_ne;  // per z slice non-empty voxels (host)
+  cm_build_timing timing{};
+
+  cmg::Tables tables() const {
+    cmg::Tables t{};
+    t.g = g;
+    t.rec = rec;
+    t.n = n;
+    t.flavor = opts.flavor;
+    t.dense_off = dense_off;
+    t.vhash = vhash;
+    t.vmask = vmask;
+    t.col_dense = col_dense;
+    t.chash = chash;
+    t.cmask = cmask;
+    t.col_vbeg = col_vbeg;
+    t.uk_k = uk_k;
+    t.ustart = ustart;
+    return t;
+  }
+};
+
+namespace cmg {
+
+// Device-memory helpers (stream-ordered pool).
+cudaError_t dev_alloc(void** p, size_t bytes, cudaStream_t st);
+void dev_free(void* p, cudaStream_t st);
+
+template <typename T>
+inline cudaError_t dev_alloc_t(T** p, size_t count, cudaStream_t st) {
+  return dev_alloc(reinterpret_cast<void**>(p), count * sizeof(T), st);
+}
+
+bool is_device_ptr(const void* p);
+
+// A buffer that is the caller's device pointer, or a device copy of a host
+// input (freed on destruction).
+struct InBuf {
+  const void* dev = nullptr;
+  void* owned = nullptr;
+  cudaStream_t st = nullptr;
+  ~InBuf() {
+    if (owned) dev_free(owned, st);
+  }
+};
+cm_status stage_input(const void* p, size_t bytes, cudaStream_t st, InBuf* out);
+
+cm_status build_index(const double* xyz_dev, uint64_t n, const cm_build_options& o,
+                      cudaStream_t st, cm_index* ix);
+
+// Query pipeline pieces (query.cu)
+struct QueryOrder {
+  uint32_t* perm = nullptr;  // sorted position -> query index
+  uint64_t nq = 0;
+  cudaStream_t st = nullptr;
+  ~QueryOrder() {
+    if (perm) dev_free(perm, st);
+  }
+};
+cm_status order_queries(const cm_index* ix, const double* q_dev, uint64_t nq, cudaStream_t st,
+                        QueryOrder* out);
+cm_status radius_count_dev(const cm_index* ix, const double* q_dev, uint64_t nq, int kernel,
+                           double r, const uint32_t* perm, uint32_t* counts_dev,
+                           uint64_t* tested_dev, cudaStream_t st);
+cm_status radius_fill_dev(const cm_index* ix, const double* q_dev, uint64_t nq, int kernel,
+                          double r, const uint32_t* perm, const uint64_t* row_ptr_dev,
+                          uint32_t* cols_dev, cudaStream_t st);
+cm_status radius_digest_dev(const cm_index* ix, const double* q_dev, uint64_t nq, int kernel,
+                            double r, const uint32_t* perm, uint32_t* counts_dev,
+                            uint64_t* digest_dev, cudaStream_t st);
+cm_status counts_to_row_ptr(const uint32_t* counts_dev, uint64_t nq, uint64_t* row_ptr_dev,
+                            cudaStream_t st);
+cm_status knn_dev(const cm_index* ix, const double* q_dev, uint64_t nq, uint32_t k,
+                  const uint32_t* perm, uint32_t* idx_dev, double* d2_dev, cudaStream_t st);
+
+int sm_count();
+
+}  // namespace cmg

@@ -1,0 +1,222 @@
+// Exact batched kNN on sm_100a, ordered by (fp64 squared distance, handle).
+// Replaces knn_search (search.cpp:87-146).
+//
+// The reference grows a ball by a density estimate (grow_radius,
+// search.cpp:58-74) and stops when k candidates lie within the visited
+// radius. Here a warp walks Chebyshev voxel shells around the centre's voxel
+// (shell L = voxels at max(|di|,|dj|,|dk|) == L; ring columns contribute
+// their whole z range, inner columns only k0 +- L) and stops once the k-th
+// best squared distance is strictly below the squared distance from the
+// centre to every unvisited voxel (less a rounding margin). Both searches are
+// exact; this one also settles ties by handle, which the reference's
+// insertion-ordered CandidateList (search.cpp:16-28) does not.
+#include <algorithm>
+
+#include "index.cuh"
+#include "sort_scan.cuh"
+
+namespace cmg {
+
+namespace {
+
+constexpr int kKThreads = 128;
+constexpr int kKWarps = kKThreads / 32;
+constexpr int kKMax = 256;
+
+__device__ __forceinline__ int64_t imax64(int64_t a, int64_t b) { return a < b ? b : a; }
+__device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return b < a ? b : a; }
+
+__device__ __forceinline__ bool pair_less(double a, uint32_t ia, double b, uint32_t ib) {
+  return a < b || (a == b && ia < ib);
+}
+
+template <int FLAVOR>
+__device__ __forceinline__ void shell_column_spans(const Tables& t, int64_t i, int64_t j,
+                                                   bool ring, int64_t kc, int64_t L,
+                                                   uint64_t kmax, uint32_t* b1, uint32_t* e1,
+                                                   uint32_t* b2, uint32_t* e2) {
+  *b1 = *e1 = *b2 = *e2 = 0;
+  if (ring) {
+    const int64_t k0 = imax64(0, kc - L);
+    const int64_t k1 = imin64((int64_t)kmax, kc + L);
+    column_span<FLAVOR>(t, (uint64_t)i, (uint64_t)j, (uint64_t)k0, (uint64_t)k1, b1, e1);
+  } else {
+    if (kc - L >= 0)
+      column_span<FLAVOR>(t, (uint64_t)i, (uint64_t)j, (uint64_t)(kc - L), (uint64_t)(kc - L), b1, e1);
+    if (kc + L <= (int64_t)kmax)
+      column_span<FLAVOR>(t, (uint64_t)i, (uint64_t)j, (uint64_t)(kc + L), (uint64_t)(kc + L), b2, e2);
+  }
+}
+
+template <int FLAVOR>
+__global__ void __launch_bounds__(kKThreads) knn_warp_kernel(const Tables t,
+                                                             const double* __restrict__ q,
+                                                             uint64_t nq, uint32_t k,
+                                                             const uint32_t* __restrict__ perm,
+                                                             uint32_t* __restrict__ idx_out,
+                                                             double* __restrict__ d2_out) {
+  __shared__ double sd[kKWarps][kKMax];
+  __shared__ uint32_t sid[kKWarps][kKMax];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  double* ld = sd[wib];
+  uint32_t* lid = sid[wib];
+  const uint64_t W = (uint64_t)gridDim.x * kKWarps;
+  const DevGrid& g = t.g;
+  const uint32_t lt = lanemask_lt();
+  const int64_t nx = (int64_t)g.nx, ny = (int64_t)g.ny, nzm = (int64_t)g.nz - 1;
+
+  for (uint64_t s = (uint64_t)blockIdx.x * kKWarps + wib; s < nq; s += W) {
+    const uint32_t qi = perm ? __ldg(perm + s) : (uint32_t)s;
+    const double cx = __ldg(q + 3 * (uint64_t)qi);
+    const double cy = __ldg(q + 3 * (uint64_t)qi + 1);
+    const double cz = __ldg(q + 3 * (uint64_t)qi + 2);
+    const int64_t ic = (int64_t)axis_index(cx, g.ox, g.sx, g.nx);
+    const int64_t jc = (int64_t)axis_index(cy, g.oy, g.sy, g.ny);
+    const int64_t kc = g.mode3d ? (int64_t)axis_index(cz, g.oz, g.sz, g.nz) : 0;
+    // rounding margin for the unvisited-distance bound (coordinates ulps)
+    const double eps = 1e-12 * (fabs(cx) + fabs(cy) + fabs(cz) + fabs(g.ox) + fabs(g.oy) +
+                                fabs(g.oz) + g.sx + g.sy + g.sz);
+    uint32_t cnt = 0;
+    for (int64_t L = 0;; ++L) {
+      const int64_t i0 = imax64(0, ic - L), i1 = imin64(nx - 1, ic + L);
+      const int64_t j0 = imax64(0, jc - L), j1 = imin64(ny - 1, jc + L);
+      const int64_t nj = j1 - j0 + 1;
+      const int64_t ncol = (i1 - i0 + 1) * nj;
+      for (int64_t cb = 0; cb < ncol; cb += 32) {
+        const int64_t c = cb + lane;
+        uint32_t b1 = 0, e1 = 0, b2 = 0, e2 = 0;
+        if (c < ncol) {
+          const int64_t i = i0 + c / nj, j = j0 + c % nj;
+          const bool ring = (i == ic - L) || (i == ic + L) || (j == jc - L) || (j == jc + L);
+          if (ring || L > 0)
+            shell_column_spans<FLAVOR>(t, i, j, ring, kc, L, (uint64_t)nzm, &b1, &e1, &b2, &e2);
+        }
+        const uint32_t l1 = e1 - b1;
+        const uint32_t len = l1 + (e2 - b2);
+        const uint32_t incl = warp_incl_scan(len);
+        const uint32_t excl = incl - len;
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        for (uint32_t t0 = 0; t0 < total; t0 += 32) {
+          const uint32_t tt = t0 + lane;
+          int Lq = 0;
+#pragma unroll
+          for (int sft = 16; sft > 0; sft >>= 1) {
+            const uint32_t v = __shfl_sync(0xffffffffu, incl, Lq + sft - 1);
+            if (v <= tt) Lq += sft;
+          }
+          const uint32_t xL = __shfl_sync(0xffffffffu, excl, Lq);
+          const uint32_t b1L = __shfl_sync(0xffffffffu, b1, Lq);
+          const uint32_t l1L = __shfl_sync(0xffffffffu, l1, Lq);
+          const uint32_t b2L = __shfl_sync(0xffffffffu, b2, Lq);
+          double d2 = 0.0;
+          uint32_t id = 0;
+          bool acc = false;
+          if (tt < total) {
+            const uint32_t o = tt - xL;
+            const uint32_t pos = o < l1L ? b1L + o : b2L + (o - l1L);
+            const PointRec pr = load_rec(t.rec + pos);
+            d2 = sqdist(pr.x, pr.y, pr.z, cx, cy, cz);
+            id = pr.id;
+            acc = cnt < k || pair_less(d2, id, ld[k - 1], lid[k - 1]);
+          }
+          uint32_t m = __ballot_sync(0xffffffffu, acc);
+          while (m) {
+            const int src = __ffs(m) - 1;
+            m &= m - 1;
+            const double d = __shfl_sync(0xffffffffu, d2, src);
+            const uint32_t di = __shfl_sync(0xffffffffu, id, src);
+            if (cnt == k && !pair_less(d, di, ld[k - 1], lid[k - 1])) continue;
+            // insertion position = #entries less than (d, di)
+            uint32_t pos = 0;
+            for (uint32_t base = 0; base < cnt; base += 32) {
+              const uint32_t x = base + lane;
+              const bool less = x < cnt && pair_less(ld[x], lid[x], d, di);
+              pos += __popc(__ballot_sync(0xffffffffu, less));
+            }
+            const uint32_t ncnt = cnt < k ? cnt + 1 : k;
+            // shift [pos, ncnt-1) -> [pos+1, ncnt)
+            double vd[kKMax / 32];
+            uint32_t vi[kKMax / 32];
+#pragma unroll
+            for (int c2 = 0; c2 < kKMax / 32; ++c2) {
+              const uint32_t x = c2 * 32 + lane;
+              if (x > pos && x < ncnt) {
+                vd[c2] = ld[x - 1];
+                vi[c2] = lid[x - 1];
+              }
+            }
+            __syncwarp();
+#pragma unroll
+            for (int c2 = 0; c2 < kKMax / 32; ++c2) {
+              const uint32_t x = c2 * 32 + lane;
+              if (x > pos && x < ncnt) {
+                ld[x] = vd[c2];
+                lid[x] = vi[c2];
+              }
+            }
+            if (lane == 0) {
+              ld[pos] = d;
+              lid[pos] = di;
+            }
+            __syncwarp();
+            cnt = ncnt;
+          }
+        }
+      }
+      // distance from c to the nearest unvisited voxel face
+      const bool all = i0 == 0 && i1 == nx - 1 && j0 == 0 && j1 == ny - 1 &&
+                       imax64(0, kc - L) == 0 && imin64(nzm, kc + L) == nzm;
+      if (all) break;
+      if (cnt == k) {
+        double dmin = 1e300;
+        if (i0 > 0) dmin = fmin(dmin, cx - (g.ox + (double)i0 * g.sx));
+        if (i1 < nx - 1) dmin = fmin(dmin, (g.ox + (double)(i1 + 1) * g.sx) - cx);
+        if (j0 > 0) dmin = fmin(dmin, cy - (g.oy + (double)j0 * g.sy));
+        if (j1 < ny - 1) dmin = fmin(dmin, (g.oy + (double)(j1 + 1) * g.sy) - cy);
+        if (g.mode3d) {
+          if (kc - L > 0) dmin = fmin(dmin, cz - (g.oz + (double)(kc - L) * g.sz));
+          if (kc + L < nzm) dmin = fmin(dmin, (g.oz + (double)(kc + L + 1) * g.sz) - cz);
+        }
+        const double dm = dmin - eps;
+        if (dm > 0.0 && ld[k - 1] < dm * dm) break;
+      }
+    }
+    for (uint32_t x = lane; x < k; x += 32) {
+      idx_out[(uint64_t)qi * k + x] = x < cnt ? lid[x] : 0xffffffffu;
+      if (d2_out) d2_out[(uint64_t)qi * k + x] = x < cnt ? ld[x] : __longlong_as_double(0x7ff0000000000000ll);
+    }
+    __syncwarp();
+  }
+  (void)lt;
+}
+
+}  // namespace
+
+cm_status knn_dev(const cm_index* ix, const double* q, uint64_t nq, uint32_t k,
+                  const uint32_t* perm, uint32_t* idx, double* d2, cudaStream_t st) {
+  if (nq == 0) return CM_OK;
+  if (k > (uint32_t)kKMax) {
+    set_error("k above the device limit of 256");
+    return CM_INVALID_ARGUMENT;
+  }
+  const Tables t = ix->tables();
+  auto run = [&](auto kern) -> cm_status {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kKThreads, 0);
+    per_sm = std::max(per_sm, 1);
+    const uint64_t need = (nq + kKWarps - 1) / kKWarps;
+    const unsigned grid =
+        (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(need, (uint64_t)sm_count() * per_sm));
+    kern<<<grid, kKThreads, 0, st>>>(t, q, nq, k, perm, idx, d2);
+    CM_CUDA_TRY(cudaGetLastError());
+    return CM_OK;
+  };
+  switch (ix->opts.flavor) {
+    case CM_DENSE: return run(knn_warp_kernel<CM_DENSE>);
+    case CM_SPARSE: return run(knn_warp_kernel<CM_SPARSE>);
+    default: return run(knn_warp_kernel<CM_MIXED>);
+  }
+}
+
+}  // namespace cmg

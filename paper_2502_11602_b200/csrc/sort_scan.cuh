@@ -1,0 +1,269 @@
+// In-house device primitives: exclusive scan and a stable LSD radix sort of
+// (key, u32 value) pairs. The sort replaces the reference's
+// std::stable_sort by cell key (map.cpp:51-54) and its counting sort
+// (map.cpp:67-81): LSD radix sort is stable, and the values start as iota,
+// so the permutation equals the reference's stable_sort permutation.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace cmg {
+
+// ------------------------------------------------------------------ scan --
+
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+template <typename T>
+__device__ __forceinline__ T warp_incl_scan(T v) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const T u = __shfl_up_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) >= o) v += u;
+  }
+  return v;
+}
+
+// Block-wide exclusive scan of one value per thread; returns the block total.
+template <typename T>
+__device__ __forceinline__ T block_excl_scan(T v, T* smem_warp /*[32]*/, T* total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const T inc = warp_incl_scan(v);
+  if (lane == 31) smem_warp[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    T w = lane < nw ? smem_warp[lane] : T(0);
+    const T wi = warp_incl_scan(w);
+    smem_warp[lane] = wi - w;
+    if (lane == 31) smem_warp[32] = wi;
+  }
+  __syncthreads();
+  const T out = smem_warp[wid] + inc - v;
+  *total = smem_warp[32];
+  __syncthreads();
+  return out;
+}
+
+template <typename TI, typename TO>
+__global__ void scan_reduce_kernel(const TI* __restrict__ in, uint64_t n, TO* __restrict__ part) {
+  __shared__ TO sw[33];
+  const uint64_t base = (uint64_t)blockIdx.x * kScanTile;
+  TO s = 0;
+#pragma unroll
+  for (int it = 0; it < kScanItems; ++it) {
+    const uint64_t i = base + (uint64_t)it * kScanThreads + threadIdx.x;
+    if (i < n) s += (TO)in[i];
+  }
+  TO tot;
+  block_excl_scan<TO>(s, sw, &tot);
+  if (threadIdx.x == 0) part[blockIdx.x] = tot;
+}
+
+// Single block: exclusive scan of the per-tile partial sums, in place.
+template <typename TO>
+__global__ void scan_partials_kernel(TO* part, uint64_t nb) {
+  __shared__ TO sw[33];
+  TO carry = 0;
+  for (uint64_t base = 0; base < nb; base += blockDim.x) {
+    const uint64_t i = base + threadIdx.x;
+    const TO v = i < nb ? part[i] : TO(0);
+    TO tot;
+    const TO ex = block_excl_scan<TO>(v, sw, &tot);
+    if (i < nb) part[i] = carry + ex;
+    carry += tot;
+  }
+}
+
+// out[i] = sum(in[0..i)) ; if total != nullptr, out[n] = total as well when
+// write_total is set.
+template <typename TI, typename TO>
+__global__ void scan_apply_kernel(const TI* __restrict__ in, uint64_t n, const TO* __restrict__ part,
+                                  TO* __restrict__ out, int write_total) {
+  __shared__ TO sw[33];
+  __shared__ TO tile_vals[kScanTile];
+  const uint64_t base = (uint64_t)blockIdx.x * kScanTile;
+  // blocked arrangement in smem: thread t owns items t*ITEMS .. +ITEMS
+  for (int it = 0; it < kScanItems; ++it) {
+    const uint64_t i = base + (uint64_t)it * kScanThreads + threadIdx.x;
+    tile_vals[it * kScanThreads + threadIdx.x] = i < n ? (TO)in[i] : TO(0);
+  }
+  __syncthreads();
+  TO loc[kScanItems];
+  TO s = 0;
+#pragma unroll
+  for (int it = 0; it < kScanItems; ++it) {
+    loc[it] = tile_vals[threadIdx.x * kScanItems + it];
+    s += loc[it];
+  }
+  TO tot;
+  TO ex = block_excl_scan<TO>(s, sw, &tot) + part[blockIdx.x];
+#pragma unroll
+  for (int it = 0; it < kScanItems; ++it) {
+    tile_vals[threadIdx.x * kScanItems + it] = ex;
+    ex += loc[it];
+  }
+  __syncthreads();
+  for (int it = 0; it < kScanItems; ++it) {
+    const uint64_t i = base + (uint64_t)it * kScanThreads + threadIdx.x;
+    if (i < n) out[i] = tile_vals[it * kScanThreads + threadIdx.x];
+  }
+  if (write_total && blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
+    out[n] = part[blockIdx.x] + tot;
+  }
+}
+
+// Exclusive scan of n inputs into out[0..n) (+ out[n] = total when
+// write_total). `part` scratch needs ceil(n / kScanTile) entries.
+template <typename TI, typename TO>
+inline void exclusive_scan(const TI* in, uint64_t n, TO* out, TO* part, int write_total,
+                           cudaStream_t st) {
+  const uint64_t nb = (n + kScanTile - 1) / kScanTile;
+  if (nb == 0) {
+    if (write_total) cudaMemsetAsync(out, 0, sizeof(TO), st);
+    return;
+  }
+  scan_reduce_kernel<TI, TO><<<(unsigned)nb, kScanThreads, 0, st>>>(in, n, part);
+  scan_partials_kernel<TO><<<1, 1024, 0, st>>>(part, nb);
+  scan_apply_kernel<TI, TO><<<(unsigned)nb, kScanThreads, 0, st>>>(in, n, part, out, write_total);
+}
+
+inline uint64_t scan_part_elems(uint64_t n) { return (n + kScanTile - 1) / kScanTile + 1; }
+
+// ------------------------------------------------------------ radix sort --
+
+constexpr int kSortThreads = 256;  // 8 warps
+constexpr int kSortWarps = kSortThreads / 32;
+constexpr int kSortItems = 16;  // per lane; a warp owns 512 consecutive keys
+constexpr int kSortTile = kSortThreads * kSortItems;
+constexpr int kRadixBits = 8;
+constexpr int kRadix = 1 << kRadixBits;
+
+template <typename K>
+__global__ void __launch_bounds__(kSortThreads) radix_upsweep(const K* __restrict__ keys,
+                                                              uint64_t n, int shift,
+                                                              uint32_t* __restrict__ hist,
+                                                              uint32_t nblocks) {
+  __shared__ uint32_t h[kRadix];
+  for (int d = threadIdx.x; d < kRadix; d += blockDim.x) h[d] = 0;
+  __syncthreads();
+  const uint64_t base = (uint64_t)blockIdx.x * kSortTile;
+  for (int it = 0; it < kSortItems; ++it) {
+    const uint64_t i = base + (uint64_t)it * kSortThreads + threadIdx.x;
+    if (i < n) atomicAdd(&h[(uint32_t)(keys[i] >> shift) & (kRadix - 1)], 1u);
+  }
+  __syncthreads();
+  for (int d = threadIdx.x; d < kRadix; d += blockDim.x)
+    hist[(uint64_t)d * nblocks + blockIdx.x] = h[d];
+}
+
+// Stable scatter. Warp w of block b owns keys [b*TILE + w*512, +512);
+// item `it` of lane l is key (it*32 + l) of that run, so processing items in
+// order with lanes in order visits keys in input order. Ranks inside a warp
+// come from __match_any_sync peer groups.
+template <typename K>
+__global__ void __launch_bounds__(kSortThreads) radix_downsweep(
+    const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, K* __restrict__ keys_out,
+    uint32_t* __restrict__ vals_out, uint64_t n, int shift,
+    const uint32_t* __restrict__ offs /* scanned hist [d][b] */, uint32_t nblocks) {
+  __shared__ uint32_t wcount[kSortWarps][kRadix];
+  __shared__ uint32_t dbase[kRadix];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int d = lane; d < kRadix; d += 32) wcount[w][d] = 0;
+  __syncwarp();
+  const uint64_t wbase = (uint64_t)blockIdx.x * kSortTile + (uint64_t)w * (32 * kSortItems);
+  K kv[kSortItems];
+  uint32_t vv[kSortItems];
+  uint32_t rank[kSortItems];
+  const uint32_t lt = lanemask_lt();
+#pragma unroll
+  for (int it = 0; it < kSortItems; ++it) {
+    const uint64_t i = wbase + (uint64_t)it * 32 + lane;
+    const bool valid = i < n;
+    kv[it] = valid ? keys_in[i] : K(0);
+    vv[it] = valid ? vals_in[i] : 0u;
+    const uint32_t d = valid ? ((uint32_t)(kv[it] >> shift) & (kRadix - 1)) : kRadix;  // kRadix = invalid
+    const uint32_t act = __ballot_sync(0xffffffffu, valid);
+    uint32_t peers = __match_any_sync(0xffffffffu, d);
+    peers &= act;
+    uint32_t r = 0;
+    if (valid) {
+      r = wcount[w][d] + __popc(peers & lt);
+    }
+    __syncwarp();
+    if (valid && (peers & lt) == 0) wcount[w][d] += __popc(peers);
+    __syncwarp();
+    rank[it] = r;
+  }
+  __syncthreads();
+  // per digit: global offset of this block + exclusive prefix over warps
+  for (int d = threadIdx.x; d < kRadix; d += blockDim.x) {
+    uint32_t s = offs[(uint64_t)d * nblocks + blockIdx.x];
+    for (int ww = 0; ww < kSortWarps; ++ww) {
+      const uint32_t c = wcount[ww][d];
+      wcount[ww][d] = s;
+      s += c;
+    }
+    dbase[d] = 0;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int it = 0; it < kSortItems; ++it) {
+    const uint64_t i = wbase + (uint64_t)it * 32 + lane;
+    if (i < n) {
+      const uint32_t d = (uint32_t)(kv[it] >> shift) & (kRadix - 1);
+      const uint32_t pos = wcount[w][d] + rank[it];
+      keys_out[pos] = kv[it];
+      vals_out[pos] = vv[it];
+    }
+  }
+}
+
+// Scratch (bytes) for radix_sort_pairs over n keys.
+template <typename K>
+inline size_t radix_scratch_bytes(uint64_t n) {
+  const uint64_t nb = (n + kSortTile - 1) / kSortTile;
+  const uint64_t h = nb * kRadix;
+  return (size_t)(n * (sizeof(K) + 4)) + (size_t)(h * 4) + (size_t)(scan_part_elems(h) * 4) + 256;
+}
+
+// Sorts (keys, vals) by the low `bits` bits of the keys, stably. n < 2^32.
+// Result ends in (keys, vals) (the function ping-pongs through scratch).
+// Returns the number of passes.
+template <typename K>
+inline int radix_sort_pairs(K* keys, uint32_t* vals, uint64_t n, int bits, void* scratch,
+                            cudaStream_t st) {
+  if (n <= 1 || bits <= 0) return 0;
+  const uint32_t nb = (uint32_t)((n + kSortTile - 1) / kSortTile);
+  const uint64_t h = (uint64_t)nb * kRadix;
+  char* p = static_cast<char*>(scratch);
+  K* k2 = reinterpret_cast<K*>(p);
+  p += n * sizeof(K);
+  uint32_t* v2 = reinterpret_cast<uint32_t*>(p);
+  p += n * 4;
+  uint32_t* hist = reinterpret_cast<uint32_t*>(p);
+  p += h * 4;
+  uint32_t* part = reinterpret_cast<uint32_t*>(p);
+  K* ka = keys;
+  uint32_t* va = vals;
+  K* kb = k2;
+  uint32_t* vb = v2;
+  int passes = 0;
+  for (int shift = 0; shift < bits; shift += kRadixBits, ++passes) {
+    radix_upsweep<K><<<nb, kSortThreads, 0, st>>>(ka, n, shift, hist, nb);
+    exclusive_scan<uint32_t, uint32_t>(hist, h, hist, part, 0, st);
+    radix_downsweep<K><<<nb, kSortThreads, 0, st>>>(ka, va, kb, vb, n, shift, hist, nb);
+    K* tk = ka; ka = kb; kb = tk;
+    uint32_t* tv = va; va = vb; vb = tv;
+  }
+  if (ka != keys) {
+    cudaMemcpyAsync(keys, ka, n * sizeof(K), cudaMemcpyDeviceToDevice, st);
+    cudaMemcpyAsync(vals, va, n * 4, cudaMemcpyDeviceToDevice, st);
+  }
+  return passes;
+}
+
+}  // namespace cmg

@@ -1,0 +1,104 @@
+"""GPU parity: the CUDA path through the C ABI against the CPU oracle on the
+same seeded inputs (bit-exact for sets, indices and fp64 distances)."""
+import numpy as np
+import pytest
+
+from paper_2502_11602_b200 import cheesemap as cm
+from paper_2502_11602_b200 import synth
+from oracle.oracle import CpuIndex
+
+pytestmark = pytest.mark.gpu
+
+FLAVORS = [cm.Flavor.Dense, cm.Flavor.Sparse, cm.Flavor.Mixed]
+
+
+@pytest.fixture(scope="module")
+def cfg0():
+    cloud = synth.config_cloud(0)
+    return cloud, synth.config_queries(0, cloud)
+
+
+@pytest.fixture(scope="module")
+def cfg0_oracle(cfg0):
+    return CpuIndex(cfg0[0], flavor=0)
+
+
+@pytest.mark.parametrize("flavor", FLAVORS)
+def test_build_parity_cfg0(cfg0, flavor):
+    cloud, _ = cfg0
+    m = cm.Cheesemap.build(cloud, cm.BuildOptions(flavor=flavor))
+    ref = CpuIndex(cloud, flavor=int(flavor))
+    g, og = m.grid(), ref.grid()
+    assert [g["nx"], g["ny"], g["nz"]] == og["dims"].tolist()
+    assert np.array_equal(np.array(g["origin"]), og["origin"])
+    keys, hs = m.export_voxels()
+    okeys, ohs = ref.export()
+    assert np.array_equal(keys, okeys)
+    assert np.array_equal(hs.astype(np.uint64), ohs)
+    occ = m.occupancy_stats()
+    assert occ["non_empty"] == ref.non_empty()
+    dense, ne = ref.slice_flags()
+    assert np.array_equal(occ["slice_dense"], dense)
+    assert np.array_equal(occ["slice_non_empty"], ne)
+
+
+@pytest.mark.parametrize("flavor", FLAVORS)
+@pytest.mark.parametrize("kernel", [cm.SPHERE, cm.CUBE])
+def test_radius_csr_cfg0(cfg0, cfg0_oracle, flavor, kernel):
+    cloud, q = cfg0
+    m = cm.Cheesemap.build(cloud, cm.BuildOptions(flavor=flavor))
+    row, cols = cm.radius_search_batch(m, q, 1.0, kernel)
+    orow, ocols = cfg0_oracle.radius_csr(q, kernel, 1.0)
+    assert np.array_equal(row, orow)
+    assert np.array_equal(cols, ocols)
+
+
+@pytest.mark.parametrize("flavor", FLAVORS)
+@pytest.mark.parametrize("r", [0.05, 0.5, 2.5, 5.0])
+def test_radius_digest_cfg0(cfg0, cfg0_oracle, flavor, r):
+    cloud, q = cfg0
+    q = q[::4]
+    m = cm.Cheesemap.build(cloud, cm.BuildOptions(flavor=flavor))
+    for kernel in (cm.SPHERE, cm.CUBE):
+        cnt, dig = cm.radius_digest_batch(m, q, r, kernel)
+        ocnt, odig = cfg0_oracle.radius(q, kernel, r)
+        assert np.array_equal(cnt, ocnt)
+        assert np.array_equal(dig, odig)
+        tested = np.zeros(q.shape[0], dtype=np.uint64)
+        cm.radius_count(m, q, r, kernel, points_tested=tested)
+        _, _, opt, _ = cfg0_oracle.radius(q, kernel, r, stats=True)
+        assert np.array_equal(tested, opt)
+
+
+@pytest.mark.parametrize("flavor", FLAVORS)
+@pytest.mark.parametrize("k", [1, 8, 16, 64])
+def test_knn_cfg0(cfg0, cfg0_oracle, flavor, k):
+    cloud, q = cfg0
+    q = q[:20000]
+    m = cm.Cheesemap.build(cloud, cm.BuildOptions(flavor=flavor))
+    idx, d2 = cm.knn_batch(m, q, k)
+    oidx, od2 = cfg0_oracle.knn(q, k)
+    assert np.array_equal(idx, oidx)
+    assert np.array_equal(d2, od2)
+
+
+def test_big_rows_sorted(cfg0, cfg0_oracle):
+    """r = 8 m gives rows above the per-warp buffer (block-sort path)."""
+    cloud, q = cfg0
+    q = q[:3000]
+    m = cm.Cheesemap.build(cloud, cm.BuildOptions(flavor=cm.Flavor.Sparse))
+    row, cols = cm.radius_search_batch(m, q, 8.0, cm.SPHERE)
+    orow, ocols = cfg0_oracle.radius_csr(q, 0, 8.0)
+    assert (np.diff(row.astype(np.int64)) > 2048).any()
+    assert np.array_equal(row, orow)
+    assert np.array_equal(cols, ocols)
+
+
+def test_corruption_detected(cfg0, cfg0_oracle):
+    cloud, q = cfg0
+    for flavor in FLAVORS:
+        m = cm.Cheesemap.build(cloud, cm.BuildOptions(flavor=flavor))
+        m.corrupt_for_testing()
+        cnt, dig = cm.radius_digest_batch(m, cloud, 1.0)
+        ocnt, odig = cfg0_oracle.radius(cloud, 0, 1.0)
+        assert not (np.array_equal(cnt, ocnt) and np.array_equal(dig, odig))
