@@ -1,0 +1,417 @@
+#!/usr/bin/env python
+"""Headline benchmark: radius-search queries/sec on the BASELINE config-1
+cloud (20M-point ALS tile + 200 buildings, cell 1 m), sphere r = 1 m, every
+point a query, full sorted CSR neighbour lists; plus index build ms.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+One JSON line on rank 0:
+  value  : queries/sec over all ranks, inputs resident in HBM, device time
+           (CUDA events on the launching stream, max over ranks)
+  e2e    : the same metric through the C ABI with HOST buffers: pinned
+           query coordinates in, full CSR (row_ptr + cols) back to pinned
+           host memory, both copies inside the timed region
+  roofline: dominant kernel's algorithmic bytes (24 B x the reference's
+           points_tested) / its event-timed duration, against
+           MEASURED_PEAKS.json hbm_gbs
+  cpu_baseline: the reference library compiled from its own sources
+           (oracle/_ref) on this host's cores, on a bounded query sample
+
+Multi-GPU (torchrun): replicated index, queries sharded in contiguous blocks
+(strong scaling; no data-path collective). --impl reference: rank 0 times the
+reference's own CPU implementation, other ranks exit.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FLAVORS = {"dense": 0, "sparse": 1, "mixed": 2}
+KERNELS = {"sphere": 0, "cube": 1}
+FALLBACK_HBM_GBS = 6650.0
+BAD_REASONS = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown")
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--scale", type=float, default=1.0, help="shrink the cloud (tests only)")
+    ap.add_argument("--radius", type=float, default=1.0)
+    ap.add_argument("--kernel", default="sphere", choices=list(KERNELS))
+    ap.add_argument("--flavor", default="mixed", choices=list(FLAVORS))
+    ap.add_argument("--cpu-sample", type=int, default=1_000_000,
+                    help="queries per CPU-baseline / reference step")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def workload_name(a):
+    return (f"cfg{a.config} ALS {int(20_000_000 * a.scale)} pts +buildings, cell 1 m, "
+            f"{a.kernel} r={a.radius:g} m, every point a query, sorted CSR")
+
+
+def read_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        self.proc.wait()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as f:
+            for line in f:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sm.append(float(parts[1]))
+                    smax.append(float(parts[2]))
+                except ValueError:
+                    continue
+                for nm, v in zip(names, parts[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+        os.unlink(self.path)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_reference_lib():
+    """The reference compiled from its own sources if present, else the port."""
+    from oracle.oracle import lib
+    try:
+        return lib("reference"), "reference"
+    except FileNotFoundError:
+        return lib("oracle"), "port"
+
+
+def run_cpu(cloud, a, steps, warmup, threads=0):
+    """Times the CPU implementation on bounded query samples. Returns a dict."""
+    from oracle.oracle import CpuIndex
+    L, kind = cpu_reference_lib()
+    t0 = time.perf_counter()
+    idx = CpuIndex(cloud, flavor=FLAVORS[a.flavor], which=kind)
+    build_s = time.perf_counter() - t0
+    nthreads = threads or os.cpu_count() or 1
+    stride = max(1, cloud.shape[0] // a.cpu_sample)
+    rates = []
+    for s in range(warmup + steps):
+        q = np.ascontiguousarray(cloud[(s % stride)::stride][: a.cpu_sample])
+        t0 = time.perf_counter()
+        idx.radius(q, KERNELS[a.kernel], a.radius, threads=nthreads)
+        dt = time.perf_counter() - t0
+        if s >= warmup:
+            rates.append(q.shape[0] / dt)
+    return dict(value=statistics.median(rates), kind=kind, cores=nthreads, build_ms=build_s * 1e3,
+                sample=f"{min(a.cpu_sample, cloud.shape[0])} of the {cloud.shape[0]} queries "
+                       f"(every {stride}th point), {a.flavor} map, {nthreads} threads, "
+                       f"median of {steps} steps; build single-threaded")
+
+
+def reference_arm(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2502_11602_b200 import synth
+    cloud = synth.config_cloud(a.config, a.scale)
+    r = run_cpu(cloud, a, a.steps, a.warmup)
+    line = {
+        "impl": "reference", "metric": "radius-search queries/sec (20M-pt ALS, r=1 m)",
+        "value": r["value"], "unit": "queries/s", "n_gpus": a.gpus, "steps": a.steps,
+        "warmup": a.warmup, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded config-1 generator)",
+        "config": {"workload": workload_name(a), "flavor": a.flavor, "n_points": int(cloud.shape[0])},
+        "build_ms": {a.flavor: r["build_ms"]},
+        "cpu_baseline": {"value": r["value"], "unit": "queries/s", "cores": r["cores"],
+                         "kind": r["kind"], "sample": r["sample"]},
+        "e2e": {"value": r["value"], "unit": "queries/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        reference_arm(a)
+        return
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2502_11602_b200 import _native, synth
+    from paper_2502_11602_b200 import cheesemap as cm
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    def allmax(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def allsum(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    L = _native.lib()
+    t0 = time.perf_counter()
+    cloud = synth.config_cloud(a.config, a.scale)
+    log(f"[rank {rank}] generated {cloud.shape[0]} points in {time.perf_counter() - t0:.1f}s")
+    d_cloud = torch.from_numpy(cloud).to(dev)
+    stream = torch.cuda.current_stream(dev)
+    sptr = ctypes.c_void_p(stream.cuda_stream)
+    kernel = KERNELS[a.kernel]
+
+    # ---- index build (device-resident points -> ready index), per flavour
+    build_ms = {}
+    build_detail = {}
+    index = None
+    for name in ("sparse", "mixed", "dense"):
+        best = None
+        for _ in range(3):
+            m = cm.Cheesemap.build(d_cloud, cm.BuildOptions(flavor=cm.Flavor(FLAVORS[name])),
+                                   device=local, stream=stream)
+            t = m.build_timing()
+            if best is None or t["total_ms"] < best["total_ms"]:
+                best = t
+            if name == a.flavor:
+                index = m
+            else:
+                del m
+        build_ms[name] = allmax(best["total_ms"])
+        build_detail[name] = {k: round(v, 3) for k, v in best.items()}
+    log(f"[rank {rank}] build ms {build_ms}")
+
+    # ---- this rank's queries: a contiguous block of the cloud
+    nq_total = cloud.shape[0]
+    lo = nq_total * rank // world
+    hi = nq_total * (rank + 1) // world
+    q_dev = d_cloud[lo:hi]
+    nq = hi - lo
+
+    # algorithmic bytes: 24 B x the reference's points_tested for these queries
+    tested = torch.zeros(nq, dtype=torch.int64, device=dev)
+    counts = torch.zeros(nq, dtype=torch.int32, device=dev)
+    cm._check(L.cm_radius_count(index.handle, ctypes.c_void_p(q_dev.data_ptr()), nq, kernel,
+                                a.radius, ctypes.c_void_p(counts.data_ptr()),
+                                ctypes.c_void_p(tested.data_ptr()), sptr))
+    torch.cuda.synchronize(dev)
+    sum_tested = int(tested.sum().item())
+    nnz_rank = int(counts.to(torch.int64).sum().item())
+    alg_bytes = 24 * sum_tested
+    del tested, counts
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def step_device():
+        csr = ctypes.c_void_p()
+        cm._check(L.cm_radius_search(index.handle, ctypes.c_void_p(q_dev.data_ptr()), nq, kernel,
+                                     a.radius, sptr, ctypes.byref(csr)))
+        return csr
+
+    for _ in range(a.warmup):
+        csr = step_device()
+        torch.cuda.synchronize(dev)
+        L.cm_csr_free(csr)
+
+    # ---- timed region (device-resident inputs)
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    torch.cuda.synchronize(dev)
+    launches0 = _native.launch_count()
+    step_ms, kern = [], []
+    for _ in range(a.steps):
+        flush.zero_()  # L2 flush (256 MB write) outside the timed events
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        csr = step_device()
+        e1.record(stream)
+        e1.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+        kern.append(_native.last_query_timing())
+        L.cm_csr_free(csr)
+    torch.cuda.synchronize(dev)
+    launches = (_native.launch_count() - launches0) // a.steps
+    barrier()
+    clk = clocks.stop()
+    ms_rank = sum(step_ms) / len(step_ms)
+    ms = allmax(ms_rank)
+    value = nq_total / (ms * 1e-3)
+
+    def mean_of(key):
+        return sum(k[key] for k in kern) / len(kern)
+
+    phase = {k: round(mean_of(k), 4) for k in ("order_ms", "count_ms", "scan_ms", "fill_ms",
+                                                "rowsort_ms")}
+    dom = "fill_ms" if phase["fill_ms"] >= phase["count_ms"] else "count_ms"
+    dom_ms = phase[dom]
+    peak, peak_src = read_peak()
+    achieved = alg_bytes / (dom_ms * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as f:
+                tj = json.load(f)
+            kname = "fill" if dom == "fill_ms" else "count"
+            traffic = tj.get(f"{a.flavor}/{kname}/r{a.radius:g}")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "kernel": "radius_warp_kernel<" + a.flavor + ", " +
+                          ("FILL" if dom == "fill_ms" else "COUNT") + ">",
+                "kernel_ms": dom_ms, "alg_bytes_per_launch": alg_bytes,
+                "peak_source": peak_src,
+                "basis": "24 B x sum of the reference's points_tested (search.hpp:116) "
+                         "over this launch's queries"}
+
+    # ---- end to end through the C ABI with host buffers
+    e2e = None
+    if not a.no_e2e:
+        q_host = torch.from_numpy(np.ascontiguousarray(cloud[lo:hi])).pin_memory()
+        row_host = torch.empty(nq + 1, dtype=torch.int64).pin_memory()
+        cols_host = torch.empty(max(nnz_rank, 1), dtype=torch.int32).pin_memory()
+
+        def step_e2e():
+            csr = ctypes.c_void_p()
+            cm._check(L.cm_radius_search(index.handle, ctypes.c_void_p(q_host.data_ptr()), nq,
+                                         kernel, a.radius, sptr, ctypes.byref(csr)))
+            cm._check(L.cm_csr_download(csr, ctypes.c_void_p(row_host.data_ptr()),
+                                        ctypes.c_void_p(cols_host.data_ptr()), sptr))
+            L.cm_csr_free(csr)
+
+        step_e2e()
+        barrier()
+        torch.cuda.synchronize(dev)
+        e2e_ms = []
+        for _ in range(a.steps):
+            flush.zero_()
+            torch.cuda.synchronize(dev)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step_e2e()
+            e1.record(stream)
+            e1.synchronize()
+            e2e_ms.append(e0.elapsed_time(e1))
+        barrier()
+        e2e_t = allmax(sum(e2e_ms) / len(e2e_ms))
+        e2e = {"value": nq_total / (e2e_t * 1e-3), "unit": "queries/s",
+               "h2d_bytes_per_step": int(allsum(nq * 24)),
+               "d2h_bytes_per_step": int(allsum((nq + 1) * 8 + nnz_rank * 4)),
+               "ms_per_step": round(e2e_t, 3)}
+
+    # ---- CPU baseline (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        try:
+            r = run_cpu(cloud, a, steps=1, warmup=0)
+            cpu = {"value": r["value"], "unit": "queries/s", "cores": r["cores"],
+                   "kind": r["kind"], "sample": r["sample"],
+                   "build_ms": {a.flavor: round(r["build_ms"], 1)}}
+        except Exception as ex:  # noqa: BLE001
+            cpu = {"value": None, "unit": "queries/s", "cores": None, "kind": None,
+                   "sample": f"unavailable: {ex}"}
+
+    nnz_total = int(allsum(nnz_rank))
+    if rank == 0:
+        line = {
+            "metric": "radius-search queries/sec (20M-pt ALS, r=1 m)",
+            "value": round(value, 1), "unit": "queries/s", "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded config-1 generator, DESIGN.md)",
+            "config": {"workload": workload_name(a), "flavor": a.flavor,
+                       "n_points": int(cloud.shape[0]), "n_queries": nq_total,
+                       "neighbours": nnz_total, "radius_m": a.radius, "kernel": a.kernel,
+                       "l2": "flushed (256 MB write) before every timed step",
+                       "parallelism": f"replicated index, queries sharded x{world}"},
+            "build_ms": {k: round(v, 3) for k, v in build_ms.items()},
+            "build_detail": build_detail,
+            "phases_ms": phase,
+            "roofline": roofline,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "gpu_launches": int(launches),
+            "clocks": clk,
+        }
+        if any(rsn in BAD_REASONS for rsn in clk.get("reasons", [])):
+            line["clocks_warning"] = "throttle reason active during the timed region"
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -105,6 +105,18 @@ typedef struct {
   uint32_t sort_passes;
 } cm_build_timing;
 
+/* Device timing of the last radius call on this host thread (CUDA events on
+ * the call's stream), milliseconds. */
+typedef struct {
+  double order_ms;    /* query cell keys + radix sort (spatial order) */
+  double count_ms;    /* K5 count kernel */
+  double scan_ms;     /* K6 row_ptr scan */
+  double fill_ms;     /* K7 fill + in-warp row sort */
+  double rowsort_ms;  /* block sort of rows longer than the warp buffer */
+  double total_ms;
+  uint64_t nq, nnz;
+} cm_query_timing;
+
 typedef struct cm_index cm_index;
 typedef struct cm_csr cm_csr;
 
@@ -162,6 +174,11 @@ cm_status cm_knn(const cm_index* index, const double* q, uint64_t nq, uint32_t k
 /* Test hook (map.cpp:194-223): drops one stored handle from the first
  * non-empty voxel so verification harnesses can prove they detect it. */
 cm_status cm_corrupt_for_testing(cm_index* index);
+
+/* Timing of the last cm_radius_search on this thread (waits for it). */
+cm_status cm_get_last_query_timing(cm_query_timing* out);
+/* Kernels launched by this library since load (all threads). */
+uint64_t cm_launch_count(void);
 
 const char* cm_last_error(void);
 const char* cm_status_name(cm_status s);

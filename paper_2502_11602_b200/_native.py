@@ -17,6 +17,7 @@ EXPORTS = [
     "cm_get_build_timing", "cm_export_voxels", "cm_size", "cm_radius_count", "cm_radius_fill",
     "cm_radius_search", "cm_csr_info", "cm_csr_download", "cm_csr_free", "cm_radius_digest",
     "cm_knn", "cm_corrupt_for_testing", "cm_last_error", "cm_status_name",
+    "cm_get_last_query_timing", "cm_launch_count",
 ]
 
 
@@ -45,6 +46,13 @@ class BuildTimingC(ctypes.Structure):
                 ("bbox_ms", ctypes.c_double), ("keys_ms", ctypes.c_double),
                 ("sort_ms", ctypes.c_double), ("gather_ms", ctypes.c_double),
                 ("tables_ms", ctypes.c_double), ("sort_passes", ctypes.c_uint32)]
+
+
+class QueryTimingC(ctypes.Structure):
+    _fields_ = [("order_ms", ctypes.c_double), ("count_ms", ctypes.c_double),
+                ("scan_ms", ctypes.c_double), ("fill_ms", ctypes.c_double),
+                ("rowsort_ms", ctypes.c_double), ("total_ms", ctypes.c_double),
+                ("nq", ctypes.c_uint64), ("nnz", ctypes.c_uint64)]
 
 
 _LIB = None
@@ -81,6 +89,8 @@ def lib():
         "cm_corrupt_for_testing": ([p], i32),
         "cm_last_error": ([], ctypes.c_char_p),
         "cm_status_name": ([i32], ctypes.c_char_p),
+        "cm_get_last_query_timing": ([ctypes.POINTER(QueryTimingC)], i32),
+        "cm_launch_count": ([], u64),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -91,3 +101,15 @@ def lib():
 
 def last_error():
     return lib().cm_last_error().decode(errors="replace")
+
+
+def last_query_timing():
+    t = QueryTimingC()
+    rc = lib().cm_get_last_query_timing(ctypes.byref(t))
+    if rc != 0:
+        raise RuntimeError(last_error())
+    return {k: getattr(t, k) for k, _ in t._fields_}
+
+
+def launch_count():
+    return int(lib().cm_launch_count())

@@ -1,4 +1,5 @@
 // C ABI (include/cmgpu.h): argument checks, host/device staging, ownership.
+#include <atomic>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -16,6 +17,9 @@ bool g_pool_configured[64] = {};
 }  // namespace
 
 void set_error(const std::string& msg) { g_last_error = msg; }
+
+static std::atomic<uint64_t> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 int sm_count() {
   static int cached[64] = {};
@@ -172,6 +176,8 @@ void cm_default_options(cm_build_options* o) {
 }
 
 const char* cm_last_error(void) { return g_last_error.c_str(); }
+
+uint64_t cm_launch_count(void) { return g_launches.load(); }
 
 const char* cm_status_name(cm_status s) {
   switch (s) {
@@ -342,7 +348,7 @@ cm_status cm_export_voxels(const cm_index* ix, uint64_t* keys, uint32_t* handles
   CM_TRY(k.init(keys, ix->n, st));
   CM_TRY(h.init(handles, ix->n, st));
   apik::export_kernel<<<(unsigned)std::min<uint64_t>((ix->n + 255) / 256, 4096), 256, 0, st>>>(
-      ix->rec, ix->n, ix->g, k.dev, h.dev);
+      ix->rec, ix->n, ix->g, k.dev, h.dev); ::cmg::note_launch();
   CM_CUDA_TRY(cudaGetLastError());
   CM_TRY(k.finish());
   CM_TRY(h.finish());
@@ -355,7 +361,7 @@ cm_status cm_corrupt_for_testing(cm_index* ix) {
   DeviceGuard dg(ix->device);
   uint64_t first = 0;
   CM_CUDA_TRY(cudaMemcpy(&first, ix->ukey, 8, cudaMemcpyDeviceToHost));
-  apik::corrupt_kernel<<<64, 256, 0, 0>>>(ix->ustart, ix->dense_off, first, ix->vhash, ix->vmask);
+  apik::corrupt_kernel<<<64, 256, 0, 0>>>(ix->ustart, ix->dense_off, first, ix->vhash, ix->vmask); ::cmg::note_launch();
   CM_CUDA_TRY(cudaGetLastError());
   CM_CUDA_TRY(cudaDeviceSynchronize());
   return CM_OK;
@@ -417,6 +423,48 @@ cm_status cm_radius_fill(const cm_index* ix, const double* q, uint64_t nq, int k
   return sync_if(c.host(), st);
 }
 
+}  // extern "C"
+
+namespace {
+struct QueryEvents {
+  cudaEvent_t e[6];
+  uint64_t nq = 0, nnz = 0;
+  bool valid = false;
+  QueryEvents() {
+    for (auto& x : e) cudaEventCreate(&x);
+  }
+};
+thread_local QueryEvents* g_qev = nullptr;
+QueryEvents& qev() {
+  if (!g_qev) g_qev = new QueryEvents();
+  return *g_qev;
+}
+}  // namespace
+
+extern "C" {
+
+cm_status cm_get_last_query_timing(cm_query_timing* o) {
+  if (!o) return CM_INVALID_ARGUMENT;
+  QueryEvents& ev = qev();
+  if (!ev.valid) {
+    set_error("no radius search has run on this thread");
+    return CM_INVALID_ARGUMENT;
+  }
+  CM_CUDA_TRY(cudaEventSynchronize(ev.e[5]));
+  float ms[5], tot;
+  for (int i = 0; i < 5; ++i) cudaEventElapsedTime(&ms[i], ev.e[i], ev.e[i + 1]);
+  cudaEventElapsedTime(&tot, ev.e[0], ev.e[5]);
+  o->order_ms = ms[0];
+  o->count_ms = ms[1];
+  o->scan_ms = ms[2];
+  o->fill_ms = ms[3];
+  o->rowsort_ms = ms[4];
+  o->total_ms = tot;
+  o->nq = ev.nq;
+  o->nnz = ev.nnz;
+  return CM_OK;
+}
+
 cm_status cm_radius_search(const cm_index* ix, const double* q, uint64_t nq, int kernel, double r,
                            void* stream, cm_csr** out) {
   CM_TRY(check_index(ix));
@@ -431,8 +479,12 @@ cm_status cm_radius_search(const cm_index* ix, const double* q, uint64_t nq, int
   InBuf in;
   CM_TRY(stage_input(q, nq * 24, st, &in));
   const double* qd = static_cast<const double*>(in.dev);
+  QueryEvents& ev = qev();
+  ev.valid = false;
+  cudaEventRecord(ev.e[0], st);
   QueryOrder ord;
   CM_TRY(order_queries(ix, qd, nq, st, &ord));
+  cudaEventRecord(ev.e[1], st);
   cm_csr* csr = new cm_csr();
   csr->nq = nq;
   csr->device = ix->device;
@@ -449,7 +501,9 @@ cm_status cm_radius_search(const cm_index* ix, const double* q, uint64_t nq, int
     return fail(CM_CUDA);
   }
   cm_status s = radius_count_dev(ix, qd, nq, kernel, r, ord.perm, counts, nullptr, st);
+  cudaEventRecord(ev.e[2], st);
   if (s == CM_OK) s = counts_to_row_ptr(counts, nq, csr->row_ptr, st);
+  cudaEventRecord(ev.e[3], st);
   if (s != CM_OK) return fail(s);
   if (cudaMemcpyAsync(&csr->nnz, csr->row_ptr + nq, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
       cudaStreamSynchronize(st) != cudaSuccess) {
@@ -460,8 +514,12 @@ cm_status cm_radius_search(const cm_index* ix, const double* q, uint64_t nq, int
     set_error("device allocation failed (columns)");
     return fail(CM_CUDA);
   }
-  s = radius_fill_dev(ix, qd, nq, kernel, r, ord.perm, csr->row_ptr, csr->cols, st);
+  s = radius_fill_dev(ix, qd, nq, kernel, r, ord.perm, csr->row_ptr, csr->cols, st, ev.e[4]);
+  cudaEventRecord(ev.e[5], st);
   if (s != CM_OK) return fail(s);
+  ev.nq = nq;
+  ev.nnz = csr->nnz;
+  ev.valid = true;
   dev_free(counts, st);
   *out = csr;
   return CM_OK;

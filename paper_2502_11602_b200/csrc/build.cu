@@ -234,7 +234,7 @@ cm_status build_typed(const double* xyz, uint64_t n, cudaStream_t st, cm_index* 
   CM_CUDA_TRY(dev_alloc_t(&keys, n, st));
   CM_CUDA_TRY(dev_alloc_t(&perm, n, st));
   CM_CUDA_TRY(dev_alloc(&scratch, radix_scratch_bytes<K>(n), st));
-  keys_kernel<K><<<grid_for(n), 256, 0, st>>>(xyz, n, g, keys, perm);
+  keys_kernel<K><<<grid_for(n), 256, 0, st>>>(xyz, n, g, keys, perm); ::cmg::note_launch();
   cudaEventRecord(ev.e[2], st);
   ix->key_bits = bit_width(ix->V - 1);
   ix->timing.sort_passes = (uint32_t)radix_sort_pairs<K>(keys, perm, n, ix->key_bits, scratch, st);
@@ -248,7 +248,7 @@ cm_status build_typed(const double* xyz, uint64_t n, cudaStream_t st, cm_index* 
   CM_CUDA_TRY(dev_alloc_t(&flags, n, st));
   CM_CUDA_TRY(dev_alloc_t(&pos, n + 1, st));
   CM_CUDA_TRY(dev_alloc_t(&part, scan_part_elems(n), st));
-  gather_kernel<K><<<grid_for(n), 256, 0, st>>>(xyz, keys, perm, n, g.nz, ix->rec, flags);
+  gather_kernel<K><<<grid_for(n), 256, 0, st>>>(xyz, keys, perm, n, g.nz, ix->rec, flags); ::cmg::note_launch();
   cudaEventRecord(ev.e[4], st);
   exclusive_scan<uint32_t, uint32_t>(flags, n, pos, part, 1, st);
   uint32_t U32 = 0;
@@ -266,7 +266,7 @@ cm_status build_typed(const double* xyz, uint64_t n, cudaStream_t st, cm_index* 
   const uint32_t n32 = (uint32_t)n;
   CM_CUDA_TRY(cudaMemcpyAsync(ix->ustart + U, &n32, 4, cudaMemcpyHostToDevice, st));
   unique_kernel<K><<<grid_for(n), 256, 0, st>>>(keys, flags, pos, n, g.nz, ix->ukey, ix->ustart,
-                                                 ix->uk_k, slice_ne);
+                                                 ix->uk_k, slice_ne); ::cmg::note_launch();
   ix->slice_ne.assign(g.nz, 0);
   CM_CUDA_TRY(cudaMemcpyAsync(ix->slice_ne.data(), slice_ne, g.nz * 8, cudaMemcpyDeviceToHost, st));
   dev_free(keys, st);
@@ -275,7 +275,7 @@ cm_status build_typed(const double* xyz, uint64_t n, cudaStream_t st, cm_index* 
   if (flavor == CM_DENSE) {
     CM_CUDA_TRY(dev_alloc_t(&ix->dense_off, ix->V + 1, st));
     CM_CUDA_TRY(cudaMemsetAsync(ix->dense_off, 0, (ix->V + 1) * 4, st));
-    dense_counts_kernel<<<grid_for(U), 256, 0, st>>>(ix->ukey, ix->ustart, U, ix->dense_off);
+    dense_counts_kernel<<<grid_for(U), 256, 0, st>>>(ix->ukey, ix->ustart, U, ix->dense_off); ::cmg::note_launch();
     uint32_t* vpart = nullptr;
     CM_CUDA_TRY(dev_alloc_t(&vpart, scan_part_elems(ix->V), st));
     exclusive_scan<uint32_t, uint32_t>(ix->dense_off, ix->V, ix->dense_off, vpart, 1, st);
@@ -286,10 +286,10 @@ cm_status build_typed(const double* xyz, uint64_t n, cudaStream_t st, cm_index* 
     CM_CUDA_TRY(dev_alloc_t(&ix->vhash, cap, st));
     CM_CUDA_TRY(cudaMemsetAsync(ix->vhash, 0xff, cap * sizeof(HashSlot), st));
     hash_insert_kernel<<<grid_for(U), 256, 0, st>>>(ix->ukey, ix->ustart, ix->ustart + 1, U,
-                                                    ix->vhash, ix->vmask, 0);
+                                                    ix->vhash, ix->vmask, 0); ::cmg::note_launch();
   } else {
     // mixed: 2D column table over the (i, j) footprint + sparse z lists
-    column_flags_kernel<<<grid_for(U), 256, 0, st>>>(ix->ukey, U, g.nz, flags);
+    column_flags_kernel<<<grid_for(U), 256, 0, st>>>(ix->ukey, U, g.nz, flags); ::cmg::note_launch();
     exclusive_scan<uint32_t, uint32_t>(flags, U, pos, part, 1, st);
     uint32_t C32 = 0;
     CM_CUDA_TRY(cudaMemcpyAsync(&C32, pos + U, 4, cudaMemcpyDeviceToHost, st));
@@ -312,14 +312,14 @@ cm_status build_typed(const double* xyz, uint64_t n, cudaStream_t st, cm_index* 
       CM_CUDA_TRY(dev_alloc_t(&col_id, C, st));
     }
     column_scatter_kernel<<<grid_for(U), 256, 0, st>>>(ix->ukey, flags, pos, U, g.nz, col_id,
-                                                       ix->col_vbeg, ix->col_dense);
+                                                       ix->col_vbeg, ix->col_dense); ::cmg::note_launch();
     if (!dense_fp) {
       const uint64_t cap = next_pow2(std::max<uint64_t>(2 * C, 1024));
       ix->cmask = cap - 1;
       CM_CUDA_TRY(dev_alloc_t(&ix->chash, cap, st));
       CM_CUDA_TRY(cudaMemsetAsync(ix->chash, 0xff, cap * sizeof(HashSlot), st));
       hash_insert_kernel<<<grid_for(C), 256, 0, st>>>(col_id, nullptr, nullptr, C, ix->chash,
-                                                      ix->cmask, 1);
+                                                      ix->cmask, 1); ::cmg::note_launch();
       dev_free(col_id, st);
     }
   }
@@ -360,7 +360,7 @@ cm_status build_index(const double* xyz, uint64_t n, const cm_build_options& o, 
   CM_CUDA_TRY(dev_alloc_t(&bb, 6, st));
   unsigned long long init[6] = {~0ull, ~0ull, ~0ull, 0ull, 0ull, 0ull};
   CM_CUDA_TRY(cudaMemcpyAsync(bb, init, sizeof(init), cudaMemcpyHostToDevice, st));
-  bbox_kernel<<<grid_for(n), 256, 0, st>>>(xyz, n, bb);
+  bbox_kernel<<<grid_for(n), 256, 0, st>>>(xyz, n, bb); ::cmg::note_launch();
   unsigned long long hb[6];
   CM_CUDA_TRY(cudaMemcpyAsync(hb, bb, sizeof(hb), cudaMemcpyDeviceToHost, st));
   cudaEventRecord(ev.e[1], st);

@@ -243,6 +243,8 @@ __device__ __forceinline__ void column_span(const Tables& t, uint64_t i, uint64_
 
 namespace cmg {
 void set_error(const std::string& msg);
+// Counts every kernel this library launches (cm_launch_count).
+void note_launch();
 }
 
 #define CM_CUDA_TRY(expr)                                                         \

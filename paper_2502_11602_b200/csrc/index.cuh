@@ -100,7 +100,7 @@ cm_status radius_count_dev(const cm_index* ix, const double* q_dev, uint64_t nq,
                            uint64_t* tested_dev, cudaStream_t st);
 cm_status radius_fill_dev(const cm_index* ix, const double* q_dev, uint64_t nq, int kernel,
                           double r, const uint32_t* perm, const uint64_t* row_ptr_dev,
-                          uint32_t* cols_dev, cudaStream_t st);
+                          uint32_t* cols_dev, cudaStream_t st, cudaEvent_t after_fill = nullptr);
 cm_status radius_digest_dev(const cm_index* ix, const double* q_dev, uint64_t nq, int kernel,
                             double r, const uint32_t* perm, uint32_t* counts_dev,
                             uint64_t* digest_dev, cudaStream_t st);

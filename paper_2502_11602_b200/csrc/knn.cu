@@ -208,7 +208,7 @@ cm_status knn_dev(const cm_index* ix, const double* q, uint64_t nq, uint32_t k,
     const uint64_t need = (nq + kKWarps - 1) / kKWarps;
     const unsigned grid =
         (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(need, (uint64_t)sm_count() * per_sm));
-    kern<<<grid, kKThreads, 0, st>>>(t, q, nq, k, perm, idx, d2);
+    kern<<<grid, kKThreads, 0, st>>>(t, q, nq, k, perm, idx, d2); ::cmg::note_launch();
     CM_CUDA_TRY(cudaGetLastError());
     return CM_OK;
   };

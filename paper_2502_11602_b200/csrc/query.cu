@@ -225,7 +225,7 @@ cm_status order_typed(const cm_index* ix, const double* q, uint64_t nq, cudaStre
   CM_CUDA_TRY(dev_alloc_t(&keys, nq, st));
   CM_CUDA_TRY(dev_alloc(&scratch, radix_scratch_bytes<K>(nq), st));
   const unsigned grid = (unsigned)std::min<uint64_t>((nq + 255) / 256, (uint64_t)sm_count() * 16);
-  query_keys_kernel<K><<<std::max(1u, grid), 256, 0, st>>>(q, nq, ix->g, keys, perm);
+  query_keys_kernel<K><<<std::max(1u, grid), 256, 0, st>>>(q, nq, ix->g, keys, perm); ::cmg::note_launch();
   radix_sort_pairs<K>(keys, perm, nq, ix->key_bits, scratch, st);
   dev_free(scratch, st);
   dev_free(keys, st);
@@ -249,7 +249,7 @@ cm_status launch_radius(const cm_index* ix, const double* q, uint64_t nq, int ke
     const unsigned grid =
         (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(need, (uint64_t)sm_count() * per_sm));
     kern<<<grid, kQThreads, smem, st>>>(t, q, nq, r, kernel == CM_CUBE, perm, counts, tested,
-                                        digests, row_ptr, cols, big_rows, n_big);
+                                        digests, row_ptr, cols, big_rows, n_big); ::cmg::note_launch();
     CM_CUDA_TRY(cudaGetLastError());
     return CM_OK;
   };
@@ -290,7 +290,7 @@ cm_status radius_digest_dev(const cm_index* ix, const double* q, uint64_t nq, in
 
 cm_status radius_fill_dev(const cm_index* ix, const double* q, uint64_t nq, int kernel, double r,
                           const uint32_t* perm, const uint64_t* row_ptr, uint32_t* cols,
-                          cudaStream_t st) {
+                          cudaStream_t st, cudaEvent_t after_fill) {
   if (nq == 0) return CM_OK;
   uint32_t* big = nullptr;
   uint32_t* nbig = nullptr;
@@ -299,6 +299,7 @@ cm_status radius_fill_dev(const cm_index* ix, const double* q, uint64_t nq, int 
   CM_CUDA_TRY(cudaMemsetAsync(nbig, 0, 4, st));
   cm_status s = launch_radius<MODE_FILL>(ix, q, nq, kernel, r, perm, nullptr, nullptr, nullptr,
                                          row_ptr, cols, big, nbig, st);
+  if (after_fill) cudaEventRecord(after_fill, st);
   if (s == CM_OK) {
     static bool configured = false;
     const int smem = kBigSmemCap * 4;
@@ -306,7 +307,7 @@ cm_status radius_fill_dev(const cm_index* ix, const double* q, uint64_t nq, int 
       cudaFuncSetAttribute(big_row_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       configured = true;
     }
-    big_row_sort_kernel<<<sm_count(), 1024, smem, st>>>(row_ptr, cols, big, nbig);
+    big_row_sort_kernel<<<sm_count(), 1024, smem, st>>>(row_ptr, cols, big, nbig); ::cmg::note_launch();
     if (cudaGetLastError() != cudaSuccess) {
       set_error("big_row_sort_kernel launch failed");
       s = CM_CUDA;

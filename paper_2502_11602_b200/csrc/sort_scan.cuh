@@ -126,9 +126,9 @@ inline void exclusive_scan(const TI* in, uint64_t n, TO* out, TO* part, int writ
     if (write_total) cudaMemsetAsync(out, 0, sizeof(TO), st);
     return;
   }
-  scan_reduce_kernel<TI, TO><<<(unsigned)nb, kScanThreads, 0, st>>>(in, n, part);
-  scan_partials_kernel<TO><<<1, 1024, 0, st>>>(part, nb);
-  scan_apply_kernel<TI, TO><<<(unsigned)nb, kScanThreads, 0, st>>>(in, n, part, out, write_total);
+  scan_reduce_kernel<TI, TO><<<(unsigned)nb, kScanThreads, 0, st>>>(in, n, part); ::cmg::note_launch();
+  scan_partials_kernel<TO><<<1, 1024, 0, st>>>(part, nb); ::cmg::note_launch();
+  scan_apply_kernel<TI, TO><<<(unsigned)nb, kScanThreads, 0, st>>>(in, n, part, out, write_total); ::cmg::note_launch();
 }
 
 inline uint64_t scan_part_elems(uint64_t n) { return (n + kScanTile - 1) / kScanTile + 1; }
@@ -253,9 +253,9 @@ inline int radix_sort_pairs(K* keys, uint32_t* vals, uint64_t n, int bits, void*
   uint32_t* vb = v2;
   int passes = 0;
   for (int shift = 0; shift < bits; shift += kRadixBits, ++passes) {
-    radix_upsweep<K><<<nb, kSortThreads, 0, st>>>(ka, n, shift, hist, nb);
+    radix_upsweep<K><<<nb, kSortThreads, 0, st>>>(ka, n, shift, hist, nb); ::cmg::note_launch();
     exclusive_scan<uint32_t, uint32_t>(hist, h, hist, part, 0, st);
-    radix_downsweep<K><<<nb, kSortThreads, 0, st>>>(ka, va, kb, vb, n, shift, hist, nb);
+    radix_downsweep<K><<<nb, kSortThreads, 0, st>>>(ka, va, kb, vb, n, shift, hist, nb); ::cmg::note_launch();
     K* tk = ka; ka = kb; kb = tk;
     uint32_t* tv = va; va = vb; vb = tv;
   }
