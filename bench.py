@@ -268,6 +268,7 @@ def main():
     nnz_rank = int(counts.to(torch.int64).sum().item())
     alg_bytes = 24 * sum_tested
     del tested, counts
+    tile_stats = _native.query_stats(reset=True)
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
@@ -400,6 +401,7 @@ def main():
             "build_ms": {k: round(v, 3) for k, v in build_ms.items()},
             "build_detail": build_detail,
             "phases_ms": phase,
+            "tile_stats": tile_stats,
             "roofline": roofline,
             "e2e": e2e,
             "cpu_baseline": cpu,

@@ -179,6 +179,9 @@ cm_status cm_corrupt_for_testing(cm_index* index);
 cm_status cm_get_last_query_timing(cm_query_timing* out);
 /* Kernels launched by this library since load (all threads). */
 uint64_t cm_launch_count(void);
+/* Query-tile counters since the last reset: tiles, tiles answered one query
+ * per warp (fallback), staged hull points, in-range candidates. */
+cm_status cm_debug_query_stats(uint64_t* out4, int reset);
 
 const char* cm_last_error(void);
 const char* cm_status_name(cm_status s);

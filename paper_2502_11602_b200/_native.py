@@ -17,7 +17,7 @@ EXPORTS = [
     "cm_get_build_timing", "cm_export_voxels", "cm_size", "cm_radius_count", "cm_radius_fill",
     "cm_radius_search", "cm_csr_info", "cm_csr_download", "cm_csr_free", "cm_radius_digest",
     "cm_knn", "cm_corrupt_for_testing", "cm_last_error", "cm_status_name",
-    "cm_get_last_query_timing", "cm_launch_count",
+    "cm_get_last_query_timing", "cm_launch_count", "cm_debug_query_stats",
 ]
 
 
@@ -91,6 +91,7 @@ def lib():
         "cm_status_name": ([i32], ctypes.c_char_p),
         "cm_get_last_query_timing": ([ctypes.POINTER(QueryTimingC)], i32),
         "cm_launch_count": ([], u64),
+        "cm_debug_query_stats": ([p, i32], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -113,3 +114,11 @@ def last_query_timing():
 
 def launch_count():
     return int(lib().cm_launch_count())
+
+
+def query_stats(reset=True):
+    import numpy as np
+    out = np.zeros(4, dtype=np.uint64)
+    lib().cm_debug_query_stats(out.ctypes.data_as(ctypes.c_void_p), int(reset))
+    return dict(tiles=int(out[0]), fallback_tiles=int(out[1]), staged=int(out[2]),
+                in_range=int(out[3]))

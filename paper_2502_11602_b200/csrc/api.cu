@@ -179,6 +179,12 @@ const char* cm_last_error(void) { return g_last_error.c_str(); }
 
 uint64_t cm_launch_count(void) { return g_launches.load(); }
 
+cm_status cm_debug_query_stats(uint64_t* out4, int reset) {
+  if (!out4) return CM_INVALID_ARGUMENT;
+  query_stats(out4, reset);
+  return CM_OK;
+}
+
 const char* cm_status_name(cm_status s) {
   switch (s) {
     case CM_OK: return "CM_OK";

@@ -110,5 +110,6 @@ cm_status knn_dev(const cm_index* ix, const double* q_dev, uint64_t nq, uint32_t
                   const uint32_t* perm, uint32_t* idx_dev, double* d2_dev, cudaStream_t st);
 
 int sm_count();
+void query_stats(uint64_t* out, int reset);
 
 }  // namespace cmg

@@ -1,0 +1,4 @@
+# tests, bench, then one ncu capture of the tile kernels
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/ -m gpu -x -q 2>&1 | tail -4
+bash scripts/gpu_prof.sh
