@@ -268,7 +268,6 @@ def main():
     nnz_rank = int(counts.to(torch.int64).sum().item())
     alg_bytes = 24 * sum_tested
     del tested, counts
-    tile_stats = _native.query_stats(reset=True)
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
@@ -282,6 +281,11 @@ def main():
         csr = step_device()
         torch.cuda.synchronize(dev)
         L.cm_csr_free(csr)
+    _native.query_stats(reset=True)
+    csr = step_device()
+    torch.cuda.synchronize(dev)
+    L.cm_csr_free(csr)
+    step_stats = _native.query_stats(reset=True)  # one step: count + fill passes
 
     # ---- timed region (device-resident inputs)
     clocks = ClockSampler(local)
@@ -312,9 +316,11 @@ def main():
     def mean_of(key):
         return sum(k[key] for k in kern) / len(kern)
 
-    phase = {k: round(mean_of(k), 4) for k in ("order_ms", "count_ms", "scan_ms", "fill_ms",
-                                                "rowsort_ms")}
-    dom = "fill_ms" if phase["fill_ms"] >= phase["count_ms"] else "count_ms"
+    phase = {k: round(mean_of(k), 4) for k in ("order_ms", "pass1_ms", "rowsort_ms", "scan_ms",
+                                                "pass2_ms")}
+    two_pass = any(k["two_pass"] for k in kern)
+    phase["two_pass"] = bool(two_pass)
+    dom = "pass1_ms"
     dom_ms = phase[dom]
     peak, peak_src = read_peak()
     achieved = alg_bytes / (dom_ms * 1e-3) / 1e9
@@ -324,14 +330,13 @@ def main():
         try:
             with open(tpath) as f:
                 tj = json.load(f)
-            kname = "fill" if dom == "fill_ms" else "count"
-            traffic = tj.get(f"{a.flavor}/{kname}/r{a.radius:g}")
+            traffic = tj.get(f"{a.flavor}/collect/r{a.radius:g}")
         except Exception:
             traffic = None
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
-                "kernel": "radius_warp_kernel<" + a.flavor + ", " +
-                          ("FILL" if dom == "fill_ms" else "COUNT") + ">",
+                "kernel": "radius_tile_kernel<" + a.flavor + ", " +
+                          ("COUNT (two-pass fallback)" if two_pass else "COLLECT") + ">",
                 "kernel_ms": dom_ms, "alg_bytes_per_launch": alg_bytes,
                 "peak_source": peak_src,
                 "basis": "24 B x sum of the reference's points_tested (search.hpp:116) "
@@ -401,7 +406,7 @@ def main():
             "build_ms": {k: round(v, 3) for k, v in build_ms.items()},
             "build_detail": build_detail,
             "phases_ms": phase,
-            "tile_stats": tile_stats,
+            "tile_stats": step_stats,
             "roofline": roofline,
             "e2e": e2e,
             "cpu_baseline": cpu,

@@ -109,12 +109,14 @@ typedef struct {
  * the call's stream), milliseconds. */
 typedef struct {
   double order_ms;    /* query cell keys + radix sort (spatial order) */
-  double count_ms;    /* K5 count kernel */
-  double scan_ms;     /* K6 row_ptr scan */
-  double fill_ms;     /* K7 fill + in-warp row sort */
-  double rowsort_ms;  /* block sort of rows longer than the warp buffer */
+  double pass1_ms;    /* single pass: collect kernel (sorted rows -> arena);
+                         two-pass fallback: count kernel */
+  double rowsort_ms;  /* block sort of rows longer than a warp buffer */
+  double scan_ms;     /* row_ptr scan */
+  double pass2_ms;    /* single pass: gather arena -> CSR; two-pass: fill */
   double total_ms;
   uint64_t nq, nnz;
+  int32_t two_pass;   /* 1 when the arena overflowed and count+fill ran */
 } cm_query_timing;
 
 typedef struct cm_index cm_index;
@@ -179,9 +181,10 @@ cm_status cm_corrupt_for_testing(cm_index* index);
 cm_status cm_get_last_query_timing(cm_query_timing* out);
 /* Kernels launched by this library since load (all threads). */
 uint64_t cm_launch_count(void);
-/* Query-tile counters since the last reset: tiles, tiles answered one query
- * per warp (fallback), staged hull points, in-range candidates. */
-cm_status cm_debug_query_stats(uint64_t* out4, int reset);
+/* Query-tile counters since the last reset, count pass then fill pass:
+ * tiles, tiles answered one query per warp (fallback), hull points,
+ * in-range candidates (count pass only). out8 has 8 entries. */
+cm_status cm_debug_query_stats(uint64_t* out8, int reset);
 
 const char* cm_last_error(void);
 const char* cm_status_name(cm_status s);

@@ -49,10 +49,10 @@ class BuildTimingC(ctypes.Structure):
 
 
 class QueryTimingC(ctypes.Structure):
-    _fields_ = [("order_ms", ctypes.c_double), ("count_ms", ctypes.c_double),
-                ("scan_ms", ctypes.c_double), ("fill_ms", ctypes.c_double),
-                ("rowsort_ms", ctypes.c_double), ("total_ms", ctypes.c_double),
-                ("nq", ctypes.c_uint64), ("nnz", ctypes.c_uint64)]
+    _fields_ = [("order_ms", ctypes.c_double), ("pass1_ms", ctypes.c_double),
+                ("rowsort_ms", ctypes.c_double), ("scan_ms", ctypes.c_double),
+                ("pass2_ms", ctypes.c_double), ("total_ms", ctypes.c_double),
+                ("nq", ctypes.c_uint64), ("nnz", ctypes.c_uint64), ("two_pass", ctypes.c_int32)]
 
 
 _LIB = None
@@ -118,7 +118,9 @@ def launch_count():
 
 def query_stats(reset=True):
     import numpy as np
-    out = np.zeros(4, dtype=np.uint64)
+    out = np.zeros(8, dtype=np.uint64)
     lib().cm_debug_query_stats(out.ctypes.data_as(ctypes.c_void_p), int(reset))
-    return dict(tiles=int(out[0]), fallback_tiles=int(out[1]), staged=int(out[2]),
-                in_range=int(out[3]))
+    return dict(count_tiles=int(out[0]), count_fallback_tiles=int(out[1]),
+                count_hull_points=int(out[2]), in_range=int(out[3]), fill_tiles=int(out[4]),
+                fill_fallback_tiles=int(out[5]), fill_hull_points=int(out[6]),
+                fill_long_rows=int(out[7]))

@@ -1,4 +1,5 @@
 // C ABI (include/cmgpu.h): argument checks, host/device staging, ownership.
+#include <algorithm>
 #include <atomic>
 #include <cstring>
 #include <mutex>
@@ -179,9 +180,9 @@ const char* cm_last_error(void) { return g_last_error.c_str(); }
 
 uint64_t cm_launch_count(void) { return g_launches.load(); }
 
-cm_status cm_debug_query_stats(uint64_t* out4, int reset) {
-  if (!out4) return CM_INVALID_ARGUMENT;
-  query_stats(out4, reset);
+cm_status cm_debug_query_stats(uint64_t* out8, int reset) {
+  if (!out8) return CM_INVALID_ARGUMENT;
+  query_stats(out8, reset);
   return CM_OK;
 }
 
@@ -435,6 +436,7 @@ namespace {
 struct QueryEvents {
   cudaEvent_t e[6];
   uint64_t nq = 0, nnz = 0;
+  bool two_pass = false;
   bool valid = false;
   QueryEvents() {
     for (auto& x : e) cudaEventCreate(&x);
@@ -461,13 +463,14 @@ cm_status cm_get_last_query_timing(cm_query_timing* o) {
   for (int i = 0; i < 5; ++i) cudaEventElapsedTime(&ms[i], ev.e[i], ev.e[i + 1]);
   cudaEventElapsedTime(&tot, ev.e[0], ev.e[5]);
   o->order_ms = ms[0];
-  o->count_ms = ms[1];
-  o->scan_ms = ms[2];
-  o->fill_ms = ms[3];
-  o->rowsort_ms = ms[4];
+  o->pass1_ms = ms[1];
+  o->rowsort_ms = ms[2];
+  o->scan_ms = ms[3];
+  o->pass2_ms = ms[4];
   o->total_ms = tot;
   o->nq = ev.nq;
   o->nnz = ev.nnz;
+  o->two_pass = ev.two_pass ? 1 : 0;
   return CM_OK;
 }
 
@@ -495,38 +498,87 @@ cm_status cm_radius_search(const cm_index* ix, const double* q, uint64_t nq, int
   csr->nq = nq;
   csr->device = ix->device;
   uint32_t* counts = nullptr;
-  auto fail = [&](cm_status s) {
+  uint64_t* toff = nullptr;
+  uint32_t* temp = nullptr;
+  unsigned long long* cursor = nullptr;
+  auto release = [&]() {
     if (counts) dev_free(counts, st);
+    if (toff) dev_free(toff, st);
+    if (temp) dev_free(temp, st);
+    if (cursor) dev_free(cursor, st);
+    counts = nullptr, toff = nullptr, temp = nullptr, cursor = nullptr;
+  };
+  auto fail = [&](cm_status s) {
+    release();
     cudaStreamSynchronize(st);
     cm_csr_free(csr);
     return s;
   };
   if (dev_alloc_t(&counts, nq + 1, st) != cudaSuccess ||
-      dev_alloc_t(&csr->row_ptr, nq + 1, st) != cudaSuccess) {
+      dev_alloc_t(&csr->row_ptr, nq + 1, st) != cudaSuccess ||
+      dev_alloc_t(&toff, nq + 1, st) != cudaSuccess || dev_alloc_t(&cursor, 1, st) != cudaSuccess) {
     set_error("device allocation failed (row pointers)");
     return fail(CM_CUDA);
   }
-  cm_status s = radius_count_dev(ix, qd, nq, kernel, r, ord.perm, counts, nullptr, st);
-  cudaEventRecord(ev.e[2], st);
-  if (s == CM_OK) s = counts_to_row_ptr(counts, nq, csr->row_ptr, st);
-  cudaEventRecord(ev.e[3], st);
+  // Single pass: sorted rows into an arena sized from the running
+  // neighbours-per-query estimate; if the arena overflows, fall back to
+  // count + scan + fill.
+  uint64_t cap = (uint64_t)((double)nq * ix->nnz_per_query * 1.05) + (1u << 20);
+  bool two_pass = dev_alloc_t(&temp, cap, st) != cudaSuccess;
+  if (two_pass) cudaGetLastError();
+  cm_status s = CM_OK;
+  unsigned long long used = 0;
+  if (!two_pass) {
+    s = radius_collect_dev(ix, qd, nq, kernel, r, ord.perm, temp, cap, toff, counts, cursor, st,
+                           ev.e[2]);
+    cudaEventRecord(ev.e[3], st);
+    if (s != CM_OK) return fail(s);
+    if (cudaMemcpyAsync(&used, cursor, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess) {
+      set_error("arena cursor readback failed");
+      return fail(CM_CUDA);
+    }
+    if (nq) ix->nnz_per_query = std::max(1.0, (double)used / (double)nq);
+    two_pass = used > cap;
+    if (two_pass) {
+      dev_free(temp, st);
+      temp = nullptr;
+    }
+  }
+  if (two_pass) {
+    cudaEventRecord(ev.e[1], st);
+    s = radius_count_dev(ix, qd, nq, kernel, r, ord.perm, counts, nullptr, st);
+    cudaEventRecord(ev.e[2], st);
+    cudaEventRecord(ev.e[3], st);
+    if (s != CM_OK) return fail(s);
+  }
+  s = counts_to_row_ptr(counts, nq, csr->row_ptr, st);
+  cudaEventRecord(ev.e[4], st);
   if (s != CM_OK) return fail(s);
-  if (cudaMemcpyAsync(&csr->nnz, csr->row_ptr + nq, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
-      cudaStreamSynchronize(st) != cudaSuccess) {
-    set_error("row pointer readback failed");
-    return fail(CM_CUDA);
+  if (two_pass) {
+    if (cudaMemcpyAsync(&csr->nnz, csr->row_ptr + nq, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess) {
+      set_error("row pointer readback failed");
+      return fail(CM_CUDA);
+    }
+  } else {
+    csr->nnz = used;
   }
   if (dev_alloc_t(&csr->cols, csr->nnz, st) != cudaSuccess) {
     set_error("device allocation failed (columns)");
     return fail(CM_CUDA);
   }
-  s = radius_fill_dev(ix, qd, nq, kernel, r, ord.perm, csr->row_ptr, csr->cols, st, ev.e[4]);
+  if (two_pass)
+    s = radius_fill_dev(ix, qd, nq, kernel, r, ord.perm, csr->row_ptr, csr->cols, st, nullptr);
+  else
+    s = gather_rows_dev(temp, toff, counts, csr->row_ptr, csr->cols, nq, st);
   cudaEventRecord(ev.e[5], st);
   if (s != CM_OK) return fail(s);
   ev.nq = nq;
   ev.nnz = csr->nnz;
+  ev.two_pass = two_pass;
   ev.valid = true;
-  dev_free(counts, st);
+  release();
   *out = csr;
   return CM_OK;
 }

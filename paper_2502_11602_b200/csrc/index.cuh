@@ -35,6 +35,8 @@ struct cm_index {
   uint32_t* col_vbeg = nullptr;   // C + 1
 
   std::vector<uint64_t> slice_ne;  // per z slice non-empty voxels (host)
+  // Running estimate of neighbours per query, sizing the single-pass arena.
+  mutable double nnz_per_query = 64.0;
   cm_build_timing timing{};
 
   cmg::Tables tables() const {
@@ -104,6 +106,12 @@ cm_status radius_fill_dev(const cm_index* ix, const double* q_dev, uint64_t nq, 
 cm_status radius_digest_dev(const cm_index* ix, const double* q_dev, uint64_t nq, int kernel,
                             double r, const uint32_t* perm, uint32_t* counts_dev,
                             uint64_t* digest_dev, cudaStream_t st);
+cm_status radius_collect_dev(const cm_index* ix, const double* q_dev, uint64_t nq, int kernel,
+                             double r, const uint32_t* perm, uint32_t* temp, uint64_t cap,
+                             uint64_t* toff, uint32_t* counts, unsigned long long* cursor,
+                             cudaStream_t st, cudaEvent_t after_collect);
+cm_status gather_rows_dev(const uint32_t* temp, const uint64_t* toff, const uint32_t* counts,
+                          const uint64_t* row_ptr, uint32_t* cols, uint64_t nq, cudaStream_t st);
 cm_status counts_to_row_ptr(const uint32_t* counts_dev, uint64_t nq, uint64_t* row_ptr_dev,
                             cudaStream_t st);
 cm_status knn_dev(const cm_index* ix, const double* q_dev, uint64_t nq, uint32_t k,

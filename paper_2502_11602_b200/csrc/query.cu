@@ -1,17 +1,29 @@
 // Batched fixed-radius queries (sphere / cube) on sm_100a.
 // Replaces kernel_search<Kernel> (search.hpp:102-127) for a batch of centres.
 //
-// Pipeline: query cell keys -> radix sort (spatial order, so neighbouring
-// warps touch the same candidate records in L1/L2) -> warp-per-query count
-// (K5) -> exclusive scan (K6) -> warp-per-query fill + in-warp bitonic sort
-// of each row (K7). Rows too long for the per-warp buffer are written
-// unsorted and sorted afterwards by a persistent block-per-row kernel.
-//
 // Candidate enumeration is exactly the reference's: every point of every
 // voxel of clamped_range(c +- r) (grid.cpp:90-114). The points of one
 // (i, j) column inside [k0, k1] are one contiguous span of the cell-sorted
-// records, so a query is ncol spans; the warp flattens them and tests 32
-// candidates per step with the reference's predicate arithmetic.
+// records (global_index is k-fastest, grid.hpp:65-67), so a query is a
+// handful of spans.
+//
+// Work decomposition:
+//  * queries are radix-sorted by cell key, so a warp's 32 consecutive
+//    queries are spatial neighbours (a query TILE);
+//  * a tile whose clamped ranges have a compact hull (<= 32 columns) walks
+//    the hull's points once, warp-uniformly (one L1 broadcast per record);
+//    each lane tests every point against its own query, keeping only points
+//    whose voxel is in that query's own range, with the reference's exact
+//    predicate arithmetic;
+//  * hits go to a per-lane row buffer in shared memory; each row is then
+//    sorted by the whole warp (register bitonic) and written coalesced;
+//  * lanes whose rows overflow the buffer, and tiles that are not compact,
+//    are answered one query per warp (flattened spans, 32 candidates/step).
+//
+// Passes: COUNT (counts + QueryStats::points_tested), DIGEST (count + set
+// digest), FILL (sorted rows at caller row_ptr), COLLECT (single pass: sorted
+// rows into a scratch arena at atomically allocated offsets; a gather copies
+// them into CSR order after the row_ptr scan).
 #include <algorithm>
 
 #include "index.cuh"
@@ -23,16 +35,33 @@ namespace {
 
 constexpr int kQThreads = 128;
 constexpr int kQWarps = kQThreads / 32;
-constexpr int kTileCap = 512;                  // hull points per warp (fill pass)
-constexpr int kFillWarpBytes = kTileCap * 12;  // u64 keys + u32 positions
-constexpr int kRowCap = kFillWarpBytes / 4;    // fallback per-warp row buffer (u32)
-constexpr int kBigSmemCap = 32768;  // block sort in shared memory (128 KB)
+constexpr int kLaneRowCap = 96;                       // per-lane row buffer
+constexpr int kRowWarpBytes = kLaneRowCap * 33 * 4;   // interleaved, stride 33
+constexpr int kRowCap = kRowWarpBytes / 4;            // one-query row buffer (u32)
+constexpr int kBigSmemCap = 32768;                    // block sort in smem (128 KB)
 
-enum { MODE_COUNT = 0, MODE_FILL = 1, MODE_DIGEST = 2 };
+enum { MODE_COUNT = 0, MODE_FILL = 1, MODE_DIGEST = 2, MODE_COLLECT = 3 };
 
-// Tile statistics (cm_debug_query_stats): [0] tiles, [1] fallback tiles,
-// [2] staged points (tile mode), [3] in-range candidates (tile mode).
-__device__ unsigned long long g_qstats[4];
+// Tile statistics (cm_debug_query_stats): count pass [0..3], row passes
+// (fill / collect) [4..7]: tiles, non-compact tiles, hull points, and
+// in-range candidates (count) / long rows answered per query (row passes).
+__device__ unsigned long long g_qstats[8];
+
+// Kernel outputs; which fields are used depends on the pass.
+struct Out {
+  uint32_t* counts;
+  uint64_t* tested;
+  uint64_t* digests;
+  const uint64_t* row_ptr;        // FILL
+  uint32_t* cols;                 // FILL
+  uint32_t* temp;                 // COLLECT arena
+  uint64_t cap;                   // COLLECT arena capacity (entries)
+  uint64_t* toff;                 // COLLECT per-query arena offset
+  unsigned long long* cursor;     // COLLECT arena bump pointer
+  uint64_t* big_off;              // rows sorted afterwards: offset into `rows`
+  uint32_t* big_len;
+  uint32_t* n_big;
+};
 
 template <typename K>
 __global__ void query_keys_kernel(const double* __restrict__ q, uint64_t nq, DevGrid g,
@@ -100,132 +129,6 @@ __device__ __forceinline__ uint32_t warp_sort32(uint32_t v, int lane) {
 
 // One query answered by a whole warp (the fallback when a 32-query tile is
 // not compact): ncol column spans flattened, 32 candidates per step.
-template <int FLAVOR, int MODE>
-__device__ __forceinline__ void query_warp(const Tables& t, uint32_t qi, double cx, double cy,
-                                           double cz, double r, int cube, int lane, uint32_t lt,
-                                           uint32_t* counts, uint64_t* tested, uint64_t* digests,
-                                           const uint64_t* row_ptr, uint32_t* cols,
-                                           uint32_t* big_rows, uint32_t* n_big, uint32_t* wbuf) {
-  Range R;
-  const bool ok = clamped_range(t.g, cx, cy, cz, r, &R);
-  Predicate P;
-  P.init(cx, cy, cz, r, cube);
-  uint32_t cnt = 0;
-  uint64_t ntested = 0, dig = 0;
-  uint64_t rowb = 0;
-  bool direct = false;
-  if (MODE == MODE_FILL) {
-    rowb = __ldg(row_ptr + qi);
-    direct = (__ldg(row_ptr + qi + 1) - rowb) > (uint64_t)kRowCap;
-  }
-  if (ok) {
-    const uint64_t nj = R.j1 - R.j0 + 1;
-    const uint64_t ncol = (R.i1 - R.i0 + 1) * nj;
-    for (uint64_t cb = 0; cb < ncol; cb += 32) {
-      const uint64_t c = cb + lane;
-      uint32_t b = 0, e = 0;
-      if (c < ncol) column_span<FLAVOR>(t, R.i0 + c / nj, R.j0 + c % nj, R.k0, R.k1, &b, &e);
-      const uint32_t len = e - b;
-      const uint32_t incl = warp_incl_scan(len);
-      const uint32_t excl = incl - len;
-      const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-      ntested += total;
-      for (uint32_t t0 = 0; t0 < total; t0 += 32) {
-        const uint32_t tt = t0 + lane;
-        int L = 0;
-#pragma unroll
-        for (int sft = 16; sft > 0; sft >>= 1) {
-          const uint32_t v = __shfl_sync(0xffffffffu, incl, L + sft - 1);
-          if (v <= tt) L += sft;
-        }
-        const uint32_t bL = __shfl_sync(0xffffffffu, b, L);
-        const uint32_t xL = __shfl_sync(0xffffffffu, excl, L);
-        bool hit = false;
-        uint32_t id = 0;
-        if (tt < total) {
-          const PointRec pr = load_rec(t.rec + bL + (tt - xL));
-          hit = P(pr.x, pr.y, pr.z);
-          id = pr.id;
-        }
-        const uint32_t m = __ballot_sync(0xffffffffu, hit);
-        if (MODE == MODE_DIGEST && hit) dig += mix64(id);
-        if (MODE == MODE_FILL && hit) {
-          const uint32_t off = cnt + __popc(m & lt);
-          if (direct) cols[rowb + off] = id;
-          else wbuf[off] = id;
-        }
-        cnt += __popc(m);
-      }
-    }
-  }
-  if (MODE == MODE_COUNT) {
-    if (lane == 0) {
-      if (counts) counts[qi] = cnt;
-      if (tested) tested[qi] = ntested;
-    }
-  } else if (MODE == MODE_DIGEST) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) dig += __shfl_xor_sync(0xffffffffu, dig, o);
-    if (lane == 0) {
-      counts[qi] = cnt;
-      digests[qi] = dig;
-    }
-  } else {
-    if (direct) {
-      if (lane == 0) big_rows[atomicAdd(n_big, 1u)] = qi;
-    } else if (cnt <= 32) {
-      __syncwarp();
-      uint32_t v = lane < (int)cnt ? wbuf[lane] : 0xffffffffu;
-      v = warp_sort32(v, lane);
-      if (lane < (int)cnt) cols[rowb + lane] = v;
-    } else {
-      __syncwarp();
-      bitonic_sort(wbuf, cnt, lane, 32, [] { __syncwarp(); });
-      for (uint32_t x = lane; x < cnt; x += 32) cols[rowb + x] = wbuf[x];
-    }
-  }
-  __syncwarp();
-}
-
-// Ascending bitonic sort of a[0..n) (u64) by one warp; P = pow2 >= n,
-// indices >= n act as +inf. Iterates compare pairs directly.
-__device__ __forceinline__ void warp_bitonic_u64(uint64_t* a, uint32_t n, int lane) {
-  uint32_t P = 1, lg = 0;
-  while (P < n) P <<= 1, ++lg;
-  const uint32_t half = P >> 1;
-  for (uint32_t lk = 1; lk <= lg; ++lk) {
-    const uint32_t k = 1u << lk;
-    // flip step: i in the lower half of its k-block, partner i ^ (k - 1)
-    for (uint32_t tq = lane; tq < half; tq += 32) {
-      const uint32_t i = ((tq >> (lk - 1)) << lk) | (tq & ((k >> 1) - 1));
-      const uint32_t p = i ^ (k - 1);
-      if (p < n) {
-        const uint64_t x = a[i], y = a[p];
-        if (x > y) {
-          a[i] = y;
-          a[p] = x;
-        }
-      }
-    }
-    __syncwarp();
-    for (int lj = (int)lk - 2; lj >= 0; --lj) {
-      const uint32_t j = 1u << lj;
-      for (uint32_t tq = lane; tq < half; tq += 32) {
-        const uint32_t i = ((tq >> lj) << (lj + 1)) | (tq & (j - 1));
-        const uint32_t p = i + j;
-        if (p < n) {
-          const uint64_t x = a[i], y = a[p];
-          if (x > y) {
-            a[i] = y;
-            a[p] = x;
-          }
-        }
-      }
-      __syncwarp();
-    }
-  }
-}
-
 __device__ __forceinline__ uint32_t warp_min_u32(uint32_t v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
@@ -235,6 +138,63 @@ __device__ __forceinline__ uint32_t warp_max_u32(uint32_t v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
+}
+
+// Ascending bitonic sort of P = 32 * ITEMS u32 keys held by one warp in
+// registers, striped: element e = r * 32 + lane lives in v[r] of `lane`.
+// Exchanges at distance < 32 go through shuffles, the rest stay in-lane.
+template <int ITEMS>
+__device__ __forceinline__ void warp_sort_regs(uint32_t (&v)[ITEMS], int lane) {
+  constexpr int LOGP = ITEMS == 1 ? 5 : ITEMS == 2 ? 6 : ITEMS == 4 ? 7 : ITEMS == 8 ? 8 : 9;
+#pragma unroll
+  for (int lk = 1; lk <= LOGP; ++lk) {
+    const int k = 1 << lk;
+#pragma unroll
+    for (int lj = lk - 1; lj >= 0; --lj) {
+      const int j = 1 << lj;
+      if (lj < 5) {
+#pragma unroll
+        for (int r = 0; r < ITEMS; ++r) {
+          const int e = r * 32 + lane;
+          const uint32_t o = __shfl_xor_sync(0xffffffffu, v[r], j);
+          const bool asc = (e & k) == 0;
+          const bool lower = (lane & j) == 0;
+          v[r] = (lower == asc) ? min(v[r], o) : max(v[r], o);
+        }
+      } else {
+        const int jr = j >> 5;
+#pragma unroll
+        for (int r = 0; r < ITEMS; ++r) {
+          if ((r & jr) == 0) {
+            const int e = r * 32 + lane;
+            const bool asc = (e & k) == 0;
+            const uint32_t x = v[r], y = v[r | jr];
+            v[r] = asc ? min(x, y) : max(x, y);
+            v[r | jr] = asc ? max(x, y) : min(x, y);
+          }
+        }
+      }
+    }
+  }
+}
+
+// Sorts lane l's interleaved row (srow[i * 33 + l], i < len) with the whole
+// warp and writes it ascending to dst[0..len) (coalesced).
+template <int ITEMS>
+__device__ __forceinline__ void warp_sort_row_out(const uint32_t* srow, int l, uint32_t len,
+                                                  uint32_t* dst, int lane) {
+  uint32_t v[ITEMS];
+#pragma unroll
+  for (int r = 0; r < ITEMS; ++r) {
+    const uint32_t e = r * 32 + lane;
+    v[r] = e < len ? srow[e * 33 + l] : 0xffffffffu;
+  }
+  warp_sort_regs<ITEMS>(v, lane);
+#pragma unroll
+  for (int r = 0; r < ITEMS; ++r) {
+    const uint32_t e = r * 32 + lane;
+    if (e < len) dst[e] = v[r];
+  }
 }
 
 template <int CUBE>
@@ -258,30 +218,176 @@ __device__ __forceinline__ void load_uniform(const PointRec* p, double& x, doubl
   k = t.y;
 }
 
-// Query-tile kernel. A warp takes 32 consecutive (cell-sorted) queries, one
-// per lane. When their clamped ranges have a compact hull (<= 32 columns,
-// <= kTileCap points), the warp walks the hull's points once, warp-uniformly
-// (every lane reads the same record: an L1 broadcast), and each lane tests
-// each point against its own query: a point counts for lane q only if its
-// voxel lies in q's own clamped_range (the reference's exact candidate set,
-// search.hpp:110-122) and q's predicate holds. The fill pass first sorts the
-// hull's (handle, slot) keys in shared memory, so each lane's hits come out
-// ascending and go straight to its CSR row. Tiles that are not compact fall
-// back to query_warp for each of their queries.
+
+// One query answered by a whole warp: count pass over the flattened spans.
+template <int FLAVOR, int CUBE, bool DIG>
+__device__ __forceinline__ void warp_query_count(const Tables& t, double cx, double cy, double cz,
+                                                 double r, int lane, uint32_t* cnt_out,
+                                                 uint64_t* tested_out, uint64_t* dig_out) {
+  Range R;
+  const bool ok = clamped_range(t.g, cx, cy, cz, r, &R);
+  Predicate P;
+  P.init(cx, cy, cz, r, CUBE);
+  uint32_t cnt = 0;
+  uint64_t ntested = 0, dig = 0;
+  if (ok) {
+    const uint64_t nj = R.j1 - R.j0 + 1;
+    const uint64_t ncol = (R.i1 - R.i0 + 1) * nj;
+    for (uint64_t cb = 0; cb < ncol; cb += 32) {
+      const uint64_t c = cb + lane;
+      uint32_t b = 0, e = 0;
+      if (c < ncol) column_span<FLAVOR>(t, R.i0 + c / nj, R.j0 + c % nj, R.k0, R.k1, &b, &e);
+      const uint32_t len = e - b;
+      const uint32_t incl = warp_incl_scan(len);
+      const uint32_t excl = incl - len;
+      const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+      ntested += total;
+      for (uint32_t t0 = 0; t0 < total; t0 += 32) {
+        const uint32_t tt = t0 + lane;
+        int L = 0;
+#pragma unroll
+        for (int sft = 16; sft > 0; sft >>= 1) {
+          const uint32_t v = __shfl_sync(0xffffffffu, incl, L + sft - 1);
+          if (v <= tt) L += sft;
+        }
+        const uint32_t bL = __shfl_sync(0xffffffffu, b, L);
+        const uint32_t xL = __shfl_sync(0xffffffffu, excl, L);
+        bool hit = false;
+        if (tt < total) {
+          const PointRec pr = load_rec(t.rec + bL + (tt - xL));
+          hit = pred<CUBE>(P, pr.x, pr.y, pr.z);
+          if (DIG && hit) dig += mix64(pr.id);
+        }
+        cnt += __popc(__ballot_sync(0xffffffffu, hit));
+      }
+    }
+  }
+  if (DIG) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dig += __shfl_xor_sync(0xffffffffu, dig, o);
+  }
+  *cnt_out = cnt;
+  *tested_out = ntested;
+  *dig_out = dig;
+}
+
+// One query answered by a whole warp: its `len` hits, sorted, to dst. Rows
+// longer than the warp buffer are written unsorted and registered for the
+// block sort (offset `big_base` into the row buffer).
+template <int FLAVOR, int CUBE>
+__device__ __forceinline__ void warp_query_fill(const Tables& t, double cx, double cy, double cz,
+                                                double r, int lane, uint32_t lt, uint32_t* dst,
+                                                uint32_t len, uint64_t big_base, const Out& o,
+                                                uint32_t* wbuf) {
+  Range R;
+  const bool ok = clamped_range(t.g, cx, cy, cz, r, &R);
+  Predicate P;
+  P.init(cx, cy, cz, r, CUBE);
+  const bool direct = len > (uint32_t)kRowCap;
+  uint32_t cnt = 0;
+  if (ok) {
+    const uint64_t nj = R.j1 - R.j0 + 1;
+    const uint64_t ncol = (R.i1 - R.i0 + 1) * nj;
+    for (uint64_t cb = 0; cb < ncol; cb += 32) {
+      const uint64_t c = cb + lane;
+      uint32_t b = 0, e = 0;
+      if (c < ncol) column_span<FLAVOR>(t, R.i0 + c / nj, R.j0 + c % nj, R.k0, R.k1, &b, &e);
+      const uint32_t ln = e - b;
+      const uint32_t incl = warp_incl_scan(ln);
+      const uint32_t excl = incl - ln;
+      const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+      for (uint32_t t0 = 0; t0 < total; t0 += 32) {
+        const uint32_t tt = t0 + lane;
+        int L = 0;
+#pragma unroll
+        for (int sft = 16; sft > 0; sft >>= 1) {
+          const uint32_t v = __shfl_sync(0xffffffffu, incl, L + sft - 1);
+          if (v <= tt) L += sft;
+        }
+        const uint32_t bL = __shfl_sync(0xffffffffu, b, L);
+        const uint32_t xL = __shfl_sync(0xffffffffu, excl, L);
+        bool hit = false;
+        uint32_t id = 0;
+        if (tt < total) {
+          const PointRec pr = load_rec(t.rec + bL + (tt - xL));
+          hit = pred<CUBE>(P, pr.x, pr.y, pr.z);
+          id = pr.id;
+        }
+        const uint32_t m = __ballot_sync(0xffffffffu, hit);
+        if (hit) {
+          const uint32_t off = cnt + __popc(m & lt);
+          if (direct) dst[off] = id;
+          else wbuf[off] = id;
+        }
+        cnt += __popc(m);
+      }
+    }
+  }
+  __syncwarp();
+  if (direct) {
+    if (lane == 0) {
+      const uint32_t slot = atomicAdd(o.n_big, 1u);
+      o.big_off[slot] = big_base;
+      o.big_len[slot] = cnt;
+    }
+  } else if (cnt <= 32) {
+    uint32_t v = lane < (int)cnt ? wbuf[lane] : 0xffffffffu;
+    v = warp_sort32(v, lane);
+    if (lane < (int)cnt) dst[lane] = v;
+  } else {
+    bitonic_sort(wbuf, cnt, lane, 32, [] { __syncwarp(); });
+    for (uint32_t x = lane; x < cnt; x += 32) dst[x] = wbuf[x];
+  }
+  __syncwarp();
+}
+
+// One query, one warp, any pass.
+template <int FLAVOR, int MODE, int CUBE>
+__device__ __forceinline__ void single_query(const Tables& t, uint32_t qi, double cx, double cy,
+                                             double cz, double r, int lane, uint32_t lt,
+                                             const Out& o, uint32_t* wbuf) {
+  if (MODE == MODE_COUNT || MODE == MODE_DIGEST) {
+    uint32_t cnt;
+    uint64_t tested, dig;
+    warp_query_count<FLAVOR, CUBE, MODE == MODE_DIGEST>(t, cx, cy, cz, r, lane, &cnt, &tested,
+                                                        &dig);
+    if (lane == 0) {
+      if (o.counts) o.counts[qi] = cnt;
+      if (MODE == MODE_COUNT && o.tested) o.tested[qi] = tested;
+      if (MODE == MODE_DIGEST) o.digests[qi] = dig;
+    }
+  } else if (MODE == MODE_FILL) {
+    const uint64_t rb = __ldg(o.row_ptr + qi);
+    const uint32_t len = (uint32_t)(__ldg(o.row_ptr + qi + 1) - rb);
+    warp_query_fill<FLAVOR, CUBE>(t, cx, cy, cz, r, lane, lt, o.cols + rb, len, rb, o, wbuf);
+  } else {
+    uint32_t cnt;
+    uint64_t tested, dig;
+    warp_query_count<FLAVOR, CUBE, false>(t, cx, cy, cz, r, lane, &cnt, &tested, &dig);
+    unsigned long long base = 0;
+    if (lane == 0) {
+      base = atomicAdd(o.cursor, (unsigned long long)cnt);
+      o.counts[qi] = cnt;
+      o.toff[qi] = base;
+    }
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (base + cnt <= o.cap)
+      warp_query_fill<FLAVOR, CUBE>(t, cx, cy, cz, r, lane, lt, o.temp + base, cnt, base, o, wbuf);
+  }
+}
+
+// Query-tile kernel (see the file comment).
 template <int FLAVOR, int MODE, int CUBE>
 __global__ void __launch_bounds__(kQThreads, 4) radius_tile_kernel(
     const Tables t, const double* __restrict__ q, uint64_t nq, double r,
-    const uint32_t* __restrict__ perm, uint32_t* __restrict__ counts,
-    uint64_t* __restrict__ tested, uint64_t* __restrict__ digests,
-    const uint64_t* __restrict__ row_ptr, uint32_t* __restrict__ cols,
-    uint32_t* __restrict__ big_rows, uint32_t* __restrict__ n_big) {
+    const uint32_t* __restrict__ perm, const Out o) {
   extern __shared__ __align__(16) unsigned char smraw[];
+  constexpr bool ROWS = MODE == MODE_FILL || MODE == MODE_COLLECT;
+  constexpr int so = ROWS ? 4 : 0;
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  unsigned char* wbase = smraw + (size_t)wib * kFillWarpBytes;
-  uint64_t* skey = reinterpret_cast<uint64_t*>(wbase);                  // kTileCap
-  uint32_t* spos = reinterpret_cast<uint32_t*>(wbase + kTileCap * 8);   // kTileCap
-  uint32_t* wbuf = reinterpret_cast<uint32_t*>(wbase);                  // fallback rows
+  uint32_t* srow = reinterpret_cast<uint32_t*>(smraw + (size_t)wib * kRowWarpBytes);
+  uint32_t* wbuf = srow;
   const uint32_t lt = lanemask_lt();
   const uint64_t ntiles = (nq + 31) / 32;
   const uint64_t W = (uint64_t)gridDim.x * kQWarps;
@@ -303,7 +409,7 @@ __global__ void __launch_bounds__(kQThreads, 4) radius_tile_kernel(
     const uint32_t okmask = __ballot_sync(0xffffffffu, ok);
     bool use_tile = small_grid && okmask != 0;
     uint32_t I0 = 0, J0 = 0, nj = 0, ncol = 0, total = 0;
-    uint32_t b = 0, e = 0, incl = 0, excl = 0;
+    uint32_t b = 0, e = 0;
     if (use_tile) {
       I0 = warp_min_u32(ok ? (uint32_t)R.i0 : 0xffffffffu);
       const uint32_t I1 = warp_max_u32(ok ? (uint32_t)R.i1 : 0u);
@@ -318,20 +424,13 @@ __global__ void __launch_bounds__(kQThreads, 4) radius_tile_kernel(
         ncol = (uint32_t)nc;
         if ((uint32_t)lane < ncol)
           column_span<FLAVOR>(t, I0 + lane / nj, J0 + lane % nj, K0, K1, &b, &e);
-        const uint32_t len = e - b;
-        incl = warp_incl_scan(len);
-        excl = incl - len;
-        total = __shfl_sync(0xffffffffu, incl, 31);
-        use_tile = MODE != MODE_FILL || total <= (uint32_t)kTileCap;
-        if (lane == 0) {
-          atomicAdd(&g_qstats[0], 1ull);
-          if (use_tile) atomicAdd(&g_qstats[2], (unsigned long long)total);
-          else atomicAdd(&g_qstats[1], 1ull);
-        }
-      } else if (lane == 0) {
-        atomicAdd(&g_qstats[0], 1ull);
-        atomicAdd(&g_qstats[1], 1ull);
+        total = __shfl_sync(0xffffffffu, warp_incl_scan(e - b), 31);
       }
+    }
+    if (lane == 0) {
+      atomicAdd(&g_qstats[so + 0], 1ull);
+      if (use_tile) atomicAdd(&g_qstats[so + 2], (unsigned long long)total);
+      else atomicAdd(&g_qstats[so + 1], 1ull);
     }
     if (!use_tile) {
       const uint32_t am = __ballot_sync(0xffffffffu, active);
@@ -341,8 +440,7 @@ __global__ void __launch_bounds__(kQThreads, 4) radius_tile_kernel(
         const double xl = __shfl_sync(0xffffffffu, cx, l);
         const double yl = __shfl_sync(0xffffffffu, cy, l);
         const double zl = __shfl_sync(0xffffffffu, cz, l);
-        query_warp<FLAVOR, MODE>(t, ql, xl, yl, zl, r, CUBE, lane, lt, counts, tested, digests,
-                                 row_ptr, cols, big_rows, n_big, wbuf);
+        single_query<FLAVOR, MODE, CUBE>(t, ql, xl, yl, zl, r, lane, lt, o, wbuf);
       }
       continue;
     }
@@ -359,122 +457,113 @@ __global__ void __launch_bounds__(kQThreads, 4) radius_tile_kernel(
     P.init(cx, cy, cz, r, CUBE);
     uint32_t cnt = 0, ntest = 0;
     uint64_t dig = 0;
-    if (MODE != MODE_FILL) {
-      // column by column, in stored order
-      for (uint32_t c = 0; c < ncol; ++c) {
-        const uint32_t cb = __shfl_sync(0xffffffffu, b, c);
-        const uint32_t ce = __shfl_sync(0xffffffffu, e, c);
-        const bool need = (colmask >> c) & 1u;
-        if (__ballot_sync(0xffffffffu, need) == 0) continue;
-        uint32_t p = cb;
-        for (; p + 4 <= ce; p += 4) {
-          double x[4], y[4], z[4];
-          uint32_t id[4], kz[4];
+    // walk the hull column by column, in stored order
+    for (uint32_t c = 0; c < ncol; ++c) {
+      const uint32_t cb = __shfl_sync(0xffffffffu, b, c);
+      const uint32_t ce = __shfl_sync(0xffffffffu, e, c);
+      const bool need = (colmask >> c) & 1u;
+      if (__ballot_sync(0xffffffffu, need) == 0) continue;
+      uint32_t p = cb;
+      for (; p + 8 <= ce; p += 8) {
+        double x[8], y[8], z[8];
+        uint32_t id[8], kz[8];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) load_uniform(rec + p + u, x[u], y[u], z[u], id[u], kz[u]);
+        for (int u = 0; u < 8; ++u) load_uniform(rec + p + u, x[u], y[u], z[u], id[u], kz[u]);
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const bool in = need & (kz[u] - kk0 <= kspan);
-            const bool hit = in & pred<CUBE>(P, x[u], y[u], z[u]);
-            if (MODE == MODE_DIGEST && hit) dig += mix64(id[u]);
-            cnt += hit;
-            ntest += in;
-          }
-        }
-        for (; p < ce; ++p) {
-          double x, y, z;
-          uint32_t id, kz;
-          load_uniform(rec + p, x, y, z, id, kz);
-          const bool in = need & (kz - kk0 <= kspan);
-          const bool hit = in & pred<CUBE>(P, x, y, z);
-          if (MODE == MODE_DIGEST && hit) dig += mix64(id);
+        for (int u = 0; u < 8; ++u) {
+          const bool in = need & (kz[u] - kk0 <= kspan);
+          const bool hit = in & pred<CUBE>(P, x[u], y[u], z[u]);
+          if (MODE == MODE_DIGEST && hit) dig += mix64(id[u]);
+          if (ROWS && hit && cnt < (uint32_t)kLaneRowCap) srow[cnt * 33 + lane] = id[u];
           cnt += hit;
           ntest += in;
         }
       }
-    } else {
-      // keys (handle << 32 | column << 16 | slot) and record positions
-      for (uint32_t t0 = 0; t0 < total; t0 += 32) {
-        const uint32_t tt = t0 + lane;
-        int L = 0;
-#pragma unroll
-        for (int sft = 16; sft > 0; sft >>= 1) {
-          const uint32_t v = __shfl_sync(0xffffffffu, incl, L + sft - 1);
-          if (v <= tt) L += sft;
-        }
-        const uint32_t bL = __shfl_sync(0xffffffffu, b, L);
-        const uint32_t xL = __shfl_sync(0xffffffffu, excl, L);
-        if (tt < total) {
-          const uint32_t pos = bL + (tt - xL);
-          const uint32_t id = __ldg(reinterpret_cast<const uint32_t*>(rec + pos) + 6);
-          skey[tt] = ((uint64_t)id << 32) | ((uint32_t)L << 16) | tt;
-          spos[tt] = pos;
-        }
-      }
-      __syncwarp();
-      warp_bitonic_u64(skey, total, lane);
-      const uint64_t rowb = active ? __ldg(row_ptr + qi) : 0;
-      uint32_t u = 0;
-      for (; u + 4 <= total; u += 4) {
-        double x[4], y[4], z[4];
-        uint32_t id[4], kz[4], col[4];
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          const uint64_t key = skey[u + v];
-          col[v] = ((uint32_t)key >> 16) & 0xffffu;
-          load_uniform(rec + spos[(uint32_t)key & 0xffffu], x[v], y[v], z[v], id[v], kz[v]);
-        }
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          const bool in = ((colmask >> col[v]) & 1u) & (kz[v] - kk0 <= kspan);
-          const bool hit = in & pred<CUBE>(P, x[v], y[v], z[v]);
-          if (hit) cols[rowb + cnt] = id[v];
-          cnt += hit;
-        }
-      }
-      for (; u < total; ++u) {
-        const uint64_t key = skey[u];
-        const uint32_t cl = ((uint32_t)key >> 16) & 0xffffu;
+      for (; p < ce; ++p) {
         double x, y, z;
         uint32_t id, kz;
-        load_uniform(rec + spos[(uint32_t)key & 0xffffu], x, y, z, id, kz);
-        const bool in = ((colmask >> cl) & 1u) & (kz - kk0 <= kspan);
+        load_uniform(rec + p, x, y, z, id, kz);
+        const bool in = need & (kz - kk0 <= kspan);
         const bool hit = in & pred<CUBE>(P, x, y, z);
-        if (hit) cols[rowb + cnt] = id;
+        if (MODE == MODE_DIGEST && hit) dig += mix64(id);
+        if (ROWS && hit && cnt < (uint32_t)kLaneRowCap) srow[cnt * 33 + lane] = id;
         cnt += hit;
+        ntest += in;
       }
     }
     if (MODE == MODE_COUNT) {
       uint32_t sum = ntest;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      for (int sh = 16; sh > 0; sh >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, sh);
       if (lane == 0) atomicAdd(&g_qstats[3], (unsigned long long)sum);
-    }
-    if (active) {
-      if (MODE == MODE_COUNT) {
-        if (counts) counts[qi] = cnt;
-        if (tested) tested[qi] = ntest;
-      } else if (MODE == MODE_DIGEST) {
-        counts[qi] = cnt;
-        digests[qi] = dig;
+      if (active) {
+        if (o.counts) o.counts[qi] = cnt;
+        if (o.tested) o.tested[qi] = ntest;
+      }
+    } else if (MODE == MODE_DIGEST) {
+      if (active) {
+        o.counts[qi] = cnt;
+        o.digests[qi] = dig;
+      }
+    } else {
+      // rows: lanes whose hits overflowed the buffer are redone per query
+      const bool longrow = cnt > (uint32_t)kLaneRowCap;
+      const uint32_t mine = (active && !longrow) ? cnt : 0u;
+      uint64_t dst;
+      bool write_ok = true;
+      if (MODE == MODE_FILL) {
+        dst = active ? __ldg(o.row_ptr + qi) : 0;
+      } else {
+        const uint32_t inc = warp_incl_scan(mine);
+        const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
+        unsigned long long base = 0;
+        if (lane == 0 && tot) base = atomicAdd(o.cursor, (unsigned long long)tot);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        dst = base + (inc - mine);
+        write_ok = base + tot <= o.cap;
+        if (active && !longrow) {
+          o.counts[qi] = cnt;
+          o.toff[qi] = dst;
+        }
+      }
+      __syncwarp();
+      uint32_t* rows = MODE == MODE_FILL ? o.cols : o.temp;
+      if (write_ok) {
+        for (int l = 0; l < 32; ++l) {
+          const uint32_t len = __shfl_sync(0xffffffffu, mine, l);
+          const uint64_t off = __shfl_sync(0xffffffffu, dst, l);
+          if (len == 0) continue;
+          if (len <= 32) warp_sort_row_out<1>(srow, l, len, rows + off, lane);
+          else if (len <= 64) warp_sort_row_out<2>(srow, l, len, rows + off, lane);
+          else warp_sort_row_out<4>(srow, l, len, rows + off, lane);
+        }
+      }
+      __syncwarp();
+      const uint32_t lm = __ballot_sync(0xffffffffu, active && longrow);
+      if (lane == 0 && lm) atomicAdd(&g_qstats[7], (unsigned long long)__popc(lm));
+      for (int l = 0; l < 32; ++l) {
+        if (!((lm >> l) & 1u)) continue;
+        const uint32_t ql = __shfl_sync(0xffffffffu, qi, l);
+        const double xl = __shfl_sync(0xffffffffu, cx, l);
+        const double yl = __shfl_sync(0xffffffffu, cy, l);
+        const double zl = __shfl_sync(0xffffffffu, cz, l);
+        single_query<FLAVOR, MODE, CUBE>(t, ql, xl, yl, zl, r, lane, lt, o, wbuf);
       }
     }
     __syncwarp();
   }
 }
 
-// Rows longer than the per-warp buffer: one block per row (persistent).
-__global__ void __launch_bounds__(1024) big_row_sort_kernel(const uint64_t* __restrict__ row_ptr,
-                                                            uint32_t* __restrict__ cols,
-                                                            const uint32_t* __restrict__ big_rows,
+// Rows too long for a warp buffer: one block per row (persistent blocks).
+__global__ void __launch_bounds__(1024) big_row_sort_kernel(uint32_t* __restrict__ rows,
+                                                            const uint64_t* __restrict__ big_off,
+                                                            const uint32_t* __restrict__ big_len,
                                                             const uint32_t* __restrict__ n_big) {
   extern __shared__ uint32_t sm[];
   const uint32_t nb = *n_big;
-  for (uint32_t b = blockIdx.x; b < nb; b += gridDim.x) {
-    const uint32_t qi = big_rows[b];
-    const uint64_t beg = row_ptr[qi];
-    const uint32_t len = (uint32_t)(row_ptr[qi + 1] - beg);
-    uint32_t* row = cols + beg;
+  for (uint32_t bi = blockIdx.x; bi < nb; bi += gridDim.x) {
+    uint32_t* row = rows + big_off[bi];
+    const uint32_t len = big_len[bi];
     if (len <= (uint32_t)kBigSmemCap) {
       for (uint32_t x = threadIdx.x; x < len; x += blockDim.x) sm[x] = row[x];
       __syncthreads();
@@ -484,6 +573,22 @@ __global__ void __launch_bounds__(1024) big_row_sort_kernel(const uint64_t* __re
       bitonic_sort(row, len, threadIdx.x, blockDim.x, [] { __syncthreads(); });
     }
     __syncthreads();
+  }
+}
+
+// Arena rows -> CSR order (a warp per query, coalesced copies).
+__global__ void gather_rows_kernel(const uint32_t* __restrict__ temp,
+                                   const uint64_t* __restrict__ toff,
+                                   const uint32_t* __restrict__ counts,
+                                   const uint64_t* __restrict__ row_ptr,
+                                   uint32_t* __restrict__ cols, uint64_t nq) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t W = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t q = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); q < nq; q += W) {
+    const uint32_t len = __ldg(counts + q);
+    const uint32_t* src = temp + __ldg(toff + q);
+    uint32_t* dst = cols + __ldg(row_ptr + q);
+    for (uint32_t i = lane; i < len; i += 32) dst[i] = __ldg(src + i);
   }
 }
 
@@ -504,11 +609,9 @@ cm_status order_typed(const cm_index* ix, const double* q, uint64_t nq, cudaStre
 
 template <int MODE>
 cm_status launch_radius(const cm_index* ix, const double* q, uint64_t nq, int kernel, double r,
-                        const uint32_t* perm, uint32_t* counts, uint64_t* tested,
-                        uint64_t* digests, const uint64_t* row_ptr, uint32_t* cols,
-                        uint32_t* big_rows, uint32_t* n_big, cudaStream_t st) {
+                        const uint32_t* perm, const Out& o, cudaStream_t st) {
   const Tables t = ix->tables();
-  const size_t smem = MODE == MODE_FILL ? (size_t)kQWarps * kFillWarpBytes : 0;
+  const size_t smem = (size_t)kQWarps * kRowWarpBytes;
   auto run = [&](auto kern) -> cm_status {
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -518,8 +621,7 @@ cm_status launch_radius(const cm_index* ix, const double* q, uint64_t nq, int ke
     const uint64_t need = ((nq + 31) / 32 + kQWarps - 1) / kQWarps;
     const unsigned grid =
         (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(need, (uint64_t)sm_count() * per_sm));
-    kern<<<grid, kQThreads, smem, st>>>(t, q, nq, r, perm, counts, tested, digests, row_ptr, cols,
-                                        big_rows, n_big); ::cmg::note_launch();
+    kern<<<grid, kQThreads, smem, st>>>(t, q, nq, r, perm, o); ::cmg::note_launch();
     CM_CUDA_TRY(cudaGetLastError());
     return CM_OK;
   };
@@ -536,14 +638,42 @@ cm_status launch_radius(const cm_index* ix, const double* q, uint64_t nq, int ke
   }
 }
 
+cm_status sort_big_rows(uint32_t* rows, const Out& o, cudaStream_t st) {
+  const int smem = kBigSmemCap * 4;
+  cudaFuncSetAttribute(big_row_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  big_row_sort_kernel<<<sm_count(), 1024, smem, st>>>(rows, o.big_off, o.big_len, o.n_big); ::cmg::note_launch();
+  CM_CUDA_TRY(cudaGetLastError());
+  return CM_OK;
+}
+
+struct BigRows {
+  uint64_t* off = nullptr;
+  uint32_t* len = nullptr;
+  uint32_t* n = nullptr;
+  cudaStream_t st = nullptr;
+  cm_status init(uint64_t nq, cudaStream_t s) {
+    st = s;
+    CM_CUDA_TRY(dev_alloc_t(&off, nq, s));
+    CM_CUDA_TRY(dev_alloc_t(&len, nq, s));
+    CM_CUDA_TRY(dev_alloc_t(&n, 1, s));
+    CM_CUDA_TRY(cudaMemsetAsync(n, 0, 4, s));
+    return CM_OK;
+  }
+  ~BigRows() {
+    dev_free(off, st);
+    dev_free(len, st);
+    dev_free(n, st);
+  }
+};
+
 }  // namespace
 
 void query_stats(uint64_t* out, int reset) {
-  unsigned long long h[4];
+  unsigned long long h[8];
   cudaMemcpyFromSymbol(h, g_qstats, sizeof(h));
-  for (int i = 0; i < 4; ++i) out[i] = h[i];
+  for (int i = 0; i < 8; ++i) out[i] = h[i];
   if (reset) {
-    const unsigned long long z[4] = {0, 0, 0, 0};
+    const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     cudaMemcpyToSymbol(g_qstats, z, sizeof(z));
   }
 }
@@ -562,46 +692,72 @@ cm_status radius_count_dev(const cm_index* ix, const double* q, uint64_t nq, int
                            const uint32_t* perm, uint32_t* counts, uint64_t* tested,
                            cudaStream_t st) {
   if (nq == 0) return CM_OK;
-  return launch_radius<MODE_COUNT>(ix, q, nq, kernel, r, perm, counts, tested, nullptr, nullptr,
-                                   nullptr, nullptr, nullptr, st);
+  Out o{};
+  o.counts = counts;
+  o.tested = tested;
+  return launch_radius<MODE_COUNT>(ix, q, nq, kernel, r, perm, o, st);
 }
 
 cm_status radius_digest_dev(const cm_index* ix, const double* q, uint64_t nq, int kernel, double r,
                             const uint32_t* perm, uint32_t* counts, uint64_t* digests,
                             cudaStream_t st) {
   if (nq == 0) return CM_OK;
-  return launch_radius<MODE_DIGEST>(ix, q, nq, kernel, r, perm, counts, nullptr, digests, nullptr,
-                                    nullptr, nullptr, nullptr, st);
+  Out o{};
+  o.counts = counts;
+  o.digests = digests;
+  return launch_radius<MODE_DIGEST>(ix, q, nq, kernel, r, perm, o, st);
 }
 
 cm_status radius_fill_dev(const cm_index* ix, const double* q, uint64_t nq, int kernel, double r,
                           const uint32_t* perm, const uint64_t* row_ptr, uint32_t* cols,
                           cudaStream_t st, cudaEvent_t after_fill) {
   if (nq == 0) return CM_OK;
-  uint32_t* big = nullptr;
-  uint32_t* nbig = nullptr;
-  CM_CUDA_TRY(dev_alloc_t(&big, nq, st));
-  CM_CUDA_TRY(dev_alloc_t(&nbig, 1, st));
-  CM_CUDA_TRY(cudaMemsetAsync(nbig, 0, 4, st));
-  cm_status s = launch_radius<MODE_FILL>(ix, q, nq, kernel, r, perm, nullptr, nullptr, nullptr,
-                                         row_ptr, cols, big, nbig, st);
+  BigRows big;
+  cm_status s = big.init(nq, st);
+  if (s != CM_OK) return s;
+  Out o{};
+  o.row_ptr = row_ptr;
+  o.cols = cols;
+  o.big_off = big.off;
+  o.big_len = big.len;
+  o.n_big = big.n;
+  s = launch_radius<MODE_FILL>(ix, q, nq, kernel, r, perm, o, st);
   if (after_fill) cudaEventRecord(after_fill, st);
-  if (s == CM_OK) {
-    static bool configured = false;
-    const int smem = kBigSmemCap * 4;
-    if (!configured) {
-      cudaFuncSetAttribute(big_row_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      configured = true;
-    }
-    big_row_sort_kernel<<<sm_count(), 1024, smem, st>>>(row_ptr, cols, big, nbig); ::cmg::note_launch();
-    if (cudaGetLastError() != cudaSuccess) {
-      set_error("big_row_sort_kernel launch failed");
-      s = CM_CUDA;
-    }
-  }
-  dev_free(big, st);
-  dev_free(nbig, st);
+  if (s == CM_OK) s = sort_big_rows(cols, o, st);
   return s;
+}
+
+cm_status radius_collect_dev(const cm_index* ix, const double* q, uint64_t nq, int kernel,
+                             double r, const uint32_t* perm, uint32_t* temp, uint64_t cap,
+                             uint64_t* toff, uint32_t* counts, unsigned long long* cursor,
+                             cudaStream_t st, cudaEvent_t after_collect) {
+  if (nq == 0) return CM_OK;
+  BigRows big;
+  cm_status s = big.init(nq, st);
+  if (s != CM_OK) return s;
+  CM_CUDA_TRY(cudaMemsetAsync(cursor, 0, 8, st));
+  Out o{};
+  o.counts = counts;
+  o.temp = temp;
+  o.cap = cap;
+  o.toff = toff;
+  o.cursor = cursor;
+  o.big_off = big.off;
+  o.big_len = big.len;
+  o.n_big = big.n;
+  s = launch_radius<MODE_COLLECT>(ix, q, nq, kernel, r, perm, o, st);
+  if (after_collect) cudaEventRecord(after_collect, st);
+  if (s == CM_OK) s = sort_big_rows(temp, o, st);
+  return s;
+}
+
+cm_status gather_rows_dev(const uint32_t* temp, const uint64_t* toff, const uint32_t* counts,
+                          const uint64_t* row_ptr, uint32_t* cols, uint64_t nq, cudaStream_t st) {
+  if (nq == 0) return CM_OK;
+  const unsigned grid = (unsigned)std::min<uint64_t>((nq + 7) / 8, (uint64_t)sm_count() * 16);
+  gather_rows_kernel<<<grid, 256, 0, st>>>(temp, toff, counts, row_ptr, cols, nq); ::cmg::note_launch();
+  CM_CUDA_TRY(cudaGetLastError());
+  return CM_OK;
 }
 
 cm_status counts_to_row_ptr(const uint32_t* counts, uint64_t nq, uint64_t* row_ptr,

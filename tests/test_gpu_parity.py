@@ -102,3 +102,43 @@ def test_corruption_detected(cfg0, cfg0_oracle):
         cnt, dig = cm.radius_digest_batch(m, cloud, 1.0)
         ocnt, odig = cfg0_oracle.radius(cloud, 0, 1.0)
         assert not (np.array_equal(cnt, ocnt) and np.array_equal(dig, odig))
+
+
+def test_arena_overflow_falls_back(cfg0, cfg0_oracle):
+    """A small-radius call shrinks the arena estimate; the next, larger query
+    overflows it and must take the two-pass path with identical results."""
+    from paper_2502_11602_b200 import _native
+    cloud, q = cfg0
+    q = q[:20000]
+    m = cm.Cheesemap.build(cloud, cm.BuildOptions(flavor=cm.Flavor.Mixed))
+    cm.radius_search_batch(m, q, 0.05, cm.SPHERE)
+    row, cols = cm.radius_search_batch(m, q, 3.0, cm.SPHERE)
+    assert _native.last_query_timing()["two_pass"] == 1
+    orow, ocols = cfg0_oracle.radius_csr(q, 0, 3.0)
+    assert np.array_equal(row, orow) and np.array_equal(cols, ocols)
+    row, cols = cm.radius_search_batch(m, q, 3.0, cm.SPHERE)
+    assert _native.last_query_timing()["two_pass"] == 0
+    assert np.array_equal(row, orow) and np.array_equal(cols, ocols)
+
+
+@pytest.mark.parametrize("flavor", FLAVORS)
+def test_count_then_fill_api(cfg0, cfg0_oracle, flavor):
+    """The two-call CSR API (cm_radius_count, caller scan, cm_radius_fill)."""
+    import ctypes
+    from paper_2502_11602_b200 import _native
+    cloud, q = cfg0
+    q = np.ascontiguousarray(q[:30000])
+    m = cm.Cheesemap.build(cloud, cm.BuildOptions(flavor=flavor))
+    L = _native.lib()
+    counts = np.zeros(q.shape[0], dtype=np.uint32)
+    qp = q.ctypes.data_as(ctypes.c_void_p)
+    cm._check(L.cm_radius_count(m.handle, qp, q.shape[0], 1, 1.5,
+                                counts.ctypes.data_as(ctypes.c_void_p), None, None))
+    row = np.zeros(q.shape[0] + 1, dtype=np.uint64)
+    np.cumsum(counts, out=row[1:])
+    cols = np.zeros(int(row[-1]), dtype=np.uint32)
+    cm._check(L.cm_radius_fill(m.handle, qp, q.shape[0], 1, 1.5,
+                               row.ctypes.data_as(ctypes.c_void_p),
+                               cols.ctypes.data_as(ctypes.c_void_p), None))
+    orow, ocols = cfg0_oracle.radius_csr(q, 1, 1.5)
+    assert np.array_equal(row, orow) and np.array_equal(cols, ocols)
