@@ -422,6 +422,7 @@ uint64_t orc_non_empty(const orc_index* m) { return m->non_empty; }
 // densifies iff (double)non_empty / (double)(nx*ny) >= tau (map.cpp:106-108);
 // non_empty only grows, so the final flag is the test on the final count.
 uint64_t orc_slice_flags(const orc_index* m, uint8_t* dense, uint64_t* non_empty) {
+  if (m->flavor != 2) return 0;  // slices are reported for the mixed flavour only
   const double fp = static_cast<double>(m->g.n[0] * m->g.n[1]);
   for (std::uint64_t k = 0; k < m->slice_non_empty.size(); ++k) {
     if (non_empty) non_empty[k] = m->slice_non_empty[k];

@@ -17,6 +17,7 @@
 #include <thread>
 #include <vector>
 
+#include "cheesemap/io.hpp"
 #include "cheesemap/map.hpp"
 #include "cheesemap/search.hpp"
 
@@ -89,6 +90,25 @@ std::vector<PointHandle> run_kernel(const Cheesemap& m, int kernel, const Point3
 }  // namespace
 
 extern "C" {
+
+// The reference's own UniformBox generator (io.cpp:252-272), to pin the RNG
+// conventions the BASELINE-config generators reuse.
+int ref_generate_uniform(uint64_t seed, uint64_t n, double ex, double ey, double ez, double* out) {
+  SyntheticSpec spec;
+  spec.kind = SyntheticSpec::Kind::UniformBox;
+  spec.count = n;
+  spec.extent_x = ex;
+  spec.extent_y = ey;
+  spec.extent_z = ez;
+  spec.seed = seed;
+  try {
+    const PointCloud c = generate(spec);
+    std::memcpy(out, c.data(), n * sizeof(Point3));
+  } catch (const std::exception& e) {
+    return status_of(e);
+  }
+  return 0;
+}
 
 int ref_build(const double* xyz, uint64_t n, int flavor, int mode, double cx, double cy,
               double cz, double tau, uint64_t dense_cap, ref_index** out) {

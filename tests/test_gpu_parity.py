@@ -37,9 +37,10 @@ def test_build_parity_cfg0(cfg0, flavor):
     assert np.array_equal(hs.astype(np.uint64), ohs)
     occ = m.occupancy_stats()
     assert occ["non_empty"] == ref.non_empty()
-    dense, ne = ref.slice_flags()
-    assert np.array_equal(occ["slice_dense"], dense)
-    assert np.array_equal(occ["slice_non_empty"], ne)
+    if flavor == cm.Flavor.Mixed:  # the reference reports slices for mixed maps
+        dense, ne = ref.slice_flags()
+        assert np.array_equal(occ["slice_dense"], dense)
+        assert np.array_equal(occ["slice_non_empty"], ne)
 
 
 @pytest.mark.parametrize("flavor", FLAVORS)
