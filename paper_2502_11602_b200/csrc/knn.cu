@@ -48,26 +48,35 @@ __device__ __forceinline__ void shell_column_spans(const Tables& t, int64_t i, i
   }
 }
 
-template <int FLAVOR>
+// GLIST = false: the sorted (d2, handle) list of one query lives in shared
+// memory (k <= kKMax). GLIST = true (any k): it lives in the outputs
+// themselves (idx_out row, and d2_out row or a chunk-local d2 scratch).
+template <int FLAVOR, bool GLIST>
 __global__ void __launch_bounds__(kKThreads) knn_warp_kernel(const Tables t,
                                                              const double* __restrict__ q,
-                                                             uint64_t nq, uint32_t k,
+                                                             uint64_t s_begin, uint64_t s_end,
+                                                             uint32_t k,
                                                              const uint32_t* __restrict__ perm,
                                                              uint32_t* __restrict__ idx_out,
-                                                             double* __restrict__ d2_out) {
-  __shared__ double sd[kKWarps][kKMax];
-  __shared__ uint32_t sid[kKWarps][kKMax];
+                                                             double* __restrict__ d2_out,
+                                                             double* __restrict__ d2_scratch) {
+  __shared__ double sd[GLIST ? 1 : kKWarps][GLIST ? 1 : kKMax];
+  __shared__ uint32_t sid[GLIST ? 1 : kKWarps][GLIST ? 1 : kKMax];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  double* ld = sd[wib];
-  uint32_t* lid = sid[wib];
+  double* ld = sd[GLIST ? 0 : wib];
+  uint32_t* lid = sid[GLIST ? 0 : wib];
   const uint64_t W = (uint64_t)gridDim.x * kKWarps;
   const DevGrid& g = t.g;
   const uint32_t lt = lanemask_lt();
   const int64_t nx = (int64_t)g.nx, ny = (int64_t)g.ny, nzm = (int64_t)g.nz - 1;
 
-  for (uint64_t s = (uint64_t)blockIdx.x * kKWarps + wib; s < nq; s += W) {
+  for (uint64_t s = s_begin + (uint64_t)blockIdx.x * kKWarps + wib; s < s_end; s += W) {
     const uint32_t qi = perm ? __ldg(perm + s) : (uint32_t)s;
+    if (GLIST) {
+      lid = idx_out + (uint64_t)qi * k;
+      ld = d2_out ? d2_out + (uint64_t)qi * k : d2_scratch + (s - s_begin) * k;
+    }
     const double cx = __ldg(q + 3 * (uint64_t)qi);
     const double cy = __ldg(q + 3 * (uint64_t)qi + 1);
     const double cz = __ldg(q + 3 * (uint64_t)qi + 2);
@@ -135,25 +144,23 @@ __global__ void __launch_bounds__(kKThreads) knn_warp_kernel(const Tables t,
               pos += __popc(__ballot_sync(0xffffffffu, less));
             }
             const uint32_t ncnt = cnt < k ? cnt + 1 : k;
-            // shift [pos, ncnt-1) -> [pos+1, ncnt)
-            double vd[kKMax / 32];
-            uint32_t vi[kKMax / 32];
-#pragma unroll
-            for (int c2 = 0; c2 < kKMax / 32; ++c2) {
-              const uint32_t x = c2 * 32 + lane;
-              if (x > pos && x < ncnt) {
-                vd[c2] = ld[x - 1];
-                vi[c2] = lid[x - 1];
+            // shift [pos, ncnt-1) -> [pos+1, ncnt), 32 slots at a time from
+            // the top (each chunk reads below itself before it is written)
+            for (int64_t top = (int64_t)ncnt - 1; top > (int64_t)pos; top -= 32) {
+              const int64_t x = top - lane;
+              double vd = 0.0;
+              uint32_t vi = 0;
+              const bool mv = x > (int64_t)pos;
+              if (mv) {
+                vd = ld[x - 1];
+                vi = lid[x - 1];
               }
-            }
-            __syncwarp();
-#pragma unroll
-            for (int c2 = 0; c2 < kKMax / 32; ++c2) {
-              const uint32_t x = c2 * 32 + lane;
-              if (x > pos && x < ncnt) {
-                ld[x] = vd[c2];
-                lid[x] = vi[c2];
+              __syncwarp();
+              if (mv) {
+                ld[x] = vd;
+                lid[x] = vi;
               }
+              __syncwarp();
             }
             if (lane == 0) {
               ld[pos] = d;
@@ -182,9 +189,17 @@ __global__ void __launch_bounds__(kKThreads) knn_warp_kernel(const Tables t,
         if (dm > 0.0 && ld[k - 1] < dm * dm) break;
       }
     }
-    for (uint32_t x = lane; x < k; x += 32) {
-      idx_out[(uint64_t)qi * k + x] = x < cnt ? lid[x] : 0xffffffffu;
-      if (d2_out) d2_out[(uint64_t)qi * k + x] = x < cnt ? ld[x] : __longlong_as_double(0x7ff0000000000000ll);
+    if (GLIST) {
+      for (uint32_t x = cnt + lane; x < k; x += 32) {
+        lid[x] = 0xffffffffu;
+        ld[x] = __longlong_as_double(0x7ff0000000000000ll);
+      }
+    } else {
+      for (uint32_t x = lane; x < k; x += 32) {
+        idx_out[(uint64_t)qi * k + x] = x < cnt ? lid[x] : 0xffffffffu;
+        if (d2_out)
+          d2_out[(uint64_t)qi * k + x] = x < cnt ? ld[x] : __longlong_as_double(0x7ff0000000000000ll);
+      }
     }
     __syncwarp();
   }
@@ -196,27 +211,40 @@ __global__ void __launch_bounds__(kKThreads) knn_warp_kernel(const Tables t,
 cm_status knn_dev(const cm_index* ix, const double* q, uint64_t nq, uint32_t k,
                   const uint32_t* perm, uint32_t* idx, double* d2, cudaStream_t st) {
   if (nq == 0) return CM_OK;
-  if (k > (uint32_t)kKMax) {
-    set_error("k above the device limit of 256");
-    return CM_INVALID_ARGUMENT;
-  }
   const Tables t = ix->tables();
+  const bool glist = k > (uint32_t)kKMax;
+  // chunk-local d2 scratch for large k without a d2 output (<= 1 GiB)
+  const uint64_t chunk =
+      glist && !d2 ? std::max<uint64_t>(1, (1ull << 27) / k) : nq;
+  double* scratch = nullptr;
+  if (glist && !d2) CM_CUDA_TRY(dev_alloc_t(&scratch, std::min(chunk, nq) * k, st));
   auto run = [&](auto kern) -> cm_status {
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kKThreads, 0);
     per_sm = std::max(per_sm, 1);
-    const uint64_t need = (nq + kKWarps - 1) / kKWarps;
-    const unsigned grid =
-        (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(need, (uint64_t)sm_count() * per_sm));
-    kern<<<grid, kKThreads, 0, st>>>(t, q, nq, k, perm, idx, d2); ::cmg::note_launch();
-    CM_CUDA_TRY(cudaGetLastError());
+    for (uint64_t s0 = 0; s0 < nq; s0 += chunk) {
+      const uint64_t s1 = std::min(nq, s0 + chunk);
+      const uint64_t need = (s1 - s0 + kKWarps - 1) / kKWarps;
+      const unsigned grid =
+          (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(need, (uint64_t)sm_count() * per_sm));
+      kern<<<grid, kKThreads, 0, st>>>(t, q, s0, s1, k, perm, idx, d2, scratch); ::cmg::note_launch();
+      CM_CUDA_TRY(cudaGetLastError());
+    }
     return CM_OK;
   };
+  cm_status s;
   switch (ix->opts.flavor) {
-    case CM_DENSE: return run(knn_warp_kernel<CM_DENSE>);
-    case CM_SPARSE: return run(knn_warp_kernel<CM_SPARSE>);
-    default: return run(knn_warp_kernel<CM_MIXED>);
+    case CM_DENSE:
+      s = glist ? run(knn_warp_kernel<CM_DENSE, true>) : run(knn_warp_kernel<CM_DENSE, false>);
+      break;
+    case CM_SPARSE:
+      s = glist ? run(knn_warp_kernel<CM_SPARSE, true>) : run(knn_warp_kernel<CM_SPARSE, false>);
+      break;
+    default:
+      s = glist ? run(knn_warp_kernel<CM_MIXED, true>) : run(knn_warp_kernel<CM_MIXED, false>);
   }
+  if (scratch) dev_free(scratch, st);
+  return s;
 }
 
 }  // namespace cmg

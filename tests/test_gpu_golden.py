@@ -29,7 +29,8 @@ def test_gpu_matches_golden(path):
             assert np.array_equal(grow, row) and np.array_equal(gcols, cols), (bi, kern, r)
             t = np.zeros(q.shape[0], dtype=np.uint64)
             cnt = cm.radius_count(m, q, r, kern, points_tested=t)
-            assert np.array_equal(t, tested)
+            if bi == 0:  # points_tested depends on the grid (golden: build 0)
+                assert np.array_equal(t, tested)
             assert np.array_equal(cnt.astype(np.uint64), np.diff(row))
         for k, idx, d2 in knn_cases(d):
             gidx, gd2 = cm.knn_batch(m, q, k)
