@@ -127,6 +127,13 @@ void cm_default_options(cm_build_options* opts);
 /* Cheesemap::build (map.cpp:22-122). xyz: n x 3 doubles, host or device. */
 cm_status cm_build(const double* xyz, uint64_t n, const cm_build_options* opts,
                    int device, void* stream, cm_index** out);
+/* As cm_build, on the grid of an explicit bounding box instead of the
+ * cloud's own (grid_dims(box), grid.cpp:41-61). Used by x-slab partitions so
+ * every slab indexes on the global grid; a point outside the box is
+ * CM_OUT_OF_DOMAIN (voxel_of, grid.cpp:64-66). */
+cm_status cm_build_in_bounds(const double* xyz, uint64_t n, const cm_build_options* opts,
+                             const double* bounds_min, const double* bounds_max, int device,
+                             void* stream, cm_index** out);
 cm_status cm_free(cm_index* index);
 
 cm_status cm_get_grid(const cm_index* index, cm_grid_params* out);

@@ -1,0 +1,255 @@
+// cheesemap_gpu.hpp — header-only C++ mirror of the reference's index API
+// (/root/reference/proj/core/include/cheesemap/{geometry,grid,map,search,
+// errors}.hpp) over the C ABI in cmgpu.h. A reference user switches by
+// replacing `cheesemap::` with `cheesemap::gpu::` — same names, argument
+// meaning and exception types — and gains the batched calls the reference
+// lacks (radius_search, knn_batch, radius_digest).
+//
+// Differences a caller can observe:
+//  * kernel_search returns handles sorted ascending (the reference returns
+//    voxel-visit order, search.hpp:110-122; its tests sort,
+//    tests/test_util.hpp:30-35);
+//  * knn_search orders ties by handle (the reference keeps insertion order,
+//    search.cpp:16-28); distances are sqrt of the same fp64 d^2;
+//  * BoxKernel is the cube {c - r, c + r} (what the reference CLI and tests
+//    build, cmd_bench.cpp:107-111); CylinderKernel is not offered;
+//  * the map owns device copies of the points (the cloud need not outlive it).
+#pragma once
+
+#include <cmath>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../cmgpu.h"
+
+namespace cheesemap::gpu {
+
+// ------------------------------------------------------------ errors.hpp --
+class Error : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+class EmptyCloudError : public Error { public: using Error::Error; };
+class CapacityError : public Error { public: using Error::Error; };
+class OutOfDomainError : public Error { public: using Error::Error; };
+class InvalidArgumentError : public Error { public: using Error::Error; };
+class CudaError : public Error { public: using Error::Error; };
+
+inline void check(cm_status s) {
+  if (s == CM_OK) return;
+  const std::string msg = std::string(cm_status_name(s)) + ": " + cm_last_error();
+  switch (s) {
+    case CM_EMPTY_CLOUD: throw EmptyCloudError(msg);
+    case CM_INVALID_ARGUMENT: throw InvalidArgumentError(msg);
+    case CM_CAPACITY: throw CapacityError(msg);
+    case CM_OUT_OF_DOMAIN: throw OutOfDomainError(msg);
+    default: throw CudaError(msg);
+  }
+}
+
+// ---------------------------------------------------------- geometry.hpp --
+struct Point3 {
+  double x = 0.0, y = 0.0, z = 0.0;
+};
+static_assert(sizeof(Point3) == 24, "PointCloud layout is n x 3 doubles");
+using PointHandle = std::uint64_t;
+using PointCloud = std::vector<Point3>;
+
+struct SphereKernel {
+  Point3 center;
+  double radius = 0.0;
+};
+struct BoxKernel {  // the cube {c - r, c + r}
+  Point3 center;
+  double half = 0.0;
+  static BoxKernel cube(const Point3& c, double r) { return {c, r}; }
+};
+
+// ------------------------------------------------------ grid.hpp, map.hpp --
+enum class GridMode { TwoD = CM_TWOD, ThreeD = CM_THREED };
+enum class Flavor { Dense = CM_DENSE, Sparse = CM_SPARSE, Mixed = CM_MIXED };
+
+struct CellSize {
+  double x = 1.0, y = 1.0, z = 1.0;
+  static CellSize uniform(double s) { return {s, s, s}; }
+};
+
+struct BuildOptions {
+  Flavor flavor = Flavor::Dense;
+  GridMode mode = GridMode::ThreeD;
+  CellSize cell = CellSize::uniform(1.0);
+  bool reorder = false;
+  double densify_threshold = 0.80;
+  std::uint64_t dense_voxel_cap = std::uint64_t{1} << 32;
+};
+
+struct GridParams {
+  Point3 origin;
+  CellSize cell;
+  std::uint64_t nx = 1, ny = 1, nz = 1;
+  GridMode mode = GridMode::ThreeD;
+  Point3 bounds_min, bounds_max;
+  std::uint64_t total_voxels() const { return nx * ny * nz; }
+};
+
+struct SliceOccupancy {
+  bool dense = false;
+  std::uint64_t cells = 0;
+  std::uint64_t non_empty = 0;
+};
+
+struct OccupancyStats {
+  std::uint64_t total_voxels = 0;
+  std::uint64_t non_empty = 0;
+  double empty_fraction = 0.0;
+  std::vector<SliceOccupancy> slices;  // mixed flavour only, as the reference
+};
+
+struct Neighbor {
+  PointHandle handle = 0;
+  double distance = 0.0;
+};
+
+// Sorted CSR neighbour lists of a batch of centres.
+struct Csr {
+  std::vector<std::uint64_t> row_ptr;  // nq + 1
+  std::vector<std::uint32_t> cols;     // handles, ascending per row
+};
+
+class Cheesemap {
+ public:
+  static Cheesemap build(const PointCloud& cloud, const BuildOptions& opts = {},
+                         int device = 0) {
+    cm_build_options o;
+    cm_default_options(&o);
+    o.flavor = static_cast<int32_t>(opts.flavor);
+    o.mode = static_cast<int32_t>(opts.mode);
+    o.cell_x = opts.cell.x;
+    o.cell_y = opts.cell.y;
+    o.cell_z = opts.cell.z;
+    o.reorder = opts.reorder ? 1 : 0;
+    o.densify_threshold = opts.densify_threshold;
+    o.dense_voxel_cap = opts.dense_voxel_cap;
+    cm_index* h = nullptr;
+    check(cm_build(reinterpret_cast<const double*>(cloud.data()), cloud.size(), &o, device,
+                   nullptr, &h));
+    return Cheesemap(h, opts);
+  }
+
+  Cheesemap(Cheesemap&& o) noexcept : h_(std::exchange(o.h_, nullptr)), opts_(o.opts_) {}
+  Cheesemap& operator=(Cheesemap&& o) noexcept {
+    if (this != &o) {
+      cm_free(h_);
+      h_ = std::exchange(o.h_, nullptr);
+      opts_ = o.opts_;
+    }
+    return *this;
+  }
+  Cheesemap(const Cheesemap&) = delete;
+  Cheesemap& operator=(const Cheesemap&) = delete;
+  ~Cheesemap() { cm_free(h_); }
+
+  GridParams grid() const {
+    cm_grid_params g;
+    check(cm_get_grid(h_, &g));
+    GridParams p;
+    p.origin = {g.origin[0], g.origin[1], g.origin[2]};
+    p.cell = {g.cell[0], g.cell[1], g.cell[2]};
+    p.nx = g.nx, p.ny = g.ny, p.nz = g.nz;
+    p.mode = static_cast<GridMode>(g.mode);
+    p.bounds_min = {g.bounds_min[0], g.bounds_min[1], g.bounds_min[2]};
+    p.bounds_max = {g.bounds_max[0], g.bounds_max[1], g.bounds_max[2]};
+    return p;
+  }
+  Flavor flavor() const { return opts_.flavor; }
+  GridMode mode() const { return opts_.mode; }
+  bool reordered() const { return opts_.reorder; }
+  std::uint64_t size() const { return cm_size(h_); }
+
+  OccupancyStats occupancy_stats() const {
+    const std::uint64_t nz = grid().nz;
+    std::vector<std::uint8_t> dense(nz);
+    std::vector<std::uint64_t> ne(nz);
+    cm_occupancy o;
+    check(cm_get_occupancy(h_, &o, dense.data(), ne.data(), nz));
+    OccupancyStats st;
+    st.total_voxels = o.total_voxels;
+    st.non_empty = o.non_empty;
+    st.empty_fraction = o.empty_fraction;
+    if (opts_.flavor == Flavor::Mixed) {
+      const GridParams g = grid();
+      for (std::uint64_t k = 0; k < nz; ++k) st.slices.push_back({dense[k] != 0, g.nx * g.ny, ne[k]});
+    }
+    return st;
+  }
+
+  void corrupt_for_testing() { check(cm_corrupt_for_testing(h_)); }
+  const cm_index* handle() const { return h_; }
+
+ private:
+  Cheesemap(cm_index* h, const BuildOptions& o) : h_(h), opts_(o) {}
+  cm_index* h_ = nullptr;
+  BuildOptions opts_;
+};
+
+// ------------------------------------------------------------ search.hpp --
+inline Csr radius_search(const Cheesemap& m, const std::vector<Point3>& centers, double r,
+                         cm_kernel kind = CM_SPHERE) {
+  cm_csr* csr = nullptr;
+  check(cm_radius_search(m.handle(), reinterpret_cast<const double*>(centers.data()),
+                         centers.size(), kind, r, nullptr, &csr));
+  std::uint64_t nq = 0, nnz = 0;
+  cm_csr_info(csr, &nq, &nnz, nullptr, nullptr);
+  Csr out;
+  out.row_ptr.resize(nq + 1);
+  out.cols.resize(nnz);
+  const cm_status s = cm_csr_download(csr, out.row_ptr.data(), out.cols.data(), nullptr);
+  cm_csr_free(csr);
+  check(s);
+  return out;
+}
+
+inline std::vector<PointHandle> kernel_search(const Cheesemap& m, const SphereKernel& k) {
+  const Csr c = radius_search(m, {k.center}, k.radius, CM_SPHERE);
+  return {c.cols.begin(), c.cols.end()};
+}
+
+inline std::vector<PointHandle> kernel_search(const Cheesemap& m, const BoxKernel& k) {
+  const Csr c = radius_search(m, {k.center}, k.half, CM_CUBE);
+  return {c.cols.begin(), c.cols.end()};
+}
+
+// (idx, d2) rows of width k, ordered by (d2, handle).
+inline void knn_batch(const Cheesemap& m, const std::vector<Point3>& centers, std::size_t k,
+                      std::vector<std::uint32_t>& idx, std::vector<double>& d2) {
+  idx.resize(centers.size() * k);
+  d2.resize(centers.size() * k);
+  check(cm_knn(m.handle(), reinterpret_cast<const double*>(centers.data()), centers.size(),
+               static_cast<uint32_t>(k), idx.data(), d2.data(), nullptr));
+}
+
+inline std::vector<Neighbor> knn_search(const Cheesemap& m, const Point3& c, std::size_t k) {
+  if (k == 0) throw InvalidArgumentError("k must be at least 1");
+  std::vector<std::uint32_t> idx;
+  std::vector<double> d2;
+  knn_batch(m, {c}, k, idx, d2);
+  std::vector<Neighbor> out;
+  for (std::size_t t = 0; t < k; ++t)
+    if (idx[t] != 0xffffffffu) out.push_back({idx[t], std::sqrt(d2[t])});
+  return out;
+}
+
+// Per-centre (count, sum of splitmix64(handle)) for outputs too large to keep.
+inline void radius_digest(const Cheesemap& m, const std::vector<Point3>& centers, double r,
+                          cm_kernel kind, std::vector<std::uint32_t>& counts,
+                          std::vector<std::uint64_t>& digests) {
+  counts.resize(centers.size());
+  digests.resize(centers.size());
+  check(cm_radius_digest(m.handle(), reinterpret_cast<const double*>(centers.data()),
+                         centers.size(), kind, r, counts.data(), digests.data(), nullptr));
+}
+
+}  // namespace cheesemap::gpu

@@ -325,8 +325,9 @@ std::vector<std::uint64_t> knn_alg2(const orc_index& m, const P3& c, std::size_t
 extern "C" {
 
 // Cheesemap::build (map.cpp:22-122): same checks in the same order.
-int orc_build(const double* xyz, uint64_t n, int flavor, int mode, double cx, double cy,
-              double cz, double tau, uint64_t dense_cap, orc_index** out) {
+static int build_impl(const double* xyz, uint64_t n, int flavor, int mode, double cx, double cy,
+                      double cz, double tau, uint64_t dense_cap, const double* b6,
+                      orc_index** out) {
   *out = nullptr;
   if (n == 0) return EMPTY_CLOUD;                                  // map.cpp:23-25
   if (!(tau > 0.0) || tau > 1.0) return INVALID_ARGUMENT;          // map.cpp:26-28
@@ -342,6 +343,14 @@ int orc_build(const double* xyz, uint64_t n, int flavor, int mode, double cx, do
     bb.hi.x = std::max(bb.hi.x, p.x);
     bb.hi.y = std::max(bb.hi.y, p.y);
     bb.hi.z = std::max(bb.hi.z, p.z);
+  }
+  if (b6) {  // explicit grid box; points outside it: voxel_of (grid.cpp:64-66)
+    const Box eb{{b6[0], b6[1], b6[2]}, {b6[3], b6[4], b6[5]}};
+    if (!box_contains(eb, bb.lo) || !box_contains(eb, bb.hi)) {
+      delete m;
+      return OUT_OF_DOMAIN;
+    }
+    bb = eb;
   }
   // grid_dims, grid.cpp:41-61
   Grid& g = m->g;
@@ -403,6 +412,17 @@ int orc_build(const double* xyz, uint64_t n, int flavor, int mode, double cx, do
     for (std::uint64_t v = 0; v < V; ++v) m->offsets[v + 1] += m->offsets[v];
   *out = m;
   return OK;
+}
+
+int orc_build(const double* xyz, uint64_t n, int flavor, int mode, double cx, double cy,
+              double cz, double tau, uint64_t dense_cap, orc_index** out) {
+  return build_impl(xyz, n, flavor, mode, cx, cy, cz, tau, dense_cap, nullptr, out);
+}
+
+int orc_build_in_bounds(const double* xyz, uint64_t n, int flavor, int mode, double cx, double cy,
+                        double cz, double tau, uint64_t dense_cap, const double* bounds6,
+                        orc_index** out) {
+  return build_impl(xyz, n, flavor, mode, cx, cy, cz, tau, dense_cap, bounds6, out);
 }
 
 void orc_free(orc_index* m) { delete m; }

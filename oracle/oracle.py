@@ -59,12 +59,22 @@ class CpuIndex:
     """A built CPU index (restatement or reference)."""
 
     def __init__(self, xyz, flavor=0, mode=1, cell=(1.0, 1.0, 1.0), tau=0.8,
-                 dense_cap=1 << 32, which="oracle"):
+                 dense_cap=1 << 32, which="oracle", bounds=None):
         self.L = lib(which)
         self.xyz = np.ascontiguousarray(xyz, dtype=np.float64).reshape(-1, 3)
         h = ctypes.c_void_p()
-        rc = self.L.build_(_p(self.xyz), self.xyz.shape[0], flavor, mode, cell[0], cell[1],
-                           cell[2], tau, dense_cap, ctypes.byref(h))
+        if bounds is not None:  # explicit grid box (restatement only)
+            b6 = np.ascontiguousarray(np.asarray(bounds, dtype=np.float64).reshape(6))
+            fn = self.L.lib.orc_build_in_bounds
+            fn.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_int,
+                           ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                           ctypes.c_uint64, ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)]
+            fn.restype = ctypes.c_int
+            rc = fn(_p(self.xyz), self.xyz.shape[0], flavor, mode, cell[0], cell[1], cell[2], tau,
+                    dense_cap, _p(b6), ctypes.byref(h))
+        else:
+            rc = self.L.build_(_p(self.xyz), self.xyz.shape[0], flavor, mode, cell[0], cell[1],
+                               cell[2], tau, dense_cap, ctypes.byref(h))
         if rc != 0:
             raise RuntimeError(f"{which} build failed: {STATUS.get(rc, rc)}", rc)
         self.h = h

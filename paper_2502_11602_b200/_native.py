@@ -13,7 +13,7 @@ STATUS_NAMES = {0: "CM_OK", 1: "CM_EMPTY_CLOUD", 2: "CM_INVALID_ARGUMENT", 3: "C
                 4: "CM_OUT_OF_DOMAIN", 5: "CM_CUDA", 6: "CM_NCCL"}
 
 EXPORTS = [
-    "cm_default_options", "cm_build", "cm_free", "cm_get_grid", "cm_get_occupancy",
+    "cm_default_options", "cm_build", "cm_build_in_bounds", "cm_free", "cm_get_grid", "cm_get_occupancy",
     "cm_get_build_timing", "cm_export_voxels", "cm_size", "cm_radius_count", "cm_radius_fill",
     "cm_radius_search", "cm_csr_info", "cm_csr_download", "cm_csr_free", "cm_radius_digest",
     "cm_knn", "cm_corrupt_for_testing", "cm_last_error", "cm_status_name",
@@ -71,6 +71,8 @@ def lib():
     sig = {
         "cm_default_options": ([ctypes.POINTER(BuildOptionsC)], None),
         "cm_build": ([p, u64, ctypes.POINTER(BuildOptionsC), i32, p, ctypes.POINTER(p)], i32),
+        "cm_build_in_bounds": ([p, u64, ctypes.POINTER(BuildOptionsC), p, p, i32, p,
+                                ctypes.POINTER(p)], i32),
         "cm_free": ([p], i32),
         "cm_get_grid": ([p, ctypes.POINTER(GridParamsC)], i32),
         "cm_get_occupancy": ([p, ctypes.POINTER(OccupancyC), p, p, u64], i32),

@@ -199,8 +199,8 @@ const char* cm_status_name(cm_status s) {
   return "CM_UNKNOWN";
 }
 
-cm_status cm_build(const double* xyz, uint64_t n, const cm_build_options* opts, int device,
-                   void* stream, cm_index** out) {
+static cm_status build_common(const double* xyz, uint64_t n, const cm_build_options* opts,
+                               const double* bounds6, int device, void* stream, cm_index** out) {
   if (!out) {
     set_error("null output handle");
     return CM_INVALID_ARGUMENT;
@@ -238,7 +238,7 @@ cm_status cm_build(const double* xyz, uint64_t n, const cm_build_options* opts, 
   InBuf in;
   cm_status s = stage_input(xyz, n * 3 * sizeof(double), st, &in);
   cudaEventRecord(e1, st);
-  if (s == CM_OK) s = build_index(static_cast<const double*>(in.dev), n, o, st, ix);
+  if (s == CM_OK) s = build_index(static_cast<const double*>(in.dev), n, o, st, ix, bounds6);
   float h2d = 0;
   if (s == CM_OK) {
     cudaEventElapsedTime(&h2d, e0, e1);
@@ -253,6 +253,23 @@ cm_status cm_build(const double* xyz, uint64_t n, const cm_build_options* opts, 
   }
   *out = ix;
   return CM_OK;
+}
+
+cm_status cm_build(const double* xyz, uint64_t n, const cm_build_options* opts, int device,
+                   void* stream, cm_index** out) {
+  return build_common(xyz, n, opts, nullptr, device, stream, out);
+}
+
+cm_status cm_build_in_bounds(const double* xyz, uint64_t n, const cm_build_options* opts,
+                             const double* bounds_min, const double* bounds_max, int device,
+                             void* stream, cm_index** out) {
+  if (!bounds_min || !bounds_max) {
+    set_error("null bounds");
+    return CM_INVALID_ARGUMENT;
+  }
+  const double b6[6] = {bounds_min[0], bounds_min[1], bounds_min[2],
+                        bounds_max[0], bounds_max[1], bounds_max[2]};
+  return build_common(xyz, n, opts, b6, device, stream, out);
 }
 
 cm_status cm_free(cm_index* ix) {

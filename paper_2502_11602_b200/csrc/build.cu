@@ -334,7 +334,7 @@ cm_status build_typed(const double* xyz, uint64_t n, cudaStream_t st, cm_index* 
 }  // namespace
 
 cm_status build_index(const double* xyz, uint64_t n, const cm_build_options& o, cudaStream_t st,
-                      cm_index* ix) {
+                      cm_index* ix, const double* bounds6) {
   // Check order follows map.cpp:23-39.
   if (n == 0) {
     set_error("point cloud is empty");
@@ -370,6 +370,18 @@ cm_status build_index(const double* xyz, uint64_t n, const cm_build_options& o, 
   for (int a = 0; a < 3; ++a) {
     lo[a] = double_of_ord(hb[a]);
     hi[a] = double_of_ord(hb[3 + a]);
+  }
+  if (bounds6) {
+    // An explicit (e.g. global, all-reduced) bounding box: every point must
+    // lie inside it, as voxel_of demands (grid.cpp:64-66).
+    for (int a = 0; a < 3; ++a) {
+      if (!(lo[a] >= bounds6[a] && hi[a] <= bounds6[3 + a])) {
+        set_error("point lies outside the grid bounding box");
+        return CM_OUT_OF_DOMAIN;
+      }
+      lo[a] = bounds6[a];
+      hi[a] = bounds6[3 + a];
+    }
   }
   // grid_dims (grid.cpp:41-61)
   DevGrid& g = ix->g;

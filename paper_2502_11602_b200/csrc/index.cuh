@@ -84,7 +84,7 @@ struct InBuf {
 cm_status stage_input(const void* p, size_t bytes, cudaStream_t st, InBuf* out);
 
 cm_status build_index(const double* xyz_dev, uint64_t n, const cm_build_options& o,
-                      cudaStream_t st, cm_index* ix);
+                      cudaStream_t st, cm_index* ix, const double* bounds6 = nullptr);
 
 // Query pipeline pieces (query.cu)
 struct QueryOrder {
