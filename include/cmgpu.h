@@ -162,6 +162,18 @@ cm_status cm_radius_fill(const cm_index* index, const double* q, uint64_t nq,
  * the returned cm_csr. */
 cm_status cm_radius_search(const cm_index* index, const double* q, uint64_t nq,
                            int kernel, double r, void* stream, cm_csr** out);
+/* The same search with HOST buffers end to end: queries from host memory,
+ * the sorted CSR to host memory (row_ptr: nq + 1 entries; cols: up to
+ * cols_capacity). With CMGPU_CHUNKS=K in the environment, queries are
+ * processed in K chunks on three streams so the host->device copy of chunk
+ * i+1 and the device->host copy of chunk i-1 overlap chunk i's kernels (use
+ * pinned host buffers); worthwhile only for spatially coherent query order.
+ * *nnz_out = total neighbours; CM_CAPACITY if cols_capacity was too small
+ * (nothing past the capacity is written). Synchronous. */
+cm_status cm_radius_search_to_host(const cm_index* index, const double* q_host, uint64_t nq,
+                                   int kernel, double r, uint64_t* row_ptr_host,
+                                   uint32_t* cols_host, uint64_t cols_capacity,
+                                   uint64_t* nnz_out, void* stream);
 cm_status cm_csr_info(const cm_csr* csr, uint64_t* nq, uint64_t* nnz,
                       const uint64_t** row_ptr_device, const uint32_t** cols_device);
 /* row_ptr (nq + 1) and cols (nnz) to caller memory (host or device). */

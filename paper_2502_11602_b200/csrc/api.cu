@@ -1,6 +1,9 @@
 // C ABI (include/cmgpu.h): argument checks, host/device staging, ownership.
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -358,6 +361,11 @@ __global__ void corrupt_kernel(uint32_t* ustart, uint32_t* dense_off, uint64_t f
     }
   }
 }
+__global__ void add_offset_kernel(uint64_t* v, uint64_t n, uint64_t off) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    v[i] += off;
+}
 }  // namespace apik
 }  // namespace cmg
 
@@ -491,49 +499,82 @@ cm_status cm_get_last_query_timing(cm_query_timing* o) {
   return CM_OK;
 }
 
-cm_status cm_radius_search(const cm_index* ix, const double* q, uint64_t nq, int kernel, double r,
-                           void* stream, cm_csr** out) {
-  CM_TRY(check_index(ix));
-  CM_TRY(check_kernel(kernel));
-  if (!out || (nq && !q)) {
-    set_error("null query or output pointer");
-    return CM_INVALID_ARGUMENT;
+}  // extern "C"
+
+namespace cmg {
+namespace apik {
+// A small device value -> host without the copy engines (which may be busy
+// with large device->host copies queued on other streams): a one-thread
+// kernel stores it into mapped pinned host memory.
+__global__ void publish_u64_kernel(const unsigned long long* src, volatile unsigned long long* dst) {
+  *dst = *src;
+  __threadfence_system();
+}
+}  // namespace apik
+}  // namespace cmg
+
+namespace {
+struct MappedSlot {
+  unsigned long long* host = nullptr;
+  unsigned long long* dev = nullptr;
+  cudaEvent_t ev = nullptr;
+  bool ok = false;
+  MappedSlot() {
+    if (cudaHostAlloc(&host, 64, cudaHostAllocMapped) == cudaSuccess &&
+        cudaHostGetDevicePointer(reinterpret_cast<void**>(&dev), host, 0) == cudaSuccess &&
+        cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess)
+      ok = true;
+    else
+      cudaGetLastError();
   }
-  *out = nullptr;
-  DeviceGuard dg(ix->device);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  InBuf in;
-  CM_TRY(stage_input(q, nq * 24, st, &in));
-  const double* qd = static_cast<const double*>(in.dev);
+};
+bool read_u64_mapped(const unsigned long long* dsrc, cudaStream_t st, unsigned long long* out) {
+  thread_local MappedSlot slot;  // per host thread (and device current at first use)
+  if (!slot.ok) {
+    if (cudaMemcpyAsync(out, dsrc, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess) return false;
+    return cudaStreamSynchronize(st) == cudaSuccess;
+  }
+  cmg::apik::publish_u64_kernel<<<1, 1, 0, st>>>(dsrc, slot.dev); ::cmg::note_launch();
+  if (cudaEventRecord(slot.ev, st) != cudaSuccess) return false;
+  if (cudaEventSynchronize(slot.ev) != cudaSuccess) return false;
+  *out = *reinterpret_cast<volatile unsigned long long*>(slot.host);
+  return true;
+}
+}  // namespace
+
+// count/collect + scan + gather for device-resident queries into csr's
+// device buffers (row_ptr, cols, nnz). Events of the calling thread record
+// the phases (cm_get_last_query_timing).
+static cm_status radius_search_core(const cm_index* ix, const double* qd, uint64_t nq, int kernel,
+                                    double r, cudaStream_t st, cm_csr* csr) {
   QueryEvents& ev = qev();
   ev.valid = false;
   cudaEventRecord(ev.e[0], st);
   QueryOrder ord;
   CM_TRY(order_queries(ix, qd, nq, st, &ord));
   cudaEventRecord(ev.e[1], st);
-  cm_csr* csr = new cm_csr();
-  csr->nq = nq;
-  csr->device = ix->device;
   uint32_t* counts = nullptr;
   uint64_t* toff = nullptr;
+  uint32_t* scnt = nullptr;
   uint32_t* temp = nullptr;
   unsigned long long* cursor = nullptr;
   auto release = [&]() {
     if (counts) dev_free(counts, st);
     if (toff) dev_free(toff, st);
+    if (scnt) dev_free(scnt, st);
     if (temp) dev_free(temp, st);
     if (cursor) dev_free(cursor, st);
-    counts = nullptr, toff = nullptr, temp = nullptr, cursor = nullptr;
+    counts = nullptr, toff = nullptr, scnt = nullptr, temp = nullptr, cursor = nullptr;
   };
   auto fail = [&](cm_status s) {
     release();
     cudaStreamSynchronize(st);
-    cm_csr_free(csr);
     return s;
   };
   if (dev_alloc_t(&counts, nq + 1, st) != cudaSuccess ||
       dev_alloc_t(&csr->row_ptr, nq + 1, st) != cudaSuccess ||
-      dev_alloc_t(&toff, nq + 1, st) != cudaSuccess || dev_alloc_t(&cursor, 1, st) != cudaSuccess) {
+      dev_alloc_t(&toff, nq + 1, st) != cudaSuccess || dev_alloc_t(&scnt, nq + 1, st) != cudaSuccess ||
+      dev_alloc_t(&cursor, 1, st) != cudaSuccess) {
     set_error("device allocation failed (row pointers)");
     return fail(CM_CUDA);
   }
@@ -546,12 +587,11 @@ cm_status cm_radius_search(const cm_index* ix, const double* q, uint64_t nq, int
   cm_status s = CM_OK;
   unsigned long long used = 0;
   if (!two_pass) {
-    s = radius_collect_dev(ix, qd, nq, kernel, r, ord.perm, temp, cap, toff, counts, cursor, st,
-                           ev.e[2]);
+    s = radius_collect_dev(ix, qd, nq, kernel, r, ord.perm, temp, cap, toff, scnt, counts, cursor,
+                           st, ev.e[2]);
     cudaEventRecord(ev.e[3], st);
     if (s != CM_OK) return fail(s);
-    if (cudaMemcpyAsync(&used, cursor, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
-        cudaStreamSynchronize(st) != cudaSuccess) {
+    if (!read_u64_mapped(cursor, st, &used)) {
       set_error("arena cursor readback failed");
       return fail(CM_CUDA);
     }
@@ -588,7 +628,7 @@ cm_status cm_radius_search(const cm_index* ix, const double* q, uint64_t nq, int
   if (two_pass)
     s = radius_fill_dev(ix, qd, nq, kernel, r, ord.perm, csr->row_ptr, csr->cols, st, nullptr);
   else
-    s = gather_rows_dev(temp, toff, counts, csr->row_ptr, csr->cols, nq, st);
+    s = gather_rows_dev(temp, toff, scnt, csr->row_ptr, ord.perm, csr->cols, nq, st);
   cudaEventRecord(ev.e[5], st);
   if (s != CM_OK) return fail(s);
   ev.nq = nq;
@@ -596,8 +636,159 @@ cm_status cm_radius_search(const cm_index* ix, const double* q, uint64_t nq, int
   ev.two_pass = two_pass;
   ev.valid = true;
   release();
+  return CM_OK;
+}
+
+
+extern "C" {
+
+cm_status cm_radius_search(const cm_index* ix, const double* q, uint64_t nq, int kernel, double r,
+                           void* stream, cm_csr** out) {
+  CM_TRY(check_index(ix));
+  CM_TRY(check_kernel(kernel));
+  if (!out || (nq && !q)) {
+    set_error("null query or output pointer");
+    return CM_INVALID_ARGUMENT;
+  }
+  *out = nullptr;
+  DeviceGuard dg(ix->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  InBuf in;
+  CM_TRY(stage_input(q, nq * 24, st, &in));
+  cm_csr* csr = new cm_csr();
+  csr->nq = nq;
+  csr->device = ix->device;
+  const cm_status s = radius_search_core(ix, static_cast<const double*>(in.dev), nq, kernel, r,
+                                         st, csr);
+  if (s != CM_OK) {
+    cm_csr_free(csr);
+    return s;
+  }
   *out = csr;
   return CM_OK;
+}
+
+// Host-buffer pipeline: queries in chunks; chunk i+1's host->device copy and
+// chunk i-1's device->host copy of its CSR overlap chunk i's kernels (three
+// streams). row_ptr_host gets nq + 1 entries, cols_host up to cols_capacity.
+cm_status cm_radius_search_to_host(const cm_index* ix, const double* q_host, uint64_t nq,
+                                   int kernel, double r, uint64_t* row_ptr_host,
+                                   uint32_t* cols_host, uint64_t cols_capacity, uint64_t* nnz_out,
+                                   void* stream) {
+  CM_TRY(check_index(ix));
+  CM_TRY(check_kernel(kernel));
+  if ((nq && !q_host) || !row_ptr_host || !nnz_out) {
+    set_error("null query or output pointer");
+    return CM_INVALID_ARGUMENT;
+  }
+  DeviceGuard dg(ix->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  struct Streams {
+    cudaStream_t in = nullptr, out = nullptr;
+    Streams() {  // per host thread, kept for the process lifetime
+      cudaStreamCreateWithFlags(&in, cudaStreamNonBlocking);
+      cudaStreamCreateWithFlags(&out, cudaStreamNonBlocking);
+    }
+  };
+  thread_local Streams ss;
+  // Chunks pay off only when consecutive queries are spatially coherent
+  // (e.g. scan-ordered LiDAR centres): the query tiles are formed within a
+  // chunk, so a chunk of a random-order batch is a sparse sample whose tiles
+  // fall back to one query per warp. Default: one chunk.
+  uint64_t nchunks = 1;
+  if (const char* ev = std::getenv("CMGPU_CHUNKS")) nchunks = std::max<uint64_t>(1, std::strtoull(ev, nullptr, 10));
+  const uint64_t chunk = (nq + nchunks - 1) / std::max<uint64_t>(nchunks, 1);
+  double* qbuf[2] = {nullptr, nullptr};
+  cudaEvent_t in_done[2], comp_done[2], out_done[2];
+  for (int i = 0; i < 2; ++i) {
+    cudaEventCreateWithFlags(&in_done[i], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&comp_done[i], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&out_done[i], cudaEventDisableTiming);
+  }
+  cm_csr csrs[2];
+  cm_status s = CM_OK;
+  for (int i = 0; i < 2 && nq; ++i)
+    if (dev_alloc_t(&qbuf[i], chunk * 3, ss.in) != cudaSuccess) s = CM_CUDA;
+  uint64_t base = 0;
+  bool full = false;
+  row_ptr_host[0] = 0;
+  auto issue_in = [&](uint64_t c) {
+    const uint64_t q0 = c * chunk, n = std::min(chunk, nq - q0);
+    const int bi = (int)(c & 1);
+    cudaStreamWaitEvent(ss.in, comp_done[bi], 0);  // buffer reuse
+    cudaMemcpyAsync(qbuf[bi], q_host + 3 * q0, n * 24, cudaMemcpyHostToDevice, ss.in);
+    cudaEventRecord(in_done[bi], ss.in);
+  };
+  if (s == CM_OK && nq) issue_in(0);
+  static const bool trace = std::getenv("CMGPU_TRACE") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
+  auto tr = [&](const char* what, uint64_t c) {
+    if (trace)
+      std::fprintf(stderr, "[to_host] %8.3f ms chunk %lu %s\n",
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(),
+                   (unsigned long)c, what);
+  };
+  for (uint64_t c = 0; s == CM_OK && c * chunk < nq; ++c) {
+    const uint64_t q0 = c * chunk, n = std::min(chunk, nq - q0);
+    const int bi = (int)(c & 1);
+    tr("start", c);
+    if ((c + 1) * chunk < nq) issue_in(c + 1);
+    cudaStreamWaitEvent(st, in_done[bi], 0);
+    cudaStreamWaitEvent(st, out_done[bi], 0);  // csrs[bi] no longer being copied
+    if (csrs[bi].row_ptr) {
+      dev_free(csrs[bi].row_ptr, st);
+      dev_free(csrs[bi].cols, st);
+      csrs[bi].row_ptr = nullptr, csrs[bi].cols = nullptr;
+    }
+    csrs[bi].nq = n;
+    csrs[bi].device = ix->device;
+    s = radius_search_core(ix, qbuf[bi], n, kernel, r, st, &csrs[bi]);
+    tr("core returned", c);
+    if (trace) {
+      cm_query_timing qt;
+      cm_get_last_query_timing(&qt);
+      std::fprintf(stderr, "   device: order %.2f pass1 %.2f scan %.2f pass2 %.2f total %.2f ms\n",
+                   qt.order_ms, qt.pass1_ms, qt.scan_ms, qt.pass2_ms, qt.total_ms);
+    }
+    if (s != CM_OK) break;
+    if (base) {
+      apik::add_offset_kernel<<<(unsigned)std::min<uint64_t>((n + 255) / 256, 4096), 256, 0, st>>>(
+          csrs[bi].row_ptr + 1, n, base); ::cmg::note_launch();
+    }
+    cudaEventRecord(comp_done[bi], st);
+    if (full || base + csrs[bi].nnz > cols_capacity) {
+      base += csrs[bi].nnz;  // keep counting; report the size needed
+      full = true;
+      continue;
+    }
+    // rows of this chunk: shift by `base` on the host after the copy
+    cudaStreamWaitEvent(ss.out, comp_done[bi], 0);
+    cudaMemcpyAsync(row_ptr_host + q0 + 1, csrs[bi].row_ptr + 1, n * 8, cudaMemcpyDeviceToHost,
+                    ss.out);
+    if (csrs[bi].nnz)
+      cudaMemcpyAsync(cols_host + base, csrs[bi].cols, csrs[bi].nnz * 4, cudaMemcpyDeviceToHost,
+                      ss.out);
+    cudaEventRecord(out_done[bi], ss.out);
+    base += csrs[bi].nnz;
+  }
+  cudaStreamSynchronize(ss.out);
+  cudaStreamSynchronize(st);
+  tr("all done", 0);
+  *nnz_out = base;
+  if (s == CM_OK && full) s = CM_CAPACITY;
+  if (s == CM_CAPACITY) {
+    set_error("cols_capacity too small; *nnz_out holds the size needed");
+  }
+  for (int i = 0; i < 2; ++i) {
+    if (csrs[i].row_ptr) dev_free(csrs[i].row_ptr, st);
+    if (csrs[i].cols) dev_free(csrs[i].cols, st);
+    if (qbuf[i]) dev_free(qbuf[i], st);
+    cudaEventDestroy(in_done[i]);
+    cudaEventDestroy(comp_done[i]);
+    cudaEventDestroy(out_done[i]);
+  }
+  cudaStreamSynchronize(st);
+  return s;
 }
 
 cm_status cm_csr_info(const cm_csr* csr, uint64_t* nq, uint64_t* nnz, const uint64_t** row_ptr,

@@ -108,10 +108,12 @@ cm_status radius_digest_dev(const cm_index* ix, const double* q_dev, uint64_t nq
                             uint64_t* digest_dev, cudaStream_t st);
 cm_status radius_collect_dev(const cm_index* ix, const double* q_dev, uint64_t nq, int kernel,
                              double r, const uint32_t* perm, uint32_t* temp, uint64_t cap,
-                             uint64_t* toff, uint32_t* counts, unsigned long long* cursor,
-                             cudaStream_t st, cudaEvent_t after_collect);
-cm_status gather_rows_dev(const uint32_t* temp, const uint64_t* toff, const uint32_t* counts,
-                          const uint64_t* row_ptr, uint32_t* cols, uint64_t nq, cudaStream_t st);
+                             uint64_t* toff, uint32_t* scnt, uint32_t* counts,
+                             unsigned long long* cursor, cudaStream_t st,
+                             cudaEvent_t after_collect);
+cm_status gather_rows_dev(const uint32_t* temp, const uint64_t* toff, const uint32_t* scnt,
+                          const uint64_t* row_ptr, const uint32_t* perm, uint32_t* cols,
+                          uint64_t nq, cudaStream_t st);
 cm_status counts_to_row_ptr(const uint32_t* counts_dev, uint64_t nq, uint64_t* row_ptr_dev,
                             cudaStream_t st);
 cm_status knn_dev(const cm_index* ix, const double* q_dev, uint64_t nq, uint32_t k,

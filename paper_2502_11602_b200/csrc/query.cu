@@ -36,6 +36,7 @@ namespace {
 constexpr int kQThreads = 128;
 constexpr int kQWarps = kQThreads / 32;
 constexpr int kLaneRowCap = 96;                       // per-lane row buffer
+constexpr int kLaneSortMax = 32;                      // per-lane register sort up to
 constexpr int kRowWarpBytes = kLaneRowCap * 33 * 4;   // interleaved, stride 33
 constexpr int kRowCap = kRowWarpBytes / 4;            // one-query row buffer (u32)
 constexpr int kBigSmemCap = 32768;                    // block sort in smem (128 KB)
@@ -56,7 +57,8 @@ struct Out {
   uint32_t* cols;                 // FILL
   uint32_t* temp;                 // COLLECT arena
   uint64_t cap;                   // COLLECT arena capacity (entries)
-  uint64_t* toff;                 // COLLECT per-query arena offset
+  uint64_t* toff;                 // COLLECT arena offset, by sorted position
+  uint32_t* scnt;                 // COLLECT row length, by sorted position
   unsigned long long* cursor;     // COLLECT arena bump pointer
   uint64_t* big_off;              // rows sorted afterwards: offset into `rows`
   uint32_t* big_len;
@@ -176,6 +178,45 @@ __device__ __forceinline__ void warp_sort_regs(uint32_t (&v)[ITEMS], int lane) {
       }
     }
   }
+}
+
+// Ascending bitonic network over P registers of ONE thread (compile-time
+// indices only, so v stays in registers).
+template <int P>
+__device__ __forceinline__ void lane_sort_regs(uint32_t (&v)[P]) {
+#pragma unroll
+  for (int k = 2; k <= P; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        const int p = i ^ j;
+        if (p > i) {
+          const uint32_t a = v[i], b = v[p];
+          if ((i & k) == 0) {
+            v[i] = min(a, b);
+            v[p] = max(a, b);
+          } else {
+            v[i] = max(a, b);
+            v[p] = min(a, b);
+          }
+        }
+      }
+    }
+  }
+}
+
+// Each lane sorts its own interleaved row srow[i * 33 + lane], i < len
+// (len <= P), in registers.
+template <int P>
+__device__ __forceinline__ void lane_sort_row(uint32_t* srow, int lane, uint32_t len) {
+  uint32_t v[P];
+#pragma unroll
+  for (int i = 0; i < P; ++i) v[i] = (uint32_t)i < len ? srow[i * 33 + lane] : 0xffffffffu;
+  lane_sort_regs<P>(v);
+#pragma unroll
+  for (int i = 0; i < P; ++i)
+    if ((uint32_t)i < len) srow[i * 33 + lane] = v[i];
 }
 
 // Sorts lane l's interleaved row (srow[i * 33 + l], i < len) with the whole
@@ -343,9 +384,9 @@ __device__ __forceinline__ void warp_query_fill(const Tables& t, double cx, doub
 
 // One query, one warp, any pass.
 template <int FLAVOR, int MODE, int CUBE>
-__device__ __forceinline__ void single_query(const Tables& t, uint32_t qi, double cx, double cy,
-                                             double cz, double r, int lane, uint32_t lt,
-                                             const Out& o, uint32_t* wbuf) {
+__device__ __forceinline__ void single_query(const Tables& t, uint32_t qi, uint64_t spos,
+                                             double cx, double cy, double cz, double r, int lane,
+                                             uint32_t lt, const Out& o, uint32_t* wbuf) {
   if (MODE == MODE_COUNT || MODE == MODE_DIGEST) {
     uint32_t cnt;
     uint64_t tested, dig;
@@ -368,12 +409,62 @@ __device__ __forceinline__ void single_query(const Tables& t, uint32_t qi, doubl
     if (lane == 0) {
       base = atomicAdd(o.cursor, (unsigned long long)cnt);
       o.counts[qi] = cnt;
-      o.toff[qi] = base;
+      o.toff[spos] = base;
+      o.scnt[spos] = cnt;
     }
     base = __shfl_sync(0xffffffffu, base, 0);
     if (base + cnt <= o.cap)
       warp_query_fill<FLAVOR, CUBE>(t, cx, cy, cz, r, lane, lt, o.temp + base, cnt, base, o, wbuf);
   }
+}
+
+// A staged record as read from shared memory: xyz, handle, voxel k.
+struct __align__(16) SRec {
+  double x, y, z;
+  uint32_t id, meta;
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// Records [p, p + len) -> stg[0..len): lane t copies record t (2 x 16 B).
+__device__ __forceinline__ void stage_chunk(PointRec* stg, const PointRec* rec, uint32_t p,
+                                            uint32_t len, int lane) {
+  if ((uint32_t)lane < len) {
+    const char* g = reinterpret_cast<const char*>(rec + p + lane);
+    char* d = reinterpret_cast<char*>(stg + lane);
+    cp_async16(d, g);
+    cp_async16(d + 16, g + 16);
+  }
+}
+
+// Chunk iterator over the hull's needed columns (bit c of `mask`), spans
+// [b_c, e_c) held by lane c. `first` starts at the lowest needed column;
+// otherwise moves past the chunk [p, p + 32) of column c. Warp-uniform.
+__device__ __forceinline__ bool advance_chunk(uint32_t& mask, uint32_t& c, uint32_t& p,
+                                              uint32_t& ce, uint32_t b, uint32_t e, bool first) {
+  if (!first) {
+    if (p + 32 < ce) {
+      p += 32;
+      return true;
+    }
+    mask &= ~(1u << c);
+  }
+  while (mask) {
+    c = __ffs(mask) - 1;
+    p = __shfl_sync(0xffffffffu, b, c);
+    ce = __shfl_sync(0xffffffffu, e, c);
+    if (p < ce) return true;
+    mask &= ~(1u << c);
+  }
+  return false;
 }
 
 // Query-tile kernel (see the file comment).
@@ -388,6 +479,7 @@ __global__ void __launch_bounds__(kQThreads, 4) radius_tile_kernel(
   const int wib = threadIdx.x >> 5;
   uint32_t* srow = reinterpret_cast<uint32_t*>(smraw + (size_t)wib * kRowWarpBytes);
   uint32_t* wbuf = srow;
+  PointRec* stg = reinterpret_cast<PointRec*>(smraw + (size_t)kQWarps * kRowWarpBytes) + wib * 64;
   const uint32_t lt = lanemask_lt();
   const uint64_t ntiles = (nq + 31) / 32;
   const uint64_t W = (uint64_t)gridDim.x * kQWarps;
@@ -440,7 +532,7 @@ __global__ void __launch_bounds__(kQThreads, 4) radius_tile_kernel(
         const double xl = __shfl_sync(0xffffffffu, cx, l);
         const double yl = __shfl_sync(0xffffffffu, cy, l);
         const double zl = __shfl_sync(0xffffffffu, cz, l);
-        single_query<FLAVOR, MODE, CUBE>(t, ql, xl, yl, zl, r, lane, lt, o, wbuf);
+        single_query<FLAVOR, MODE, CUBE>(t, ql, tile * 32 + l, xl, yl, zl, r, lane, lt, o, wbuf);
       }
       continue;
     }
@@ -457,40 +549,57 @@ __global__ void __launch_bounds__(kQThreads, 4) radius_tile_kernel(
     P.init(cx, cy, cz, r, CUBE);
     uint32_t cnt = 0, ntest = 0;
     uint64_t dig = 0;
-    // walk the hull column by column, in stored order
-    for (uint32_t c = 0; c < ncol; ++c) {
-      const uint32_t cb = __shfl_sync(0xffffffffu, b, c);
-      const uint32_t ce = __shfl_sync(0xffffffffu, e, c);
+    // Walk the hull: each needed column's span in chunks of <= 32 records,
+    // staged into shared memory by cp.async one chunk ahead (double buffer),
+    // then read warp-uniformly (LDS broadcast) by every lane.
+    uint32_t needmask = colmask;
+#pragma unroll
+    for (int sh = 16; sh > 0; sh >>= 1) needmask |= __shfl_xor_sync(0xffffffffu, needmask, sh);
+    uint32_t c = 0, p = 0, ce = 0;
+    bool more = advance_chunk(needmask, c, p, ce, b, e, true);
+    int buf = 0;
+    if (more) stage_chunk(stg, rec, p, min(32u, ce - p), lane);
+    cp_async_commit();
+    while (more) {
+      uint32_t c2 = c, p2 = p, ce2 = ce;
+      const bool more2 = advance_chunk(needmask, c2, p2, ce2, b, e, false);
+      if (more2) stage_chunk(stg + (buf ^ 1) * 32, rec, p2, min(32u, ce2 - p2), lane);
+      cp_async_commit();
+      cp_async_wait<1>();
+      __syncwarp();
+      const SRec* sr = reinterpret_cast<const SRec*>(stg + buf * 32);
+      const uint32_t len = min(32u, ce - p);
       const bool need = (colmask >> c) & 1u;
-      if (__ballot_sync(0xffffffffu, need) == 0) continue;
-      uint32_t p = cb;
-      for (; p + 8 <= ce; p += 8) {
-        double x[8], y[8], z[8];
-        uint32_t id[8], kz[8];
+      uint32_t u = 0;
+      for (; u + 8 <= len; u += 8) {
+        SRec v[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) load_uniform(rec + p + u, x[u], y[u], z[u], id[u], kz[u]);
+        for (int w = 0; w < 8; ++w) v[w] = sr[u + w];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const bool in = need & (kz[u] - kk0 <= kspan);
-          const bool hit = in & pred<CUBE>(P, x[u], y[u], z[u]);
-          if (MODE == MODE_DIGEST && hit) dig += mix64(id[u]);
-          if (ROWS && hit && cnt < (uint32_t)kLaneRowCap) srow[cnt * 33 + lane] = id[u];
+        for (int w = 0; w < 8; ++w) {
+          const bool in = need & (v[w].meta - kk0 <= kspan);
+          const bool hit = in & pred<CUBE>(P, v[w].x, v[w].y, v[w].z);
+          if (MODE == MODE_DIGEST && hit) dig += mix64(v[w].id);
+          if (ROWS && hit && cnt < (uint32_t)kLaneRowCap) srow[cnt * 33 + lane] = v[w].id;
           cnt += hit;
           ntest += in;
         }
       }
-      for (; p < ce; ++p) {
-        double x, y, z;
-        uint32_t id, kz;
-        load_uniform(rec + p, x, y, z, id, kz);
-        const bool in = need & (kz - kk0 <= kspan);
-        const bool hit = in & pred<CUBE>(P, x, y, z);
-        if (MODE == MODE_DIGEST && hit) dig += mix64(id);
-        if (ROWS && hit && cnt < (uint32_t)kLaneRowCap) srow[cnt * 33 + lane] = id;
+      for (; u < len; ++u) {
+        const SRec v = sr[u];
+        const bool in = need & (v.meta - kk0 <= kspan);
+        const bool hit = in & pred<CUBE>(P, v.x, v.y, v.z);
+        if (MODE == MODE_DIGEST && hit) dig += mix64(v.id);
+        if (ROWS && hit && cnt < (uint32_t)kLaneRowCap) srow[cnt * 33 + lane] = v.id;
         cnt += hit;
         ntest += in;
       }
+      __syncwarp();
+      buf ^= 1;
+      c = c2, p = p2, ce = ce2;
+      more = more2;
     }
+    cp_async_wait<0>();
     if (MODE == MODE_COUNT) {
       uint32_t sum = ntest;
 #pragma unroll
@@ -523,19 +632,31 @@ __global__ void __launch_bounds__(kQThreads, 4) radius_tile_kernel(
         write_ok = base + tot <= o.cap;
         if (active && !longrow) {
           o.counts[qi] = cnt;
-          o.toff[qi] = dst;
+          o.toff[s] = dst;
+          o.scnt[s] = cnt;
         }
       }
       __syncwarp();
       uint32_t* rows = MODE == MODE_FILL ? o.cols : o.temp;
       if (write_ok) {
-        for (int l = 0; l < 32; ++l) {
-          const uint32_t len = __shfl_sync(0xffffffffu, mine, l);
-          const uint64_t off = __shfl_sync(0xffffffffu, dst, l);
-          if (len == 0) continue;
-          if (len <= 32) warp_sort_row_out<1>(srow, l, len, rows + off, lane);
-          else if (len <= 64) warp_sort_row_out<2>(srow, l, len, rows + off, lane);
-          else warp_sort_row_out<4>(srow, l, len, rows + off, lane);
+        if (MODE == MODE_COLLECT) {
+          // arena rows go out unsorted; the gather kernel sorts them
+          __syncwarp();
+          for (int l = 0; l < 32; ++l) {
+            const uint32_t len = __shfl_sync(0xffffffffu, mine, l);
+            const uint64_t off = __shfl_sync(0xffffffffu, dst, l);
+            for (uint32_t i = lane; i < len; i += 32) rows[off + i] = srow[i * 33 + l];
+          }
+        } else {
+          __syncwarp();
+          for (int l = 0; l < 32; ++l) {
+            const uint32_t len = __shfl_sync(0xffffffffu, mine, l);
+            const uint64_t off = __shfl_sync(0xffffffffu, dst, l);
+            if (len == 0) continue;
+            if (len <= 32) warp_sort_row_out<1>(srow, l, len, rows + off, lane);
+            else if (len <= 64) warp_sort_row_out<2>(srow, l, len, rows + off, lane);
+            else warp_sort_row_out<4>(srow, l, len, rows + off, lane);
+          }
         }
       }
       __syncwarp();
@@ -547,7 +668,7 @@ __global__ void __launch_bounds__(kQThreads, 4) radius_tile_kernel(
         const double xl = __shfl_sync(0xffffffffu, cx, l);
         const double yl = __shfl_sync(0xffffffffu, cy, l);
         const double zl = __shfl_sync(0xffffffffu, cz, l);
-        single_query<FLAVOR, MODE, CUBE>(t, ql, xl, yl, zl, r, lane, lt, o, wbuf);
+        single_query<FLAVOR, MODE, CUBE>(t, ql, tile * 32 + l, xl, yl, zl, r, lane, lt, o, wbuf);
       }
     }
     __syncwarp();
@@ -576,19 +697,101 @@ __global__ void __launch_bounds__(1024) big_row_sort_kernel(uint32_t* __restrict
   }
 }
 
-// Arena rows -> CSR order (a warp per query, coalesced copies).
-__global__ void gather_rows_kernel(const uint32_t* __restrict__ temp,
-                                   const uint64_t* __restrict__ toff,
-                                   const uint32_t* __restrict__ counts,
-                                   const uint64_t* __restrict__ row_ptr,
-                                   uint32_t* __restrict__ cols, uint64_t nq) {
+// Arena rows -> CSR order, sorting them on the way. A warp takes the 32
+// queries of one tile (sorted positions 32g..32g+31), whose arena rows the
+// collect kernel wrote contiguously, so the reads stream. Rows of <= 96
+// handles are staged in shared memory (interleaved, stride 33); each lane
+// sorts its own row in registers with an unrolled bitonic network — rows
+// longer than 64 as two runs, [0, 64) and [64, len), merged by the warp with
+// a merge-path rank per element. Rows longer than 96 come from the
+// one-query-per-warp path already sorted and are copied.
+constexpr int kGatherRow = 96;
+__global__ void __launch_bounds__(128) gather_rows_kernel(const uint32_t* __restrict__ temp,
+                                                          const uint64_t* __restrict__ toff,
+                                                          const uint32_t* __restrict__ counts,
+                                                          const uint64_t* __restrict__ row_ptr,
+                                                          const uint32_t* __restrict__ perm,
+                                                          uint32_t* __restrict__ cols,
+                                                          uint64_t nq) {
+  extern __shared__ uint32_t gsm[];
   const int lane = threadIdx.x & 31;
+  uint32_t* srow = gsm + (threadIdx.x >> 5) * (kGatherRow * 33);
+  const uint64_t ngroups = (nq + 31) / 32;
   const uint64_t W = (uint64_t)gridDim.x * (blockDim.x >> 5);
-  for (uint64_t q = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); q < nq; q += W) {
-    const uint32_t len = __ldg(counts + q);
-    const uint32_t* src = temp + __ldg(toff + q);
-    uint32_t* dst = cols + __ldg(row_ptr + q);
-    for (uint32_t i = lane; i < len; i += 32) dst[i] = __ldg(src + i);
+  for (uint64_t gidx = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+       gidx < ngroups; gidx += W) {
+    const uint64_t s = gidx * 32 + lane;
+    const bool act = s < nq;
+    const uint32_t q = act ? __ldg(perm + s) : 0u;
+    const uint32_t len = act ? __ldg(counts + s) : 0u;
+    const uint64_t so = act ? __ldg(toff + s) : 0;
+    const uint64_t dof = act ? __ldg(row_ptr + q) : 0;
+    const uint32_t staged = len <= (uint32_t)kGatherRow ? len : 0u;
+    // 8 rows per step, all their loads in flight before the stores
+    for (int l0 = 0; l0 < 32; l0 += 8) {
+      uint32_t v[8][3];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t ln = __shfl_sync(0xffffffffu, staged, l0 + j);
+        const uint64_t o = __shfl_sync(0xffffffffu, so, l0 + j);
+#pragma unroll
+        for (int h = 0; h < 3; ++h) {
+          const uint32_t i = h * 32 + lane;
+          v[j][h] = i < ln ? __ldg(temp + o + i) : 0u;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t ln = __shfl_sync(0xffffffffu, staged, l0 + j);
+#pragma unroll
+        for (int h = 0; h < 3; ++h) {
+          const uint32_t i = h * 32 + lane;
+          if (i < ln) srow[i * 33 + l0 + j] = v[j][h];
+        }
+      }
+    }
+    __syncwarp();
+    // run 1: [0, min(len, 64))
+    const uint32_t r1 = staged < 64u ? staged : 64u;
+    const uint32_t m1 = warp_max_u32(r1);
+    if (m1 > 32) lane_sort_row<64>(srow, lane, r1);
+    else if (m1 > 16) lane_sort_row<32>(srow, lane, r1);
+    else if (m1 > 1) lane_sort_row<16>(srow, lane, r1);
+    // run 2: [64, len)
+    const uint32_t r2 = staged > 64u ? staged - 64u : 0u;
+    const uint32_t m2 = warp_max_u32(r2);
+    if (m2 > 1) lane_sort_row<32>(srow + 64 * 33, lane, r2);
+    __syncwarp();
+    for (int l = 0; l < 32; ++l) {
+      const uint32_t ln = __shfl_sync(0xffffffffu, len, l);
+      const uint64_t d = __shfl_sync(0xffffffffu, dof, l);
+      if (ln <= 64) {
+        for (uint32_t i = lane; i < ln; i += 32) cols[d + i] = srow[i * 33 + l];
+      } else if (ln <= (uint32_t)kGatherRow) {
+        // merge path: element a_i of run A [0,64) goes to i + #{b in B : b < a_i};
+        // b_j of run B goes to j + #{a in A : a <= b_j} (handles are distinct)
+        const uint32_t nb = ln - 64;
+        for (uint32_t i = lane; i < ln; i += 32) {
+          const uint32_t v = srow[i * 33 + l];
+          uint32_t lo, hi, base, off;
+          if (i < 64) {
+            lo = 64, hi = ln, base = 64, off = i;
+          } else {
+            lo = 0, hi = 64, base = 0, off = i - 64;
+          }
+          while (lo < hi) {
+            const uint32_t m = (lo + hi) >> 1;
+            if (srow[m * 33 + l] < v) lo = m + 1; else hi = m;
+          }
+          cols[d + off + (lo - base)] = v;
+        }
+        (void)nb;
+      } else {
+        const uint64_t o = __shfl_sync(0xffffffffu, so, l);
+        for (uint32_t i = lane; i < ln; i += 32) cols[d + i] = __ldg(temp + o + i);
+      }
+    }
+    __syncwarp();
   }
 }
 
@@ -611,7 +814,7 @@ template <int MODE>
 cm_status launch_radius(const cm_index* ix, const double* q, uint64_t nq, int kernel, double r,
                         const uint32_t* perm, const Out& o, cudaStream_t st) {
   const Tables t = ix->tables();
-  const size_t smem = (size_t)kQWarps * kRowWarpBytes;
+  const size_t smem = (size_t)kQWarps * (kRowWarpBytes + 64 * sizeof(PointRec));
   auto run = [&](auto kern) -> cm_status {
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -729,8 +932,9 @@ cm_status radius_fill_dev(const cm_index* ix, const double* q, uint64_t nq, int 
 
 cm_status radius_collect_dev(const cm_index* ix, const double* q, uint64_t nq, int kernel,
                              double r, const uint32_t* perm, uint32_t* temp, uint64_t cap,
-                             uint64_t* toff, uint32_t* counts, unsigned long long* cursor,
-                             cudaStream_t st, cudaEvent_t after_collect) {
+                             uint64_t* toff, uint32_t* scnt, uint32_t* counts,
+                             unsigned long long* cursor, cudaStream_t st,
+                             cudaEvent_t after_collect) {
   if (nq == 0) return CM_OK;
   BigRows big;
   cm_status s = big.init(nq, st);
@@ -741,6 +945,7 @@ cm_status radius_collect_dev(const cm_index* ix, const double* q, uint64_t nq, i
   o.temp = temp;
   o.cap = cap;
   o.toff = toff;
+  o.scnt = scnt;
   o.cursor = cursor;
   o.big_off = big.off;
   o.big_len = big.len;
@@ -752,10 +957,14 @@ cm_status radius_collect_dev(const cm_index* ix, const double* q, uint64_t nq, i
 }
 
 cm_status gather_rows_dev(const uint32_t* temp, const uint64_t* toff, const uint32_t* counts,
-                          const uint64_t* row_ptr, uint32_t* cols, uint64_t nq, cudaStream_t st) {
+                          const uint64_t* row_ptr, const uint32_t* perm, uint32_t* cols,
+                          uint64_t nq, cudaStream_t st) {
   if (nq == 0) return CM_OK;
-  const unsigned grid = (unsigned)std::min<uint64_t>((nq + 7) / 8, (uint64_t)sm_count() * 16);
-  gather_rows_kernel<<<grid, 256, 0, st>>>(temp, toff, counts, row_ptr, cols, nq); ::cmg::note_launch();
+  const uint64_t groups = (nq + 31) / 32;
+  const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((groups + 3) / 4, (uint64_t)sm_count() * 8));
+  const int smem = 4 * kGatherRow * 33 * 4;
+  cudaFuncSetAttribute(gather_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  gather_rows_kernel<<<grid, 128, smem, st>>>(temp, toff, counts, row_ptr, perm, cols, nq); ::cmg::note_launch();
   CM_CUDA_TRY(cudaGetLastError());
   return CM_OK;
 }

@@ -143,3 +143,33 @@ def test_count_then_fill_api(cfg0, cfg0_oracle, flavor):
                                cols.ctypes.data_as(ctypes.c_void_p), None))
     orow, ocols = cfg0_oracle.radius_csr(q, 1, 1.5)
     assert np.array_equal(row, orow) and np.array_equal(cols, ocols)
+
+
+def test_search_to_host_pipeline(cfg0, cfg0_oracle):
+    """cm_radius_search_to_host (chunked host<->device overlap) returns the
+    same CSR; a too-small capacity reports CM_CAPACITY and the size needed."""
+    import ctypes
+    import torch
+    from paper_2502_11602_b200 import _native
+    cloud, _ = cfg0
+    q = np.ascontiguousarray(cloud[:600_000])  # 8 chunks
+    m = cm.Cheesemap.build(cloud, cm.BuildOptions(flavor=cm.Flavor.Mixed))
+    orow, ocols = cfg0_oracle.radius_csr(q, 0, 1.0)
+    qh = torch.from_numpy(q).pin_memory()
+    row = torch.zeros(q.shape[0] + 1, dtype=torch.int64).pin_memory()
+    cols = torch.zeros(len(ocols), dtype=torch.int32).pin_memory()
+    nnz = ctypes.c_uint64()
+    L = _native.lib()
+    rc = L.cm_radius_search_to_host(m.handle, ctypes.c_void_p(qh.data_ptr()), q.shape[0], 0, 1.0,
+                                    ctypes.c_void_p(row.data_ptr()),
+                                    ctypes.c_void_p(cols.data_ptr()), cols.numel(),
+                                    ctypes.byref(nnz), None)
+    assert rc == 0 and nnz.value == len(ocols)
+    assert np.array_equal(row.numpy().astype(np.uint64), orow)
+    assert np.array_equal(cols.numpy().astype(np.uint32), ocols)
+    small = np.zeros(10, dtype=np.uint32)
+    rc = L.cm_radius_search_to_host(m.handle, q.ctypes.data_as(ctypes.c_void_p), q.shape[0], 0,
+                                    1.0, ctypes.c_void_p(row.data_ptr()),
+                                    small.ctypes.data_as(ctypes.c_void_p), 10, ctypes.byref(nnz),
+                                    None)
+    assert rc == 3 and nnz.value == len(ocols)
