@@ -45,7 +45,11 @@ static void configure_pool() {
   if (dev >= 0 && dev < 64 && !g_pool_configured[dev]) {
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = ~0ull;  // keep freed blocks cached across calls
+      // keep up to half the device's memory cached across calls (steady
+      // state batches then allocate nothing), return the rest at syncs
+      size_t fr = 0, tot = 0;
+      cudaMemGetInfo(&fr, &tot);
+      uint64_t thr = tot / 2;
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
     g_pool_configured[dev] = true;
@@ -54,7 +58,19 @@ static void configure_pool() {
 
 cudaError_t dev_alloc(void** p, size_t bytes, cudaStream_t st) {
   configure_pool();
-  return cudaMallocAsync(p, bytes == 0 ? 16 : bytes, st);
+  cudaError_t e = cudaMallocAsync(p, bytes == 0 ? 16 : bytes, st);
+  if (e == cudaErrorMemoryAllocation) {
+    // the pool keeps freed blocks cached (release threshold = max): give
+    // them back to the device and retry once
+    cudaGetLastError();
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    cudaDeviceSynchronize();
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+    e = cudaMallocAsync(p, bytes == 0 ? 16 : bytes, st);
+  }
+  return e;
 }
 
 void dev_free(void* p, cudaStream_t st) {

@@ -89,6 +89,38 @@ __device__ __forceinline__ bool clamped_range(const DevGrid& g, double cx, doubl
   return true;
 }
 
+// clamped_range computed by one warp for one (warp-uniform) query: lanes
+// 0..5 each do one of the six IEEE divisions, then broadcast. Same
+// arithmetic as clamped_range.
+__device__ __forceinline__ bool clamped_range_warp(const DevGrid& g, double cx, double cy,
+                                                   double cz, double r, int lane, Range* out) {
+  const double lx = __dsub_rn(cx, r), hx = __dadd_rn(cx, r);
+  const double ly = __dsub_rn(cy, r), hy = __dadd_rn(cy, r);
+  const double lz = __dsub_rn(cz, r), hz = __dadd_rn(cz, r);
+  if (!(lx <= g.bx1 && hx >= g.bx0 && ly <= g.by1 && hy >= g.by0 && lz <= g.bz1 &&
+        hz >= g.bz0))
+    return false;
+  uint64_t v = 0;
+  if (lane < 6) {
+    const int a = lane >> 1;
+    const bool hi = lane & 1;
+    const double c = a == 0 ? (hi ? std_min(hx, g.bx1) : std_max(lx, g.bx0))
+                   : a == 1 ? (hi ? std_min(hy, g.by1) : std_max(ly, g.by0))
+                            : (hi ? std_min(hz, g.bz1) : std_max(lz, g.bz0));
+    const double o = a == 0 ? g.ox : a == 1 ? g.oy : g.oz;
+    const double s = a == 0 ? g.sx : a == 1 ? g.sy : g.sz;
+    const uint64_t n = a == 0 ? g.nx : a == 1 ? g.ny : g.nz;
+    v = (a == 2 && !g.mode3d) ? 0 : axis_index(c, o, s, n);
+  }
+  out->i0 = __shfl_sync(0xffffffffu, v, 0);
+  out->i1 = __shfl_sync(0xffffffffu, v, 1);
+  out->j0 = __shfl_sync(0xffffffffu, v, 2);
+  out->j1 = __shfl_sync(0xffffffffu, v, 3);
+  out->k0 = __shfl_sync(0xffffffffu, v, 4);
+  out->k1 = __shfl_sync(0xffffffffu, v, 5);
+  return true;
+}
+
 // squared_distance (geometry.hpp:26-31): ((dx*dx + dy*dy) + dz*dz), dx = p - c
 __device__ __forceinline__ double sqdist(double px, double py, double pz, double cx, double cy,
                                          double cz) {

@@ -39,6 +39,7 @@ constexpr int kLaneRowCap = 96;                       // per-lane row buffer
 constexpr int kLaneSortMax = 32;                      // per-lane register sort up to
 constexpr int kRowWarpBytes = kLaneRowCap * 33 * 4;   // interleaved, stride 33
 constexpr int kRowCap = kRowWarpBytes / 4;            // one-query row buffer (u32)
+constexpr int kSortCap = (kRowCap - 512) / 2;         // one-query row sorted in smem
 constexpr int kBigSmemCap = 32768;                    // block sort in smem (128 KB)
 
 enum { MODE_COUNT = 0, MODE_FILL = 1, MODE_DIGEST = 2, MODE_COLLECT = 3 };
@@ -266,7 +267,7 @@ __device__ __forceinline__ void warp_query_count(const Tables& t, double cx, dou
                                                  double r, int lane, uint32_t* cnt_out,
                                                  uint64_t* tested_out, uint64_t* dig_out) {
   Range R;
-  const bool ok = clamped_range(t.g, cx, cy, cz, r, &R);
+  const bool ok = clamped_range_warp(t.g, cx, cy, cz, r, lane, &R);
   Predicate P;
   P.init(cx, cy, cz, r, CUBE);
   uint32_t cnt = 0;
@@ -312,19 +313,101 @@ __device__ __forceinline__ void warp_query_count(const Tables& t, double cx, dou
   *dig_out = dig;
 }
 
-// One query answered by a whole warp: its `len` hits, sorted, to dst. Rows
-// longer than the warp buffer are written unsorted and registered for the
-// block sort (offset `big_base` into the row buffer).
+// Warp LSD radix sort of a[0..n) (u32, keys < 2^bits) with 9-bit digits,
+// ping-ponging through tmp; `cnt` holds 512 counters. Stable per pass
+// (ranks inside a 32-element chunk from __match_any_sync). Returns the buffer
+// holding the result.
+__device__ __noinline__ uint32_t* warp_radix_sort(uint32_t* a, uint32_t* tmp, uint32_t* cnt,
+                                                  uint32_t n, int bits, int lane, uint32_t lt) {
+  constexpr int R = 9;
+  constexpr uint32_t M = (1u << R) - 1;
+  for (int sh = 0; sh < bits; sh += R) {
+    for (int d = lane; d <= (int)M; d += 32) cnt[d] = 0;
+    __syncwarp();
+    for (uint32_t i = lane; i < n; i += 32) atomicAdd(&cnt[(a[i] >> sh) & M], 1u);
+    __syncwarp();
+    // exclusive scan of the 512 counters: 16 per lane
+    uint32_t loc[16], sum = 0;
+#pragma unroll
+    for (int x = 0; x < 16; ++x) {
+      loc[x] = cnt[lane * 16 + x];
+      sum += loc[x];
+    }
+    const uint32_t inc = warp_incl_scan(sum);
+    uint32_t run = inc - sum;
+#pragma unroll
+    for (int x = 0; x < 16; ++x) {
+      cnt[lane * 16 + x] = run;
+      run += loc[x];
+    }
+    __syncwarp();
+    for (uint32_t base = 0; base < n; base += 32) {
+      const uint32_t i = base + lane;
+      const bool valid = i < n;
+      const uint32_t v = valid ? a[i] : 0u;
+      const uint32_t d = valid ? ((v >> sh) & M) : (M + 1);
+      const uint32_t peers = __match_any_sync(0xffffffffu, d) & __ballot_sync(0xffffffffu, valid);
+      uint32_t pos = 0;
+      if (valid) pos = cnt[d] + __popc(peers & lt);
+      __syncwarp();
+      if (valid) {
+        tmp[pos] = v;
+        if ((peers & lt) == 0) cnt[d] = pos + __popc(peers);
+      }
+      __syncwarp();
+    }
+    uint32_t* t2 = a;
+    a = tmp;
+    tmp = t2;
+  }
+  return a;
+}
+
+// Sorts buf[0..n) (n <= kSortCap) ascending with the cheapest method for n;
+// returns where the result is (buf, or the scratch half for radix).
+__device__ __forceinline__ const uint32_t* warp_sort_buffer(uint32_t* buf, uint32_t n, int bits,
+                                                            int lane, uint32_t lt) {
+  if (n <= 1) return buf;
+  if (n <= 32) {
+    uint32_t v = lane < (int)n ? buf[lane] : 0xffffffffu;
+    v = warp_sort32(v, lane);
+    __syncwarp();
+    if (lane < (int)n) buf[lane] = v;
+    __syncwarp();
+    return buf;
+  }
+  if (n <= 128) {
+    uint32_t v[4];
+#pragma unroll
+    for (int r2 = 0; r2 < 4; ++r2) {
+      const uint32_t e = r2 * 32 + lane;
+      v[r2] = e < n ? buf[e] : 0xffffffffu;
+    }
+    warp_sort_regs<4>(v, lane);
+    __syncwarp();
+#pragma unroll
+    for (int r2 = 0; r2 < 4; ++r2) {
+      const uint32_t e = r2 * 32 + lane;
+      if (e < n) buf[e] = v[r2];
+    }
+    __syncwarp();
+    return buf;
+  }
+  return warp_radix_sort(buf, buf + kSortCap, buf + 2 * kSortCap, n, bits, lane, lt);
+}
+
+// One query answered by a whole warp: walks its flattened spans (32
+// candidates per step). Hits go to buf[0..cap) (then `direct` must be null),
+// or straight to `direct` in visit order. Returns the hit count.
 template <int FLAVOR, int CUBE>
-__device__ __forceinline__ void warp_query_fill(const Tables& t, double cx, double cy, double cz,
-                                                double r, int lane, uint32_t lt, uint32_t* dst,
-                                                uint32_t len, uint64_t big_base, const Out& o,
-                                                uint32_t* wbuf) {
+__device__ __forceinline__ uint32_t warp_query_walk(const Tables& t, double cx, double cy,
+                                                    double cz, double r, int lane, uint32_t lt,
+                                                    uint32_t* buf, uint32_t cap,
+                                                    uint32_t* direct) {
   Range R;
-  const bool ok = clamped_range(t.g, cx, cy, cz, r, &R);
+  const bool ok = clamped_range_warp(t.g, cx, cy, cz, r, lane, &R);
   Predicate P;
   P.init(cx, cy, cz, r, CUBE);
-  const bool direct = len > (uint32_t)kRowCap;
   uint32_t cnt = 0;
   if (ok) {
     const uint64_t nj = R.j1 - R.j0 + 1;
@@ -357,27 +440,35 @@ __device__ __forceinline__ void warp_query_fill(const Tables& t, double cx, doub
         const uint32_t m = __ballot_sync(0xffffffffu, hit);
         if (hit) {
           const uint32_t off = cnt + __popc(m & lt);
-          if (direct) dst[off] = id;
-          else wbuf[off] = id;
+          if (direct) direct[off] = id;
+          else if (off < cap) buf[off] = id;
         }
         cnt += __popc(m);
       }
     }
   }
   __syncwarp();
-  if (direct) {
+  return cnt;
+}
+
+// Writes the buffered, sorted row, or (rows > kSortCap) walks again straight
+// into dst and registers the row for the block sort.
+template <int FLAVOR, int CUBE>
+__device__ __forceinline__ void warp_row_out(const Tables& t, double cx, double cy, double cz,
+                                             double r, int lane, uint32_t lt, uint32_t* wbuf,
+                                             uint32_t cnt, uint32_t* dst, uint64_t big_base,
+                                             const Out& o) {
+  if (cnt <= (uint32_t)kSortCap) {
+    const int bits = 32 - __clz((int)max(1u, (uint32_t)(t.n - 1)));
+    const uint32_t* res = warp_sort_buffer(wbuf, cnt, bits, lane, lt);
+    for (uint32_t x = lane; x < cnt; x += 32) dst[x] = res[x];
+  } else {
+    warp_query_walk<FLAVOR, CUBE>(t, cx, cy, cz, r, lane, lt, nullptr, 0, dst);
     if (lane == 0) {
       const uint32_t slot = atomicAdd(o.n_big, 1u);
       o.big_off[slot] = big_base;
       o.big_len[slot] = cnt;
     }
-  } else if (cnt <= 32) {
-    uint32_t v = lane < (int)cnt ? wbuf[lane] : 0xffffffffu;
-    v = warp_sort32(v, lane);
-    if (lane < (int)cnt) dst[lane] = v;
-  } else {
-    bitonic_sort(wbuf, cnt, lane, 32, [] { __syncwarp(); });
-    for (uint32_t x = lane; x < cnt; x += 32) dst[x] = wbuf[x];
   }
   __syncwarp();
 }
@@ -400,11 +491,13 @@ __device__ __forceinline__ void single_query(const Tables& t, uint32_t qi, uint6
   } else if (MODE == MODE_FILL) {
     const uint64_t rb = __ldg(o.row_ptr + qi);
     const uint32_t len = (uint32_t)(__ldg(o.row_ptr + qi + 1) - rb);
-    warp_query_fill<FLAVOR, CUBE>(t, cx, cy, cz, r, lane, lt, o.cols + rb, len, rb, o, wbuf);
+    if (len <= (uint32_t)kSortCap)
+      warp_query_walk<FLAVOR, CUBE>(t, cx, cy, cz, r, lane, lt, wbuf, kSortCap, nullptr);
+    warp_row_out<FLAVOR, CUBE>(t, cx, cy, cz, r, lane, lt, wbuf, len, o.cols + rb, rb, o);
   } else {
-    uint32_t cnt;
-    uint64_t tested, dig;
-    warp_query_count<FLAVOR, CUBE, false>(t, cx, cy, cz, r, lane, &cnt, &tested, &dig);
+    // single walk into the buffer (count exact even past the buffer)
+    const uint32_t cnt =
+        warp_query_walk<FLAVOR, CUBE>(t, cx, cy, cz, r, lane, lt, wbuf, kSortCap, nullptr);
     unsigned long long base = 0;
     if (lane == 0) {
       base = atomicAdd(o.cursor, (unsigned long long)cnt);
@@ -414,7 +507,7 @@ __device__ __forceinline__ void single_query(const Tables& t, uint32_t qi, uint6
     }
     base = __shfl_sync(0xffffffffu, base, 0);
     if (base + cnt <= o.cap)
-      warp_query_fill<FLAVOR, CUBE>(t, cx, cy, cz, r, lane, lt, o.temp + base, cnt, base, o, wbuf);
+      warp_row_out<FLAVOR, CUBE>(t, cx, cy, cz, r, lane, lt, wbuf, cnt, o.temp + base, base, o);
   }
 }
 
@@ -788,7 +881,19 @@ __global__ void __launch_bounds__(128) gather_rows_kernel(const uint32_t* __rest
         (void)nb;
       } else {
         const uint64_t o = __shfl_sync(0xffffffffu, so, l);
-        for (uint32_t i = lane; i < ln; i += 32) cols[d + i] = __ldg(temp + o + i);
+        for (uint32_t b0 = 0; b0 < ln; b0 += 256) {  // 8 loads in flight per lane
+          uint32_t v[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint32_t i = b0 + 32 * j + lane;
+            v[j] = i < ln ? __ldg(temp + o + i) : 0u;
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint32_t i = b0 + 32 * j + lane;
+            if (i < ln) cols[d + i] = v[j];
+          }
+        }
       }
     }
     __syncwarp();

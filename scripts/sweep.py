@@ -1,0 +1,152 @@
+"""Per-config sweep on one GPU: device-resident queries/s for every
+(config, radius, kernel) of BASELINE.json, kNN rates for config 3, and build
+times, each verified against the CPU oracle on a query sample.
+
+    python scripts/sweep.py [--configs 0,1,2,3] [--sample 2000] > sweep.json
+
+Not the driver's bench contract (bench.py is); evidence for DESIGN.md."""
+import argparse
+import ctypes
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from oracle.oracle import CpuIndex  # noqa: E402
+from paper_2502_11602_b200 import _native, synth  # noqa: E402
+from paper_2502_11602_b200 import cheesemap as cm  # noqa: E402
+
+L = _native.lib()
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def timed(fn, reps=3):
+    best = None
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        out = fn()
+        e1.record()
+        e1.synchronize()
+        ms = e0.elapsed_time(e1)
+        best = ms if best is None else min(best, ms)
+    return best, out
+
+
+def radius_case(m, qd, qh_sample, oracle, kernel, r, n_sample):
+    if r >= 5.0:
+        qd = qd[: qd.shape[0] // 10]  # keep the CSR (4 B x ~1000-1800 x nq) in memory
+    nq = qd.shape[0]
+
+    def run():
+        csr = ctypes.c_void_p()
+        cm._check(L.cm_radius_search(m.handle, ctypes.c_void_p(qd.data_ptr()), nq, kernel, r,
+                                     None, ctypes.byref(csr)))
+        return csr
+
+    run_ms = None
+    for _ in range(2):  # warm
+        L.cm_csr_free(run())
+    ms, csr = timed(run)
+    L.cm_csr_free(csr)
+    t = _native.last_query_timing()
+    # verification on a sample: counts + digests vs the oracle
+    cnt, dig = cm.radius_digest_batch(m, qh_sample, r, kernel)
+    ocnt, odig = oracle.radius(qh_sample, kernel, r)
+    ok = bool(np.array_equal(cnt, ocnt) and np.array_equal(dig, odig))
+    tested = torch.zeros(nq, dtype=torch.int64, device="cuda")
+    cm._check(L.cm_radius_count(m.handle, ctypes.c_void_p(qd.data_ptr()), nq, kernel, r, None,
+                                ctypes.c_void_p(tested.data_ptr()), None))
+    alg = 24 * int(tested.sum().item())
+    free_b, total_b = torch.cuda.mem_get_info()
+    log(f"    two_pass={t['two_pass']} nnz={t['nnz']} free={free_b / 1e9:.1f} GB")
+    return dict(kernel=["sphere", "cube"][kernel], r=r, nq=nq, ms=round(ms, 3),
+                qps=nq / (ms * 1e-3), nnz=int(t["nnz"]), two_pass=int(t["two_pass"]),
+                phases={k: round(t[k], 3) for k in ("order_ms", "pass1_ms", "scan_ms", "pass2_ms")},
+                alg_gb=round(alg / 1e9, 2), frac_pass1=round(alg / (t["pass1_ms"] * 1e-3) / 6542.1e9, 3),
+                verified_sample=n_sample, parity=ok)
+
+
+def knn_case(m, qd, qh_sample, oracle, k):
+    nq = qd.shape[0]
+    idx = torch.empty((nq, k), dtype=torch.int32, device="cuda")
+    d2 = torch.empty((nq, k), dtype=torch.float64, device="cuda")
+
+    def run():
+        cm._check(L.cm_knn(m.handle, ctypes.c_void_p(qd.data_ptr()), nq, k,
+                           ctypes.c_void_p(idx.data_ptr()), ctypes.c_void_p(d2.data_ptr()), None))
+
+    run()
+    ms, _ = timed(run)
+    gi, gd = cm.knn_batch(m, qh_sample, k)
+    oi, od = oracle.knn(qh_sample, k)
+    ok = bool(np.array_equal(gi, oi) and np.array_equal(gd, od))
+    return dict(k=k, nq=nq, ms=round(ms, 3), qps=nq / (ms * 1e-3), parity=ok)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="0,1,2,3")
+    ap.add_argument("--sample", type=int, default=2000)
+    ap.add_argument("--scale", type=float, default=1.0)
+    a = ap.parse_args()
+    out = {"gpu": torch.cuda.get_device_name(0), "results": []}
+    cfgs = [int(c) for c in a.configs.split(",")]
+    plan = {
+        0: dict(flavors=["dense"], cell=1.0, radii=[1.0], kernels=[0, 1], ks=[]),
+        1: dict(flavors=["mixed", "sparse"], cell=1.0, radii=[0.5, 1.0, 2.5, 5.0], kernels=[0, 1],
+                ks=[]),
+        2: dict(flavors=["mixed"], cell=0.25, radii=[0.05, 0.1, 0.25], kernels=[0], ks=[]),
+        3: dict(flavors=["mixed"], cell=1.0, radii=[], kernels=[], ks=[8, 16, 32, 64]),
+    }
+    fl = {"dense": 0, "sparse": 1, "mixed": 2}
+    for c in cfgs:
+        t0 = time.perf_counter()
+        cloud = synth.config_cloud(c, a.scale)
+        q = synth.config_queries(c, cloud)
+        log(f"config {c}: {cloud.shape[0]} points, {q.shape[0]} queries "
+            f"({time.perf_counter() - t0:.1f}s)")
+        p = plan[c]
+        dc = torch.from_numpy(cloud).cuda()
+        qd = torch.from_numpy(np.ascontiguousarray(q)).cuda()
+        rng = np.random.default_rng(c)
+        samp = np.ascontiguousarray(q[rng.choice(q.shape[0], min(a.sample, q.shape[0]),
+                                                 replace=False)])
+        oracle = CpuIndex(cloud, flavor=1, cell=(p["cell"],) * 3)
+        for f in p["flavors"]:
+            opts = cm.BuildOptions(flavor=cm.Flavor(fl[f]), cell=cm.CellSize.uniform(p["cell"]))
+            builds = []
+            for _ in range(3):
+                m = cm.Cheesemap.build(dc, opts)
+                builds.append(m.build_timing()["total_ms"])
+            entry = {"config": c, "flavor": f, "n_points": int(cloud.shape[0]),
+                     "build_ms": round(min(builds), 3), "radius": [], "knn": []}
+            for r in p["radii"]:
+                for kern in p["kernels"]:
+                    res = radius_case(m, qd, samp, oracle, kern, r, samp.shape[0])
+                    log(f"  cfg{c} {f} {res['kernel']} r={r}: {res['qps'] / 1e6:.1f} M q/s "
+                        f"parity={res['parity']} phases={res['phases']}")
+                    entry["radius"].append(res)
+            for k in p["ks"]:
+                res = knn_case(m, qd, samp, oracle, k)
+                log(f"  cfg{c} {f} knn k={k}: {res['qps'] / 1e6:.2f} M q/s parity={res['parity']}")
+                entry["knn"].append(res)
+            out["results"].append(entry)
+            del m
+        del oracle, dc, qd
+        torch.cuda.empty_cache()
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
