@@ -43,6 +43,27 @@ def timed(fn, reps=3):
     return best, out
 
 
+def digest_case(m, qd, qh_sample, oracle, kernel, r, n_sample):
+    """Outputs too large to materialise (TLS): per-query count + set digest."""
+    nq = qd.shape[0]
+    cnt = torch.empty(nq, dtype=torch.int32, device="cuda")
+    dig = torch.empty(nq, dtype=torch.int64, device="cuda")
+
+    def run():
+        cm._check(L.cm_radius_digest(m.handle, ctypes.c_void_p(qd.data_ptr()), nq, kernel, r,
+                                     ctypes.c_void_p(cnt.data_ptr()),
+                                     ctypes.c_void_p(dig.data_ptr()), None))
+
+    run()
+    ms, _ = timed(run, reps=2)
+    c2, d2 = cm.radius_digest_batch(m, qh_sample, r, kernel)
+    oc, od = oracle.radius(qh_sample, kernel, r)
+    ok = bool(np.array_equal(c2, oc) and np.array_equal(d2, od))
+    return dict(kernel=["sphere", "cube"][kernel], r=r, nq=nq, ms=round(ms, 3),
+                qps=nq / (ms * 1e-3), nnz=int(cnt.to(torch.int64).sum().item()), mode="digest",
+                verified_sample=n_sample, parity=ok)
+
+
 def radius_case(m, qd, qh_sample, oracle, kernel, r, n_sample):
     if r >= 5.0:
         qd = qd[: qd.shape[0] // 10]  # keep the CSR (4 B x ~1000-1800 x nq) in memory
@@ -97,7 +118,7 @@ def knn_case(m, qd, qh_sample, oracle, k):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="0,1,2,3")
-    ap.add_argument("--sample", type=int, default=2000)
+    ap.add_argument("--sample", type=int, default=1000)
     ap.add_argument("--scale", type=float, default=1.0)
     a = ap.parse_args()
     out = {"gpu": torch.cuda.get_device_name(0), "results": []}
@@ -106,7 +127,8 @@ def main():
         0: dict(flavors=["dense"], cell=1.0, radii=[1.0], kernels=[0, 1], ks=[]),
         1: dict(flavors=["mixed", "sparse"], cell=1.0, radii=[0.5, 1.0, 2.5, 5.0], kernels=[0, 1],
                 ks=[]),
-        2: dict(flavors=["mixed"], cell=0.25, radii=[0.05, 0.1, 0.25], kernels=[0], ks=[]),
+        2: dict(flavors=["mixed"], cell=0.25, radii=[0.05, 0.1, 0.25], kernels=[0], ks=[],
+                digest=True),
         3: dict(flavors=["mixed"], cell=1.0, radii=[], kernels=[], ks=[8, 16, 32, 64]),
     }
     fl = {"dense": 0, "sparse": 1, "mixed": 2}
@@ -133,9 +155,10 @@ def main():
                      "build_ms": round(min(builds), 3), "radius": [], "knn": []}
             for r in p["radii"]:
                 for kern in p["kernels"]:
-                    res = radius_case(m, qd, samp, oracle, kern, r, samp.shape[0])
+                    fn = digest_case if p.get("digest") else radius_case
+                    res = fn(m, qd, samp, oracle, kern, r, samp.shape[0])
                     log(f"  cfg{c} {f} {res['kernel']} r={r}: {res['qps'] / 1e6:.1f} M q/s "
-                        f"parity={res['parity']} phases={res['phases']}")
+                        f"parity={res['parity']} phases={res.get('phases', res.get('mode'))}")
                     entry["radius"].append(res)
             for k in p["ks"]:
                 res = knn_case(m, qd, samp, oracle, k)
