@@ -102,11 +102,20 @@ __global__ void gather_kernel(const double* __restrict__ xyz, const K* __restric
   }
 }
 
+// Unique voxels: key, first record, z index; per-slice non-empty counts
+// (occupancy_stats, map.cpp:160-165) through a per-block shared-memory
+// histogram when the grid has few slices.
+constexpr uint32_t kSliceSmem = 8192;
 template <typename K>
 __global__ void unique_kernel(const K* __restrict__ keys, const uint32_t* __restrict__ flags,
                               const uint32_t* __restrict__ pos, uint64_t n, uint64_t nz,
                               uint64_t* __restrict__ ukey, uint32_t* __restrict__ ustart,
                               uint32_t* __restrict__ uk_k, unsigned long long* __restrict__ slice_ne) {
+  extern __shared__ uint32_t hist[];
+  const bool local = nz <= kSliceSmem;
+  if (local)
+    for (uint32_t i = threadIdx.x; i < nz; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
   for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < n;
        s += (uint64_t)gridDim.x * blockDim.x) {
     if (flags[s]) {
@@ -116,8 +125,14 @@ __global__ void unique_kernel(const K* __restrict__ keys, const uint32_t* __rest
       ustart[u] = (uint32_t)s;
       const uint32_t k = (uint32_t)(key % nz);
       if (uk_k) uk_k[u] = k;
-      atomicAdd(slice_ne + k, 1ull);
+      if (local) atomicAdd(hist + k, 1u);
+      else atomicAdd(slice_ne + k, 1ull);
     }
+  }
+  if (local) {
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < nz; i += blockDim.x)
+      if (hist[i]) atomicAdd(slice_ne + i, (unsigned long long)hist[i]);
   }
 }
 
@@ -265,7 +280,8 @@ cm_status build_typed(const double* xyz, uint64_t n, cudaStream_t st, cm_index* 
   CM_CUDA_TRY(cudaMemsetAsync(slice_ne, 0, g.nz * 8, st));
   const uint32_t n32 = (uint32_t)n;
   CM_CUDA_TRY(cudaMemcpyAsync(ix->ustart + U, &n32, 4, cudaMemcpyHostToDevice, st));
-  unique_kernel<K><<<grid_for(n), 256, 0, st>>>(keys, flags, pos, n, g.nz, ix->ukey, ix->ustart,
+  const size_t hsmem = g.nz <= kSliceSmem ? g.nz * 4 : 0;
+  unique_kernel<K><<<grid_for(n), 256, hsmem, st>>>(keys, flags, pos, n, g.nz, ix->ukey, ix->ustart,
                                                  ix->uk_k, slice_ne); ::cmg::note_launch();
   ix->slice_ne.assign(g.nz, 0);
   CM_CUDA_TRY(cudaMemcpyAsync(ix->slice_ne.data(), slice_ne, g.nz * 8, cudaMemcpyDeviceToHost, st));
