@@ -37,7 +37,12 @@ constexpr int kQThreads = 128;
 constexpr int kQWarps = kQThreads / 32;
 constexpr int kLaneRowCap = 96;                       // per-lane row buffer
 constexpr int kLaneSortMax = 32;                      // per-lane register sort up to
-constexpr int kRowWarpBytes = kLaneRowCap * 33 * 4;   // interleaved, stride 33
+// Per warp: the tile path's per-lane rows (u16 hit keys, interleaved with
+// stride 33) followed by the cp.async staging double buffer; the one-query
+// path reuses the whole region as a u32 buffer.
+constexpr int kRowKeyBytes = kLaneRowCap * 33 * 2;
+constexpr int kStageBytes = 64 * 32;
+constexpr int kRowWarpBytes = kRowKeyBytes + kStageBytes;
 constexpr int kRowCap = kRowWarpBytes / 4;            // one-query row buffer (u32)
 constexpr int kSortCap = (kRowCap - 512) / 2;         // one-query row sorted in smem
 constexpr int kBigSmemCap = 32768;                    // block sort in smem (128 KB)
@@ -570,9 +575,10 @@ __global__ void __launch_bounds__(kQThreads, 4) radius_tile_kernel(
   constexpr int so = ROWS ? 4 : 0;
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  uint32_t* srow = reinterpret_cast<uint32_t*>(smraw + (size_t)wib * kRowWarpBytes);
-  uint32_t* wbuf = srow;
-  PointRec* stg = reinterpret_cast<PointRec*>(smraw + (size_t)kQWarps * kRowWarpBytes) + wib * 64;
+  unsigned char* wreg = smraw + (size_t)wib * kRowWarpBytes;
+  uint16_t* skey = reinterpret_cast<uint16_t*>(wreg);  // hit = column << 11 | offset in span
+  uint32_t* wbuf = reinterpret_cast<uint32_t*>(wreg);
+  PointRec* stg = reinterpret_cast<PointRec*>(wreg + kRowKeyBytes);
   const uint32_t lt = lanemask_lt();
   const uint64_t ntiles = (nq + 31) / 32;
   const uint64_t W = (uint64_t)gridDim.x * kQWarps;
@@ -610,6 +616,8 @@ __global__ void __launch_bounds__(kQThreads, 4) radius_tile_kernel(
         if ((uint32_t)lane < ncol)
           column_span<FLAVOR>(t, I0 + lane / nj, J0 + lane % nj, K0, K1, &b, &e);
         total = __shfl_sync(0xffffffffu, warp_incl_scan(e - b), 31);
+        // row keys hold a 11-bit offset within a column span
+        if (ROWS && warp_max_u32(e - b) > 2048u) use_tile = false;
       }
     }
     if (lane == 0) {
@@ -663,6 +671,7 @@ __global__ void __launch_bounds__(kQThreads, 4) radius_tile_kernel(
       const SRec* sr = reinterpret_cast<const SRec*>(stg + buf * 32);
       const uint32_t len = min(32u, ce - p);
       const bool need = (colmask >> c) & 1u;
+      const uint32_t kbase = (c << 11) | (p - __shfl_sync(0xffffffffu, b, c));
       uint32_t u = 0;
       for (; u + 8 <= len; u += 8) {
         SRec v[8];
@@ -673,7 +682,7 @@ __global__ void __launch_bounds__(kQThreads, 4) radius_tile_kernel(
           const bool in = need & (v[w].meta - kk0 <= kspan);
           const bool hit = in & pred<CUBE>(P, v[w].x, v[w].y, v[w].z);
           if (MODE == MODE_DIGEST && hit) dig += mix64(v[w].id);
-          if (ROWS && hit && cnt < (uint32_t)kLaneRowCap) srow[cnt * 33 + lane] = v[w].id;
+          if (ROWS && hit && cnt < (uint32_t)kLaneRowCap) skey[cnt * 33 + lane] = (uint16_t)(kbase + u + w);
           cnt += hit;
           ntest += in;
         }
@@ -683,7 +692,7 @@ __global__ void __launch_bounds__(kQThreads, 4) radius_tile_kernel(
         const bool in = need & (v.meta - kk0 <= kspan);
         const bool hit = in & pred<CUBE>(P, v.x, v.y, v.z);
         if (MODE == MODE_DIGEST && hit) dig += mix64(v.id);
-        if (ROWS && hit && cnt < (uint32_t)kLaneRowCap) srow[cnt * 33 + lane] = v.id;
+        if (ROWS && hit && cnt < (uint32_t)kLaneRowCap) skey[cnt * 33 + lane] = (uint16_t)(kbase + u);
         cnt += hit;
         ntest += in;
       }
@@ -732,23 +741,33 @@ __global__ void __launch_bounds__(kQThreads, 4) radius_tile_kernel(
       __syncwarp();
       uint32_t* rows = MODE == MODE_FILL ? o.cols : o.temp;
       if (write_ok) {
-        if (MODE == MODE_COLLECT) {
-          // arena rows go out unsorted; the gather kernel sorts them
-          __syncwarp();
-          for (int l = 0; l < 32; ++l) {
-            const uint32_t len = __shfl_sync(0xffffffffu, mine, l);
-            const uint64_t off = __shfl_sync(0xffffffffu, dst, l);
-            for (uint32_t i = lane; i < len; i += 32) rows[off + i] = srow[i * 33 + l];
+        // hit keys -> handles (the records were just walked: L1/L2 hits)
+        __syncwarp();
+        for (int l = 0; l < 32; ++l) {
+          const uint32_t len = __shfl_sync(0xffffffffu, mine, l);
+          const uint64_t off = __shfl_sync(0xffffffffu, dst, l);
+          if (len == 0) continue;
+          uint32_t v[4];
+#pragma unroll
+          for (int r2 = 0; r2 < 4; ++r2) {
+            const uint32_t i = r2 * 32 + lane;
+            const uint32_t key = i < len ? skey[i * 33 + l] : 0u;
+            const uint32_t cb2 = __shfl_sync(0xffffffffu, b, key >> 11);
+            v[r2] = i < len ? __ldg(&rec[cb2 + (key & 2047u)].id) : 0xffffffffu;
           }
-        } else {
-          __syncwarp();
-          for (int l = 0; l < 32; ++l) {
-            const uint32_t len = __shfl_sync(0xffffffffu, mine, l);
-            const uint64_t off = __shfl_sync(0xffffffffu, dst, l);
-            if (len == 0) continue;
-            if (len <= 32) warp_sort_row_out<1>(srow, l, len, rows + off, lane);
-            else if (len <= 64) warp_sort_row_out<2>(srow, l, len, rows + off, lane);
-            else warp_sort_row_out<4>(srow, l, len, rows + off, lane);
+          if (MODE == MODE_COLLECT) {  // arena rows go out unsorted; the gather sorts
+#pragma unroll
+            for (int r2 = 0; r2 < 4; ++r2) {
+              const uint32_t i = r2 * 32 + lane;
+              if (i < len) rows[off + i] = v[r2];
+            }
+          } else {
+            warp_sort_regs<4>(v, lane);
+#pragma unroll
+            for (int r2 = 0; r2 < 4; ++r2) {
+              const uint32_t i = r2 * 32 + lane;
+              if (i < len) rows[off + i] = v[r2];
+            }
           }
         }
       }
@@ -919,7 +938,7 @@ template <int MODE>
 cm_status launch_radius(const cm_index* ix, const double* q, uint64_t nq, int kernel, double r,
                         const uint32_t* perm, const Out& o, cudaStream_t st) {
   const Tables t = ix->tables();
-  const size_t smem = (size_t)kQWarps * (kRowWarpBytes + 64 * sizeof(PointRec));
+  const size_t smem = (size_t)kQWarps * kRowWarpBytes;
   auto run = [&](auto kern) -> cm_status {
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
