@@ -198,26 +198,38 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one process per GPU; BENCH_DIST_BACKEND=gloo lets several ranks share
+    # one GPU for a functional check of the N > 1 path (no kernel waits on
+    # another rank: collectives run on the host)
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    cdev = dev if backend == "nccl" else torch.device("cpu")
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            if backend == "nccl":
+                dist.barrier(device_ids=[local])
+            else:
+                dist.barrier()
 
     def allmax(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
     def allsum(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return float(t.item())
 
@@ -250,11 +262,18 @@ def main():
         build_detail[name] = {k: round(v, 3) for k, v in best.items()}
     log(f"[rank {rank}] build ms {build_ms}")
 
-    # ---- this rank's queries: a contiguous block of the cloud
+    # ---- this rank's queries: an equal-count x-slab of the cloud, so each
+    # rank's share stays spatially dense (query tiles stay compact)
     nq_total = cloud.shape[0]
     lo = nq_total * rank // world
     hi = nq_total * (rank + 1) // world
-    q_dev = d_cloud[lo:hi]
+    if world > 1:
+        shard = torch.argsort(d_cloud[:, 0], stable=True)[lo:hi]
+        q_dev = d_cloud[shard].contiguous()
+        shard_host = shard.cpu().numpy()
+    else:
+        q_dev = d_cloud
+        shard_host = None
     nq = hi - lo
 
     # algorithmic bytes: 24 B x the reference's points_tested for these queries
@@ -345,7 +364,8 @@ def main():
     # ---- end to end through the C ABI with host buffers
     e2e = None
     if not a.no_e2e:
-        q_host = torch.from_numpy(np.ascontiguousarray(cloud[lo:hi])).pin_memory()
+        q_host = torch.from_numpy(np.ascontiguousarray(
+            cloud if shard_host is None else cloud[shard_host])).pin_memory()
         row_host = torch.empty(nq + 1, dtype=torch.int64).pin_memory()
         cols_host = torch.empty(max(nnz_rank, 1), dtype=torch.int32).pin_memory()
 
@@ -404,7 +424,8 @@ def main():
                        "n_points": int(cloud.shape[0]), "n_queries": nq_total,
                        "neighbours": nnz_total, "radius_m": a.radius, "kernel": a.kernel,
                        "l2": "flushed (256 MB write) before every timed step",
-                       "parallelism": f"replicated index, queries sharded x{world}"},
+                       "parallelism": f"replicated index, queries sharded x{world} "
+                                      "(equal-count x-slabs)"},
             "build_ms": {k: round(v, 3) for k, v in build_ms.items()},
             "build_detail": build_detail,
             "phases_ms": phase,
