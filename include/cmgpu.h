@@ -62,9 +62,11 @@ typedef enum {
 typedef enum { CM_DENSE = 0, CM_SPARSE = 1, CM_MIXED = 2 } cm_flavor;
 /* grid.hpp:10 */
 typedef enum { CM_TWOD = 0, CM_THREED = 1 } cm_grid_mode;
-/* geometry.hpp:73-92: SphereKernel{c, r}; BoxKernel{{c-r}, {c+r}} (the cube
- * the reference CLI/tests build, cmd_bench.cpp:107-111) */
-typedef enum { CM_SPHERE = 0, CM_CUBE = 1 } cm_kernel;
+/* geometry.hpp:73-113: SphereKernel{c, r}; BoxKernel{{c-r}, {c+r}} (the cube
+ * the reference CLI/tests build, cmd_bench.cpp:107-111); CylinderKernel
+ * {c.x, c.y, r} with the default unbounded z range (the kernel
+ * weighted_density uses, analysis.cpp:55-59; c.z is ignored) */
+typedef enum { CM_SPHERE = 0, CM_CUBE = 1, CM_CYLINDER = 2 } cm_kernel;
 
 /* BuildOptions, field for field (map.hpp:17-26). `reorder` is accepted and
  * ignored: the device index is always stored in cell order, and results are
@@ -191,6 +193,20 @@ cm_status cm_radius_digest(const cm_index* index, const double* q, uint64_t nq,
  * cloud with fewer than k points are padded with UINT32_MAX / +inf. */
 cm_status cm_knn(const cm_index* index, const double* q, uint64_t nq, uint32_t k,
                  uint32_t* idx, double* d2, void* stream);
+
+/* Dataset density metrics (analysis.hpp:17-35), the cylinder-kernel caller
+ * of the index.
+ * global_density (analysis.cpp:17-24): points per m^2 of the xy bounding
+ * rectangle; CM_INVALID_ARGUMENT for a zero-area rectangle.
+ * weighted_density (analysis.cpp:26-86): over all points (sample_size = 0)
+ * or a seeded subsample (the reference's partial Fisher-Yates with
+ * mt19937_64(seed)), count the points in a vertical 1 m cylinder (2D sparse
+ * map, 1 m cells), bin count/pi into bins256[256] (last bin clamps) and
+ * return the histogram-weighted mean bin in *value. Synchronous. */
+cm_status cm_global_density(const double* xyz, uint64_t n, int device, void* stream,
+                            double* value);
+cm_status cm_weighted_density(const double* xyz, uint64_t n, uint64_t sample_size, uint64_t seed,
+                              int device, void* stream, double* value, uint64_t* bins256);
 
 /* Test hook (map.cpp:194-223): drops one stored handle from the first
  * non-empty voxel so verification harnesses can prove they detect it. */

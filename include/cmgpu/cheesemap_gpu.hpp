@@ -12,7 +12,8 @@
 //  * knn_search orders ties by handle (the reference keeps insertion order,
 //    search.cpp:16-28); distances are sqrt of the same fp64 d^2;
 //  * BoxKernel is the cube {c - r, c + r} (what the reference CLI and tests
-//    build, cmd_bench.cpp:107-111); CylinderKernel is not offered;
+//    build, cmd_bench.cpp:107-111); CylinderKernel keeps the default
+//    unbounded z range (the one weighted_density uses);
 //  * the map owns device copies of the points (the cloud need not outlive it).
 #pragma once
 
@@ -66,6 +67,9 @@ struct BoxKernel {  // the cube {c - r, c + r}
   Point3 center;
   double half = 0.0;
   static BoxKernel cube(const Point3& c, double r) { return {c, r}; }
+};
+struct CylinderKernel {  // vertical, unbounded z range (geometry.hpp:97-113)
+  double center_x = 0.0, center_y = 0.0, radius = 0.0;
 };
 
 // ------------------------------------------------------ grid.hpp, map.hpp --
@@ -220,6 +224,36 @@ inline std::vector<PointHandle> kernel_search(const Cheesemap& m, const SphereKe
 inline std::vector<PointHandle> kernel_search(const Cheesemap& m, const BoxKernel& k) {
   const Csr c = radius_search(m, {k.center}, k.half, CM_CUBE);
   return {c.cols.begin(), c.cols.end()};
+}
+
+inline std::vector<PointHandle> kernel_search(const Cheesemap& m, const CylinderKernel& k) {
+  const Csr c = radius_search(m, {Point3{k.center_x, k.center_y, 0.0}}, k.radius, CM_CYLINDER);
+  return {c.cols.begin(), c.cols.end()};
+}
+
+// ---------------------------------------------------------- analysis.hpp --
+struct DensityHistogram {
+  std::uint64_t bins[256] = {};
+};
+struct WeightedDensity {
+  double value = 0.0;
+  DensityHistogram histogram;
+};
+
+inline double global_density(const PointCloud& cloud, int device = 0) {
+  double v = 0.0;
+  check(cm_global_density(reinterpret_cast<const double*>(cloud.data()), cloud.size(), device,
+                          nullptr, &v));
+  return v;
+}
+
+inline WeightedDensity weighted_density(const PointCloud& cloud, std::uint64_t sample_size = 0,
+                                        std::uint64_t sample_seed = 0, int device = 0) {
+  WeightedDensity wd;
+  check(cm_weighted_density(reinterpret_cast<const double*>(cloud.data()), cloud.size(),
+                            sample_size, sample_seed, device, nullptr, &wd.value,
+                            wd.histogram.bins));
+  return wd;
 }
 
 // (idx, d2) rows of width k, ordered by (d2, handle).

@@ -19,7 +19,9 @@
 #include <cstdint>
 #include <cstring>
 #include <numbers>
+#include <limits>
 #include <optional>
+#include <random>
 #include <thread>
 #include <unordered_map>
 #include <vector>
@@ -190,6 +192,20 @@ void kernel_search(const orc_index& m, const Box& kbox, Inside&& inside, Emit&& 
 // (cmd_bench.cpp:107-111, test_search.cpp:177): the same box for both.
 inline Box radius_box(const P3& c, double r) {
   return {{c.x - r, c.y - r, c.z - r}, {c.x + r, c.y + r, c.z + r}};
+}
+
+// CylinderKernel{c.x, c.y, r} with the default unbounded z range
+// (geometry.hpp:97-113): box (c.x +- r, c.y +- r, -inf..inf), member iff
+// z in range && squared_distance_xy <= r*r (geometry.hpp:39-43).
+inline Box cylinder_box(const P3& c, double r) {
+  const double inf = std::numeric_limits<double>::infinity();
+  return {{c.x - r, c.y - r, -inf}, {c.x + r, c.y + r, inf}};
+}
+inline bool in_cylinder(const P3& p, const P3& c, double rr) {
+  const double inf = std::numeric_limits<double>::infinity();
+  const double dx = p.x - c.x;
+  const double dy = p.y - c.y;
+  return p.z >= -inf && p.z <= inf && dx * dx + dy * dy <= rr;
 }
 
 template <class F>
@@ -467,7 +483,7 @@ uint64_t orc_mix64(uint64_t x) { return mix64(x); }
 int orc_radius(const orc_index* m, const double* q, uint64_t nq, int kernel, double r,
                unsigned threads, uint32_t* counts, uint64_t* digests,
                uint64_t* points_tested, uint64_t* voxels_visited) {
-  if (kernel != 0 && kernel != 1) return INVALID_ARGUMENT;
+  if (kernel < 0 || kernel > 2) return INVALID_ARGUMENT;
   const double rr = r * r;
   parallel_queries(nq, threads, [&](std::uint64_t qi) {
     const P3 c{q[3 * qi], q[3 * qi + 1], q[3 * qi + 2]};
@@ -480,8 +496,11 @@ int orc_radius(const orc_index* m, const double* q, uint64_t nq, int kernel, dou
     };
     if (kernel == 0)
       kernel_search(*m, kb, [&](const P3& p) { return sqdist(p, c) <= rr; }, emit, &st);
-    else
+    else if (kernel == 1)
       kernel_search(*m, kb, [&](const P3& p) { return box_contains(kb, p); }, emit, &st);
+    else
+      kernel_search(*m, cylinder_box(c, r), [&](const P3& p) { return in_cylinder(p, c, rr); },
+                    emit, &st);
     if (counts) counts[qi] = static_cast<uint32_t>(cnt);
     if (digests) digests[qi] = dig;
     if (points_tested) points_tested[qi] = st.tested;
@@ -494,7 +513,7 @@ int orc_radius(const orc_index* m, const double* q, uint64_t nq, int kernel, dou
 // tests/test_util.hpp:30-35) written at row_ptr[q] (row_ptr from the counts).
 int orc_radius_fill(const orc_index* m, const double* q, uint64_t nq, int kernel, double r,
                     unsigned threads, const uint64_t* row_ptr, uint32_t* cols) {
-  if (kernel != 0 && kernel != 1) return INVALID_ARGUMENT;
+  if (kernel < 0 || kernel > 2) return INVALID_ARGUMENT;
   const double rr = r * r;
   parallel_queries(nq, threads, [&](std::uint64_t qi) {
     const P3 c{q[3 * qi], q[3 * qi + 1], q[3 * qi + 2]};
@@ -504,8 +523,11 @@ int orc_radius_fill(const orc_index* m, const double* q, uint64_t nq, int kernel
     auto emit = [&](std::uint64_t h) { hits.push_back(static_cast<uint32_t>(h)); };
     if (kernel == 0)
       kernel_search(*m, kb, [&](const P3& p) { return sqdist(p, c) <= rr; }, emit, &st);
-    else
+    else if (kernel == 1)
       kernel_search(*m, kb, [&](const P3& p) { return box_contains(kb, p); }, emit, &st);
+    else
+      kernel_search(*m, cylinder_box(c, r), [&](const P3& p) { return in_cylinder(p, c, rr); },
+                    emit, &st);
     std::sort(hits.begin(), hits.end());
     std::copy(hits.begin(), hits.end(), cols + row_ptr[qi]);
   });
@@ -554,6 +576,52 @@ int orc_knn(const orc_index* m, const double* q, uint64_t nq, uint32_t k, unsign
       points_tested_rk[qi] = st3.tested;
     }
   });
+  return OK;
+}
+
+// weighted_density (analysis.cpp:26-86): optional seeded subsample (partial
+// Fisher-Yates with mt19937_64, :36-45), a 2D sparse map at 1 m, per sampled
+// point the count of points in a vertical 1 m cylinder, local density
+// count / pi floored into 256 bins (last bin clamps), value = histogram-
+// weighted mean of the bin indices.
+int orc_weighted_density(const double* xyz, uint64_t n, uint64_t sample_size, uint64_t seed,
+                         unsigned threads, double* value, uint64_t* bins256) {
+  if (n == 0) return EMPTY_CLOUD;
+  std::vector<std::uint64_t> sample;
+  if (sample_size && sample_size < n) {
+    sample.resize(n);
+    for (std::uint64_t i = 0; i < n; ++i) sample[i] = i;
+    std::mt19937_64 eng(seed);
+    for (std::uint64_t i = 0; i < sample_size; ++i) {
+      const std::uint64_t j = i + eng() % (sample.size() - i);
+      std::swap(sample[i], sample[j]);
+    }
+    sample.resize(sample_size);
+  } else {
+    sample.resize(n);
+    for (std::uint64_t i = 0; i < n; ++i) sample[i] = i;
+  }
+  orc_index* m = nullptr;
+  int s = orc_build(xyz, n, 1, 0, 1.0, 1.0, 1.0, 0.8, 1ull << 32, &m);
+  if (s) return s;
+  std::vector<double> q(3 * sample.size());
+  for (std::size_t i = 0; i < sample.size(); ++i)
+    for (int a = 0; a < 3; ++a) q[3 * i + a] = xyz[3 * sample[i] + a];
+  std::vector<uint32_t> counts(sample.size());
+  orc_radius(m, q.data(), sample.size(), 2, 1.0, threads, counts.data(), nullptr, nullptr, nullptr);
+  orc_free(m);
+  for (int b = 0; b < 256; ++b) bins256[b] = 0;
+  for (uint32_t c : counts) {
+    const double local = static_cast<double>(c) / std::numbers::pi;
+    const auto bin = std::min<std::uint64_t>(255, static_cast<std::uint64_t>(local));
+    ++bins256[bin];
+  }
+  std::uint64_t ws = 0, tot = 0;
+  for (int b = 0; b < 256; ++b) {
+    ws += b * bins256[b];
+    tot += bins256[b];
+  }
+  *value = static_cast<double>(ws) / static_cast<double>(tot);
   return OK;
 }
 

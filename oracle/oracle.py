@@ -43,6 +43,8 @@ class CpuIndexLib:
         self.radius_ = f("radius", [p, p, u64, i, dbl, ctypes.c_uint, p, p, p, p], i)
         self.radius_fill_ = f("radius_fill", [p, p, u64, i, dbl, ctypes.c_uint, p, p], i)
         self.knn_ = f("knn", [p, p, u64, u32, ctypes.c_uint, p, p, p, p], i)
+        self.weighted_density_ = f("weighted_density",
+                                   [p, u64, u64, u64, ctypes.c_uint, ctypes.POINTER(dbl), p], i)
         self.lib = lib
 
 
@@ -141,3 +143,16 @@ class CpuIndex:
         if rc:
             raise RuntimeError(STATUS.get(rc, rc))
         return (idx, d2, prk, pa2) if stats else (idx, d2)
+
+
+def weighted_density(xyz, sample_size=0, seed=0, which="oracle", threads=0):
+    """(value, bins[256]) from the restatement or the reference."""
+    L = lib(which)
+    xyz = np.ascontiguousarray(xyz, dtype=np.float64).reshape(-1, 3)
+    v = ctypes.c_double()
+    bins = np.zeros(256, dtype=np.uint64)
+    rc = L.weighted_density_(_p(xyz), xyz.shape[0], sample_size, seed, threads, ctypes.byref(v),
+                             _p(bins))
+    if rc:
+        raise RuntimeError(STATUS.get(rc, rc), rc)
+    return v.value, bins

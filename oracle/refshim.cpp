@@ -17,6 +17,7 @@
 #include <thread>
 #include <vector>
 
+#include "cheesemap/analysis.hpp"
 #include "cheesemap/io.hpp"
 #include "cheesemap/map.hpp"
 #include "cheesemap/search.hpp"
@@ -83,6 +84,13 @@ struct NoneKernel {
 std::vector<PointHandle> run_kernel(const Cheesemap& m, int kernel, const Point3& c, double r,
                                     QueryStats* st) {
   if (kernel == 0) return kernel_search(m, SphereKernel{c, r}, st);
+  if (kernel == 2) {
+    CylinderKernel k;
+    k.center_x = c.x;
+    k.center_y = c.y;
+    k.radius = r;
+    return kernel_search(m, k, st);
+  }
   const Aabb b{{c.x - r, c.y - r, c.z - r}, {c.x + r, c.y + r, c.z + r}};
   return kernel_search(m, BoxKernel{b}, st);
 }
@@ -178,7 +186,7 @@ void ref_export(const ref_index* r, uint64_t* keys, uint64_t* handles) {
 int ref_radius(const ref_index* r, const double* q, uint64_t nq, int kernel, double rad,
                unsigned threads, uint32_t* counts, uint64_t* digests, uint64_t* points_tested,
                uint64_t* voxels_visited) {
-  if (kernel != 0 && kernel != 1) return 2;
+  if (kernel < 0 || kernel > 2) return 2;
   parallel_queries(nq, threads, [&](std::uint64_t qi) {
     QueryStats st;
     const auto res = run_kernel(*r->map, kernel, {q[3 * qi], q[3 * qi + 1], q[3 * qi + 2]}, rad, &st);
@@ -196,7 +204,7 @@ int ref_radius(const ref_index* r, const double* q, uint64_t nq, int kernel, dou
 
 int ref_radius_fill(const ref_index* r, const double* q, uint64_t nq, int kernel, double rad,
                     unsigned threads, const uint64_t* row_ptr, uint32_t* cols) {
-  if (kernel != 0 && kernel != 1) return 2;
+  if (kernel < 0 || kernel > 2) return 2;
   parallel_queries(nq, threads, [&](std::uint64_t qi) {
     auto res = run_kernel(*r->map, kernel, {q[3 * qi], q[3 * qi + 1], q[3 * qi + 2]}, rad, nullptr);
     std::sort(res.begin(), res.end());  // tests/test_util.hpp:30-35
@@ -234,6 +242,22 @@ int ref_knn(const ref_index* r, const double* q, uint64_t nq, uint32_t k, unsign
       points_tested_rk[qi] = s3.points_tested;
     }
   });
+  return 0;
+}
+
+// The reference's own weighted_density (analysis.cpp:26-86).
+int ref_weighted_density(const double* xyz, uint64_t n, uint64_t sample_size, uint64_t seed,
+                         unsigned /*threads*/, double* value, uint64_t* bins256) {
+  PointCloud cloud(n);
+  if (n) std::memcpy(cloud.data(), xyz, n * sizeof(Point3));
+  try {
+    const WeightedDensity wd = sample_size ? weighted_density(cloud, sample_size, seed)
+                                           : weighted_density(cloud);
+    *value = wd.value;
+    for (int b = 0; b < 256; ++b) bins256[b] = wd.histogram.bins[b];
+  } catch (const std::exception& e) {
+    return status_of(e);
+  }
   return 0;
 }
 

@@ -18,6 +18,7 @@ EXPORTS = [
     "cm_radius_search", "cm_radius_search_to_host", "cm_csr_info", "cm_csr_download", "cm_csr_free", "cm_radius_digest",
     "cm_knn", "cm_corrupt_for_testing", "cm_last_error", "cm_status_name",
     "cm_get_last_query_timing", "cm_launch_count", "cm_debug_query_stats",
+    "cm_global_density", "cm_weighted_density",
 ]
 
 
@@ -89,6 +90,8 @@ def lib():
         "cm_radius_search_to_host": ([p, p, u64, i32, dbl, p, p, u64, ctypes.POINTER(u64), p], i32),
         "cm_radius_digest": ([p, p, u64, i32, dbl, p, p, p], i32),
         "cm_knn": ([p, p, u64, u32, p, p, p], i32),
+        "cm_global_density": ([p, u64, i32, p, ctypes.POINTER(dbl)], i32),
+        "cm_weighted_density": ([p, u64, u64, u64, i32, p, ctypes.POINTER(dbl), p], i32),
         "cm_corrupt_for_testing": ([p], i32),
         "cm_last_error": ([], ctypes.c_char_p),
         "cm_status_name": ([i32], ctypes.c_char_p),

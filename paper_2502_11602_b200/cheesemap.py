@@ -123,12 +123,19 @@ class BoxKernel:  # geometry.hpp:87-92; the device path takes cubes c +- r
 
 
 @dataclass
+class CylinderKernel:  # geometry.hpp:97-113, unbounded z (the weighted_density kernel)
+    center_x: float
+    center_y: float
+    radius: float
+
+
+@dataclass
 class Neighbor:  # search.hpp:19-24 (distance = sqrt of the fp64 d^2)
     handle: int
     distance: float
 
 
-SPHERE, CUBE = 0, 1
+SPHERE, CUBE, CYLINDER = 0, 1, 2
 
 
 # -------------------------------------------------------------- buffers --
@@ -246,7 +253,10 @@ def _kernel_args(kernel):
         return np.asarray(kernel.center, dtype=np.float64).reshape(1, 3), SPHERE, kernel.radius
     if isinstance(kernel, BoxKernel):
         return np.asarray(kernel.center, dtype=np.float64).reshape(1, 3), CUBE, kernel.half
-    raise InvalidArgumentError("kernel must be SphereKernel or BoxKernel.cube")
+    if isinstance(kernel, CylinderKernel):
+        c = np.array([[kernel.center_x, kernel.center_y, 0.0]])
+        return c, CYLINDER, kernel.radius
+    raise InvalidArgumentError("kernel must be SphereKernel, BoxKernel.cube or CylinderKernel")
 
 
 def radius_count(m, centers, r, kernel=SPHERE, counts=None, points_tested=None, stream=None):
@@ -330,3 +340,23 @@ def knn_search(m, c, k):
     idx, d2 = knn_batch(m, np.asarray(c, dtype=np.float64).reshape(1, 3), k)
     return [Neighbor(int(i), float(np.sqrt(d))) for i, d in zip(idx[0], d2[0])
             if i != 0xFFFFFFFF]
+
+
+# -------------------------------------------------------------- analysis --
+def global_density(cloud, device=0):
+    """global_density (analysis.cpp:17-24): points per m^2 of the xy box."""
+    p, keep = _in_ptr(cloud)
+    v = ctypes.c_double()
+    _check(_native.lib().cm_global_density(p, _nrows(keep), device, None, ctypes.byref(v)))
+    return v.value
+
+
+def weighted_density(cloud, sample_size=None, sample_seed=0, device=0):
+    """weighted_density (analysis.cpp:26-86) -> (value, bins[256])."""
+    p, keep = _in_ptr(cloud)
+    v = ctypes.c_double()
+    bins = np.zeros(256, dtype=np.uint64)
+    _check(_native.lib().cm_weighted_density(p, _nrows(keep), int(sample_size or 0),
+                                             int(sample_seed), device, None, ctypes.byref(v),
+                                             bins.ctypes.data_as(ctypes.c_void_p)))
+    return v.value, bins

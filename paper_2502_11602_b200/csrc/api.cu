@@ -6,6 +6,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <random>
 #include <string>
 #include <vector>
 
@@ -164,8 +165,8 @@ cm_status check_index(const cm_index* ix) {
 }
 
 cm_status check_kernel(int kernel) {
-  if (kernel != CM_SPHERE && kernel != CM_CUBE) {
-    set_error("unknown kernel (CM_SPHERE = 0, CM_CUBE = 1)");
+  if (kernel != CM_SPHERE && kernel != CM_CUBE && kernel != CM_CYLINDER) {
+    set_error("unknown kernel (CM_SPHERE = 0, CM_CUBE = 1, CM_CYLINDER = 2)");
     return CM_INVALID_ARGUMENT;
   }
   return CM_OK;
@@ -869,6 +870,114 @@ cm_status cm_radius_digest(const cm_index* ix, const double* q, uint64_t nq, int
   CM_TRY(c.finish());
   CM_TRY(d.finish());
   return sync_if(c.host() || d.host(), st);
+}
+
+// global_density (analysis.cpp:17-24): points per m^2 of the xy bounding
+// rectangle, from a device-built index's bounds.
+cm_status cm_global_density(const double* xyz, uint64_t n, int device, void* stream,
+                            double* value) {
+  if (!value) {
+    set_error("null output");
+    return CM_INVALID_ARGUMENT;
+  }
+  cm_build_options o;
+  cm_default_options(&o);
+  o.flavor = CM_SPARSE;
+  o.mode = CM_TWOD;
+  cm_index* ix = nullptr;
+  CM_TRY(cm_build(xyz, n, &o, device, stream, &ix));
+  const DevGrid& g = ix->g;
+  const double area = (g.bx1 - g.bx0) * (g.by1 - g.by0);
+  cm_free(ix);
+  if (!(area > 0.0)) {
+    set_error("bounding rectangle has zero area");
+    return CM_INVALID_ARGUMENT;
+  }
+  *value = static_cast<double>(n) / area;
+  return CM_OK;
+}
+
+// weighted_density (analysis.cpp:26-86) on the device: the seeded subsample
+// (host, the reference's partial Fisher-Yates over mt19937_64), a 2D sparse
+// map at 1 m, cylinder counts for every sampled point (the COUNT pass with
+// CM_CYLINDER r = 1), then the 256-bin histogram and its weighted mean.
+cm_status cm_weighted_density(const double* xyz, uint64_t n, uint64_t sample_size, uint64_t seed,
+                              int device, void* stream, double* value, uint64_t* bins256) {
+  if (!value || !bins256) {
+    set_error("null output");
+    return CM_INVALID_ARGUMENT;
+  }
+  if (n == 0) {
+    set_error("point cloud is empty");
+    return CM_EMPTY_CLOUD;
+  }
+  if (!xyz) {
+    set_error("null point pointer");
+    return CM_INVALID_ARGUMENT;
+  }
+  cm_build_options o;
+  cm_default_options(&o);
+  o.flavor = CM_SPARSE;
+  o.mode = CM_TWOD;
+  cm_index* ix = nullptr;
+  CM_TRY(cm_build(xyz, n, &o, device, stream, &ix));
+  DeviceGuard dg(device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  struct Cleanup {
+    cm_index* ix;
+    std::vector<void*> bufs;
+    cudaStream_t st;
+    ~Cleanup() {
+      for (void* p : bufs) dev_free(p, st);
+      cudaStreamSynchronize(st);
+      cm_free(ix);
+    }
+  } cl{ix, {}, st};
+  InBuf in;
+  CM_TRY(stage_input(xyz, n * 24, st, &in));
+  const double* qd = static_cast<const double*>(in.dev);
+  uint64_t nq = n;
+  if (sample_size && sample_size < n) {
+    std::vector<uint64_t> sample(n);
+    for (uint64_t i = 0; i < n; ++i) sample[i] = i;
+    std::mt19937_64 eng(seed);
+    for (uint64_t i = 0; i < sample_size; ++i) {
+      const uint64_t j = i + eng() % (sample.size() - i);
+      std::swap(sample[i], sample[j]);
+    }
+    nq = sample_size;
+    uint64_t* didx = nullptr;
+    double* dq = nullptr;
+    CM_CUDA_TRY(dev_alloc_t(&didx, nq, st));
+    cl.bufs.push_back(didx);
+    CM_CUDA_TRY(dev_alloc_t(&dq, nq * 3, st));
+    cl.bufs.push_back(dq);
+    CM_CUDA_TRY(cudaMemcpyAsync(didx, sample.data(), nq * 8, cudaMemcpyHostToDevice, st));
+    CM_TRY(gather_points_dev(qd, didx, nq, dq, st));
+    CM_CUDA_TRY(cudaStreamSynchronize(st));  // `sample` goes out of scope
+    qd = dq;
+  }
+  uint32_t* counts = nullptr;
+  unsigned long long* bins = nullptr;
+  CM_CUDA_TRY(dev_alloc_t(&counts, nq, st));
+  cl.bufs.push_back(counts);
+  CM_CUDA_TRY(dev_alloc_t(&bins, 256, st));
+  cl.bufs.push_back(bins);
+  QueryOrder ord;
+  CM_TRY(order_queries(ix, qd, nq, st, &ord));
+  CM_TRY(radius_count_dev(ix, qd, nq, CM_CYLINDER, 1.0, ord.perm, counts, nullptr, st));
+  CM_TRY(density_histogram_dev(counts, nq, bins, st));
+  unsigned long long hb[256];
+  CM_CUDA_TRY(cudaMemcpyAsync(hb, bins, sizeof(hb), cudaMemcpyDeviceToHost, st));
+  CM_CUDA_TRY(cudaStreamSynchronize(st));
+  uint64_t ws = 0, tot = 0;
+  for (int b = 0; b < 256; ++b) {
+    bins256[b] = hb[b];
+    ws += (uint64_t)b * hb[b];
+    tot += hb[b];
+  }
+  *value = static_cast<double>(ws) / static_cast<double>(tot);
+  return CM_OK;
 }
 
 cm_status cm_knn(const cm_index* ix, const double* q, uint64_t nq, uint32_t k, uint32_t* idx,

@@ -68,11 +68,25 @@ __device__ __forceinline__ double std_min(double a, double b) { return (b < a) ?
 // The query box of both kernels: c +- r per axis (geometry.hpp:77-80,
 // cmd_bench.cpp:107-111), then clamped_range (grid.cpp:90-114) including the
 // intersects() test against the bounds (geometry.hpp:53-56).
+// Kernel kinds: 0 SphereKernel{c, r}, 1 BoxKernel{c - r, c + r}, 2 CylinderKernel
+// {c.x, c.y, r} with an unbounded z range (geometry.hpp:97-113; its
+// infinite box is clamped to the grid by clamped_range).
+__device__ __forceinline__ void kernel_zbox(int kind, double cz, double r, double* lz, double* hz) {
+  if (kind == 2) {
+    *lz = __longlong_as_double(0xfff0000000000000ll);  // -inf
+    *hz = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+  } else {
+    *lz = __dsub_rn(cz, r);
+    *hz = __dadd_rn(cz, r);
+  }
+}
+
 __device__ __forceinline__ bool clamped_range(const DevGrid& g, double cx, double cy, double cz,
-                                              double r, Range* out) {
+                                              double r, Range* out, int kind = 0) {
   const double lx = __dsub_rn(cx, r), hx = __dadd_rn(cx, r);
   const double ly = __dsub_rn(cy, r), hy = __dadd_rn(cy, r);
-  const double lz = __dsub_rn(cz, r), hz = __dadd_rn(cz, r);
+  double lz, hz;
+  kernel_zbox(kind, cz, r, &lz, &hz);
   if (!(lx <= g.bx1 && hx >= g.bx0 && ly <= g.by1 && hy >= g.by0 && lz <= g.bz1 &&
         hz >= g.bz0))
     return false;
@@ -93,10 +107,12 @@ __device__ __forceinline__ bool clamped_range(const DevGrid& g, double cx, doubl
 // 0..5 each do one of the six IEEE divisions, then broadcast. Same
 // arithmetic as clamped_range.
 __device__ __forceinline__ bool clamped_range_warp(const DevGrid& g, double cx, double cy,
-                                                   double cz, double r, int lane, Range* out) {
+                                                   double cz, double r, int lane, Range* out,
+                                                   int kind = 0) {
   const double lx = __dsub_rn(cx, r), hx = __dadd_rn(cx, r);
   const double ly = __dsub_rn(cy, r), hy = __dadd_rn(cy, r);
-  const double lz = __dsub_rn(cz, r), hz = __dadd_rn(cz, r);
+  double lz, hz;
+  kernel_zbox(kind, cz, r, &lz, &hz);
   if (!(lx <= g.bx1 && hx >= g.bx0 && ly <= g.by1 && hy >= g.by0 && lz <= g.bz1 &&
         hz >= g.bz0))
     return false;
@@ -137,12 +153,13 @@ struct Predicate {
   double lx, ly, lz, hx, hy, hz;      // c -+ r (cube)
   int cube;
 
-  __device__ __forceinline__ void init(double x, double y, double z, double r, int is_cube) {
+  __device__ __forceinline__ void init(double x, double y, double z, double r, int kind) {
     cx = x, cy = y, cz = z;
     rr = __dmul_rn(r, r);
-    lx = __dsub_rn(x, r), ly = __dsub_rn(y, r), lz = __dsub_rn(z, r);
-    hx = __dadd_rn(x, r), hy = __dadd_rn(y, r), hz = __dadd_rn(z, r);
-    cube = is_cube;
+    lx = __dsub_rn(x, r), ly = __dsub_rn(y, r);
+    hx = __dadd_rn(x, r), hy = __dadd_rn(y, r);
+    kernel_zbox(kind, z, r, &lz, &hz);
+    cube = kind;
   }
   __device__ __forceinline__ bool operator()(double px, double py, double pz) const {
     if (cube)

@@ -119,6 +119,10 @@ cm_status counts_to_row_ptr(const uint32_t* counts_dev, uint64_t nq, uint64_t* r
 cm_status knn_dev(const cm_index* ix, const double* q_dev, uint64_t nq, uint32_t k,
                   const uint32_t* perm, uint32_t* idx_dev, double* d2_dev, cudaStream_t st);
 
+cm_status density_histogram_dev(const uint32_t* counts, uint64_t n, unsigned long long* bins,
+                                cudaStream_t st);
+cm_status gather_points_dev(const double* xyz, const uint64_t* idx, uint64_t n, double* out,
+                            cudaStream_t st);
 int sm_count();
 void query_stats(uint64_t* out, int reset);
 

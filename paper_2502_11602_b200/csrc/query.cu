@@ -246,9 +246,13 @@ __device__ __forceinline__ void warp_sort_row_out(const uint32_t* srow, int l, u
 
 template <int CUBE>
 __device__ __forceinline__ bool pred(const Predicate& P, double x, double y, double z) {
-  if (CUBE)
+  if (CUBE == 1)  // closed box (geometry.hpp:48-51)
     return (x >= P.lx) & (x <= P.hx) & (y >= P.ly) & (y <= P.hy) & (z >= P.lz) & (z <= P.hz);
-  return sqdist(x, y, z, P.cx, P.cy, P.cz) <= P.rr;
+  if (CUBE == 2) {  // vertical cylinder (geometry.hpp:107-110)
+    const double dx = __dsub_rn(x, P.cx), dy = __dsub_rn(y, P.cy);
+    return (z >= P.lz) & (z <= P.hz) & (__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)) <= P.rr);
+  }
+  return sqdist(x, y, z, P.cx, P.cy, P.cz) <= P.rr;  // sphere (geometry.hpp:82-84)
 }
 
 // Warp-uniform record read: every lane loads the same 32 bytes (one L1
@@ -272,7 +276,7 @@ __device__ __forceinline__ void warp_query_count(const Tables& t, double cx, dou
                                                  double r, int lane, uint32_t* cnt_out,
                                                  uint64_t* tested_out, uint64_t* dig_out) {
   Range R;
-  const bool ok = clamped_range_warp(t.g, cx, cy, cz, r, lane, &R);
+  const bool ok = clamped_range_warp(t.g, cx, cy, cz, r, lane, &R, CUBE);
   Predicate P;
   P.init(cx, cy, cz, r, CUBE);
   uint32_t cnt = 0;
@@ -410,7 +414,7 @@ __device__ __forceinline__ uint32_t warp_query_walk(const Tables& t, double cx, 
                                                     uint32_t* buf, uint32_t cap,
                                                     uint32_t* direct) {
   Range R;
-  const bool ok = clamped_range_warp(t.g, cx, cy, cz, r, lane, &R);
+  const bool ok = clamped_range_warp(t.g, cx, cy, cz, r, lane, &R, CUBE);
   Predicate P;
   P.init(cx, cy, cz, r, CUBE);
   uint32_t cnt = 0;
@@ -596,7 +600,7 @@ __global__ void __launch_bounds__(kQThreads, 4) radius_tile_kernel(
       cz = __ldg(q + 3 * (uint64_t)qi + 2);
     }
     Range R{};
-    const bool ok = active && clamped_range(t.g, cx, cy, cz, r, &R);
+    const bool ok = active && clamped_range(t.g, cx, cy, cz, r, &R, CUBE);
     const uint32_t okmask = __ballot_sync(0xffffffffu, ok);
     bool use_tile = small_grid && okmask != 0;
     uint32_t I0 = 0, J0 = 0, nj = 0, ncol = 0, total = 0;
@@ -954,14 +958,17 @@ cm_status launch_radius(const cm_index* ix, const double* q, uint64_t nq, int ke
   };
   switch (ix->opts.flavor) {
     case CM_DENSE:
-      return kernel == CM_CUBE ? run(radius_tile_kernel<CM_DENSE, MODE, 1>)
-                               : run(radius_tile_kernel<CM_DENSE, MODE, 0>);
+      return kernel == CM_CUBE       ? run(radius_tile_kernel<CM_DENSE, MODE, 1>)
+             : kernel == CM_CYLINDER ? run(radius_tile_kernel<CM_DENSE, MODE, 2>)
+                                     : run(radius_tile_kernel<CM_DENSE, MODE, 0>);
     case CM_SPARSE:
-      return kernel == CM_CUBE ? run(radius_tile_kernel<CM_SPARSE, MODE, 1>)
-                               : run(radius_tile_kernel<CM_SPARSE, MODE, 0>);
+      return kernel == CM_CUBE       ? run(radius_tile_kernel<CM_SPARSE, MODE, 1>)
+             : kernel == CM_CYLINDER ? run(radius_tile_kernel<CM_SPARSE, MODE, 2>)
+                                     : run(radius_tile_kernel<CM_SPARSE, MODE, 0>);
     default:
-      return kernel == CM_CUBE ? run(radius_tile_kernel<CM_MIXED, MODE, 1>)
-                               : run(radius_tile_kernel<CM_MIXED, MODE, 0>);
+      return kernel == CM_CUBE       ? run(radius_tile_kernel<CM_MIXED, MODE, 1>)
+             : kernel == CM_CYLINDER ? run(radius_tile_kernel<CM_MIXED, MODE, 2>)
+                                     : run(radius_tile_kernel<CM_MIXED, MODE, 0>);
   }
 }
 
@@ -1089,6 +1096,60 @@ cm_status gather_rows_dev(const uint32_t* temp, const uint64_t* toff, const uint
   const int smem = 4 * kGatherRow * 33 * 4;
   cudaFuncSetAttribute(gather_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   gather_rows_kernel<<<grid, 128, smem, st>>>(temp, toff, counts, row_ptr, perm, cols, nq); ::cmg::note_launch();
+  CM_CUDA_TRY(cudaGetLastError());
+  return CM_OK;
+}
+
+namespace {
+// weighted_density's binning (analysis.cpp:67-70): local = count / pi,
+// bin = min(255, (u64)local); per-block shared histograms.
+__global__ void density_hist_kernel(const uint32_t* __restrict__ counts, uint64_t n,
+                                    unsigned long long* __restrict__ bins) {
+  __shared__ uint32_t h[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const double local = __ddiv_rn((double)counts[i], 3.141592653589793);
+    const uint64_t b = (uint64_t)local;
+    atomicAdd(&h[b < 255 ? b : 255], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 256; i += blockDim.x)
+    if (h[i]) atomicAdd(bins + i, (unsigned long long)h[i]);
+}
+
+__global__ void gather_points_kernel(const double* __restrict__ xyz,
+                                     const uint64_t* __restrict__ idx, uint64_t n,
+                                     double* __restrict__ out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t h = idx[i];
+    out[3 * i] = xyz[3 * h];
+    out[3 * i + 1] = xyz[3 * h + 1];
+    out[3 * i + 2] = xyz[3 * h + 2];
+  }
+}
+}  // namespace
+
+cm_status density_histogram_dev(const uint32_t* counts, uint64_t n, unsigned long long* bins,
+                                cudaStream_t st) {
+  CM_CUDA_TRY(cudaMemsetAsync(bins, 0, 256 * 8, st));
+  if (n) {
+    const unsigned grid = (unsigned)std::max<uint64_t>(
+        1, std::min<uint64_t>((n + 255) / 256, (uint64_t)sm_count() * 8));
+    density_hist_kernel<<<grid, 256, 0, st>>>(counts, n, bins); ::cmg::note_launch();
+  }
+  CM_CUDA_TRY(cudaGetLastError());
+  return CM_OK;
+}
+
+cm_status gather_points_dev(const double* xyz, const uint64_t* idx, uint64_t n, double* out,
+                            cudaStream_t st) {
+  if (!n) return CM_OK;
+  const unsigned grid =
+      (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, (uint64_t)sm_count() * 8));
+  gather_points_kernel<<<grid, 256, 0, st>>>(xyz, idx, n, out); ::cmg::note_launch();
   CM_CUDA_TRY(cudaGetLastError());
   return CM_OK;
 }
