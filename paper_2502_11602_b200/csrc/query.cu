@@ -747,6 +747,30 @@ __global__ void __launch_bounds__(kQThreads, 4) radius_tile_kernel(
       if (write_ok) {
         // hit keys -> handles (the records were just walked: L1/L2 hits)
         __syncwarp();
+        if (MODE == MODE_COLLECT) {
+          // Arena rows go out unsorted (the gather sorts), so each lane
+          // translates and stores its own row: independent loads, many in
+          // flight, no warp-wide round trip per row. Column starts move to
+          // the (now idle) staging buffer so the loop needs no shuffles.
+          uint32_t* cbeg = reinterpret_cast<uint32_t*>(stg);
+          cbeg[lane] = b;
+          __syncwarp();
+          uint32_t* out = rows + dst;
+          uint32_t i = 0;
+          for (; i + 8 <= mine; i += 8) {
+            uint32_t kv[8], v[8];
+#pragma unroll
+            for (int w = 0; w < 8; ++w) kv[w] = skey[(i + w) * 33 + lane];
+#pragma unroll
+            for (int w = 0; w < 8; ++w) v[w] = __ldg(&rec[cbeg[kv[w] >> 11] + (kv[w] & 2047u)].id);
+#pragma unroll
+            for (int w = 0; w < 8; ++w) out[i + w] = v[w];
+          }
+          for (; i < mine; ++i) {
+            const uint32_t kv = skey[i * 33 + lane];
+            out[i] = __ldg(&rec[cbeg[kv >> 11] + (kv & 2047u)].id);
+          }
+        } else
         for (int l = 0; l < 32; ++l) {
           const uint32_t len = __shfl_sync(0xffffffffu, mine, l);
           const uint64_t off = __shfl_sync(0xffffffffu, dst, l);
