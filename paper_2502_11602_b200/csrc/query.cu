@@ -63,8 +63,8 @@ struct Out {
   uint32_t* cols;                 // FILL
   uint32_t* temp;                 // COLLECT arena
   uint64_t cap;                   // COLLECT arena capacity (entries)
-  uint64_t* toff;                 // COLLECT arena offset, by sorted position
-  uint32_t* scnt;                 // COLLECT row length, by sorted position
+  uint64_t* toff;                 // COLLECT arena offset, by query
+  uint32_t* scnt;                 // COLLECT row length, by query
   unsigned long long* cursor;     // COLLECT arena bump pointer
   uint64_t* big_off;              // rows sorted afterwards: offset into `rows`
   uint32_t* big_len;
@@ -511,8 +511,8 @@ __device__ __forceinline__ void single_query(const Tables& t, uint32_t qi, uint6
     if (lane == 0) {
       base = atomicAdd(o.cursor, (unsigned long long)cnt);
       o.counts[qi] = cnt;
-      o.toff[spos] = base;
-      o.scnt[spos] = cnt;
+      o.toff[qi] = base;
+      o.scnt[qi] = cnt;
     }
     base = __shfl_sync(0xffffffffu, base, 0);
     if (base + cnt <= o.cap)
@@ -738,8 +738,8 @@ __global__ void __launch_bounds__(kQThreads, 4) radius_tile_kernel(
         write_ok = base + tot <= o.cap;
         if (active && !longrow) {
           o.counts[qi] = cnt;
-          o.toff[s] = dst;
-          o.scnt[s] = cnt;
+          o.toff[qi] = dst;
+          o.scnt[qi] = cnt;
         }
       }
       __syncwarp();
@@ -837,9 +837,10 @@ __global__ void __launch_bounds__(1024) big_row_sort_kernel(uint32_t* __restrict
   }
 }
 
-// Arena rows -> CSR order, sorting them on the way. A warp takes the 32
-// queries of one tile (sorted positions 32g..32g+31), whose arena rows the
-// collect kernel wrote contiguously, so the reads stream. Rows of <= 96
+// Arena rows -> CSR order, sorting them on the way. A warp takes 32
+// consecutive queries in the caller's order, so its output is one contiguous
+// stretch of cols (whole sectors, no partial-sector read-modify-write in L2);
+// the arena rows it reads are scattered but each is a short burst. Rows of <= 96
 // handles are staged in shared memory (interleaved, stride 33); each lane
 // sorts its own row in registers with an unrolled bitonic network — rows
 // longer than 64 as two runs, [0, 64) and [64, len), merged by the warp with
@@ -860,11 +861,10 @@ __global__ void __launch_bounds__(128) gather_rows_kernel(const uint32_t* __rest
   const uint64_t W = (uint64_t)gridDim.x * (blockDim.x >> 5);
   for (uint64_t gidx = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
        gidx < ngroups; gidx += W) {
-    const uint64_t s = gidx * 32 + lane;
-    const bool act = s < nq;
-    const uint32_t q = act ? __ldg(perm + s) : 0u;
-    const uint32_t len = act ? __ldg(counts + s) : 0u;
-    const uint64_t so = act ? __ldg(toff + s) : 0;
+    const uint64_t q = gidx * 32 + lane;
+    const bool act = q < nq;
+    const uint32_t len = act ? __ldg(counts + q) : 0u;
+    const uint64_t so = act ? __ldg(toff + q) : 0;
     const uint64_t dof = act ? __ldg(row_ptr + q) : 0;
     const uint32_t staged = len <= (uint32_t)kGatherRow ? len : 0u;
     // 8 rows per step, all their loads in flight before the stores
