@@ -843,8 +843,8 @@ __global__ void __launch_bounds__(1024) big_row_sort_kernel(uint32_t* __restrict
 // the arena rows it reads are scattered but each is a short burst. Rows of <= 96
 // handles are staged in shared memory (interleaved, stride 33); each lane
 // sorts its own row in registers with an unrolled bitonic network — rows
-// longer than 64 as two runs, [0, 64) and [64, len), merged by the warp with
-// a merge-path rank per element. Rows longer than 96 come from the
+// longer than 64 as two runs, [0, 64) and [64, len), merged by the warp
+// along the merge path (three outputs per lane). Rows longer than 96 come from the
 // one-query-per-warp path already sorted and are copied.
 constexpr int kGatherRow = 96;
 __global__ void __launch_bounds__(128) gather_rows_kernel(const uint32_t* __restrict__ temp,
@@ -859,13 +859,34 @@ __global__ void __launch_bounds__(128) gather_rows_kernel(const uint32_t* __rest
   uint32_t* srow = gsm + (threadIdx.x >> 5) * (kGatherRow * 33);
   const uint64_t ngroups = (nq + 31) / 32;
   const uint64_t W = (uint64_t)gridDim.x * (blockDim.x >> 5);
-  for (uint64_t gidx = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
-       gidx < ngroups; gidx += W) {
+  uint64_t gidx = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  uint32_t nlen = 0;
+  uint64_t nso = 0;
+  if (gidx < ngroups && gidx * 32 + lane < nq) {
+    nlen = __ldg(counts + gidx * 32 + lane);
+    nso = __ldg(toff + gidx * 32 + lane);
+  }
+  for (; gidx < ngroups; gidx += W) {
     const uint64_t q = gidx * 32 + lane;
     const bool act = q < nq;
-    const uint32_t len = act ? __ldg(counts + q) : 0u;
-    const uint64_t so = act ? __ldg(toff + q) : 0;
+    const uint32_t len = nlen;
+    const uint64_t so = nso;
     const uint64_t dof = act ? __ldg(row_ptr + q) : 0;
+    // the next group's arena rows start moving into L2 while this one sorts
+    {
+      const uint64_t nq2 = (gidx + W) * 32 + lane;
+      nlen = 0, nso = 0;
+      if (nq2 < nq) {
+        nlen = __ldg(counts + nq2);
+        nso = __ldg(toff + nq2);
+        if (nlen <= (uint32_t)kGatherRow) {
+          const char* a = reinterpret_cast<const char*>(temp + nso);
+          const char* e = reinterpret_cast<const char*>(temp + nso + nlen);
+          for (const char* x = reinterpret_cast<const char*>((uintptr_t)a & ~(uintptr_t)127); x < e; x += 128)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(x));
+        }
+      }
+    }
     const uint32_t staged = len <= (uint32_t)kGatherRow ? len : 0u;
     // 8 rows per step, all their loads in flight before the stores
     for (int l0 = 0; l0 < 32; l0 += 8) {
@@ -908,24 +929,30 @@ __global__ void __launch_bounds__(128) gather_rows_kernel(const uint32_t* __rest
       if (ln <= 64) {
         for (uint32_t i = lane; i < ln; i += 32) cols[d + i] = srow[i * 33 + l];
       } else if (ln <= (uint32_t)kGatherRow) {
-        // merge path: element a_i of run A [0,64) goes to i + #{b in B : b < a_i};
-        // b_j of run B goes to j + #{a in A : a <= b_j} (handles are distinct)
+        // merge path: lane takes outputs [3 lane, 3 lane + 3) — co-rank of
+        // its diagonal by binary search, then three sequential merge steps
+        // (handles are distinct, so ties never occur)
         const uint32_t nb = ln - 64;
-        for (uint32_t i = lane; i < ln; i += 32) {
-          const uint32_t v = srow[i * 33 + l];
-          uint32_t lo, hi, base, off;
-          if (i < 64) {
-            lo = 64, hi = ln, base = 64, off = i;
-          } else {
-            lo = 0, hi = 64, base = 0, off = i - 64;
-          }
-          while (lo < hi) {
-            const uint32_t m = (lo + hi) >> 1;
-            if (srow[m * 33 + l] < v) lo = m + 1; else hi = m;
-          }
-          cols[d + off + (lo - base)] = v;
+        const uint32_t* A = srow + l;
+        const uint32_t* B = srow + 64 * 33 + l;
+        const uint32_t dg = min(3u * (uint32_t)lane, ln);
+        uint32_t lo = dg > nb ? dg - nb : 0u, hi = min(dg, 64u);
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (A[mid * 33] < B[(dg - 1 - mid) * 33]) lo = mid + 1; else hi = mid;
         }
-        (void)nb;
+        uint32_t ia = lo, ib = dg - lo;
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+          if (dg + t < ln) {
+            const uint32_t av = ia < 64u ? A[ia * 33] : 0xffffffffu;
+            const uint32_t bv = ib < nb ? B[ib * 33] : 0xffffffffu;
+            const bool ta = av < bv;
+            cols[d + dg + t] = ta ? av : bv;
+            ia += ta;
+            ib += !ta;
+          }
+        }
       } else {
         const uint64_t o = __shfl_sync(0xffffffffu, so, l);
         for (uint32_t b0 = 0; b0 < ln; b0 += 256) {  // 8 loads in flight per lane
