@@ -847,6 +847,7 @@ __global__ void __launch_bounds__(1024) big_row_sort_kernel(uint32_t* __restrict
 // along the merge path (three outputs per lane). Rows longer than 96 come from the
 // one-query-per-warp path already sorted and are copied.
 constexpr int kGatherRow = 96;
+constexpr int kGatherWarpWords = kGatherRow * 33 + 96;  // rows, sfin[32], srel[32] (u64)
 __global__ void __launch_bounds__(128) gather_rows_kernel(const uint32_t* __restrict__ temp,
                                                           const uint64_t* __restrict__ toff,
                                                           const uint32_t* __restrict__ counts,
@@ -856,7 +857,9 @@ __global__ void __launch_bounds__(128) gather_rows_kernel(const uint32_t* __rest
                                                           uint64_t nq) {
   extern __shared__ uint32_t gsm[];
   const int lane = threadIdx.x & 31;
-  uint32_t* srow = gsm + (threadIdx.x >> 5) * (kGatherRow * 33);
+  uint32_t* srow = gsm + (threadIdx.x >> 5) * kGatherWarpWords;
+  uint32_t* sfin = srow + kGatherRow * 33;                          // flat row ends
+  uint64_t* srel = reinterpret_cast<uint64_t*>(sfin + 32);           // row starts - row 0's
   const uint64_t ngroups = (nq + 31) / 32;
   const uint64_t W = (uint64_t)gridDim.x * (blockDim.x >> 5);
   uint64_t gidx = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -923,12 +926,34 @@ __global__ void __launch_bounds__(128) gather_rows_kernel(const uint32_t* __rest
     const uint32_t m2 = warp_max_u32(r2);
     if (m2 > 1) lane_sort_row<32>(srow + 64 * 33, lane, r2);
     __syncwarp();
-    for (int l = 0; l < 32; ++l) {
+    // Rows of <= 64 (one sorted run) leave as one flat stream: flat element
+    // f belongs to the row whose flat range holds it; every lane walks the
+    // small row table forward (rows average fewer than 32 handles per lane
+    // step, so the walk is one or two probes).
+    {
+      const uint32_t flen = len <= 64u ? len : 0u;
+      const uint32_t fin = warp_incl_scan(flen);
+      const uint32_t ftot = __shfl_sync(0xffffffffu, fin, 31);
+      const uint64_t d0 = __shfl_sync(0xffffffffu, dof, 0);
+      sfin[lane] = fin;
+      srel[lane] = dof - d0;
+      __syncwarp();
+      uint32_t l = 0, fstart = 0;
+      for (uint32_t f = lane; f < ftot; f += 32) {
+        uint32_t e = sfin[l];
+        while (e <= f) {
+          fstart = e;
+          e = sfin[++l];
+        }
+        const uint32_t i = f - fstart;
+        cols[d0 + srel[l] + i] = srow[i * 33 + l];
+      }
+    }
+    for (uint32_t lm = __ballot_sync(0xffffffffu, len > 64u); lm; lm &= lm - 1) {
+      const int l = __ffs(lm) - 1;
       const uint32_t ln = __shfl_sync(0xffffffffu, len, l);
       const uint64_t d = __shfl_sync(0xffffffffu, dof, l);
-      if (ln <= 64) {
-        for (uint32_t i = lane; i < ln; i += 32) cols[d + i] = srow[i * 33 + l];
-      } else if (ln <= (uint32_t)kGatherRow) {
+      if (ln <= (uint32_t)kGatherRow) {
         // merge path: lane takes outputs [3 lane, 3 lane + 3) — co-rank of
         // its diagonal by binary search, then three sequential merge steps
         // (handles are distinct, so ties never occur)
@@ -1144,7 +1169,7 @@ cm_status gather_rows_dev(const uint32_t* temp, const uint64_t* toff, const uint
   if (nq == 0) return CM_OK;
   const uint64_t groups = (nq + 31) / 32;
   const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((groups + 3) / 4, (uint64_t)sm_count() * 8));
-  const int smem = 4 * kGatherRow * 33 * 4;
+  const int smem = 4 * kGatherWarpWords * 4;
   cudaFuncSetAttribute(gather_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   gather_rows_kernel<<<grid, 128, smem, st>>>(temp, toff, counts, row_ptr, perm, cols, nq); ::cmg::note_launch();
   CM_CUDA_TRY(cudaGetLastError());
