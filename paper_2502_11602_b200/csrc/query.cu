@@ -571,7 +571,7 @@ __device__ __forceinline__ bool advance_chunk(uint32_t& mask, uint32_t& c, uint3
 
 // Query-tile kernel (see the file comment).
 template <int FLAVOR, int MODE, int CUBE>
-__global__ void __launch_bounds__(kQThreads, 4) radius_tile_kernel(
+__global__ void __launch_bounds__(kQThreads, 5) radius_tile_kernel(
     const Tables t, const double* __restrict__ q, uint64_t nq, double r,
     const uint32_t* __restrict__ perm, const Out o) {
   extern __shared__ __align__(16) unsigned char smraw[];
