@@ -598,9 +598,13 @@ static cm_status radius_search_core(const cm_index* ix, const double* qd, uint64
   // Single pass: sorted rows into an arena sized from the running
   // neighbours-per-query estimate; if the arena overflows, fall back to
   // count + scan + fill.
+  // Large radii go count + scan + fill (wide tiles) + in-place row sort.
   uint64_t cap = (uint64_t)((double)nq * ix->nnz_per_query * 1.05) + (1u << 20);
-  bool two_pass = dev_alloc_t(&temp, cap, st) != cudaSuccess;
-  if (two_pass) cudaGetLastError();
+  bool two_pass = radius_is_wide(ix, r);
+  if (!two_pass && dev_alloc_t(&temp, cap, st) != cudaSuccess) {
+    two_pass = true;
+    cudaGetLastError();
+  }
   cm_status s = CM_OK;
   unsigned long long used = 0;
   if (!two_pass) {

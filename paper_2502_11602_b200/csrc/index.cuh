@@ -100,6 +100,7 @@ cm_status order_queries(const cm_index* ix, const double* q_dev, uint64_t nq, cu
 cm_status radius_count_dev(const cm_index* ix, const double* q_dev, uint64_t nq, int kernel,
                            double r, const uint32_t* perm, uint32_t* counts_dev,
                            uint64_t* tested_dev, cudaStream_t st);
+bool radius_is_wide(const cm_index* ix, double r);
 cm_status radius_fill_dev(const cm_index* ix, const double* q_dev, uint64_t nq, int kernel,
                           double r, const uint32_t* perm, const uint64_t* row_ptr_dev,
                           uint32_t* cols_dev, cudaStream_t st, cudaEvent_t after_fill = nullptr);

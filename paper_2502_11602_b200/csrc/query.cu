@@ -42,7 +42,9 @@ constexpr int kLaneSortMax = 32;                      // per-lane register sort 
 // path reuses the whole region as a u32 buffer.
 constexpr int kRowKeyBytes = kLaneRowCap * 33 * 2;
 constexpr int kStageBytes = 64 * 32;
-constexpr int kRowWarpBytes = kRowKeyBytes + kStageBytes;
+constexpr int kColBegBytes = 32 * 4;                  // wide-tile FILL: key -> record base
+constexpr int kRowWarpBytes = kRowKeyBytes + kStageBytes + kColBegBytes;
+constexpr int kWideMaxCols = 4096;                    // wide tiles: hull column limit
 constexpr int kRowCap = kRowWarpBytes / 4;            // one-query row buffer (u32)
 constexpr int kSortCap = (kRowCap - 512) / 2;         // one-query row sorted in smem
 constexpr int kBigSmemCap = 32768;                    // block sort in smem (128 KB)
@@ -69,6 +71,7 @@ struct Out {
   uint64_t* big_off;              // rows sorted afterwards: offset into `rows`
   uint32_t* big_len;
   uint32_t* n_big;
+  int wide_fill;                  // FILL: wide tiles may leave rows unsorted (sorted afterwards)
 };
 
 template <typename K>
@@ -153,7 +156,12 @@ __device__ __forceinline__ uint32_t warp_max_u32(uint32_t v) {
 // Exchanges at distance < 32 go through shuffles, the rest stay in-lane.
 template <int ITEMS>
 __device__ __forceinline__ void warp_sort_regs(uint32_t (&v)[ITEMS], int lane) {
-  constexpr int LOGP = ITEMS == 1 ? 5 : ITEMS == 2 ? 6 : ITEMS == 4 ? 7 : ITEMS == 8 ? 8 : 9;
+  constexpr int LOGP = ITEMS == 1    ? 5
+                       : ITEMS == 2  ? 6
+                       : ITEMS == 4  ? 7
+                       : ITEMS == 8  ? 8
+                       : ITEMS == 16 ? 9
+                                     : 10;
 #pragma unroll
   for (int lk = 1; lk <= LOGP; ++lk) {
     const int k = 1 << lk;
@@ -569,6 +577,169 @@ __device__ __forceinline__ bool advance_chunk(uint32_t& mask, uint32_t& c, uint3
   return false;
 }
 
+// Wide query tile: a hull of more than 32 columns (large radii), walked in
+// batches of 32 columns — lane c of a batch holds column 32 * batch + c's
+// span — with the same staged, warp-uniform record stream and per-lane
+// column mask + z window as the compact tile. COUNT / DIGEST keep counters.
+// FILL writes each lane's hits UNSORTED at its row (row_ptr from the count
+// pass): the per-lane u16 key buffers are flushed whenever one could
+// overflow, before a column offset leaves the 11-bit key range (the column's
+// key base moves up), and at every batch end; sort_rows_kernel sorts the
+// rows afterwards.
+template <int FLAVOR, int MODE, int CUBE>
+__device__ __forceinline__ void wide_tile(const Tables& t, const Range& R, bool ok, bool active,
+                                          uint32_t qi, uint32_t I0, uint32_t J0, uint32_t nj,
+                                          uint32_t nc, uint32_t K0, uint32_t K1,
+                                          const Predicate& P, int lane, PointRec* stg,
+                                          uint16_t* skey, uint32_t* cbeg, const Out& o) {
+  constexpr bool FILL = MODE == MODE_FILL;
+  const PointRec* __restrict__ rec = t.rec;
+  const uint32_t kk0 = ok ? (uint32_t)R.k0 : 1u;
+  const uint32_t kspan = ok ? (uint32_t)(R.k1 - R.k0) : 0u;
+  // this lane's own columns, in hull coordinates (an empty range when !ok)
+  const uint32_t ri0 = ok ? (uint32_t)R.i0 - I0 : 1u, ri1 = ok ? (uint32_t)R.i1 - I0 : 0u;
+  const uint32_t rj0 = ok ? (uint32_t)R.j0 - J0 : 0u, rj1 = ok ? (uint32_t)R.j1 - J0 : 0u;
+  uint32_t cnt = 0, ntest = 0, nb = 0, hull = 0;
+  uint64_t dig = 0;
+  uint64_t wpos = (FILL && active) ? __ldg(o.row_ptr + qi) : 0;
+  // Buffered keys -> handles -> the rows, one row at a time by the whole warp
+  // (coalesced stores: a per-lane store stream would cost one L2 write
+  // request per handle), four rows' loads in flight.
+  auto flush = [&]() {
+    __syncwarp();
+    for (int l0 = 0; l0 < 32; l0 += 4) {
+      uint32_t v[4][3];
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        const uint32_t n = __shfl_sync(0xffffffffu, nb, l0 + jj);
+#pragma unroll
+        for (int h = 0; h < 3; ++h) {
+          const uint32_t i = h * 32 + lane;
+          uint32_t x = 0;
+          if (i < n) {
+            const uint32_t kv = skey[i * 33 + l0 + jj];
+            x = __ldg(&rec[cbeg[kv >> 11] + (kv & 2047u)].id);
+          }
+          v[jj][h] = x;
+        }
+      }
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        const uint32_t n = __shfl_sync(0xffffffffu, nb, l0 + jj);
+        const uint64_t wp = __shfl_sync(0xffffffffu, wpos, l0 + jj);
+#pragma unroll
+        for (int h = 0; h < 3; ++h) {
+          const uint32_t i = h * 32 + lane;
+          if (i < n) o.cols[wp + i] = v[jj][h];
+        }
+      }
+    }
+    wpos += nb;
+    nb = 0;
+    __syncwarp();
+  };
+  for (uint32_t cb = 0; cb < nc; cb += 32) {
+    const uint32_t col = cb + lane;
+    uint32_t b = 0, e = 0;
+    if (col < nc) column_span<FLAVOR>(t, I0 + col / nj, J0 + col % nj, K0, K1, &b, &e);
+    hull += e - b;
+    uint32_t colmask = 0;
+    for (uint32_t ci = ri0; ci <= ri1; ++ci) {
+      const int64_t lo = (int64_t)ci * nj + rj0 - cb, hi = (int64_t)ci * nj + rj1 - cb;
+      if (hi < 0 || lo > 31) continue;
+      const uint32_t l2 = lo < 0 ? 0u : (uint32_t)lo, h2 = hi > 31 ? 31u : (uint32_t)hi;
+      colmask |= (uint32_t)((((uint64_t)2 << (h2 - l2)) - 1ull) << l2);
+    }
+    uint32_t needmask = colmask;
+#pragma unroll
+    for (int sh = 16; sh > 0; sh >>= 1) needmask |= __shfl_xor_sync(0xffffffffu, needmask, sh);
+    needmask &= __ballot_sync(0xffffffffu, e > b);
+    if (FILL) {
+      cbeg[lane] = b;
+      __syncwarp();
+    }
+    uint32_t c = 0, p = 0, ce = 0;
+    bool more = advance_chunk(needmask, c, p, ce, b, e, true);
+    int buf = 0;
+    if (more) stage_chunk(stg, rec, p, min(32u, ce - p), lane);
+    cp_async_commit();
+    while (more) {
+      uint32_t c2 = c, p2 = p, ce2 = ce;
+      const bool more2 = advance_chunk(needmask, c2, p2, ce2, b, e, false);
+      if (more2) stage_chunk(stg + (buf ^ 1) * 32, rec, p2, min(32u, ce2 - p2), lane);
+      cp_async_commit();
+      cp_async_wait<1>();
+      __syncwarp();
+      const SRec* sr = reinterpret_cast<const SRec*>(stg + buf * 32);
+      const uint32_t len = min(32u, ce - p);
+      const bool need = (colmask >> c) & 1u;
+      uint32_t kbase = 0;
+      if (FILL) {
+        uint32_t cbase = cbeg[c];
+        const bool rebase = p + len - cbase > 2048u;
+        if (rebase || __any_sync(0xffffffffu, nb > (uint32_t)kLaneRowCap - 32u)) {
+          flush();
+          if (rebase) {
+            if (lane == 0) cbeg[c] = p;
+            __syncwarp();
+            cbase = p;
+          }
+        }
+        kbase = (c << 11) | (p - cbase);
+      }
+      uint32_t u = 0;
+      for (; u + 8 <= len; u += 8) {
+        SRec v[8];
+#pragma unroll
+        for (int w = 0; w < 8; ++w) v[w] = sr[u + w];
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+          const bool in = need & (v[w].meta - kk0 <= kspan);
+          const bool hit = in & pred<CUBE>(P, v[w].x, v[w].y, v[w].z);
+          if (MODE == MODE_DIGEST && hit) dig += mix64(v[w].id);
+          if (FILL && hit) skey[nb * 33 + lane] = (uint16_t)(kbase + u + w);
+          if (FILL) nb += hit;
+          cnt += hit;
+          ntest += in;
+        }
+      }
+      for (; u < len; ++u) {
+        const SRec v = sr[u];
+        const bool in = need & (v.meta - kk0 <= kspan);
+        const bool hit = in & pred<CUBE>(P, v.x, v.y, v.z);
+        if (MODE == MODE_DIGEST && hit) dig += mix64(v.id);
+        if (FILL && hit) skey[nb * 33 + lane] = (uint16_t)(kbase + u);
+        if (FILL) nb += hit;
+        cnt += hit;
+        ntest += in;
+      }
+      __syncwarp();
+      buf ^= 1;
+      c = c2, p = p2, ce = ce2;
+      more = more2;
+    }
+    cp_async_wait<0>();
+    if (FILL) flush();  // keys refer to this batch's column bases
+  }
+  const uint32_t hsum = warp_incl_scan(hull);
+  if (lane == 31) atomicAdd(&g_qstats[(FILL ? 4 : 0) + 2], (unsigned long long)hsum);
+  if (MODE == MODE_COUNT) {
+    uint32_t sum = ntest;
+#pragma unroll
+    for (int sh = 16; sh > 0; sh >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, sh);
+    if (lane == 0) atomicAdd(&g_qstats[3], (unsigned long long)sum);
+    if (active) {
+      if (o.counts) o.counts[qi] = cnt;
+      if (o.tested) o.tested[qi] = ntest;
+    }
+  } else if (MODE == MODE_DIGEST) {
+    if (active) {
+      o.counts[qi] = cnt;
+      o.digests[qi] = dig;
+    }
+  }
+}
+
 // Query-tile kernel (see the file comment).
 template <int FLAVOR, int MODE, int CUBE>
 __global__ void __launch_bounds__(kQThreads, 5) radius_tile_kernel(
@@ -603,18 +774,28 @@ __global__ void __launch_bounds__(kQThreads, 5) radius_tile_kernel(
     const bool ok = active && clamped_range(t.g, cx, cy, cz, r, &R, CUBE);
     const uint32_t okmask = __ballot_sync(0xffffffffu, ok);
     bool use_tile = small_grid && okmask != 0;
-    uint32_t I0 = 0, J0 = 0, nj = 0, ncol = 0, total = 0;
+    bool wide = false;
+    uint32_t I0 = 0, J0 = 0, nj = 0, ncol = 0, total = 0, K0 = 0, K1 = 0;
+    uint64_t nc = 0;
     uint32_t b = 0, e = 0;
     if (use_tile) {
       I0 = warp_min_u32(ok ? (uint32_t)R.i0 : 0xffffffffu);
       const uint32_t I1 = warp_max_u32(ok ? (uint32_t)R.i1 : 0u);
       J0 = warp_min_u32(ok ? (uint32_t)R.j0 : 0xffffffffu);
       const uint32_t J1 = warp_max_u32(ok ? (uint32_t)R.j1 : 0u);
-      const uint32_t K0 = warp_min_u32(ok ? (uint32_t)R.k0 : 0xffffffffu);
-      const uint32_t K1 = warp_max_u32(ok ? (uint32_t)R.k1 : 0u);
+      K0 = warp_min_u32(ok ? (uint32_t)R.k0 : 0xffffffffu);
+      K1 = warp_max_u32(ok ? (uint32_t)R.k1 : 0u);
       nj = J1 - J0 + 1;
-      const uint64_t nc = (uint64_t)(I1 - I0 + 1) * nj;
+      nc = (uint64_t)(I1 - I0 + 1) * nj;
       use_tile = nc <= 32;
+      if (!use_tile && MODE != MODE_COLLECT && (MODE != MODE_FILL || o.wide_fill) &&
+          nc <= (uint64_t)kWideMaxCols) {
+        // worth it while the lanes' own columns cover >= 1/8 of the hull on average
+        uint32_t own = ok ? (uint32_t)((R.i1 - R.i0 + 1) * (R.j1 - R.j0 + 1)) : 0u;
+#pragma unroll
+        for (int sh = 16; sh > 0; sh >>= 1) own += __shfl_xor_sync(0xffffffffu, own, sh);
+        wide = (uint64_t)own * 8 >= nc * 32;
+      }
       if (use_tile) {
         ncol = (uint32_t)nc;
         if ((uint32_t)lane < ncol)
@@ -627,7 +808,16 @@ __global__ void __launch_bounds__(kQThreads, 5) radius_tile_kernel(
     if (lane == 0) {
       atomicAdd(&g_qstats[so + 0], 1ull);
       if (use_tile) atomicAdd(&g_qstats[so + 2], (unsigned long long)total);
-      else atomicAdd(&g_qstats[so + 1], 1ull);
+      else if (!wide) atomicAdd(&g_qstats[so + 1], 1ull);
+    }
+    if (wide) {
+      Predicate P;
+      P.init(cx, cy, cz, r, CUBE);
+      wide_tile<FLAVOR, MODE, CUBE>(t, R, ok, active, qi, I0, J0, nj, (uint32_t)nc, K0, K1, P,
+                                    lane, stg, skey,
+                                    reinterpret_cast<uint32_t*>(wreg + kRowKeyBytes + kStageBytes), o);
+      __syncwarp();
+      continue;
     }
     if (!use_tile) {
       const uint32_t am = __ballot_sync(0xffffffffu, active);
@@ -848,15 +1038,21 @@ __global__ void __launch_bounds__(1024) big_row_sort_kernel(uint32_t* __restrict
 // one-query-per-warp path already sorted and are copied.
 constexpr int kGatherRow = 96;
 constexpr int kGatherWarpWords = kGatherRow * 33 + 96;  // rows, sfin[32], srel[32] (u64)
-__global__ void __launch_bounds__(128) gather_rows_kernel(const uint32_t* __restrict__ temp,
+//
+// SORT = true is the in-place row sort after a wide-tile FILL (temp == cols,
+// toff == row_ptr): rows > 96 are sorted too — in shared memory by the warp
+// (radix, <= kSortCap) or listed for big_row_sort_kernel.
+template <bool SORT>
+__global__ void __launch_bounds__(128) gather_rows_kernel(const uint32_t* temp,
                                                           const uint64_t* __restrict__ toff,
                                                           const uint32_t* __restrict__ counts,
                                                           const uint64_t* __restrict__ row_ptr,
-                                                          const uint32_t* __restrict__ perm,
-                                                          uint32_t* __restrict__ cols,
-                                                          uint64_t nq) {
+                                                          uint32_t* cols, uint64_t nq, int bits,
+                                                          uint64_t* big_off, uint32_t* big_len,
+                                                          uint32_t* n_big) {
   extern __shared__ uint32_t gsm[];
   const int lane = threadIdx.x & 31;
+  const uint32_t lt = lanemask_lt();
   uint32_t* srow = gsm + (threadIdx.x >> 5) * kGatherWarpWords;
   uint32_t* sfin = srow + kGatherRow * 33;                          // flat row ends
   uint64_t* srel = reinterpret_cast<uint64_t*>(sfin + 32);           // row starts - row 0's
@@ -865,8 +1061,11 @@ __global__ void __launch_bounds__(128) gather_rows_kernel(const uint32_t* __rest
   uint64_t gidx = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   uint32_t nlen = 0;
   uint64_t nso = 0;
+  auto row_len = [&](uint64_t qq) -> uint32_t {
+    return SORT ? (uint32_t)(__ldg(row_ptr + qq + 1) - __ldg(row_ptr + qq)) : __ldg(counts + qq);
+  };
   if (gidx < ngroups && gidx * 32 + lane < nq) {
-    nlen = __ldg(counts + gidx * 32 + lane);
+    nlen = row_len(gidx * 32 + lane);
     nso = __ldg(toff + gidx * 32 + lane);
   }
   for (; gidx < ngroups; gidx += W) {
@@ -880,7 +1079,7 @@ __global__ void __launch_bounds__(128) gather_rows_kernel(const uint32_t* __rest
       const uint64_t nq2 = (gidx + W) * 32 + lane;
       nlen = 0, nso = 0;
       if (nq2 < nq) {
-        nlen = __ldg(counts + nq2);
+        nlen = row_len(nq2);
         nso = __ldg(toff + nq2);
         if (nlen <= (uint32_t)kGatherRow) {
           const char* a = reinterpret_cast<const char*>(temp + nso);
@@ -949,7 +1148,8 @@ __global__ void __launch_bounds__(128) gather_rows_kernel(const uint32_t* __rest
         cols[d0 + srel[l] + i] = srow[i * 33 + l];
       }
     }
-    for (uint32_t lm = __ballot_sync(0xffffffffu, len > 64u); lm; lm &= lm - 1) {
+    for (uint32_t lm = __ballot_sync(0xffffffffu, len > 64u && (!SORT || len <= (uint32_t)kGatherRow));
+         lm; lm &= lm - 1) {
       const int l = __ffs(lm) - 1;
       const uint32_t ln = __shfl_sync(0xffffffffu, len, l);
       const uint64_t d = __shfl_sync(0xffffffffu, dof, l);
@@ -996,6 +1196,207 @@ __global__ void __launch_bounds__(128) gather_rows_kernel(const uint32_t* __rest
       }
     }
     __syncwarp();
+  }
+}
+
+// In-place sort of the rows of 97..8192 handles (after a wide-tile FILL;
+// shorter rows were sorted by the gather pass, longer ones are listed for
+// big_row_sort_kernel). A block of 128 threads packs consecutive rows into a
+// GROUP of at most 128 runs of 64 handles (row-aligned) and stages it in
+// shared memory, each row contiguous from 64 * (its first run), with an XOR
+// swizzle (word p at p ^ ((p >> 6) & 31)) so that both the run-per-thread
+// and the linear accesses are bank-conflict free. Thread t sorts run t in
+// registers (unrolled bitonic), then every row's runs are merged pairwise,
+// 64 -> 128 -> ..., along the merge path: each round, thread t produces the
+// 64 outputs at its run's position as four independent 16-output streams
+// (co-rank by binary search for each; branch-free steps), ping-ponging
+// between two buffers. A row stops after ceil(log2(runs)) rounds and is
+// written back from whichever buffer holds it.
+constexpr int kMidThreads = 128;
+constexpr int kMidMax = 64 * kMidThreads;
+constexpr int kMidBuf = kMidMax + 64;  // one slot past a row end stays in bounds
+
+__device__ __forceinline__ uint32_t mid_swz(uint32_t p) { return p ^ ((p >> 6) & 31u); }
+
+__global__ void __launch_bounds__(kMidThreads) sort_mid_rows_kernel(
+    uint32_t* cols, const uint64_t* __restrict__ row_ptr, uint64_t nq, uint64_t* big_off,
+    uint32_t* big_len, uint32_t* n_big) {
+  extern __shared__ uint32_t msm[];
+  uint32_t* const bufs[2] = {msm, msm + kMidBuf};
+  __shared__ uint32_t s_off[kMidThreads], s_len[kMidThreads], s_rb[kMidThreads],
+      s_runs[kMidThreads];
+  __shared__ uint32_t s_wsum[kMidThreads / 32], s_wfit[kMidThreads / 32],
+      s_wmax[kMidThreads / 32], s_wbig[kMidThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  constexpr uint64_t kTask = 1024;
+  const uint64_t ntasks = (nq + kTask - 1) / kTask;
+  for (uint64_t task = blockIdx.x; task < ntasks; task += gridDim.x) {
+    uint64_t q = task * kTask;
+    const uint64_t qend = min(nq, q + kTask);
+    while (q < qend) {
+      const uint64_t ql = q + tid;
+      uint64_t st = 0;
+      uint32_t len = 0;
+      if (ql < qend) {
+        st = __ldg(row_ptr + ql);
+        len = (uint32_t)(__ldg(row_ptr + ql + 1) - st);
+      }
+      const uint32_t runs =
+          (len > (uint32_t)kGatherRow && len <= (uint32_t)kMidMax) ? (len + 63) >> 6 : 0u;
+      const uint32_t winc = warp_incl_scan(runs);
+      // a group ends at the 128-run budget and before the first row past
+      // kMidMax (which, when first, forms a group of its own: listed for the
+      // block sort), so the group's handles are one short contiguous span
+      const uint32_t bigm = __ballot_sync(0xffffffffu, ql < qend && len > (uint32_t)kMidMax);
+      if (lane == 31) s_wsum[wid] = winc;
+      if (lane == 0) s_wbig[wid] = bigm ? (uint32_t)(wid * 32 + __ffs(bigm) - 1) : 0xffffffffu;
+      __syncthreads();
+      uint32_t woff = 0, firstbig = 0xffffffffu;
+#pragma unroll
+      for (int w = 0; w < kMidThreads / 32; ++w) {
+        woff += w < wid ? s_wsum[w] : 0u;
+        firstbig = min(firstbig, s_wbig[w]);
+      }
+      const uint32_t rincl = woff + winc;
+      const uint32_t cut = firstbig == 0 ? 1u : firstbig;
+      const bool fit = ql < qend && rincl <= (uint32_t)kMidThreads && (uint32_t)tid < cut;
+      const uint32_t fm = __ballot_sync(0xffffffffu, fit);
+      const uint32_t rm = fit ? runs : 0u;
+      const uint32_t wmax = warp_max_u32(rm);
+      if (lane == 0) s_wfit[wid] = __popc(fm), s_wmax[wid] = wmax;
+      const uint32_t big = fm & bigm;
+      if (big) {
+        uint32_t slot = 0;
+        if (lane == 0) slot = atomicAdd(n_big, (uint32_t)__popc(big));
+        slot = __shfl_sync(0xffffffffu, slot, 0);
+        if ((big >> lane) & 1u) {
+          const uint32_t at = slot + __popc(big & lanemask_lt());
+          big_off[at] = st;
+          big_len[at] = len;
+        }
+      }
+      const uint64_t g0 = __ldg(row_ptr + q);  // the group's first handle
+      s_off[tid] = (uint32_t)(st - g0);         // meaningful for the group's rows
+      s_len[tid] = len;
+      s_rb[tid] = rincl - runs;
+      s_runs[tid] = rm;
+      __syncthreads();
+      uint32_t g = 0, maxruns = 0;
+#pragma unroll
+      for (int w = 0; w < kMidThreads / 32; ++w) g += s_wfit[w], maxruns = max(maxruns, s_wmax[w]);
+      const uint32_t nruns = s_rb[g - 1] + s_runs[g - 1];
+      if (nruns) {
+        uint32_t* b0 = bufs[0];
+        const uint32_t span = s_off[g - 1] + s_len[g - 1];
+        {  // load the span flat, 8 loads in flight per thread
+          uint32_t r = 0;
+          for (uint32_t f0 = 0; f0 < span; f0 += 8 * kMidThreads) {
+            uint32_t v[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const uint32_t f = f0 + k * kMidThreads + tid;
+              v[k] = f < span ? cols[g0 + f] : 0u;
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const uint32_t f = f0 + k * kMidThreads + tid;
+              if (f < span) {
+                while (r + 1 < g && s_off[r + 1] <= f) ++r;
+                if (s_runs[r]) b0[mid_swz(64u * s_rb[r] + (f - s_off[r]))] = v[k];
+              }
+            }
+          }
+        }
+        __syncthreads();
+        // this thread's run: row L = the last row with runs whose rb <= tid
+        const bool own = (uint32_t)tid < nruns;
+        uint32_t L = 0;
+        if (own) {
+          uint32_t lo = 0, hi = g - 1;
+          while (lo < hi) {
+            const uint32_t m = (lo + hi + 1) >> 1;
+            if (s_rb[m] <= (uint32_t)tid) lo = m; else hi = m - 1;
+          }
+          L = lo;
+          while (s_runs[L] == 0) --L;
+        }
+        const uint32_t rl = own ? s_len[L] : 0u;
+        const uint32_t base = own ? 64u * s_rb[L] : 0u;
+        const uint32_t j = (uint32_t)tid - (own ? s_rb[L] : 0u);
+        if (own) {
+          const uint32_t n = min(64u, rl - 64u * j);
+          uint32_t v[64];
+#pragma unroll
+          for (int i = 0; i < 64; ++i)
+            v[i] = (uint32_t)i < n ? b0[mid_swz(base + 64u * j + i)] : 0xffffffffu;
+          lane_sort_regs<64>(v);
+#pragma unroll
+          for (int i = 0; i < 64; ++i)
+            if ((uint32_t)i < n) b0[mid_swz(base + 64u * j + i)] = v[i];
+        }
+        __syncthreads();
+        int cur = 0;
+        for (uint32_t w = 64; w < 64u * maxruns; w <<= 1) {
+          if (own && w < rl) {  // this row still has runs to merge
+            const uint32_t* src = bufs[cur];
+            uint32_t* dst = bufs[cur ^ 1];
+            const uint32_t o0 = 64u * j;
+            const uint32_t pb = o0 / (2 * w) * (2 * w);
+            const uint32_t a1 = min(pb + w, rl), b1 = min(pb + 2 * w, rl);
+            const uint32_t na = a1 - pb, nb = b1 - a1;
+            const uint32_t A0 = base + pb, B0 = base + a1;
+            uint32_t ia[4], ib[4], av[4], bv[4];
+#pragma unroll
+            for (int s4 = 0; s4 < 4; ++s4) {
+              const uint32_t dd = min(o0 + 16u * s4, rl) - pb;
+              uint32_t lo = dd > nb ? dd - nb : 0u, hi = min(dd, na);
+              while (lo < hi) {
+                const uint32_t m = (lo + hi) >> 1;
+                if (src[mid_swz(A0 + m)] < src[mid_swz(B0 + dd - 1 - m)]) lo = m + 1; else hi = m;
+              }
+              ia[s4] = lo;
+              ib[s4] = dd - lo;
+              const uint32_t x = src[mid_swz(A0 + lo)], y = src[mid_swz(B0 + dd - lo)];
+              av[s4] = lo < na ? x : 0xffffffffu;
+              bv[s4] = dd - lo < nb ? y : 0xffffffffu;
+            }
+            const uint32_t oend = min(o0 + 64u, rl);
+#pragma unroll 2
+            for (int step = 0; step < 16; ++step) {
+#pragma unroll
+              for (int s4 = 0; s4 < 4; ++s4) {
+                const uint32_t o = o0 + 16u * s4 + step;
+                const bool ta = av[s4] < bv[s4];  // handles are distinct
+                if (o < oend) dst[mid_swz(base + o)] = ta ? av[s4] : bv[s4];
+                ia[s4] += ta;
+                ib[s4] += !ta;
+                const uint32_t idx = ta ? A0 + ia[s4] : B0 + ib[s4];
+                const bool more = ta ? ia[s4] < na : ib[s4] < nb;
+                const uint32_t nv = src[mid_swz(idx)];
+                const uint32_t nv2 = more ? nv : 0xffffffffu;
+                av[s4] = ta ? nv2 : av[s4];
+                bv[s4] = ta ? bv[s4] : nv2;
+              }
+            }
+          }
+          cur ^= 1;
+          __syncthreads();
+        }
+        {  // write back: a row with R runs ended in buffer (ceil(log2 R) & 1)
+          uint32_t r = 0;
+          for (uint32_t f = tid; f < span; f += kMidThreads) {
+            while (r + 1 < g && s_off[r + 1] <= f) ++r;
+            const uint32_t rr = s_runs[r];
+            if (rr) {
+              const int which = (32 - __clz((int)(rr - 1))) & 1;  // ceil(log2 rr) parity
+              cols[g0 + f] = bufs[which][mid_swz(64u * s_rb[r] + (f - s_off[r]))];
+            }
+          }
+        }
+      }
+      __syncthreads();
+      q += g;
+    }
   }
 }
 
@@ -1098,6 +1499,14 @@ cm_status order_queries(const cm_index* ix, const double* q, uint64_t nq, cudaSt
                                : order_typed<uint64_t>(ix, q, nq, st, out->perm);
 }
 
+// Radii whose clamped ranges span more columns than a compact 32-column
+// tile hull can hold: rows come from wide tiles (count + fill + row sort).
+bool radius_is_wide(const cm_index* ix, double r) {
+  const double cx = std::floor(2.0 * r / ix->g.sx) + 2.0;
+  const double cy = std::floor(2.0 * r / ix->g.sy) + 2.0;
+  return cx * cy > 20.0;
+}
+
 cm_status radius_count_dev(const cm_index* ix, const double* q, uint64_t nq, int kernel, double r,
                            const uint32_t* perm, uint32_t* counts, uint64_t* tested,
                            cudaStream_t st) {
@@ -1131,10 +1540,36 @@ cm_status radius_fill_dev(const cm_index* ix, const double* q, uint64_t nq, int 
   o.big_off = big.off;
   o.big_len = big.len;
   o.n_big = big.n;
+  o.wide_fill = radius_is_wide(ix, r) ? 1 : 0;
   s = launch_radius<MODE_FILL>(ix, q, nq, kernel, r, perm, o, st);
   if (after_fill) cudaEventRecord(after_fill, st);
-  if (s == CM_OK) s = sort_big_rows(cols, o, st);
-  return s;
+  if (s != CM_OK) return s;
+  if (!o.wide_fill) return sort_big_rows(cols, o, st);
+  // wide tiles left rows unsorted: sort every row in place
+  BigRows big2;
+  s = big2.init(nq, st);
+  if (s != CM_OK) return s;
+  const uint64_t groups = (nq + 31) / 32;
+  const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((groups + 3) / 4, (uint64_t)sm_count() * 8));
+  const int smem = 4 * kGatherWarpWords * 4;
+  const int bits = 64 - __builtin_clzll(std::max<uint64_t>(1, ix->n - 1));
+  cudaFuncSetAttribute(gather_rows_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  gather_rows_kernel<true><<<grid, 128, smem, st>>>(cols, row_ptr, nullptr, row_ptr, cols, nq, bits,
+                                                    big2.off, big2.len, big2.n); ::cmg::note_launch();
+  CM_CUDA_TRY(cudaGetLastError());
+  {
+    const int msmem = 2 * kMidBuf * 4;
+    cudaFuncSetAttribute(sort_mid_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, msmem);
+    const uint64_t tasks = (nq + 1023) / 1024;
+    const unsigned mgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(tasks, (uint64_t)sm_count() * 3));
+    sort_mid_rows_kernel<<<mgrid, kMidThreads, msmem, st>>>(cols, row_ptr, nq, big2.off, big2.len, big2.n); ::cmg::note_launch();
+  }
+  CM_CUDA_TRY(cudaGetLastError());
+  Out o2{};
+  o2.big_off = big2.off;
+  o2.big_len = big2.len;
+  o2.n_big = big2.n;
+  return sort_big_rows(cols, o2, st);
 }
 
 cm_status radius_collect_dev(const cm_index* ix, const double* q, uint64_t nq, int kernel,
@@ -1170,8 +1605,10 @@ cm_status gather_rows_dev(const uint32_t* temp, const uint64_t* toff, const uint
   const uint64_t groups = (nq + 31) / 32;
   const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((groups + 3) / 4, (uint64_t)sm_count() * 8));
   const int smem = 4 * kGatherWarpWords * 4;
-  cudaFuncSetAttribute(gather_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  gather_rows_kernel<<<grid, 128, smem, st>>>(temp, toff, counts, row_ptr, perm, cols, nq); ::cmg::note_launch();
+  (void)perm;
+  cudaFuncSetAttribute(gather_rows_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  gather_rows_kernel<false><<<grid, 128, smem, st>>>(temp, toff, counts, row_ptr, cols, nq, 32,
+                                                     nullptr, nullptr, nullptr); ::cmg::note_launch();
   CM_CUDA_TRY(cudaGetLastError());
   return CM_OK;
 }

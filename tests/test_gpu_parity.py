@@ -110,20 +110,63 @@ def test_arena_overflow_falls_back(cfg0, cfg0_oracle):
     overflows it and must take the two-pass path with identical results."""
     from paper_2502_11602_b200 import _native
     cloud, q = cfg0
-    q = q[:20000]
+    q = q[:60000]
     m = cm.Cheesemap.build(cloud, cm.BuildOptions(flavor=cm.Flavor.Mixed))
     cm.radius_search_batch(m, q, 0.05, cm.SPHERE)
-    row, cols = cm.radius_search_batch(m, q, 3.0, cm.SPHERE)
+    row, cols = cm.radius_search_batch(m, q, 1.4, cm.SPHERE)
     assert _native.last_query_timing()["two_pass"] == 1
-    orow, ocols = cfg0_oracle.radius_csr(q, 0, 3.0)
+    orow, ocols = cfg0_oracle.radius_csr(q, 0, 1.4)
     assert np.array_equal(row, orow) and np.array_equal(cols, ocols)
-    row, cols = cm.radius_search_batch(m, q, 3.0, cm.SPHERE)
+    row, cols = cm.radius_search_batch(m, q, 1.4, cm.SPHERE)
     assert _native.last_query_timing()["two_pass"] == 0
     assert np.array_equal(row, orow) and np.array_equal(cols, ocols)
 
 
 @pytest.mark.parametrize("flavor", FLAVORS)
-def test_count_then_fill_api(cfg0, cfg0_oracle, flavor):
+@pytest.mark.parametrize("kernel", [cm.SPHERE, cm.CUBE, cm.CYLINDER])
+@pytest.mark.parametrize("r", [2.5, 4.0])
+def test_wide_radius_csr(cfg0, cfg0_oracle, flavor, kernel, r):
+    """Large radii: wide tiles (hulls of > 32 columns in batches of 32), count
+    + scan + unsorted fill + in-place row sort."""
+    from paper_2502_11602_b200 import _native
+    cloud, _ = cfg0
+    # a spatially dense query set (every point of a corner), so tiles are compact
+    q = cloud[(cloud[:, 0] < cloud[:, 0].min() + 40) & (cloud[:, 1] < cloud[:, 1].min() + 40)]
+    q = np.ascontiguousarray(q[:8000])
+    m = cm.Cheesemap.build(cloud, cm.BuildOptions(flavor=flavor))
+    _native.query_stats(reset=True)
+    row, cols = cm.radius_search_batch(m, q, r, kernel)
+    assert _native.last_query_timing()["two_pass"] == 1
+    st = _native.query_stats()
+    # most fill tiles went wide, not one query per warp
+    assert st["fill_tiles"] > 0 and st["fill_fallback_tiles"] < st["fill_tiles"] // 4
+    orow, ocols = cfg0_oracle.radius_csr(q, int(kernel), r)
+    assert np.array_equal(row, orow)
+    assert np.array_equal(cols, ocols)
+
+
+def test_wide_tall_columns():
+    """A dense vertical column: spans past the 11-bit key range (key base
+    moves up mid-column) and rows past the warp sort (block sort)."""
+    rng = np.random.default_rng(17)
+    tower = np.column_stack([rng.uniform(0, 1.5, 30000), rng.uniform(0, 1.5, 30000),
+                             rng.uniform(0, 3, 30000)])
+    bg = rng.uniform(0, 20, (20000, 3))
+    cloud = np.ascontiguousarray(np.vstack([bg, tower]))
+    q = np.ascontiguousarray(np.vstack([tower[::50], bg[::10]]))
+    o = CpuIndex(cloud, flavor=1)
+    for flavor in FLAVORS:
+        m = cm.Cheesemap.build(cloud, cm.BuildOptions(flavor=flavor))
+        for r in (2.5, 3.5):
+            row, cols = cm.radius_search_batch(m, q, r, cm.SPHERE)
+            orow, ocols = o.radius_csr(q, 0, r)
+            assert (np.diff(orow.astype(np.int64)) > 4096).any()
+            assert np.array_equal(row, orow) and np.array_equal(cols, ocols)
+
+
+@pytest.mark.parametrize("flavor", FLAVORS)
+@pytest.mark.parametrize("r", [1.5, 2.5])
+def test_count_then_fill_api(cfg0, cfg0_oracle, flavor, r):
     """The two-call CSR API (cm_radius_count, caller scan, cm_radius_fill)."""
     import ctypes
     from paper_2502_11602_b200 import _native
@@ -133,15 +176,15 @@ def test_count_then_fill_api(cfg0, cfg0_oracle, flavor):
     L = _native.lib()
     counts = np.zeros(q.shape[0], dtype=np.uint32)
     qp = q.ctypes.data_as(ctypes.c_void_p)
-    cm._check(L.cm_radius_count(m.handle, qp, q.shape[0], 1, 1.5,
+    cm._check(L.cm_radius_count(m.handle, qp, q.shape[0], 1, r,
                                 counts.ctypes.data_as(ctypes.c_void_p), None, None))
     row = np.zeros(q.shape[0] + 1, dtype=np.uint64)
     np.cumsum(counts, out=row[1:])
     cols = np.zeros(int(row[-1]), dtype=np.uint32)
-    cm._check(L.cm_radius_fill(m.handle, qp, q.shape[0], 1, 1.5,
+    cm._check(L.cm_radius_fill(m.handle, qp, q.shape[0], 1, r,
                                row.ctypes.data_as(ctypes.c_void_p),
                                cols.ctypes.data_as(ctypes.c_void_p), None))
-    orow, ocols = cfg0_oracle.radius_csr(q, 1, 1.5)
+    orow, ocols = cfg0_oracle.radius_csr(q, 1, r)
     assert np.array_equal(row, orow) and np.array_equal(cols, ocols)
 
 
