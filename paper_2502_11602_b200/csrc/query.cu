@@ -1222,7 +1222,6 @@ __global__ void __launch_bounds__(kMidThreads) sort_mid_rows_kernel(
     uint32_t* cols, const uint64_t* __restrict__ row_ptr, uint64_t nq, uint64_t* big_off,
     uint32_t* big_len, uint32_t* n_big) {
   extern __shared__ uint32_t msm[];
-  uint32_t* const bufs[2] = {msm, msm + kMidBuf};
   __shared__ uint32_t s_off[kMidThreads], s_len[kMidThreads], s_rb[kMidThreads],
       s_runs[kMidThreads];
   __shared__ uint32_t s_wsum[kMidThreads / 32], s_wfit[kMidThreads / 32],
@@ -1286,7 +1285,7 @@ __global__ void __launch_bounds__(kMidThreads) sort_mid_rows_kernel(
       for (int w = 0; w < kMidThreads / 32; ++w) g += s_wfit[w], maxruns = max(maxruns, s_wmax[w]);
       const uint32_t nruns = s_rb[g - 1] + s_runs[g - 1];
       if (nruns) {
-        uint32_t* b0 = bufs[0];
+        uint32_t* b0 = msm;
         const uint32_t span = s_off[g - 1] + s_len[g - 1];
         {  // load the span flat, 8 loads in flight per thread
           uint32_t r = 0;
@@ -1338,8 +1337,11 @@ __global__ void __launch_bounds__(kMidThreads) sort_mid_rows_kernel(
         int cur = 0;
         for (uint32_t w = 64; w < 64u * maxruns; w <<= 1) {
           if (own && w < rl) {  // this row still has runs to merge
-            const uint32_t* src = bufs[cur];
-            uint32_t* dst = bufs[cur ^ 1];
+            const uint32_t* src = msm + cur * kMidBuf;
+            uint32_t* dst = msm + (cur ^ 1) * kMidBuf;
+            // outputs [o0, o0 + 64) are one 64-word block: constant swizzle
+            uint32_t* dblk = dst + base + 64u * j;
+            const uint32_t dsw = (base / 64u + j) & 31u;
             const uint32_t o0 = 64u * j;
             const uint32_t pb = o0 / (2 * w) * (2 * w);
             const uint32_t a1 = min(pb + w, rl), b1 = min(pb + 2 * w, rl);
@@ -1367,7 +1369,7 @@ __global__ void __launch_bounds__(kMidThreads) sort_mid_rows_kernel(
               for (int s4 = 0; s4 < 4; ++s4) {
                 const uint32_t o = o0 + 16u * s4 + step;
                 const bool ta = av[s4] < bv[s4];  // handles are distinct
-                if (o < oend) dst[mid_swz(base + o)] = ta ? av[s4] : bv[s4];
+                if (o < oend) dblk[(16u * s4 + step) ^ dsw] = ta ? av[s4] : bv[s4];
                 ia[s4] += ta;
                 ib[s4] += !ta;
                 const uint32_t idx = ta ? A0 + ia[s4] : B0 + ib[s4];
@@ -1389,7 +1391,7 @@ __global__ void __launch_bounds__(kMidThreads) sort_mid_rows_kernel(
             const uint32_t rr = s_runs[r];
             if (rr) {
               const int which = (32 - __clz((int)(rr - 1))) & 1;  // ceil(log2 rr) parity
-              cols[g0 + f] = bufs[which][mid_swz(64u * s_rb[r] + (f - s_off[r]))];
+              cols[g0 + f] = msm[which * kMidBuf + mid_swz(64u * s_rb[r] + (f - s_off[r]))];
             }
           }
         }
