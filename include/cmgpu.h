@@ -220,6 +220,10 @@ uint64_t cm_launch_count(void);
  * tiles, tiles answered one query per warp (fallback), hull points,
  * in-range candidates (count pass only). out8 has 8 entries. */
 cm_status cm_debug_query_stats(uint64_t* out8, int reset);
+/* Device memory held by this library's stream-ordered pool on `device`:
+ * reserved (cached + in use) and in use, in bytes; trim != 0 first returns
+ * the cached part to the device. */
+cm_status cm_debug_pool_bytes(int device, int trim, uint64_t* reserved, uint64_t* used);
 
 const char* cm_last_error(void);
 const char* cm_status_name(cm_status s);

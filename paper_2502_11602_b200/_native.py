@@ -17,7 +17,7 @@ EXPORTS = [
     "cm_get_build_timing", "cm_export_voxels", "cm_size", "cm_radius_count", "cm_radius_fill",
     "cm_radius_search", "cm_radius_search_to_host", "cm_csr_info", "cm_csr_download", "cm_csr_free", "cm_radius_digest",
     "cm_knn", "cm_corrupt_for_testing", "cm_last_error", "cm_status_name",
-    "cm_get_last_query_timing", "cm_launch_count", "cm_debug_query_stats",
+    "cm_get_last_query_timing", "cm_launch_count", "cm_debug_query_stats", "cm_debug_pool_bytes",
     "cm_global_density", "cm_weighted_density",
 ]
 
@@ -98,6 +98,7 @@ def lib():
         "cm_get_last_query_timing": ([ctypes.POINTER(QueryTimingC)], i32),
         "cm_launch_count": ([], u64),
         "cm_debug_query_stats": ([p, i32], i32),
+        "cm_debug_pool_bytes": ([i32, i32, p, p], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -130,3 +131,12 @@ def query_stats(reset=True):
                 count_hull_points=int(out[2]), in_range=int(out[3]), fill_tiles=int(out[4]),
                 fill_fallback_tiles=int(out[5]), fill_hull_points=int(out[6]),
                 fill_long_rows=int(out[7]))
+
+
+def pool_bytes(device=0, trim=False):
+    """(reserved, in use) bytes of the library's device memory pool."""
+    r, u = ctypes.c_uint64(), ctypes.c_uint64()
+    rc = lib().cm_debug_pool_bytes(device, int(trim), ctypes.byref(r), ctypes.byref(u))
+    if rc != 0:
+        raise RuntimeError(f"cm_debug_pool_bytes failed ({rc})")
+    return r.value, u.value

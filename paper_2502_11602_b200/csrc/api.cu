@@ -206,6 +206,26 @@ cm_status cm_debug_query_stats(uint64_t* out8, int reset) {
   return CM_OK;
 }
 
+cm_status cm_debug_pool_bytes(int device, int trim, uint64_t* reserved, uint64_t* used) {
+  if (!reserved || !used) {
+    set_error("null output pointer");
+    return CM_INVALID_ARGUMENT;
+  }
+  DeviceGuard dg(device);
+  cudaMemPool_t pool;
+  CM_CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, device));
+  if (trim) {
+    CM_CUDA_TRY(cudaDeviceSynchronize());
+    CM_CUDA_TRY(cudaMemPoolTrimTo(pool, 0));
+  }
+  uint64_t r = 0, u = 0;  // the attributes are cuuint64_t (64-bit)
+  CM_CUDA_TRY(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &r));
+  CM_CUDA_TRY(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &u));
+  *reserved = r;
+  *used = u;
+  return CM_OK;
+}
+
 const char* cm_status_name(cm_status s) {
   switch (s) {
     case CM_OK: return "CM_OK";

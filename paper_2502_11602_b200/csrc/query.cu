@@ -25,6 +25,7 @@
 // rows into a scratch arena at atomically allocated offsets; a gather copies
 // them into CSR order after the row_ptr scan).
 #include <algorithm>
+#include <cstdlib>
 
 #include "index.cuh"
 #include "sort_scan.cuh"
@@ -72,6 +73,7 @@ struct Out {
   uint32_t* big_len;
   uint32_t* n_big;
   int wide_fill;                  // FILL: wide tiles may leave rows unsorted (sorted afterwards)
+  int no_wide;                    // diagnostics (CMGPU_NO_WIDE): wide tiles off
 };
 
 template <typename K>
@@ -673,6 +675,9 @@ __device__ __forceinline__ void wide_tile(const Tables& t, const Range& R, bool 
       const SRec* sr = reinterpret_cast<const SRec*>(stg + buf * 32);
       const uint32_t len = min(32u, ce - p);
       const bool need = (colmask >> c) & 1u;
+      // chunks (k-sorted) outside every lane's z window are skipped whole
+      const bool want = need & (sr[len - 1].meta >= kk0) & (sr[0].meta <= kk0 + kspan);
+      const bool anyw = __any_sync(0xffffffffu, want);
       uint32_t kbase = 0;
       if (FILL) {
         uint32_t cbase = cbeg[c];
@@ -687,7 +692,7 @@ __device__ __forceinline__ void wide_tile(const Tables& t, const Range& R, bool 
         }
         kbase = (c << 11) | (p - cbase);
       }
-      uint32_t u = 0;
+      uint32_t u = anyw ? 0u : len;
       for (; u + 8 <= len; u += 8) {
         SRec v[8];
 #pragma unroll
@@ -788,7 +793,7 @@ __global__ void __launch_bounds__(kQThreads, 5) radius_tile_kernel(
       nj = J1 - J0 + 1;
       nc = (uint64_t)(I1 - I0 + 1) * nj;
       use_tile = nc <= 32;
-      if (!use_tile && MODE != MODE_COLLECT && (MODE != MODE_FILL || o.wide_fill) &&
+      if (!use_tile && !o.no_wide && MODE != MODE_COLLECT && (MODE != MODE_FILL || o.wide_fill) &&
           nc <= (uint64_t)kWideMaxCols) {
         // worth it while the lanes' own columns cover >= 1/8 of the hull on average
         uint32_t own = ok ? (uint32_t)((R.i1 - R.i0 + 1) * (R.j1 - R.j0 + 1)) : 0u;
@@ -866,7 +871,9 @@ __global__ void __launch_bounds__(kQThreads, 5) radius_tile_kernel(
       const uint32_t len = min(32u, ce - p);
       const bool need = (colmask >> c) & 1u;
       const uint32_t kbase = (c << 11) | (p - __shfl_sync(0xffffffffu, b, c));
-      uint32_t u = 0;
+      // chunks (k-sorted) outside every lane's z window are skipped whole
+      const bool want = need & (sr[len - 1].meta >= kk0) & (sr[0].meta <= kk0 + kspan);
+      uint32_t u = __any_sync(0xffffffffu, want) ? 0u : len;
       for (; u + 8 <= len; u += 8) {
         SRec v[8];
 #pragma unroll
@@ -1431,7 +1438,10 @@ cm_status launch_radius(const cm_index* ix, const double* q, uint64_t nq, int ke
     const uint64_t need = ((nq + 31) / 32 + kQWarps - 1) / kQWarps;
     const unsigned grid =
         (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(need, (uint64_t)sm_count() * per_sm));
-    kern<<<grid, kQThreads, smem, st>>>(t, q, nq, r, perm, o); ::cmg::note_launch();
+    static const bool no_wide = std::getenv("CMGPU_NO_WIDE") != nullptr;
+    Out o2 = o;
+    o2.no_wide = no_wide ? 1 : 0;
+    kern<<<grid, kQThreads, smem, st>>>(t, q, nq, r, perm, o2); ::cmg::note_launch();
     CM_CUDA_TRY(cudaGetLastError());
     return CM_OK;
   };

@@ -29,9 +29,11 @@ def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
-def timed(fn, reps=3):
+def timed(fn, reps=3, release=None):
+    """Best of `reps` device-timed calls; `release(out)` runs after each
+    call except the last, outside the timed region."""
     best = None
-    for _ in range(reps):
+    for i in range(reps):
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -40,6 +42,8 @@ def timed(fn, reps=3):
         e1.synchronize()
         ms = e0.elapsed_time(e1)
         best = ms if best is None else min(best, ms)
+        if release is not None and i + 1 < reps:
+            release(out)
     return best, out
 
 
@@ -78,7 +82,7 @@ def radius_case(m, qd, qh_sample, oracle, kernel, r, n_sample):
     run_ms = None
     for _ in range(2):  # warm
         L.cm_csr_free(run())
-    ms, csr = timed(run)
+    ms, csr = timed(run, release=L.cm_csr_free)
     L.cm_csr_free(csr)
     t = _native.last_query_timing()
     # verification on a sample: counts + digests vs the oracle
