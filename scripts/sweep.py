@@ -134,6 +134,9 @@ def main():
         2: dict(flavors=["mixed"], cell=0.25, radii=[0.05, 0.1, 0.25], kernels=[0], ks=[],
                 digest=True),
         3: dict(flavors=["mixed"], cell=1.0, radii=[], kernels=[], ks=[8, 16, 32, 64]),
+        # 200M points on one GPU; r = 2.5 as digests (its CSR would be ~170 GB)
+        4: dict(flavors=["mixed"], cell=1.0, radii=[1.0, 2.5], kernels=[0], ks=[],
+                digest_radii=[2.5]),
     }
     fl = {"dense": 0, "sparse": 1, "mixed": 2}
     for c in cfgs:
@@ -159,7 +162,8 @@ def main():
                      "build_ms": round(min(builds), 3), "radius": [], "knn": []}
             for r in p["radii"]:
                 for kern in p["kernels"]:
-                    fn = digest_case if p.get("digest") else radius_case
+                    fn = (digest_case if p.get("digest") or r in p.get("digest_radii", ())
+                          else radius_case)
                     res = fn(m, qd, samp, oracle, kern, r, samp.shape[0])
                     log(f"  cfg{c} {f} {res['kernel']} r={r}: {res['qps'] / 1e6:.1f} M q/s "
                         f"parity={res['parity']} phases={res.get('phases', res.get('mode'))}")
