@@ -55,7 +55,9 @@ typedef enum {
   CM_CAPACITY = 3,         /* CapacityError        errors.hpp:19-22 */
   CM_OUT_OF_DOMAIN = 4,    /* OutOfDomainError     errors.hpp:24-27 */
   CM_CUDA = 5,             /* CUDA runtime failure (no reference analogue) */
-  CM_NCCL = 6              /* collective failure (multi-GPU slabs) */
+  CM_NCCL = 6,             /* collective failure (multi-GPU slabs) */
+  CM_PARSE = 7,            /* ParseError           errors.hpp:29-32 */
+  CM_IO = 8                /* IoError              errors.hpp:39-42 */
 } cm_status;
 
 /* map.hpp:15 */
@@ -224,6 +226,31 @@ cm_status cm_debug_query_stats(uint64_t* out8, int reset);
  * reserved (cached + in use) and in use, in bytes; trim != 0 first returns
  * the cached part to the device. */
 cm_status cm_debug_pool_bytes(int device, int trim, uint64_t* reserved, uint64_t* used);
+
+/* ---- LAS ingestion: read_las (io.hpp:39-42, io.cpp:33-106) ----------------
+ * The header is checked on the host with the reference's checks, messages
+ * and order (CM_PARSE = ParseError, CM_IO = IoError); the point records are
+ * decoded on the device, coordinate = raw * scale + offset in fp64 without
+ * FMA (io.cpp:97-103). Point formats 0-8, LAS 1.2-1.4 (64-bit 1.4 counts). */
+typedef struct {
+  uint8_t version_major, version_minor, point_format;
+  uint16_t header_size, record_length;
+  uint32_t data_offset;
+  uint64_t point_count;
+  double scale[3], offset[3];
+  double bounds_min[3], bounds_max[3];
+} cm_las_header;
+
+/* Header of a LAS image in HOST memory (io.cpp:38-89 checks). */
+cm_status cm_las_parse_header(const void* bytes, uint64_t nbytes, cm_las_header* out);
+/* Decodes a whole LAS image (host or device memory) into xyz (n x 3 doubles,
+ * host or device, capacity in points). xyz == NULL returns the header only.
+ * Truncated images fail like the reference (io.cpp:92-96). */
+cm_status cm_las_decode(const void* bytes, uint64_t nbytes, double* xyz, uint64_t xyz_capacity,
+                        cm_las_header* hdr, int device, void* stream);
+/* read_las(path): CM_IO when the file cannot be opened, then cm_las_decode. */
+cm_status cm_las_read(const char* path, double* xyz, uint64_t xyz_capacity, cm_las_header* hdr,
+                      int device, void* stream);
 
 const char* cm_last_error(void);
 const char* cm_status_name(cm_status s);

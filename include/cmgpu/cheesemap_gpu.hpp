@@ -38,6 +38,8 @@ class CapacityError : public Error { public: using Error::Error; };
 class OutOfDomainError : public Error { public: using Error::Error; };
 class InvalidArgumentError : public Error { public: using Error::Error; };
 class CudaError : public Error { public: using Error::Error; };
+class ParseError : public Error { public: using Error::Error; };
+class IoError : public Error { public: using Error::Error; };
 
 inline void check(cm_status s) {
   if (s == CM_OK) return;
@@ -47,6 +49,8 @@ inline void check(cm_status s) {
     case CM_INVALID_ARGUMENT: throw InvalidArgumentError(msg);
     case CM_CAPACITY: throw CapacityError(msg);
     case CM_OUT_OF_DOMAIN: throw OutOfDomainError(msg);
+    case CM_PARSE: throw ParseError(msg);
+    case CM_IO: throw IoError(msg);
     default: throw CudaError(msg);
   }
 }
@@ -229,6 +233,41 @@ inline std::vector<PointHandle> kernel_search(const Cheesemap& m, const BoxKerne
 inline std::vector<PointHandle> kernel_search(const Cheesemap& m, const CylinderKernel& k) {
   const Csr c = radius_search(m, {Point3{k.center_x, k.center_y, 0.0}}, k.radius, CM_CYLINDER);
   return {c.cols.begin(), c.cols.end()};
+}
+
+// ---------------------------------------------------------------- io.hpp --
+struct Aabb {
+  Point3 min, max;
+};
+struct LasHeaderInfo {  // io.hpp:11-19
+  std::uint8_t version_major = 0, version_minor = 0, point_format = 0;
+  std::uint64_t point_count = 0;
+  double scale_x = 0.0, scale_y = 0.0, scale_z = 0.0;
+  double offset_x = 0.0, offset_y = 0.0, offset_z = 0.0;
+  Aabb bounds;
+};
+struct LasFile {  // io.hpp:21-24
+  PointCloud cloud;
+  LasHeaderInfo header;
+};
+
+// read_las (io.hpp:39-42): header checks on the host, records decoded on
+// the device; throws IoError / ParseError with the reference's messages.
+inline LasFile read_las(const std::string& path, int device = 0) {
+  cm_las_header h;
+  check(cm_las_read(path.c_str(), nullptr, 0, &h, device, nullptr));
+  LasFile f;
+  f.cloud.resize(h.point_count);
+  check(cm_las_read(path.c_str(), reinterpret_cast<double*>(f.cloud.data()), h.point_count, &h,
+                    device, nullptr));
+  LasHeaderInfo& o = f.header;
+  o.version_major = h.version_major, o.version_minor = h.version_minor;
+  o.point_format = h.point_format, o.point_count = h.point_count;
+  o.scale_x = h.scale[0], o.scale_y = h.scale[1], o.scale_z = h.scale[2];
+  o.offset_x = h.offset[0], o.offset_y = h.offset[1], o.offset_z = h.offset[2];
+  o.bounds.min = {h.bounds_min[0], h.bounds_min[1], h.bounds_min[2]};
+  o.bounds.max = {h.bounds_max[0], h.bounds_max[1], h.bounds_max[2]};
+  return f;
 }
 
 // ---------------------------------------------------------- analysis.hpp --

@@ -22,6 +22,7 @@
 #include <limits>
 #include <optional>
 #include <random>
+#include <string>
 #include <thread>
 #include <unordered_map>
 #include <vector>
@@ -623,6 +624,92 @@ int orc_weighted_density(const double* xyz, uint64_t n, uint64_t sample_size, ui
   }
   *value = static_cast<double>(ws) / static_cast<double>(tot);
   return OK;
+}
+
+// ---- read_las restated (io.cpp:33-106) over an in-memory image ------------
+// Same checks, messages and order as the reference; coordinate =
+// raw * scale + offset (int32 promoted to double, no FMA: -ffp-contract=off).
+// Status: 0 ok, 7 ParseError, 2 capacity too small. `msg` gets the message.
+struct orc_las_header {
+  uint8_t version_major, version_minor, point_format;
+  uint16_t header_size, record_length;
+  uint32_t data_offset;
+  uint64_t point_count;
+  double scale[3], offset[3];
+  double bounds_min[3], bounds_max[3];
+};
+
+static int las_fail(char* msg, int msglen, const std::string& m, int code) {
+  if (msg && msglen > 0) {
+    std::strncpy(msg, m.c_str(), (size_t)msglen - 1);
+    msg[msglen - 1] = 0;
+  }
+  return code;
+}
+
+extern "C++" {
+template <class T>
+static T las_rd(const unsigned char* b, size_t off) {
+  T v;
+  std::memcpy(&v, b + off, sizeof(T));
+  return v;
+}
+}
+
+int orc_las_read(const void* bytes, uint64_t n, const char* name, orc_las_header* h,
+                 double* xyz, uint64_t cap, char* msg, int msglen) {
+  const unsigned char* b = static_cast<const unsigned char*>(bytes);
+  const std::string nm = name ? name : "";
+  if (n < 227 || std::memcmp(b, "LASF", 4) != 0)  // io.cpp:44-47
+    return las_fail(msg, msglen, "bad LAS magic at byte 0 in " + nm, 7);
+  std::memset(h, 0, sizeof(*h));
+  h->version_major = b[24];  // io.cpp:49-56
+  h->version_minor = b[25];
+  if (h->version_major != 1 || h->version_minor < 2 || h->version_minor > 4)
+    return las_fail(msg, msglen,
+                    "unsupported LAS version " + std::to_string(h->version_major) + "." +
+                        std::to_string(h->version_minor), 7);
+  h->header_size = las_rd<uint16_t>(b, 94);  // io.cpp:57-62
+  h->data_offset = las_rd<uint32_t>(b, 96);
+  h->point_format = b[104];
+  if (h->point_format > 8)
+    return las_fail(msg, msglen,
+                    "unsupported LAS point record format " + std::to_string(h->point_format), 7);
+  h->record_length = las_rd<uint16_t>(b, 105);  // io.cpp:63-67
+  if (h->record_length < 12)
+    return las_fail(msg, msglen,
+                    "LAS point record length " + std::to_string(h->record_length) +
+                        " is too short", 7);
+  h->point_count = las_rd<uint32_t>(b, 107);  // io.cpp:68-71
+  if (h->point_count == 0 && h->version_minor == 4 && h->header_size >= 255)
+    h->point_count = n >= 255 ? las_rd<uint64_t>(b, 247) : 0;
+  for (int a = 0; a < 3; ++a) h->scale[a] = las_rd<double>(b, 131 + 8 * a);  // io.cpp:72-77
+  if (!(h->scale[0] > 0.0) || !(h->scale[1] > 0.0) || !(h->scale[2] > 0.0))
+    return las_fail(msg, msglen, "non-positive LAS scale factor at byte 131", 7);
+  for (int a = 0; a < 3; ++a) h->offset[a] = las_rd<double>(b, 155 + 8 * a);  // io.cpp:78-86
+  for (int a = 0; a < 3; ++a) {
+    h->bounds_max[a] = las_rd<double>(b, 179 + 16 * a);
+    h->bounds_min[a] = las_rd<double>(b, 187 + 16 * a);
+  }
+  if (h->data_offset < h->header_size || h->data_offset > n)  // io.cpp:88-91
+    return las_fail(msg, msglen,
+                    "LAS point data offset " + std::to_string(h->data_offset) +
+                        " is out of range", 7);
+  if (!xyz) return 0;
+  uint64_t pos = h->data_offset;
+  for (uint64_t i = 0; i < h->point_count; ++i, pos += h->record_length) {  // io.cpp:93-105
+    if (pos + h->record_length > n)
+      return las_fail(msg, msglen,
+                      "truncated LAS point record " + std::to_string(i) + " at byte " +
+                          std::to_string(pos), 7);
+    if (i >= cap) return las_fail(msg, msglen, "capacity", 2);
+    const int32_t rx = las_rd<int32_t>(b, pos), ry = las_rd<int32_t>(b, pos + 4),
+                  rz = las_rd<int32_t>(b, pos + 8);
+    xyz[3 * i] = rx * h->scale[0] + h->offset[0];
+    xyz[3 * i + 1] = ry * h->scale[1] + h->offset[1];
+    xyz[3 * i + 2] = rz * h->scale[2] + h->offset[2];
+  }
+  return 0;
 }
 
 }  // extern "C"

@@ -156,3 +156,64 @@ def weighted_density(xyz, sample_size=0, seed=0, which="oracle", threads=0):
     if rc:
         raise RuntimeError(STATUS.get(rc, rc), rc)
     return v.value, bins
+
+
+# ---- read_las / write_las (io.cpp:33-166) -----------------------------------
+class LasHeader(ctypes.Structure):  # orc_las_header / ref_las_header
+    _fields_ = [("version_major", ctypes.c_uint8), ("version_minor", ctypes.c_uint8),
+                ("point_format", ctypes.c_uint8), ("header_size", ctypes.c_uint16),
+                ("record_length", ctypes.c_uint16), ("data_offset", ctypes.c_uint32),
+                ("point_count", ctypes.c_uint64), ("scale", ctypes.c_double * 3),
+                ("offset", ctypes.c_double * 3), ("bounds_min", ctypes.c_double * 3),
+                ("bounds_max", ctypes.c_double * 3)]
+
+
+def las_read(image=None, path=None, which="oracle", name=None):
+    """-> (status, message, header LasHeader, xyz or None). The restatement
+    reads an in-memory image (`image`, or the file at `path`); the reference
+    reads `path` through its own read_las."""
+    L = lib(which).lib
+    h = LasHeader()
+    msg = ctypes.create_string_buffer(512)
+    if which == "oracle":
+        if image is None:
+            with open(path, "rb") as f:
+                image = f.read()
+        buf = np.frombuffer(bytes(image), dtype=np.uint8)
+        fn = L.orc_las_read
+        fn.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_char_p, ctypes.POINTER(LasHeader),
+                       ctypes.c_void_p, ctypes.c_uint64, ctypes.c_char_p, ctypes.c_int]
+        fn.restype = ctypes.c_int
+        nm = os.fsencode(name if name is not None else (path or "<memory>"))
+        rc = fn(buf.ctypes.data_as(ctypes.c_void_p), buf.size, nm, ctypes.byref(h), None, 0, msg,
+                512)
+        if rc != 0:
+            return rc, msg.value.decode(), h, None
+        xyz = np.empty((h.point_count, 3), dtype=np.float64)
+        rc = fn(buf.ctypes.data_as(ctypes.c_void_p), buf.size, nm, ctypes.byref(h), _p(xyz),
+                xyz.shape[0], msg, 512)
+        return rc, msg.value.decode(), h, (xyz if rc == 0 else None)
+    fn = L.ref_las_read
+    fn.argtypes = [ctypes.c_char_p, ctypes.POINTER(LasHeader), ctypes.c_void_p, ctypes.c_uint64,
+                   ctypes.c_char_p, ctypes.c_int]
+    fn.restype = ctypes.c_int
+    rc = fn(os.fsencode(path), ctypes.byref(h), None, 0, msg, 512)
+    if rc != 0:
+        return rc, msg.value.decode(), h, None
+    xyz = np.empty((h.point_count, 3), dtype=np.float64)
+    rc = fn(os.fsencode(path), ctypes.byref(h), _p(xyz), xyz.shape[0], msg, 512)
+    return rc, msg.value.decode(), h, (xyz if rc == 0 else None)
+
+
+def las_write_reference(xyz, path, scale=0.001):
+    """The reference's write_las (io.cpp:108-166)."""
+    L = lib("reference").lib
+    fn = L.ref_las_write
+    fn.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_char_p, ctypes.c_double,
+                   ctypes.c_char_p, ctypes.c_int]
+    fn.restype = ctypes.c_int
+    a = np.ascontiguousarray(xyz, dtype=np.float64).reshape(-1, 3)
+    msg = ctypes.create_string_buffer(512)
+    rc = fn(_p(a), a.shape[0], os.fsencode(path), scale, msg, 512)
+    if rc != 0:
+        raise RuntimeError(f"ref write_las failed ({rc}): {msg.value.decode()}")

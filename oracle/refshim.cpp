@@ -36,6 +36,8 @@ int status_of(const std::exception& e) {
   if (dynamic_cast<const InvalidArgumentError*>(&e)) return 2;
   if (dynamic_cast<const CapacityError*>(&e)) return 3;
   if (dynamic_cast<const OutOfDomainError*>(&e)) return 4;
+  if (dynamic_cast<const ParseError*>(&e)) return 7;
+  if (dynamic_cast<const IoError*>(&e)) return 8;
   return 99;
 }
 
@@ -256,6 +258,64 @@ int ref_weighted_density(const double* xyz, uint64_t n, uint64_t sample_size, ui
     *value = wd.value;
     for (int b = 0; b < 256; ++b) bins256[b] = wd.histogram.bins[b];
   } catch (const std::exception& e) {
+    return status_of(e);
+  }
+  return 0;
+}
+
+// read_las / write_las through the reference (io.cpp:33-166). The header
+// struct has orc_las_header's layout. Status as status_of; `msg` gets what().
+struct ref_las_header {
+  uint8_t version_major, version_minor, point_format;
+  uint16_t header_size, record_length;
+  uint32_t data_offset;
+  uint64_t point_count;
+  double scale[3], offset[3];
+  double bounds_min[3], bounds_max[3];
+};
+
+static void copy_msg(char* msg, int msglen, const char* m) {
+  if (msg && msglen > 0) {
+    std::strncpy(msg, m, (size_t)msglen - 1);
+    msg[msglen - 1] = 0;
+  }
+}
+
+int ref_las_read(const char* path, ref_las_header* h, double* xyz, uint64_t cap, char* msg,
+                 int msglen) {
+  try {
+    const LasFile f = read_las(path);
+    std::memset(h, 0, sizeof(*h));
+    h->version_major = f.header.version_major;
+    h->version_minor = f.header.version_minor;
+    h->point_format = f.header.point_format;
+    h->point_count = f.header.point_count;
+    h->scale[0] = f.header.scale_x, h->scale[1] = f.header.scale_y, h->scale[2] = f.header.scale_z;
+    h->offset[0] = f.header.offset_x, h->offset[1] = f.header.offset_y,
+    h->offset[2] = f.header.offset_z;
+    h->bounds_min[0] = f.header.bounds.min.x, h->bounds_min[1] = f.header.bounds.min.y,
+    h->bounds_min[2] = f.header.bounds.min.z;
+    h->bounds_max[0] = f.header.bounds.max.x, h->bounds_max[1] = f.header.bounds.max.y,
+    h->bounds_max[2] = f.header.bounds.max.z;
+    if (xyz) {
+      if (f.cloud.size() > cap) return 2;
+      std::memcpy(xyz, f.cloud.data(), f.cloud.size() * sizeof(Point3));
+    }
+  } catch (const std::exception& e) {
+    copy_msg(msg, msglen, e.what());
+    return status_of(e);
+  }
+  return 0;
+}
+
+int ref_las_write(const double* xyz, uint64_t n, const char* path, double scale, char* msg,
+                  int msglen) {
+  try {
+    PointCloud c(n);
+    if (n) std::memcpy(c.data(), xyz, n * sizeof(Point3));
+    write_las(c, path, scale);
+  } catch (const std::exception& e) {
+    copy_msg(msg, msglen, e.what());
     return status_of(e);
   }
   return 0;

@@ -10,7 +10,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libcmgpu.so")
 
 STATUS_NAMES = {0: "CM_OK", 1: "CM_EMPTY_CLOUD", 2: "CM_INVALID_ARGUMENT", 3: "CM_CAPACITY",
-                4: "CM_OUT_OF_DOMAIN", 5: "CM_CUDA", 6: "CM_NCCL"}
+                4: "CM_OUT_OF_DOMAIN", 5: "CM_CUDA", 6: "CM_NCCL", 7: "CM_PARSE", 8: "CM_IO"}
 
 EXPORTS = [
     "cm_default_options", "cm_build", "cm_build_in_bounds", "cm_free", "cm_get_grid", "cm_get_occupancy",
@@ -18,8 +18,25 @@ EXPORTS = [
     "cm_radius_search", "cm_radius_search_to_host", "cm_csr_info", "cm_csr_download", "cm_csr_free", "cm_radius_digest",
     "cm_knn", "cm_corrupt_for_testing", "cm_last_error", "cm_status_name",
     "cm_get_last_query_timing", "cm_launch_count", "cm_debug_query_stats", "cm_debug_pool_bytes",
-    "cm_global_density", "cm_weighted_density",
+    "cm_global_density", "cm_weighted_density", "cm_las_parse_header", "cm_las_decode",
+    "cm_las_read",
 ]
+
+
+class LasHeaderC(ctypes.Structure):  # cm_las_header
+    _fields_ = [("version_major", ctypes.c_uint8), ("version_minor", ctypes.c_uint8),
+                ("point_format", ctypes.c_uint8), ("header_size", ctypes.c_uint16),
+                ("record_length", ctypes.c_uint16), ("data_offset", ctypes.c_uint32),
+                ("point_count", ctypes.c_uint64), ("scale", ctypes.c_double * 3),
+                ("offset", ctypes.c_double * 3), ("bounds_min", ctypes.c_double * 3),
+                ("bounds_max", ctypes.c_double * 3)]
+
+    def as_dict(self):
+        d = {}
+        for k, _ in self._fields_:
+            v = getattr(self, k)
+            d[k] = list(v) if hasattr(v, "__len__") else int(v)
+        return d
 
 
 class BuildOptionsC(ctypes.Structure):
@@ -99,6 +116,9 @@ def lib():
         "cm_launch_count": ([], u64),
         "cm_debug_query_stats": ([p, i32], i32),
         "cm_debug_pool_bytes": ([i32, i32, p, p], i32),
+        "cm_las_parse_header": ([p, u64, ctypes.POINTER(LasHeaderC)], i32),
+        "cm_las_decode": ([p, u64, p, u64, ctypes.POINTER(LasHeaderC), i32, p], i32),
+        "cm_las_read": ([ctypes.c_char_p, p, u64, ctypes.POINTER(LasHeaderC), i32, p], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

@@ -17,6 +17,7 @@ radius_digest_batch, knn_batch). Inputs may be numpy arrays (host) or CUDA
 torch tensors (device); the C ABI stages host buffers itself.
 """
 import ctypes
+import os
 from dataclasses import dataclass, field
 from enum import IntEnum
 
@@ -54,8 +55,16 @@ class NcclError(Error):
     pass
 
 
+class ParseError(Error):  # errors.hpp:29-32
+    pass
+
+
+class IoError(Error):  # errors.hpp:39-42
+    pass
+
+
 _ERRORS = {1: EmptyCloudError, 2: InvalidArgumentError, 3: CapacityError, 4: OutOfDomainError,
-           5: CudaError, 6: NcclError}
+           5: CudaError, 6: NcclError, 7: ParseError, 8: IoError}
 
 
 def _check(status):
@@ -360,3 +369,61 @@ def weighted_density(cloud, sample_size=None, sample_seed=0, device=0):
                                              int(sample_seed), device, None, ctypes.byref(v),
                                              bins.ctypes.data_as(ctypes.c_void_p)))
     return v.value, bins
+
+
+# ------------------------------------------------------------- io.hpp ------
+def las_header(image):
+    """Header of an in-memory LAS image (bytes-like, host): read_las's header
+    checks (io.cpp:38-89) without decoding -> dict (cm_las_header fields)."""
+    buf = np.frombuffer(bytes(image) if not isinstance(image, np.ndarray) else image,
+                        dtype=np.uint8)
+    h = _native.LasHeaderC()
+    _check(_native.lib().cm_las_parse_header(buf.ctypes.data_as(ctypes.c_void_p), buf.size,
+                                             ctypes.byref(h)))
+    return h.as_dict()
+
+
+def decode_las(image, device_out=False, device=0, stream=None):
+    """read_las on an in-memory LAS image (bytes-like host buffer, or a CUDA
+    uint8 tensor): (cloud (n, 3) float64, header dict). The records are
+    decoded on the device; device_out=True returns a CUDA tensor."""
+    if _is_torch(image):
+        ptr, nbytes, keep = ctypes.c_void_p(image.data_ptr()), image.numel(), image
+    else:
+        keep = np.frombuffer(bytes(image) if not isinstance(image, np.ndarray) else image,
+                             dtype=np.uint8)
+        ptr, nbytes = keep.ctypes.data_as(ctypes.c_void_p), keep.size
+    h = _native.LasHeaderC()
+    L = _native.lib()
+    _check(L.cm_las_decode(ptr, nbytes, None, 0, ctypes.byref(h), device, None))
+    n = int(h.point_count)
+    out = _alloc_points(n, device_out, device)
+    _check(L.cm_las_decode(ptr, nbytes, _out_ptr(out), n, ctypes.byref(h), device,
+                           _stream_ptr(stream)))
+    return out, h.as_dict()
+
+
+def read_las(path, device_out=False, device=0, stream=None):
+    """read_las(path) (io.hpp:39-42): IoError when the file cannot be opened,
+    ParseError (the reference's messages) when it is malformed."""
+    h = _native.LasHeaderC()
+    L = _native.lib()
+    bpath = os.fsencode(path)
+    _check(L.cm_las_read(bpath, None, 0, ctypes.byref(h), device, None))
+    n = int(h.point_count)
+    out = _alloc_points(n, device_out, device)
+    _check(L.cm_las_read(bpath, _out_ptr(out), n, ctypes.byref(h), device, _stream_ptr(stream)))
+    return out, h.as_dict()
+
+
+def _alloc_points(n, device_out, device):
+    if device_out:
+        import torch
+        return torch.empty((n, 3), dtype=torch.float64, device=f"cuda:{device}")
+    return np.empty((n, 3), dtype=np.float64)
+
+
+def _out_ptr(a):
+    if _is_torch(a):
+        return ctypes.c_void_p(a.data_ptr())
+    return a.ctypes.data_as(ctypes.c_void_p)

@@ -229,6 +229,8 @@ cm_status cm_debug_pool_bytes(int device, int trim, uint64_t* reserved, uint64_t
 const char* cm_status_name(cm_status s) {
   switch (s) {
     case CM_OK: return "CM_OK";
+    case CM_PARSE: return "CM_PARSE";
+    case CM_IO: return "CM_IO";
     case CM_EMPTY_CLOUD: return "CM_EMPTY_CLOUD";
     case CM_INVALID_ARGUMENT: return "CM_INVALID_ARGUMENT";
     case CM_CAPACITY: return "CM_CAPACITY";

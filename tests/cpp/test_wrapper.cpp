@@ -1,3 +1,5 @@
+#include <cstring>
+#include <cstdio>
 // C++ host-side test of include/cmgpu/cheesemap_gpu.hpp, written the way the
 // reference's own tests are (tests/test_search.cpp:161-188 compares
 // kernel_search against a linear scan; test_map.cpp:213-223 the dense cap).
@@ -72,6 +74,46 @@ int main() {
     threw = true;
   }
   EXPECT(threw);
+  // read_las: a hand-assembled LAS 1.2 file (test_io.cpp:58-72's values)
+  {
+    std::vector<unsigned char> b(227 + 2 * 20, 0);
+    std::memcpy(b.data(), "LASF", 4);
+    b[24] = 1, b[25] = 2;
+    auto put16 = [&](size_t o, uint16_t v) { std::memcpy(&b[o], &v, 2); };
+    auto put32 = [&](size_t o, uint32_t v) { std::memcpy(&b[o], &v, 4); };
+    auto putd = [&](size_t o, double v) { std::memcpy(&b[o], &v, 8); };
+    put16(94, 227), put32(96, 227), put16(105, 20), put32(107, 2);
+    for (int a = 0; a < 3; ++a) putd(131 + 8 * a, 0.01), putd(155 + 8 * a, 100.0);
+    const int32_t raw[6] = {12345, -200, 0, 0, 1, 2};
+    for (int i = 0; i < 2; ++i) std::memcpy(&b[227 + 20 * i], raw + 3 * i, 12);
+    const char* path = "/tmp/cmgpu_wrapper_test.las";
+    FILE* f = std::fopen(path, "wb");
+    std::fwrite(b.data(), 1, b.size(), f);
+    std::fclose(f);
+    const cg::LasFile lf = cg::read_las(path);
+    EXPECT(lf.cloud.size() == 2 && lf.header.point_count == 2 && lf.header.scale_x == 0.01);
+    EXPECT(lf.cloud[0].x == 12345 * 0.01 + 100.0 && lf.cloud[0].y == -200 * 0.01 + 100.0);
+    EXPECT(lf.cloud[1].z == 2 * 0.01 + 100.0);
+    threw = false;
+    try {
+      cg::read_las("/tmp/cmgpu_wrapper_missing.las");
+    } catch (const cg::IoError&) {
+      threw = true;
+    }
+    EXPECT(threw);
+    b[0] = 'X';
+    f = std::fopen(path, "wb");
+    std::fwrite(b.data(), 1, b.size(), f);
+    std::fclose(f);
+    threw = false;
+    try {
+      cg::read_las(path);
+    } catch (const cg::ParseError&) {
+      threw = true;
+    }
+    EXPECT(threw);
+    std::remove(path);
+  }
   std::printf("cpp wrapper ok\n");
   return 0;
 }
