@@ -8,6 +8,8 @@
  *   Cheesemap::build(cloud, BuildOptions)  map.hpp:55  cm_build
  *   Cheesemap::grid()                      map.hpp:57  cm_get_grid
  *   Cheesemap::occupancy_stats()     map.hpp:104, map.cpp:150-171  cm_get_occupancy
+ *   Cheesemap::memory_report()       map.hpp:105, map.cpp:173-192  cm_get_memory_report
+ *   read_las(path)                   io.hpp:39-42, io.cpp:33-106  cm_las_read / cm_las_decode
  *   Cheesemap::voxel_lookup / for_each_in_voxel  map.hpp:69-102  cm_export_voxels
  *   kernel_search<SphereKernel|BoxKernel>  search.hpp:102-127
  *                                 cm_radius_count + cm_radius_fill, cm_radius_search,
@@ -141,6 +143,18 @@ cm_status cm_build_in_bounds(const double* xyz, uint64_t n, const cm_build_optio
 cm_status cm_free(cm_index* index);
 
 cm_status cm_get_grid(const cm_index* index, cm_grid_params* out);
+/* Cheesemap::memory_report (map.hpp:41-48, map.cpp:173-192): the
+ * reference's analytic byte model for this flavour and occupancy
+ * (handle / structure / total bytes), plus device_bytes, the HBM this index
+ * actually holds (records + tables). */
+typedef struct {
+  uint64_t handle_bytes;
+  uint64_t structure_bytes;
+  uint64_t total_bytes;
+  uint64_t device_bytes;
+} cm_memory_report;
+cm_status cm_get_memory_report(const cm_index* index, cm_memory_report* out);
+
 cm_status cm_get_occupancy(const cm_index* index, cm_occupancy* out,
                            uint8_t* slice_dense, uint64_t* slice_non_empty,
                            uint64_t slice_capacity);

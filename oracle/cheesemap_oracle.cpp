@@ -468,6 +468,28 @@ uint64_t orc_slice_flags(const orc_index* m, uint8_t* dense, uint64_t* non_empty
   return m->slice_non_empty.size();
 }
 
+// memory_report (map.cpp:173-192) with the cost model of map.cpp:14-18:
+// out3 = {handle_bytes, structure_bytes, total_bytes}.
+void orc_memory_report(const orc_index* m, uint64_t* out3) {
+  const std::uint64_t V = m->g.n[0] * m->g.n[1] * m->g.n[2];
+  const std::uint64_t hb = 8 * m->pts.size();
+  std::uint64_t sb = 0;
+  if (m->flavor == 0) {
+    sb = 8 * (V + 1);
+  } else if (m->flavor == 1) {
+    sb = 64 * m->non_empty;
+  } else {
+    const std::uint64_t fp = m->g.n[0] * m->g.n[1];
+    for (const std::uint64_t ne : m->slice_non_empty) {
+      const bool dense = static_cast<double>(ne) / static_cast<double>(fp) >= m->tau;
+      sb += 48 + (dense ? 24 * fp : 64 * ne);
+    }
+  }
+  out3[0] = hb;
+  out3[1] = sb;
+  out3[2] = hb + sb;
+}
+
 // (key, handle) in stored order: key ascending, handles ascending per voxel.
 void orc_export(const orc_index* m, uint64_t* keys, uint64_t* handles) {
   const std::uint64_t n = m->keys.size();

@@ -39,6 +39,7 @@ class CpuIndexLib:
         self.grid_ = f("grid", [p, p, p, p, p, p], None)
         self.non_empty_ = f("non_empty", [p], u64)
         self.slice_flags_ = f("slice_flags", [p, p, p], u64)
+        self.memory_report_ = f("memory_report", [p, p], None)
         self.export_ = f("export", [p, p, p], None)
         self.radius_ = f("radius", [p, p, u64, i, dbl, ctypes.c_uint, p, p, p, p], i)
         self.radius_fill_ = f("radius_fill", [p, p, u64, i, dbl, ctypes.c_uint, p, p], i)
@@ -120,6 +121,12 @@ class CpuIndex:
         if rc:
             raise RuntimeError(STATUS.get(rc, rc))
         return (cnt, dig, pt, vv) if stats else (cnt, dig)
+
+    def memory_report(self):
+        out = np.zeros(3, dtype=np.uint64)
+        self.L.memory_report_(self.h, _p(out))
+        return dict(handle_bytes=int(out[0]), structure_bytes=int(out[1]),
+                    total_bytes=int(out[2]))
 
     def radius_csr(self, q, kernel=0, r=1.0, threads=0):
         q = np.ascontiguousarray(q, dtype=np.float64).reshape(-1, 3)
@@ -217,3 +224,23 @@ def las_write_reference(xyz, path, scale=0.001):
     rc = fn(_p(a), a.shape[0], os.fsencode(path), scale, msg, 512)
     if rc != 0:
         raise RuntimeError(f"ref write_las failed ({rc}): {msg.value.decode()}")
+
+
+def generate_reference(text):
+    """The reference's parse_synthetic_spec + generate -> (status, msg, xyz),
+    run in a child process (oracle/ref_spec.py explains why)."""
+    import subprocess
+    import sys
+    import tempfile
+    with tempfile.TemporaryDirectory() as d:
+        out = os.path.join(d, "spec.bin")
+        subprocess.run([sys.executable, os.path.join(_HERE, "ref_spec.py"), text, out],
+                       check=True)
+        raw = open(out, "rb").read()
+    l1 = raw.index(b"\n")
+    l2 = raw.index(b"\n", l1 + 1)
+    rc, n = (int(v) for v in raw[:l1].split())
+    msg = raw[l1 + 1:l2].decode()
+    if rc != 0:
+        return rc, msg, None
+    return rc, msg, np.frombuffer(raw[l2 + 1:], dtype=np.float64).reshape(n, 3).copy()

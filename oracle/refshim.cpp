@@ -157,6 +157,13 @@ void ref_grid(const ref_index* r, double* origin3, double* cell3, uint64_t* dims
 
 uint64_t ref_non_empty(const ref_index* r) { return r->map->occupancy_stats().non_empty; }
 
+void ref_memory_report(const ref_index* r, uint64_t* out3) {
+  const MemoryReport m = r->map->memory_report();
+  out3[0] = m.handle_bytes;
+  out3[1] = m.structure_bytes;
+  out3[2] = m.total_bytes;
+}
+
 uint64_t ref_slice_flags(const ref_index* r, uint8_t* dense, uint64_t* non_empty) {
   const OccupancyStats st = r->map->occupancy_stats();
   for (std::size_t k = 0; k < st.slices.size(); ++k) {
@@ -314,6 +321,24 @@ int ref_las_write(const double* xyz, uint64_t n, const char* path, double scale,
     PointCloud c(n);
     if (n) std::memcpy(c.data(), xyz, n * sizeof(Point3));
     write_las(c, path, scale);
+  } catch (const std::exception& e) {
+    copy_msg(msg, msglen, e.what());
+    return status_of(e);
+  }
+  return 0;
+}
+
+// parse_synthetic_spec + generate through the reference (io.cpp:252-399):
+// returns the count in *n_out; xyz (capacity cap points) may be null.
+int ref_generate_spec(const char* text, double* xyz, uint64_t cap, uint64_t* n_out, char* msg,
+                      int msglen) {
+  try {
+    const PointCloud c = generate(parse_synthetic_spec(text));
+    *n_out = c.size();
+    if (xyz) {
+      if (c.size() > cap) return 2;
+      std::memcpy(xyz, c.data(), c.size() * sizeof(Point3));
+    }
   } catch (const std::exception& e) {
     copy_msg(msg, msglen, e.what());
     return status_of(e);

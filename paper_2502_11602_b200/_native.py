@@ -19,7 +19,7 @@ EXPORTS = [
     "cm_knn", "cm_corrupt_for_testing", "cm_last_error", "cm_status_name",
     "cm_get_last_query_timing", "cm_launch_count", "cm_debug_query_stats", "cm_debug_pool_bytes",
     "cm_global_density", "cm_weighted_density", "cm_las_parse_header", "cm_las_decode",
-    "cm_las_read",
+    "cm_las_read", "cm_get_memory_report",
 ]
 
 
@@ -37,6 +37,11 @@ class LasHeaderC(ctypes.Structure):  # cm_las_header
             v = getattr(self, k)
             d[k] = list(v) if hasattr(v, "__len__") else int(v)
         return d
+
+
+class MemoryReportC(ctypes.Structure):  # cm_memory_report
+    _fields_ = [("handle_bytes", ctypes.c_uint64), ("structure_bytes", ctypes.c_uint64),
+                ("total_bytes", ctypes.c_uint64), ("device_bytes", ctypes.c_uint64)]
 
 
 class BuildOptionsC(ctypes.Structure):
@@ -117,6 +122,7 @@ def lib():
         "cm_debug_query_stats": ([p, i32], i32),
         "cm_debug_pool_bytes": ([i32, i32, p, p], i32),
         "cm_las_parse_header": ([p, u64, ctypes.POINTER(LasHeaderC)], i32),
+        "cm_get_memory_report": ([p, ctypes.POINTER(MemoryReportC)], i32),
         "cm_las_decode": ([p, u64, p, u64, ctypes.POINTER(LasHeaderC), i32, p], i32),
         "cm_las_read": ([ctypes.c_char_p, p, u64, ctypes.POINTER(LasHeaderC), i32, p], i32),
     }

@@ -239,6 +239,19 @@ class Cheesemap:
                     empty_fraction=o.empty_fraction, n_columns=o.n_columns,
                     slice_dense=dense.astype(bool), slice_non_empty=ne)
 
+    def memory_report(self):
+        """MemoryReport (map.hpp:41-48): the reference's analytic byte model,
+        plus device_bytes (this index's actual HBM)."""
+        r = _native.MemoryReportC()
+        _check(_native.lib().cm_get_memory_report(self._h, ctypes.byref(r)))
+        return {k: int(getattr(r, k)) for k, _ in r._fields_}
+
+    def reordered(self):
+        return bool(self._opts.reorder)
+
+    def structure_name(self):
+        return structure_name(self._opts.flavor, self._opts.mode, self._opts.reorder)
+
     def build_timing(self):
         t = _native.BuildTimingC()
         _check(_native.lib().cm_get_build_timing(self._h, ctypes.byref(t)))
@@ -254,6 +267,12 @@ class Cheesemap:
 
     def corrupt_for_testing(self):
         _check(_native.lib().cm_corrupt_for_testing(self._h))
+
+
+def structure_name(flavor, mode, reordered=False):
+    """structure_name (map.cpp:225-238): "dense3", "mixed2-reordered", ..."""
+    name = ["dense", "sparse", "mixed"][int(flavor)] + ("3" if int(mode) == 1 else "2")
+    return name + ("-reordered" if reordered else "")
 
 
 # -------------------------------------------------------------- queries --
@@ -323,10 +342,19 @@ def radius_digest_batch(m, centers, r, kernel=SPHERE, stream=None):
     return counts, dig
 
 
-def knn_batch(m, centers, k, stream=None):
-    """(idx u32[nq, k], d2 f64[nq, k]) ordered by (d^2, handle)."""
+def knn_batch(m, centers, k, stream=None, device_out=False):
+    """(idx u32[nq, k], d2 f64[nq, k]) ordered by (d^2, handle); with
+    device_out=True, CUDA tensors (int32 / float64) that stay on the device."""
     qp, qk = _in_ptr(centers)
     nq = _nrows(qk)
+    if device_out:
+        import torch
+        dev = f"cuda:{m.device}"
+        idx = torch.empty((nq, k), dtype=torch.int32, device=dev)
+        d2 = torch.empty((nq, k), dtype=torch.float64, device=dev)
+        _check(_native.lib().cm_knn(m.handle, qp, nq, int(k), ctypes.c_void_p(idx.data_ptr()),
+                                    ctypes.c_void_p(d2.data_ptr()), _stream_ptr(stream)))
+        return idx, d2
     idx = np.zeros((nq, k), dtype=np.uint32)
     d2 = np.zeros((nq, k), dtype=np.float64)
     _check(_native.lib().cm_knn(m.handle, qp, nq, int(k), idx.ctypes.data_as(ctypes.c_void_p),

@@ -359,6 +359,45 @@ cm_status cm_get_occupancy(const cm_index* ix, cm_occupancy* o, uint8_t* slice_d
   return CM_OK;
 }
 
+cm_status cm_get_memory_report(const cm_index* ix, cm_memory_report* r) {
+  CM_TRY(check_index(ix));
+  if (!r) {
+    set_error("null output pointer");
+    return CM_INVALID_ARGUMENT;
+  }
+  // the reference's cost model (map.cpp:14-18)
+  constexpr uint64_t kHandleBytes = 8, kDenseSlotBytes = 8, kSparseEntryBytes = 64,
+                     kMixedDenseCellBytes = 24, kSliceHeaderBytes = 48;
+  *r = cm_memory_report{};
+  r->handle_bytes = kHandleBytes * ix->n;
+  if (ix->opts.flavor == CM_DENSE) {
+    r->structure_bytes = kDenseSlotBytes * (ix->V + 1);
+  } else if (ix->opts.flavor == CM_SPARSE) {
+    r->structure_bytes = kSparseEntryBytes * ix->U;
+  } else {
+    const uint64_t footprint = ix->g.nx * ix->g.ny;
+    for (const uint64_t ne : ix->slice_ne) {
+      const bool dense = static_cast<double>(ne) / static_cast<double>(footprint) >=
+                         ix->opts.densify_threshold;
+      r->structure_bytes += kSliceHeaderBytes + (dense ? kMixedDenseCellBytes * footprint
+                                                       : kSparseEntryBytes * ne);
+    }
+  }
+  r->total_bytes = r->handle_bytes + r->structure_bytes;
+  // this index's own HBM (cm_index, index.cuh)
+  uint64_t d = sizeof(PointRec) * ix->n;
+  if (ix->ukey) d += 8 * ix->U;
+  if (ix->ustart) d += 4 * (ix->U + 1);
+  if (ix->uk_k) d += 4 * ix->U;
+  if (ix->dense_off) d += 4 * (ix->V + 1);
+  if (ix->vhash) d += sizeof(HashSlot) * (ix->vmask + 1);
+  if (ix->col_dense) d += 4 * ix->g.nx * ix->g.ny;
+  if (ix->chash) d += sizeof(HashSlot) * (ix->cmask + 1);
+  if (ix->col_vbeg) d += 4 * (ix->C + 1);
+  r->device_bytes = d;
+  return CM_OK;
+}
+
 cm_status cm_get_build_timing(const cm_index* ix, cm_build_timing* o) {
   CM_TRY(check_index(ix));
   *o = ix->timing;

@@ -44,9 +44,25 @@ class Rng {  // io.cpp:217-248 conventions
   explicit Rng(std::uint64_t seed) : eng_(seed) {}
   double uniform01() { return static_cast<double>(eng_() >> 11) * 0x1.0p-53; }
   double uniform(double lo, double hi) { return lo + (hi - lo) * uniform01(); }
+  std::uint64_t index(std::uint64_t n) { return eng_() % n; }
+  // Box-Muller with the cached second value (io.cpp:231-243)
+  double gaussian(double mean, double sigma) {
+    if (has_spare_) {
+      has_spare_ = false;
+      return mean + sigma * spare_;
+    }
+    const double u1 = static_cast<double>((eng_() >> 11) + 1) * 0x1.0p-53;  // (0, 1]
+    const double u2 = uniform01();
+    const double mag = std::sqrt(-2.0 * std::log(u1));
+    spare_ = mag * std::sin(2.0 * std::numbers::pi * u2);
+    has_spare_ = true;
+    return mean + sigma * mag * std::cos(2.0 * std::numbers::pi * u2);
+  }
 
  private:
   std::mt19937_64 eng_;
+  bool has_spare_ = false;
+  double spare_ = 0.0;
 };
 
 unsigned worker_count(unsigned requested) {
@@ -287,6 +303,76 @@ int cms_generate_uniform(uint64_t seed, uint64_t n, double ex, double ey,
   return 0;
 }
 
+// The reference's SyntheticSpec kinds (io.cpp:252-335: UniformBox = 0,
+// VoidEllipse = 1, GaussianClusters = 2), same RNG draws in the same order,
+// same argument checks. Returns 0, or 2 (InvalidArgumentError) with the
+// reference's message in msg.
+int cms_generate_spec(int kind, uint64_t seed, uint64_t n, double ex, double ey, double ez,
+                      double cx, double cy, double ax, double ay, uint64_t clusters,
+                      double sigma, double* xyz, char* msg, int msglen) {
+  auto fail = [&](const char* m) {
+    if (msg && msglen > 0) {
+      std::strncpy(msg, m, (size_t)msglen - 1);
+      msg[msglen - 1] = 0;
+    }
+    return 2;
+  };
+  if (n == 0) return fail("synthetic point count must be positive");
+  if (!(ex > 0.0) || !(ey > 0.0) || !(ez > 0.0)) return fail("synthetic extents must be positive");
+  Rng rng(seed);
+  uint64_t have = 0;
+  auto push = [&](double x, double y, double z) {
+    xyz[3 * have] = x, xyz[3 * have + 1] = y, xyz[3 * have + 2] = z;
+    ++have;
+  };
+  if (kind == 0) {
+    for (uint64_t i = 0; i < n; ++i) {
+      const double x = rng.uniform(0.0, ex);
+      const double y = rng.uniform(0.0, ey);
+      push(x, y, rng.uniform(0.0, ez));
+    }
+    return 0;
+  }
+  if (kind == 1) {
+    if (!(ax > 0.0) || !(ay > 0.0)) return fail("ellipse axes must be positive");
+    if (cx - ax < 0.0 || cx + ax > ex || cy - ay < 0.0 || cy + ay > ey)
+      return fail("void ellipse must lie inside the extents");
+    uint64_t attempts = 0;
+    const uint64_t max_attempts = n * 1000 + 1000;
+    while (have < n) {
+      if (++attempts > max_attempts) return fail("void region rejects nearly all samples; check the spec");
+      const double x = rng.uniform(0.0, ex);
+      const double y = rng.uniform(0.0, ey);
+      const double u = (x - cx) / ax, v = (y - cy) / ay;
+      if (u * u + v * v <= 1.0) continue;
+      push(x, y, rng.uniform(0.0, ez));
+    }
+    return 0;
+  }
+  if (kind == 2) {
+    if (clusters == 0 || !(sigma > 0.0)) return fail("need at least one cluster and sigma > 0");
+    std::vector<double> c(3 * clusters);
+    for (uint64_t i = 0; i < clusters; ++i) {
+      c[3 * i] = rng.uniform(0.0, ex);
+      c[3 * i + 1] = rng.uniform(0.0, ey);
+      c[3 * i + 2] = rng.uniform(0.0, ez);
+    }
+    uint64_t attempts = 0;
+    const uint64_t max_attempts = n * 1000 + 1000;
+    while (have < n) {
+      if (++attempts > max_attempts) return fail("cluster sampling rejects nearly all points; check sigma");
+      const uint64_t k = rng.index(clusters);
+      const double x = rng.gaussian(c[3 * k], sigma);
+      const double y = rng.gaussian(c[3 * k + 1], sigma);
+      const double z = rng.gaussian(c[3 * k + 2], sigma);
+      if (x < 0.0 || x > ex || y < 0.0 || y > ey || z < 0.0 || z > ez) continue;
+      push(x, y, z);
+    }
+    return 0;
+  }
+  return fail("unknown synthetic kind");
+}
+
 // TLS-like scan from (0, 0, scanner_z): n_az azimuths (2*pi*a/n_az) x n_el
 // elevations (-60 deg + 120 deg * (e + 0.5) / n_el). Each ray returns its
 // first hit among the ground plane z = 0 and n_boxes axis-aligned boxes
@@ -401,6 +487,17 @@ void cms_center_stream(uint64_t seed, uint64_t tag, uint64_t cloud_size,
     state = mix64(state);
     out[i] = state % cloud_size;
   }
+}
+
+// The same stream as a resumable state (CenterStream, common.cpp:119-125).
+uint64_t cms_center_stream_init(uint64_t seed, uint64_t tag) { return mix64(seed ^ mix64(tag)); }
+void cms_center_stream_next(uint64_t* state, uint64_t cloud_size, uint64_t count, uint64_t* out) {
+  std::uint64_t s = *state;
+  for (std::uint64_t i = 0; i < count; ++i) {
+    s = mix64(s);
+    out[i] = s % cloud_size;
+  }
+  *state = s;
 }
 
 // Gather xyz of the given point indices (query centres drawn from a cloud).

@@ -37,6 +37,13 @@ def _lib():
         lib.cms_generate_tls.restype = ctypes.c_int
         lib.cms_center_stream.argtypes = [u64, u64, u64, u64, p]
         lib.cms_center_stream.restype = None
+        lib.cms_generate_spec.argtypes = [ctypes.c_int, u64, u64, dbl, dbl, dbl, dbl, dbl, dbl,
+                                          dbl, u64, dbl, p, ctypes.c_char_p, ctypes.c_int]
+        lib.cms_generate_spec.restype = ctypes.c_int
+        lib.cms_center_stream_init.argtypes = [u64, u64]
+        lib.cms_center_stream_init.restype = u64
+        lib.cms_center_stream_next.argtypes = [ctypes.POINTER(u64), u64, u64, p]
+        lib.cms_center_stream_next.restype = None
         lib.cms_mix64.argtypes = [u64]
         lib.cms_mix64.restype = u64
         _LIB = lib
@@ -81,6 +88,20 @@ def center_stream(seed, tag, cloud_size, count):
     return out
 
 
+class CenterStream:
+    """The reference's query-centre stream as an object (common.cpp:109-125):
+    next(count) returns the next `count` indices."""
+
+    def __init__(self, seed, tag, cloud_size):
+        self._state = ctypes.c_uint64(_lib().cms_center_stream_init(seed, tag))
+        self._n = cloud_size
+
+    def next(self, count):
+        out = np.empty(count, dtype=np.uint64)
+        _lib().cms_center_stream_next(ctypes.byref(self._state), self._n, count, _ptr(out))
+        return out
+
+
 def mix64(x):
     return int(_lib().cms_mix64(x))
 
@@ -119,3 +140,70 @@ def config_queries(cfg, cloud, count=None):
     default = {2: 2_000_000, 3: 5_000_000}[cfg]
     idx = center_stream(SEED_BASE + 100 + cfg, 0, n, count or default)
     return np.ascontiguousarray(cloud[idx.astype(np.int64)])
+
+
+# ---- the reference's synthetic specs (io.hpp:44-70, io.cpp:252-399) --------
+SPEC_KINDS = {"uniform": 0, "void-ellipse": 1, "clusters": 2}
+
+
+def parse_synthetic_spec(text):
+    """parse_synthetic_spec (io.cpp:337-399): "kind:key=value,..." -> dict.
+    Raises cheesemap.ParseError with the reference's messages."""
+    from .cheesemap import ParseError
+    colon = text.find(":")
+    if colon < 0:
+        raise ParseError("synthetic spec needs the form kind:key=value,...")
+    kind = text[:colon]
+    if kind not in SPEC_KINDS:
+        raise ParseError(f"unknown synthetic kind '{kind}'")
+    spec = dict(kind=kind, n=0, seed=0, extent=(100.0, 100.0, 50.0), cx=0.0, cy=0.0, ax=0.0,
+                ay=0.0, clusters=8, sigma=1.0)
+    rest = text[colon + 1:]
+    for item in (rest.split(",") if rest else []):
+        if "=" not in item:
+            raise ParseError(f"bad synthetic spec item '{item}'")
+        key, value = item.split("=", 1)
+        try:
+            if key in ("n", "seed", "clusters"):
+                v = int(value, 10) if value.strip().lstrip("+").isdigit() else None
+                if v is None:
+                    raise ValueError
+                if v >= 1 << 64:
+                    raise OverflowError
+                spec[key] = v
+            elif key == "extent":
+                parts = value.split("x")
+                if len(parts) != 3:
+                    raise ParseError("extent must look like 100x100x50")
+                try:
+                    spec["extent"] = tuple(float(x) for x in parts)
+                except ValueError:
+                    raise ParseError("extent must look like 100x100x50")
+            elif key in ("cx", "cy", "ax", "ay", "sigma"):
+                spec[key] = float(value)
+            else:
+                raise ParseError(f"unknown synthetic spec key '{key}'")
+        except OverflowError:
+            raise ParseError(f"value out of range for synthetic spec key '{key}'")
+        except ValueError:
+            raise ParseError(f"bad value for synthetic spec key '{key}'")
+    return spec
+
+
+def generate(spec):
+    """generate (io.cpp:252-335) for a parsed spec (dict or spec string):
+    bit-identical to the reference for all three kinds. Raises
+    cheesemap.InvalidArgumentError with the reference's messages."""
+    from .cheesemap import InvalidArgumentError
+    if isinstance(spec, str):
+        spec = parse_synthetic_spec(spec)
+    n = int(spec["n"])
+    ex, ey, ez = spec["extent"]
+    out = np.empty((max(n, 1), 3), dtype=np.float64)
+    msg = ctypes.create_string_buffer(256)
+    rc = _lib().cms_generate_spec(SPEC_KINDS[spec["kind"]], int(spec["seed"]), n, ex, ey, ez,
+                                  spec["cx"], spec["cy"], spec["ax"], spec["ay"],
+                                  int(spec["clusters"]), spec["sigma"], _ptr(out), msg, 256)
+    if rc != 0:
+        raise InvalidArgumentError(msg.value.decode())
+    return out[:n]
