@@ -588,6 +588,12 @@ __global__ void publish_u64_kernel(const unsigned long long* src, volatile unsig
   *dst = *src;
   __threadfence_system();
 }
+// dst[k] = src[idx[k]] for k < n (a few row-pointer values for the host).
+__global__ void publish_gather_kernel(const uint64_t* src, const uint64_t* idx, int n,
+                                      volatile unsigned long long* dst) {
+  for (int k = threadIdx.x; k < n; k += blockDim.x) dst[k] = src[idx[k]];
+  __threadfence_system();
+}
 }  // namespace apik
 }  // namespace cmg
 
@@ -598,7 +604,7 @@ struct MappedSlot {
   cudaEvent_t ev = nullptr;
   bool ok = false;
   MappedSlot() {
-    if (cudaHostAlloc(&host, 64, cudaHostAllocMapped) == cudaSuccess &&
+    if (cudaHostAlloc(&host, 4096, cudaHostAllocMapped) == cudaSuccess &&
         cudaHostGetDevicePointer(reinterpret_cast<void**>(&dev), host, 0) == cudaSuccess &&
         cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess)
       ok = true;
@@ -618,13 +624,44 @@ bool read_u64_mapped(const unsigned long long* dsrc, cudaStream_t st, unsigned l
   *out = *reinterpret_cast<volatile unsigned long long*>(slot.host);
   return true;
 }
+
+// row_ptr[idx[k]] for k < n (n <= 256) to the host, through mapped memory.
+// idx is a host array; it travels in the mapped page too.
+bool read_row_ptrs_mapped(const uint64_t* row_ptr, const uint64_t* idx, int n, cudaStream_t st,
+                          uint64_t* out) {
+  thread_local MappedSlot slot;
+  if (!slot.ok || n > 256) {
+    for (int k = 0; k < n; ++k)
+      if (cudaMemcpyAsync(out + k, row_ptr + idx[k], 8, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+        return false;
+    return cudaStreamSynchronize(st) == cudaSuccess;
+  }
+  uint64_t* hidx = reinterpret_cast<uint64_t*>(slot.host) + 256;
+  std::memcpy(hidx, idx, n * sizeof(uint64_t));
+  const uint64_t* didx = reinterpret_cast<const uint64_t*>(slot.dev) + 256;
+  cmg::apik::publish_gather_kernel<<<1, 256, 0, st>>>(row_ptr, didx, n, slot.dev); ::cmg::note_launch();
+  if (cudaEventRecord(slot.ev, st) != cudaSuccess) return false;
+  if (cudaEventSynchronize(slot.ev) != cudaSuccess) return false;
+  for (int k = 0; k < n; ++k) out[k] = reinterpret_cast<volatile unsigned long long*>(slot.host)[k];
+  return true;
+}
+
+// Replaces the single gather launch of radius_search_core (to_host uses it to
+// stream the CSR to the host while the gather still runs).
+struct GatherHook {
+  virtual cm_status run(const uint32_t* temp, const uint64_t* toff, const uint32_t* scnt,
+                        const uint64_t* row_ptr, const uint32_t* perm, uint32_t* cols, uint64_t nq,
+                        cudaStream_t st) = 0;
+  virtual ~GatherHook() = default;
+};
 }  // namespace
 
 // count/collect + scan + gather for device-resident queries into csr's
 // device buffers (row_ptr, cols, nnz). Events of the calling thread record
 // the phases (cm_get_last_query_timing).
 static cm_status radius_search_core(const cm_index* ix, const double* qd, uint64_t nq, int kernel,
-                                    double r, cudaStream_t st, cm_csr* csr) {
+                                    double r, cudaStream_t st, cm_csr* csr,
+                                    GatherHook* hook = nullptr) {
   QueryEvents& ev = qev();
   ev.valid = false;
   cudaEventRecord(ev.e[0], st);
@@ -710,7 +747,8 @@ static cm_status radius_search_core(const cm_index* ix, const double* qd, uint64
   if (two_pass)
     s = radius_fill_dev(ix, qd, nq, kernel, r, ord.perm, csr->row_ptr, csr->cols, st, nullptr);
   else
-    s = gather_rows_dev(temp, toff, scnt, csr->row_ptr, ord.perm, csr->cols, nq, st);
+    s = hook ? hook->run(temp, toff, scnt, csr->row_ptr, ord.perm, csr->cols, nq, st)
+             : gather_rows_dev(temp, toff, scnt, csr->row_ptr, ord.perm, csr->cols, nq, st);
   cudaEventRecord(ev.e[5], st);
   if (s != CM_OK) return fail(s);
   ev.nq = nq;
@@ -749,6 +787,57 @@ cm_status cm_radius_search(const cm_index* ix, const double* q, uint64_t nq, int
   *out = csr;
   return CM_OK;
 }
+
+namespace {
+// One-chunk to_host: once the row pointers are scanned, the gather runs in G
+// query ranges and each range's columns start their device->host copy as
+// soon as that range is gathered (the row pointers go first), so the PCIe
+// copy of the CSR overlaps the gather.
+struct StreamingGather : GatherHook {
+  static constexpr int G = 8;
+  cudaStream_t out = nullptr;
+  uint64_t* row_ptr_host = nullptr;
+  uint32_t* cols_host = nullptr;
+  uint64_t cap = 0;
+  bool copied = false, over = false;
+  uint64_t nnz = 0;
+  cm_status run(const uint32_t* temp, const uint64_t* toff, const uint32_t* scnt,
+                const uint64_t* row_ptr, const uint32_t* perm, uint32_t* cols, uint64_t nq,
+                cudaStream_t st) override {
+    struct Events {
+      cudaEvent_t e[G + 1];
+      Events() {
+        for (auto& x : e) cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
+      }
+    };
+    thread_local Events evs;
+    uint64_t qb[G + 1], rp[G + 1];
+    for (int k = 0; k <= G; ++k) qb[k] = nq * (uint64_t)k / G;
+    if (!read_row_ptrs_mapped(row_ptr, qb, G + 1, st, rp)) {
+      set_error("row pointer readback failed");
+      return CM_CUDA;
+    }
+    nnz = rp[G];
+    over = nnz > cap;
+    cudaEventRecord(evs.e[G], st);
+    cudaStreamWaitEvent(out, evs.e[G], 0);
+    CM_CUDA_TRY(cudaMemcpyAsync(row_ptr_host + 1, row_ptr + 1, nq * 8, cudaMemcpyDeviceToHost, out));
+    for (int k = 0; k < G; ++k) {
+      if (qb[k + 1] == qb[k]) continue;
+      CM_TRY(gather_rows_dev(temp, toff + qb[k], scnt + qb[k], row_ptr + qb[k], perm, cols,
+                             qb[k + 1] - qb[k], st));
+      if (!over && rp[k + 1] > rp[k]) {
+        cudaEventRecord(evs.e[k], st);
+        cudaStreamWaitEvent(out, evs.e[k], 0);
+        CM_CUDA_TRY(cudaMemcpyAsync(cols_host + rp[k], cols + rp[k], (rp[k + 1] - rp[k]) * 4,
+                                    cudaMemcpyDeviceToHost, out));
+      }
+    }
+    copied = true;
+    return CM_OK;
+  }
+};
+}  // namespace
 
 // Host-buffer pipeline: queries in chunks; chunk i+1's host->device copy and
 // chunk i-1's device->host copy of its CSR overlap chunk i's kernels (three
@@ -824,7 +913,12 @@ cm_status cm_radius_search_to_host(const cm_index* ix, const double* q_host, uin
     }
     csrs[bi].nq = n;
     csrs[bi].device = ix->device;
-    s = radius_search_core(ix, qbuf[bi], n, kernel, r, st, &csrs[bi]);
+    StreamingGather sg;
+    sg.out = ss.out;
+    sg.row_ptr_host = row_ptr_host;
+    sg.cols_host = cols_host;
+    sg.cap = cols_capacity;
+    s = radius_search_core(ix, qbuf[bi], n, kernel, r, st, &csrs[bi], nchunks == 1 ? &sg : nullptr);
     tr("core returned", c);
     if (trace) {
       cm_query_timing qt;
@@ -838,6 +932,12 @@ cm_status cm_radius_search_to_host(const cm_index* ix, const double* q_host, uin
           csrs[bi].row_ptr + 1, n, base); ::cmg::note_launch();
     }
     cudaEventRecord(comp_done[bi], st);
+    if (sg.copied) {  // streamed during the gather
+      full = full || sg.over;
+      cudaEventRecord(out_done[bi], ss.out);
+      base += csrs[bi].nnz;
+      continue;
+    }
     if (full || base + csrs[bi].nnz > cols_capacity) {
       base += csrs[bi].nnz;  // keep counting; report the size needed
       full = true;
