@@ -37,7 +37,6 @@ namespace {
 constexpr int kQThreads = 128;
 constexpr int kQWarps = kQThreads / 32;
 constexpr int kLaneRowCap = 96;                       // per-lane row buffer
-constexpr int kLaneSortMax = 32;                      // per-lane register sort up to
 // Per warp: the tile path's per-lane rows (u16 hit keys, interleaved with
 // stride 33) followed by the cp.async staging double buffer; the one-query
 // path reuses the whole region as a u32 buffer.
@@ -265,19 +264,6 @@ __device__ __forceinline__ bool pred(const Predicate& P, double x, double y, dou
   return sqdist(x, y, z, P.cx, P.cy, P.cz) <= P.rr;  // sphere (geometry.hpp:82-84)
 }
 
-// Warp-uniform record read: every lane loads the same 32 bytes (one L1
-// wavefront each, broadcast).
-__device__ __forceinline__ void load_uniform(const PointRec* p, double& x, double& y, double& z,
-                                             uint32_t& id, uint32_t& k) {
-  const double2 a = __ldg(reinterpret_cast<const double2*>(p));
-  const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
-  x = a.x;
-  y = a.y;
-  z = b.x;
-  const uint2 t = *reinterpret_cast<const uint2*>(&b.y);
-  id = t.x;
-  k = t.y;
-}
 
 
 // One query answered by a whole warp: count pass over the flattened spans.
@@ -1047,19 +1033,16 @@ constexpr int kGatherRow = 96;
 constexpr int kGatherWarpWords = kGatherRow * 33 + 96;  // rows, sfin[32], srel[32] (u64)
 //
 // SORT = true is the in-place row sort after a wide-tile FILL (temp == cols,
-// toff == row_ptr): rows > 96 are sorted too — in shared memory by the warp
-// (radix, <= kSortCap) or listed for big_row_sort_kernel.
+// toff == row_ptr, lengths from row_ptr): only rows <= 96 are handled here;
+// longer rows are sorted by sort_mid_rows_kernel / big_row_sort_kernel.
 template <bool SORT>
 __global__ void __launch_bounds__(128) gather_rows_kernel(const uint32_t* temp,
                                                           const uint64_t* __restrict__ toff,
                                                           const uint32_t* __restrict__ counts,
                                                           const uint64_t* __restrict__ row_ptr,
-                                                          uint32_t* cols, uint64_t nq, int bits,
-                                                          uint64_t* big_off, uint32_t* big_len,
-                                                          uint32_t* n_big) {
+                                                          uint32_t* cols, uint64_t nq) {
   extern __shared__ uint32_t gsm[];
   const int lane = threadIdx.x & 31;
-  const uint32_t lt = lanemask_lt();
   uint32_t* srow = gsm + (threadIdx.x >> 5) * kGatherWarpWords;
   uint32_t* sfin = srow + kGatherRow * 33;                          // flat row ends
   uint64_t* srel = reinterpret_cast<uint64_t*>(sfin + 32);           // row starts - row 0's
@@ -1564,10 +1547,8 @@ cm_status radius_fill_dev(const cm_index* ix, const double* q, uint64_t nq, int 
   const uint64_t groups = (nq + 31) / 32;
   const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((groups + 3) / 4, (uint64_t)sm_count() * 8));
   const int smem = 4 * kGatherWarpWords * 4;
-  const int bits = 64 - __builtin_clzll(std::max<uint64_t>(1, ix->n - 1));
   cudaFuncSetAttribute(gather_rows_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  gather_rows_kernel<true><<<grid, 128, smem, st>>>(cols, row_ptr, nullptr, row_ptr, cols, nq, bits,
-                                                    big2.off, big2.len, big2.n); ::cmg::note_launch();
+  gather_rows_kernel<true><<<grid, 128, smem, st>>>(cols, row_ptr, nullptr, row_ptr, cols, nq); ::cmg::note_launch();
   CM_CUDA_TRY(cudaGetLastError());
   {
     const int msmem = 2 * kMidBuf * 4;
@@ -1619,8 +1600,7 @@ cm_status gather_rows_dev(const uint32_t* temp, const uint64_t* toff, const uint
   const int smem = 4 * kGatherWarpWords * 4;
   (void)perm;
   cudaFuncSetAttribute(gather_rows_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  gather_rows_kernel<false><<<grid, 128, smem, st>>>(temp, toff, counts, row_ptr, cols, nq, 32,
-                                                     nullptr, nullptr, nullptr); ::cmg::note_launch();
+  gather_rows_kernel<false><<<grid, 128, smem, st>>>(temp, toff, counts, row_ptr, cols, nq); ::cmg::note_launch();
   CM_CUDA_TRY(cudaGetLastError());
   return CM_OK;
 }
