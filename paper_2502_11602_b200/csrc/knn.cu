@@ -30,6 +30,24 @@ __device__ __forceinline__ bool pair_less(double a, uint32_t ia, double b, uint3
   return a < b || (a == b && ia < ib);
 }
 
+// 32-wide bitonic sort of (d2, handle) pairs, one per lane, ascending by lane.
+__device__ __forceinline__ void warp_sort_pairs32(double& d, uint32_t& id, int lane) {
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const double od = __shfl_xor_sync(0xffffffffu, d, j);
+      const uint32_t oi = __shfl_xor_sync(0xffffffffu, id, j);
+      const bool up = (lane & k) == 0 || k == 32;
+      const bool lower = (lane & j) == 0;
+      const bool o_less = pair_less(od, oi, d, id);
+      const bool take_o = (lower == up) ? o_less : !o_less;
+      d = take_o ? od : d;
+      id = take_o ? oi : id;
+    }
+  }
+}
+
 template <int FLAVOR>
 __device__ __forceinline__ void shell_column_spans(const Tables& t, int64_t i, int64_t j,
                                                    bool ring, int64_t kc, int64_t L,
@@ -60,12 +78,15 @@ __global__ void __launch_bounds__(kKThreads) knn_warp_kernel(const Tables t,
                                                              uint32_t* __restrict__ idx_out,
                                                              double* __restrict__ d2_out,
                                                              double* __restrict__ d2_scratch) {
-  __shared__ double sd[GLIST ? 1 : kKWarps][GLIST ? 1 : kKMax];
-  __shared__ uint32_t sid[GLIST ? 1 : kKWarps][GLIST ? 1 : kKMax];
+  // the sorted list and, for batch merges, its second buffer
+  __shared__ double sd[GLIST ? 1 : kKWarps][2][GLIST ? 1 : kKMax];
+  __shared__ uint32_t sid[GLIST ? 1 : kKWarps][2][GLIST ? 1 : kKMax];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  double* ld = sd[GLIST ? 0 : wib];
-  uint32_t* lid = sid[GLIST ? 0 : wib];
+  double* ld = sd[GLIST ? 0 : wib][0];
+  uint32_t* lid = sid[GLIST ? 0 : wib][0];
+  double* ld2 = sd[GLIST ? 0 : wib][1];
+  uint32_t* lid2 = sid[GLIST ? 0 : wib][1];
   const uint64_t W = (uint64_t)gridDim.x * kKWarps;
   const DevGrid& g = t.g;
   const uint32_t lt = lanemask_lt();
@@ -130,6 +151,56 @@ __global__ void __launch_bounds__(kKThreads) knn_warp_kernel(const Tables t,
             acc = cnt < k || pair_less(d2, id, ld[k - 1], lid[k - 1]);
           }
           uint32_t m = __ballot_sync(0xffffffffu, acc);
+          const uint32_t nacc = __popc(m);
+          if (!GLIST && nacc > 0) {
+            // batch merge: sort the accepted candidates, then place every
+            // list and batch entry at (own index + its rank in the other
+            // sequence) in the second buffer, keeping the k smallest
+            double bd = acc ? d2 : __longlong_as_double(0x7ff0000000000000ll);
+            uint32_t bi = acc ? id : 0xffffffffu;
+            warp_sort_pairs32(bd, bi, lane);
+            const uint32_t ncnt = min(k, cnt + nacc);
+            for (uint32_t base = 0; base < cnt; base += 32) {
+              const uint32_t x = base + lane;
+              const bool valid = x < cnt;
+              const double xd = valid ? ld[x] : 0.0;
+              const uint32_t xi = valid ? lid[x] : 0u;
+              uint32_t r = 0;
+#pragma unroll
+              for (int sft = 16; sft > 0; sft >>= 1) {
+                const double od = __shfl_sync(0xffffffffu, bd, r + sft - 1);
+                const uint32_t oi = __shfl_sync(0xffffffffu, bi, r + sft - 1);
+                if (pair_less(od, oi, xd, xi)) r += sft;
+              }
+              const double od = __shfl_sync(0xffffffffu, bd, 31);
+              const uint32_t oi = __shfl_sync(0xffffffffu, bi, 31);
+              if (r == 31 && pair_less(od, oi, xd, xi)) r = 32;
+              if (valid && x + r < ncnt) {
+                ld2[x + r] = xd;
+                lid2[x + r] = xi;
+              }
+            }
+            if ((uint32_t)lane < nacc) {
+              uint32_t lo = 0, hi = cnt;
+              while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (pair_less(ld[mid], lid[mid], bd, bi)) lo = mid + 1; else hi = mid;
+              }
+              if (lane + lo < ncnt) {
+                ld2[lane + lo] = bd;
+                lid2[lane + lo] = bi;
+              }
+            }
+            __syncwarp();
+            double* td = ld;
+            ld = ld2;
+            ld2 = td;
+            uint32_t* ti = lid;
+            lid = lid2;
+            lid2 = ti;
+            cnt = ncnt;
+            m = 0;
+          }
           while (m) {
             const int src = __ffs(m) - 1;
             m &= m - 1;
