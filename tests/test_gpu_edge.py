@@ -97,3 +97,29 @@ def test_device_and_host_buffers_agree():
                                            device_out=True)
     assert np.array_equal(row_d.cpu().numpy().astype(np.uint64), a[0])
     assert np.array_equal(cols_d.cpu().numpy().astype(np.uint32), a[1])
+
+
+@pytest.mark.gpu
+def test_empty_query_batches():
+    """Zero centres: every batched call returns empty outputs (no launch
+    reads past an empty buffer), through host and device inputs."""
+    import ctypes
+    import torch
+    from paper_2502_11602_b200 import _native
+    cloud = np.random.default_rng(5).uniform(0, 10, (5000, 3))
+    m = cm.Cheesemap.build(cloud, cm.BuildOptions(flavor=cm.Flavor.Mixed))
+    for q in (np.zeros((0, 3)), torch.zeros((0, 3), dtype=torch.float64, device="cuda")):
+        for kernel in (cm.SPHERE, cm.CUBE, cm.CYLINDER):
+            for r in (1.0, 3.0):  # compact and wide paths
+                row, cols = cm.radius_search_batch(m, q, r, kernel)
+                assert row.tolist() == [0] and cols.size == 0
+                c, d = cm.radius_digest_batch(m, q, r, kernel)
+                assert c.size == 0 and d.size == 0
+        idx, d2 = cm.knn_batch(m, q, 8)
+        assert idx.shape == (0, 8) and d2.shape == (0, 8)
+    row = np.zeros(1, dtype=np.uint64)
+    nnz = ctypes.c_uint64(7)
+    rc = _native.lib().cm_radius_search_to_host(m.handle, None, 0, 0, 1.0,
+                                                row.ctypes.data_as(ctypes.c_void_p), None, 0,
+                                                ctypes.byref(nnz), None)
+    assert rc == 0 and nnz.value == 0 and row[0] == 0
