@@ -139,14 +139,15 @@ constexpr int kSortThreads = 256;  // 8 warps
 constexpr int kSortWarps = kSortThreads / 32;
 constexpr int kSortItems = 16;  // per lane; a warp owns 512 consecutive keys
 constexpr int kSortTile = kSortThreads * kSortItems;
-constexpr int kRadixBits = 8;
-constexpr int kRadix = 1 << kRadixBits;
+constexpr int kRadixBitsMax = 10;  // digits of 8..10 bits (wcount fits static smem)
+constexpr int kRadixMax = 1 << kRadixBitsMax;
 
-template <typename K>
+template <typename K, int RB>
 __global__ void __launch_bounds__(kSortThreads) radix_upsweep(const K* __restrict__ keys,
                                                               uint64_t n, int shift,
                                                               uint32_t* __restrict__ hist,
                                                               uint32_t nblocks) {
+  constexpr int kRadix = 1 << RB;
   __shared__ uint32_t h[kRadix];
   for (int d = threadIdx.x; d < kRadix; d += blockDim.x) h[d] = 0;
   __syncthreads();
@@ -164,11 +165,12 @@ __global__ void __launch_bounds__(kSortThreads) radix_upsweep(const K* __restric
 // item `it` of lane l is key (it*32 + l) of that run, so processing items in
 // order with lanes in order visits keys in input order. Ranks inside a warp
 // come from __match_any_sync peer groups.
-template <typename K>
+template <typename K, int RB>
 __global__ void __launch_bounds__(kSortThreads) radix_downsweep(
     const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, K* __restrict__ keys_out,
     uint32_t* __restrict__ vals_out, uint64_t n, int shift,
     const uint32_t* __restrict__ offs /* scanned hist [d][b] */, uint32_t nblocks) {
+  constexpr int kRadix = 1 << RB;
   __shared__ uint32_t wcount[kSortWarps][kRadix];
   __shared__ uint32_t dbase[kRadix];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -226,7 +228,7 @@ __global__ void __launch_bounds__(kSortThreads) radix_downsweep(
 template <typename K>
 inline size_t radix_scratch_bytes(uint64_t n) {
   const uint64_t nb = (n + kSortTile - 1) / kSortTile;
-  const uint64_t h = nb * kRadix;
+  const uint64_t h = nb * kRadixMax;
   return (size_t)(n * (sizeof(K) + 4)) + (size_t)(h * 4) + (size_t)(scan_part_elems(h) * 4) + 256;
 }
 
@@ -237,8 +239,11 @@ template <typename K>
 inline int radix_sort_pairs(K* keys, uint32_t* vals, uint64_t n, int bits, void* scratch,
                             cudaStream_t st) {
   if (n <= 1 || bits <= 0) return 0;
+  // the fewest passes digits of 8..10 bits allow, with the narrowest such digit
+  const int passes_min = (bits + kRadixBitsMax - 1) / kRadixBitsMax;
+  const int rb = (bits + passes_min - 1) / passes_min < 8 ? 8 : (bits + passes_min - 1) / passes_min;
   const uint32_t nb = (uint32_t)((n + kSortTile - 1) / kSortTile);
-  const uint64_t h = (uint64_t)nb * kRadix;
+  const uint64_t h = (uint64_t)nb << rb;
   char* p = static_cast<char*>(scratch);
   K* k2 = reinterpret_cast<K*>(p);
   p += n * sizeof(K);
@@ -252,10 +257,22 @@ inline int radix_sort_pairs(K* keys, uint32_t* vals, uint64_t n, int bits, void*
   K* kb = k2;
   uint32_t* vb = v2;
   int passes = 0;
-  for (int shift = 0; shift < bits; shift += kRadixBits, ++passes) {
-    radix_upsweep<K><<<nb, kSortThreads, 0, st>>>(ka, n, shift, hist, nb); ::cmg::note_launch();
+  for (int shift = 0; shift < bits; shift += rb, ++passes) {
+    if (rb == 8) {
+      radix_upsweep<K, 8><<<nb, kSortThreads, 0, st>>>(ka, n, shift, hist, nb); ::cmg::note_launch();
+    } else if (rb == 9) {
+      radix_upsweep<K, 9><<<nb, kSortThreads, 0, st>>>(ka, n, shift, hist, nb); ::cmg::note_launch();
+    } else {
+      radix_upsweep<K, 10><<<nb, kSortThreads, 0, st>>>(ka, n, shift, hist, nb); ::cmg::note_launch();
+    }
     exclusive_scan<uint32_t, uint32_t>(hist, h, hist, part, 0, st);
-    radix_downsweep<K><<<nb, kSortThreads, 0, st>>>(ka, va, kb, vb, n, shift, hist, nb); ::cmg::note_launch();
+    if (rb == 8) {
+      radix_downsweep<K, 8><<<nb, kSortThreads, 0, st>>>(ka, va, kb, vb, n, shift, hist, nb); ::cmg::note_launch();
+    } else if (rb == 9) {
+      radix_downsweep<K, 9><<<nb, kSortThreads, 0, st>>>(ka, va, kb, vb, n, shift, hist, nb); ::cmg::note_launch();
+    } else {
+      radix_downsweep<K, 10><<<nb, kSortThreads, 0, st>>>(ka, va, kb, vb, n, shift, hist, nb); ::cmg::note_launch();
+    }
     K* tk = ka; ka = kb; kb = tk;
     uint32_t* tv = va; va = vb; vb = tv;
   }
