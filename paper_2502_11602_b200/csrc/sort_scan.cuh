@@ -182,24 +182,28 @@ __global__ void __launch_bounds__(kSortThreads) radix_downsweep(
   uint32_t rank[kSortItems];
   const uint32_t lt = lanemask_lt();
 #pragma unroll
-  for (int it = 0; it < kSortItems; ++it) {
+  for (int it = 0; it < kSortItems; ++it) {  // all loads in flight first
     const uint64_t i = wbase + (uint64_t)it * 32 + lane;
     const bool valid = i < n;
     kv[it] = valid ? keys_in[i] : K(0);
     vv[it] = valid ? vals_in[i] : 0u;
-    const uint32_t d = valid ? ((uint32_t)(kv[it] >> shift) & (kRadix - 1)) : kRadix;  // kRadix = invalid
-    const uint32_t act = __ballot_sync(0xffffffffu, valid);
-    uint32_t peers = __match_any_sync(0xffffffffu, d);
-    peers &= act;
-    uint32_t r = 0;
-    if (valid) {
-      r = wcount[w][d] + __popc(peers & lt);
-    }
-    __syncwarp();
-    if (valid && (peers & lt) == 0) wcount[w][d] += __popc(peers);
-    __syncwarp();
-    rank[it] = r;
   }
+  // Stable ranks: items in order; the lowest lane of each digit's peer group
+  // bumps the warp's digit counter with one shared-memory atomic (the warp's
+  // atomics are performed in issue order) and hands the old count to its peers.
+#pragma unroll
+  for (int it = 0; it < kSortItems; ++it) {
+    const uint64_t i = wbase + (uint64_t)it * 32 + lane;
+    const bool valid = i < n;
+    const uint32_t d = valid ? ((uint32_t)(kv[it] >> shift) & (kRadix - 1)) : kRadix;  // kRadix = invalid
+    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    const int leader = __ffs(peers) - 1;
+    uint32_t old = 0;
+    if (valid && lane == leader) old = atomicAdd(&wcount[w][d], (uint32_t)__popc(peers));
+    old = __shfl_sync(0xffffffffu, old, leader);
+    rank[it] = old + __popc(peers & lt);
+  }
+  __syncwarp();
   __syncthreads();
   // per digit: global offset of this block + exclusive prefix over warps
   for (int d = threadIdx.x; d < kRadix; d += blockDim.x) {
