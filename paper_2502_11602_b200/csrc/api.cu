@@ -52,6 +52,20 @@ static void configure_pool() {
       cudaMemGetInfo(&fr, &tot);
       uint64_t thr = tot / 2;
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      // Reserve one large block up front: the pool then carves later
+      // requests out of it instead of mapping fresh physical memory for
+      // every new size (measured: 0.3-12 ms per cudaMallocAsync once the
+      // pool's chunks fragment; builds went 2.2 -> 3.9 ms). Default
+      // min(32 GiB, free / 4); CMGPU_POOL_RESERVE_GB overrides (0 = off).
+      double gb = std::min(32.0, (double)fr / 4.0 / (double)(1ull << 30));
+      if (const char* r = std::getenv("CMGPU_POOL_RESERVE_GB")) gb = std::atof(r);
+      if (gb > 0.0) {
+        void* p = nullptr;
+        if (cudaMallocAsync(&p, (size_t)(gb * (double)(1ull << 30)), 0) == cudaSuccess)
+          cudaFreeAsync(p, 0);
+        cudaStreamSynchronize(0);
+        cudaGetLastError();
+      }
     }
     g_pool_configured[dev] = true;
   }
