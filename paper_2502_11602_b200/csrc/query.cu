@@ -1189,9 +1189,90 @@ __global__ void __launch_bounds__(128) gather_rows_kernel(const uint32_t* temp,
   }
 }
 
-// In-place sort of the rows of 97..8192 handles (after a wide-tile FILL;
-// shorter rows were sorted by the gather pass, longer ones are listed for
-// big_row_sort_kernel). A block of 128 threads packs consecutive rows into a
+// Rows of 97..1024 handles, one warp per row, blocked layout: lane l holds
+// handles [l * ITEMS, (l + 1) * ITEMS) of the row in registers, so the
+// bitonic network's exchanges at distance < ITEMS stay inside a lane (no
+// shuffles) and the row's loads and stores are contiguous per lane.
+constexpr int kBlockedMax = 1024;
+
+template <int ITEMS>
+__device__ __forceinline__ void warp_sort_blocked(uint32_t (&v)[ITEMS], int lane) {
+  constexpr int P = 32 * ITEMS;
+#pragma unroll
+  for (int k = 2; k <= P; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j < ITEMS) {
+#pragma unroll
+        for (int r = 0; r < ITEMS; ++r) {
+          const int p = r ^ j;
+          if (p > r) {
+            const bool asc = (((uint32_t)lane * ITEMS + r) & k) == 0;
+            const uint32_t a = v[r], b = v[p];
+            v[r] = asc ? min(a, b) : max(a, b);
+            v[p] = asc ? max(a, b) : min(a, b);
+          }
+        }
+      } else {
+        const int jl = j / ITEMS;
+        const bool lower = (lane & jl) == 0;
+#pragma unroll
+        for (int r = 0; r < ITEMS; ++r) {
+          const uint32_t o = __shfl_xor_sync(0xffffffffu, v[r], jl);
+          const bool asc = (((uint32_t)lane * ITEMS + r) & k) == 0;
+          v[r] = (lower == asc) ? min(v[r], o) : max(v[r], o);
+        }
+      }
+    }
+  }
+}
+
+template <int ITEMS>
+__device__ __forceinline__ void warp_sort_row_blocked(uint32_t* row, uint32_t n, int lane) {
+  uint32_t v[ITEMS];
+#pragma unroll
+  for (int r = 0; r < ITEMS; ++r) {
+    const uint32_t e = (uint32_t)lane * ITEMS + r;
+    v[r] = e < n ? row[e] : 0xffffffffu;
+  }
+  warp_sort_blocked<ITEMS>(v, lane);
+#pragma unroll
+  for (int r = 0; r < ITEMS; ++r) {
+    const uint32_t e = (uint32_t)lane * ITEMS + r;
+    if (e < n) row[e] = v[r];
+  }
+}
+
+// One size class per launch (rows of (LO, 32 * ITEMS] handles), so the
+// register budget, hence the occupancy, fits the class.
+template <int ITEMS>
+__global__ void __launch_bounds__(128) sort_blocked_rows_kernel(uint32_t* cols,
+                                                                const uint64_t* __restrict__ row_ptr,
+                                                                uint64_t nq, uint32_t lo) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t ngroups = (nq + 31) / 32;
+  const uint64_t W = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t g = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); g < ngroups;
+       g += W) {
+    const uint64_t q = g * 32 + lane;
+    uint64_t b = 0;
+    uint32_t len = 0;
+    if (q < nq) {
+      b = __ldg(row_ptr + q);
+      len = (uint32_t)(__ldg(row_ptr + q + 1) - b);
+    }
+    for (uint32_t lm = __ballot_sync(0xffffffffu, len > lo && len <= 32u * ITEMS); lm;
+         lm &= lm - 1) {
+      const int l = __ffs(lm) - 1;
+      const uint32_t n = __shfl_sync(0xffffffffu, len, l);
+      warp_sort_row_blocked<ITEMS>(cols + __shfl_sync(0xffffffffu, b, l), n, lane);
+    }
+  }
+}
+
+// In-place sort of the rows of 1025..8192 handles (after a wide-tile FILL;
+// shorter rows were sorted by the gather pass and sort_blocked_rows_kernel,
+// longer ones are listed for big_row_sort_kernel). A block of 128 threads packs consecutive rows into a
 // GROUP of at most 128 runs of 64 handles (row-aligned) and stages it in
 // shared memory, each row contiguous from 64 * (its first run), with an XOR
 // swizzle (word p at p ^ ((p >> 6) & 31)) so that both the run-per-thread
@@ -1231,7 +1312,7 @@ __global__ void __launch_bounds__(kMidThreads) sort_mid_rows_kernel(
         len = (uint32_t)(__ldg(row_ptr + ql + 1) - st);
       }
       const uint32_t runs =
-          (len > (uint32_t)kGatherRow && len <= (uint32_t)kMidMax) ? (len + 63) >> 6 : 0u;
+          (len > (uint32_t)kBlockedMax && len <= (uint32_t)kMidMax) ? (len + 63) >> 6 : 0u;
       const uint32_t winc = warp_incl_scan(runs);
       // a group ends at the 128-run budget and before the first row past
       // kMidMax (which, when first, forms a group of its own: listed for the
@@ -1550,6 +1631,15 @@ cm_status radius_fill_dev(const cm_index* ix, const double* q, uint64_t nq, int 
   cudaFuncSetAttribute(gather_rows_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   gather_rows_kernel<true><<<grid, 128, smem, st>>>(cols, row_ptr, nullptr, row_ptr, cols, nq); ::cmg::note_launch();
   CM_CUDA_TRY(cudaGetLastError());
+  {
+    const unsigned bgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((groups + 3) / 4, (uint64_t)sm_count() * 16));
+    sort_blocked_rows_kernel<4><<<bgrid, 128, 0, st>>>(cols, row_ptr, nq, kGatherRow); ::cmg::note_launch();
+    sort_blocked_rows_kernel<8><<<bgrid, 128, 0, st>>>(cols, row_ptr, nq, 128); ::cmg::note_launch();
+    sort_blocked_rows_kernel<16><<<bgrid, 128, 0, st>>>(cols, row_ptr, nq, 256); ::cmg::note_launch();
+    sort_blocked_rows_kernel<32><<<bgrid, 128, 0, st>>>(cols, row_ptr, nq, 512); ::cmg::note_launch();
+
+    CM_CUDA_TRY(cudaGetLastError());
+  }
   {
     const int msmem = 2 * kMidBuf * 4;
     cudaFuncSetAttribute(sort_mid_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, msmem);
