@@ -42,8 +42,18 @@ constexpr int kLaneRowCap = 96;                       // per-lane row buffer
 // path reuses the whole region as a u32 buffer.
 constexpr int kRowKeyBytes = kLaneRowCap * 33 * 2;
 constexpr int kStageBytes = 64 * 32;
-constexpr int kColBegBytes = 32 * 4;                  // wide-tile FILL: key -> record base
-constexpr int kRowWarpBytes = kRowKeyBytes + kStageBytes + kColBegBytes;
+constexpr int kRowWarpBytes = kRowKeyBytes + kStageBytes;
+// FILL launches: the row area holds the wide tile's per-lane HANDLE buffers
+// (u32, kFillCap per lane, stride 33) — flushes then need no record lookups —
+// and still fits the compact tile's u16 key rows.
+constexpr int kFillCap = 64;
+constexpr int kFillRowBytes = kFillCap * 33 * 4 > kRowKeyBytes ? kFillCap * 33 * 4 : kRowKeyBytes;
+template <int MODE>
+__host__ __device__ constexpr int row_area_bytes() {
+  return MODE == 1 /* MODE_FILL */ ? kFillRowBytes : kRowKeyBytes;
+}
+template <int MODE>
+__host__ __device__ constexpr int warp_smem_bytes() { return row_area_bytes<MODE>() + kStageBytes; }
 constexpr int kWideMaxCols = 4096;                    // wide tiles: hull column limit
 constexpr int kRowCap = kRowWarpBytes / 4;            // one-query row buffer (u32)
 constexpr int kSortCap = (kRowCap - 512) / 2;         // one-query row sorted in smem
@@ -570,16 +580,15 @@ __device__ __forceinline__ bool advance_chunk(uint32_t& mask, uint32_t& c, uint3
 // span — with the same staged, warp-uniform record stream and per-lane
 // column mask + z window as the compact tile. COUNT / DIGEST keep counters.
 // FILL writes each lane's hits UNSORTED at its row (row_ptr from the count
-// pass): the per-lane u16 key buffers are flushed whenever one could
-// overflow, before a column offset leaves the 11-bit key range (the column's
-// key base moves up), and at every batch end; sort_rows_kernel sorts the
-// rows afterwards.
+// pass): each lane buffers its hits' handles (u32, kFillCap, stride 33) and
+// the warp flushes all buffers, one row at a time (coalesced), whenever one
+// could overflow during the next chunk; the rows are sorted afterwards.
 template <int FLAVOR, int MODE, int CUBE>
 __device__ __forceinline__ void wide_tile(const Tables& t, const Range& R, bool ok, bool active,
                                           uint32_t qi, uint32_t I0, uint32_t J0, uint32_t nj,
                                           uint32_t nc, uint32_t K0, uint32_t K1,
                                           const Predicate& P, int lane, PointRec* stg,
-                                          uint16_t* skey, uint32_t* cbeg, const Out& o) {
+                                          uint32_t* sid, const Out& o) {
   constexpr bool FILL = MODE == MODE_FILL;
   const PointRec* __restrict__ rec = t.rec;
   const uint32_t kk0 = ok ? (uint32_t)R.k0 : 1u;
@@ -590,37 +599,16 @@ __device__ __forceinline__ void wide_tile(const Tables& t, const Range& R, bool 
   uint32_t cnt = 0, ntest = 0, nb = 0, hull = 0;
   uint64_t dig = 0;
   uint64_t wpos = (FILL && active) ? __ldg(o.row_ptr + qi) : 0;
-  // Buffered keys -> handles -> the rows, one row at a time by the whole warp
-  // (coalesced stores: a per-lane store stream would cost one L2 write
-  // request per handle), four rows' loads in flight.
   auto flush = [&]() {
     __syncwarp();
-    for (int l0 = 0; l0 < 32; l0 += 4) {
-      uint32_t v[4][3];
-#pragma unroll
-      for (int jj = 0; jj < 4; ++jj) {
-        const uint32_t n = __shfl_sync(0xffffffffu, nb, l0 + jj);
-#pragma unroll
-        for (int h = 0; h < 3; ++h) {
-          const uint32_t i = h * 32 + lane;
-          uint32_t x = 0;
-          if (i < n) {
-            const uint32_t kv = skey[i * 33 + l0 + jj];
-            x = __ldg(&rec[cbeg[kv >> 11] + (kv & 2047u)].id);
-          }
-          v[jj][h] = x;
-        }
-      }
-#pragma unroll
-      for (int jj = 0; jj < 4; ++jj) {
-        const uint32_t n = __shfl_sync(0xffffffffu, nb, l0 + jj);
-        const uint64_t wp = __shfl_sync(0xffffffffu, wpos, l0 + jj);
-#pragma unroll
-        for (int h = 0; h < 3; ++h) {
-          const uint32_t i = h * 32 + lane;
-          if (i < n) o.cols[wp + i] = v[jj][h];
-        }
-      }
+#pragma unroll 4
+    for (int l = 0; l < 32; ++l) {
+      const uint32_t n = __shfl_sync(0xffffffffu, nb, l);
+      const uint64_t wp = __shfl_sync(0xffffffffu, wpos, l);
+      const uint32_t a = (uint32_t)lane < n ? sid[lane * 33 + l] : 0u;
+      const uint32_t b2 = lane + 32u < n ? sid[(lane + 32) * 33 + l] : 0u;
+      if ((uint32_t)lane < n) o.cols[wp + lane] = a;
+      if (lane + 32u < n) o.cols[wp + 32 + lane] = b2;
     }
     wpos += nb;
     nb = 0;
@@ -642,10 +630,6 @@ __device__ __forceinline__ void wide_tile(const Tables& t, const Range& R, bool 
 #pragma unroll
     for (int sh = 16; sh > 0; sh >>= 1) needmask |= __shfl_xor_sync(0xffffffffu, needmask, sh);
     needmask &= __ballot_sync(0xffffffffu, e > b);
-    if (FILL) {
-      cbeg[lane] = b;
-      __syncwarp();
-    }
     uint32_t c = 0, p = 0, ce = 0;
     bool more = advance_chunk(needmask, c, p, ce, b, e, true);
     int buf = 0;
@@ -664,20 +648,7 @@ __device__ __forceinline__ void wide_tile(const Tables& t, const Range& R, bool 
       // chunks (k-sorted) outside every lane's z window are skipped whole
       const bool want = need & (sr[len - 1].meta >= kk0) & (sr[0].meta <= kk0 + kspan);
       const bool anyw = __any_sync(0xffffffffu, want);
-      uint32_t kbase = 0;
-      if (FILL) {
-        uint32_t cbase = cbeg[c];
-        const bool rebase = p + len - cbase > 2048u;
-        if (rebase || __any_sync(0xffffffffu, nb > (uint32_t)kLaneRowCap - 32u)) {
-          flush();
-          if (rebase) {
-            if (lane == 0) cbeg[c] = p;
-            __syncwarp();
-            cbase = p;
-          }
-        }
-        kbase = (c << 11) | (p - cbase);
-      }
+      if (FILL && anyw && __any_sync(0xffffffffu, nb > (uint32_t)kFillCap - 32u)) flush();
       uint32_t u = anyw ? 0u : len;
       for (; u + 8 <= len; u += 8) {
         SRec v[8];
@@ -688,7 +659,7 @@ __device__ __forceinline__ void wide_tile(const Tables& t, const Range& R, bool 
           const bool in = need & (v[w].meta - kk0 <= kspan);
           const bool hit = in & pred<CUBE>(P, v[w].x, v[w].y, v[w].z);
           if (MODE == MODE_DIGEST && hit) dig += mix64(v[w].id);
-          if (FILL && hit) skey[nb * 33 + lane] = (uint16_t)(kbase + u + w);
+          if (FILL && hit) sid[nb * 33 + lane] = v[w].id;
           if (FILL) nb += hit;
           cnt += hit;
           ntest += in;
@@ -699,7 +670,7 @@ __device__ __forceinline__ void wide_tile(const Tables& t, const Range& R, bool 
         const bool in = need & (v.meta - kk0 <= kspan);
         const bool hit = in & pred<CUBE>(P, v.x, v.y, v.z);
         if (MODE == MODE_DIGEST && hit) dig += mix64(v.id);
-        if (FILL && hit) skey[nb * 33 + lane] = (uint16_t)(kbase + u);
+        if (FILL && hit) sid[nb * 33 + lane] = v.id;
         if (FILL) nb += hit;
         cnt += hit;
         ntest += in;
@@ -710,8 +681,8 @@ __device__ __forceinline__ void wide_tile(const Tables& t, const Range& R, bool 
       more = more2;
     }
     cp_async_wait<0>();
-    if (FILL) flush();  // keys refer to this batch's column bases
   }
+  if (FILL) flush();
   const uint32_t hsum = warp_incl_scan(hull);
   if (lane == 31) atomicAdd(&g_qstats[(FILL ? 4 : 0) + 2], (unsigned long long)hsum);
   if (MODE == MODE_COUNT) {
@@ -741,10 +712,10 @@ __global__ void __launch_bounds__(kQThreads, 5) radius_tile_kernel(
   constexpr int so = ROWS ? 4 : 0;
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  unsigned char* wreg = smraw + (size_t)wib * kRowWarpBytes;
+  unsigned char* wreg = smraw + (size_t)wib * warp_smem_bytes<MODE>();
   uint16_t* skey = reinterpret_cast<uint16_t*>(wreg);  // hit = column << 11 | offset in span
   uint32_t* wbuf = reinterpret_cast<uint32_t*>(wreg);
-  PointRec* stg = reinterpret_cast<PointRec*>(wreg + kRowKeyBytes);
+  PointRec* stg = reinterpret_cast<PointRec*>(wreg + row_area_bytes<MODE>());
   const uint32_t lt = lanemask_lt();
   const uint64_t ntiles = (nq + 31) / 32;
   const uint64_t W = (uint64_t)gridDim.x * kQWarps;
@@ -805,8 +776,7 @@ __global__ void __launch_bounds__(kQThreads, 5) radius_tile_kernel(
       Predicate P;
       P.init(cx, cy, cz, r, CUBE);
       wide_tile<FLAVOR, MODE, CUBE>(t, R, ok, active, qi, I0, J0, nj, (uint32_t)nc, K0, K1, P,
-                                    lane, stg, skey,
-                                    reinterpret_cast<uint32_t*>(wreg + kRowKeyBytes + kStageBytes), o);
+                                    lane, stg, reinterpret_cast<uint32_t*>(wreg), o);
       __syncwarp();
       continue;
     }
@@ -1492,7 +1462,7 @@ template <int MODE>
 cm_status launch_radius(const cm_index* ix, const double* q, uint64_t nq, int kernel, double r,
                         const uint32_t* perm, const Out& o, cudaStream_t st) {
   const Tables t = ix->tables();
-  const size_t smem = (size_t)kQWarps * kRowWarpBytes;
+  const size_t smem = (size_t)kQWarps * warp_smem_bytes<MODE>();
   auto run = [&](auto kern) -> cm_status {
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
