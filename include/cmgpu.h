@@ -10,6 +10,8 @@
  *   Cheesemap::occupancy_stats()     map.hpp:104, map.cpp:150-171  cm_get_occupancy
  *   Cheesemap::memory_report()       map.hpp:105, map.cpp:173-192  cm_get_memory_report
  *   read_las(path)                   io.hpp:39-42, io.cpp:33-106  cm_las_read / cm_las_decode
+ *   brute_radius / brute_knn         baseline.hpp:11-21, baseline.cpp:8-25
+ *                                                          cm_brute_radius / cm_brute_knn
  *   Cheesemap::voxel_lookup / for_each_in_voxel  map.hpp:69-102  cm_export_voxels
  *   kernel_search<SphereKernel|BoxKernel>  search.hpp:102-127
  *                                 cm_radius_count + cm_radius_fill, cm_radius_search,
@@ -240,6 +242,17 @@ cm_status cm_debug_query_stats(uint64_t* out8, int reset);
  * reserved (cached + in use) and in use, in bytes; trim != 0 first returns
  * the cached part to the device. */
 cm_status cm_debug_pool_bytes(int device, int trim, uint64_t* reserved, uint64_t* used);
+
+/* ---- brute-force baselines: brute_radius (baseline.hpp:11-21), brute_knn
+ * (baseline.cpp:8-25) — every point against every centre, no index; what the
+ * CLI's verify compares the index against. brute_radius reports each set as
+ * (count, sum of splitmix64(handle)) like cm_radius_digest; brute_knn orders
+ * by (d², handle), k <= 64. Points / centres / outputs host or device. */
+cm_status cm_brute_radius(const double* xyz, uint64_t n, const double* centers, uint64_t nq,
+                          int kernel, double r, uint32_t* counts, uint64_t* digests, int device,
+                          void* stream);
+cm_status cm_brute_knn(const double* xyz, uint64_t n, const double* centers, uint64_t nq,
+                       uint32_t k, uint32_t* idx, double* d2, int device, void* stream);
 
 /* ---- LAS ingestion: read_las (io.hpp:39-42, io.cpp:33-106) ----------------
  * The header is checked on the host with the reference's checks, messages

@@ -19,7 +19,7 @@ EXPORTS = [
     "cm_knn", "cm_corrupt_for_testing", "cm_last_error", "cm_status_name",
     "cm_get_last_query_timing", "cm_launch_count", "cm_debug_query_stats", "cm_debug_pool_bytes",
     "cm_global_density", "cm_weighted_density", "cm_las_parse_header", "cm_las_decode",
-    "cm_las_read", "cm_get_memory_report",
+    "cm_las_read", "cm_get_memory_report", "cm_brute_radius", "cm_brute_knn",
 ]
 
 
@@ -123,6 +123,8 @@ def lib():
         "cm_debug_pool_bytes": ([i32, i32, p, p], i32),
         "cm_las_parse_header": ([p, u64, ctypes.POINTER(LasHeaderC)], i32),
         "cm_get_memory_report": ([p, ctypes.POINTER(MemoryReportC)], i32),
+        "cm_brute_radius": ([p, u64, p, u64, i32, dbl, p, p, i32, p], i32),
+        "cm_brute_knn": ([p, u64, p, u64, u32, p, p, i32, p], i32),
         "cm_las_decode": ([p, u64, p, u64, ctypes.POINTER(LasHeaderC), i32, p], i32),
         "cm_las_read": ([ctypes.c_char_p, p, u64, ctypes.POINTER(LasHeaderC), i32, p], i32),
     }

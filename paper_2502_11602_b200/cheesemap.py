@@ -455,3 +455,34 @@ def _out_ptr(a):
     if _is_torch(a):
         return ctypes.c_void_p(a.data_ptr())
     return a.ctypes.data_as(ctypes.c_void_p)
+
+
+# -------------------------------------------------------- baseline.hpp ------
+def brute_radius(cloud, centers, r, kernel=SPHERE, device=0, stream=None):
+    """brute_radius (baseline.hpp:11-21) on the device: every point tested
+    against every centre -> (counts u32[nq], digests u64[nq])."""
+    pp, pk = _in_ptr(cloud)
+    qp, qk = _in_ptr(centers)
+    nq = _nrows(qk)
+    counts = np.zeros(nq, dtype=np.uint32)
+    digests = np.zeros(nq, dtype=np.uint64)
+    _check(_native.lib().cm_brute_radius(pp, _nrows(pk), qp, nq, int(kernel), float(r),
+                                         counts.ctypes.data_as(ctypes.c_void_p),
+                                         digests.ctypes.data_as(ctypes.c_void_p), device,
+                                         _stream_ptr(stream)))
+    return counts, digests
+
+
+def brute_knn(cloud, centers, k, device=0, stream=None):
+    """brute_knn (baseline.cpp:8-25) on the device, ordered by (d^2, handle):
+    (idx u32[nq, k], d2 f64[nq, k]); k <= 64."""
+    pp, pk = _in_ptr(cloud)
+    qp, qk = _in_ptr(centers)
+    nq = _nrows(qk)
+    idx = np.zeros((nq, k), dtype=np.uint32)
+    d2 = np.zeros((nq, k), dtype=np.float64)
+    _check(_native.lib().cm_brute_knn(pp, _nrows(pk), qp, nq, int(k),
+                                      idx.ctypes.data_as(ctypes.c_void_p),
+                                      d2.ctypes.data_as(ctypes.c_void_p), device,
+                                      _stream_ptr(stream)))
+    return idx, d2

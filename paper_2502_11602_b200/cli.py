@@ -8,6 +8,8 @@
             summarised together (cmd_bench.cpp:231-292)
   report    dataset metrics + per-structure occupancy and memory accounting
             (cmd_report.cpp:11-78)
+  verify    every flavour / mode / kernel against the device brute force
+            (cmd_verify.cpp:31-114; exit 1 on a mismatch)
   generate  write a synthetic cloud (.las / .xyz) (cmd_report.cpp:80-100)
 
     python -m paper_2502_11602_b200.cli bench --synthetic uniform:n=1000000,extent=100x100x50,seed=1 \\
@@ -18,7 +20,7 @@ centres (the reference times one call per centre). A bench row's queries
 are --batch centres per call drawn from the reference's CenterStream
 (common.cpp:109-125); mean_ns is total device time / queries, median_ns and
 p95_ns are over the per-batch amortised times. Exit codes follow
-common.hpp:16-20 (0 ok, 2 usage, 3 io/parse, 4 capacity).
+common.hpp:16-20 (0 ok, 1 mismatch, 2 usage, 3 io/parse, 4 capacity).
 """
 import argparse
 import json
@@ -31,7 +33,7 @@ import numpy as np
 from . import cheesemap as cm
 from . import synth
 
-EXIT_OK, EXIT_USAGE, EXIT_IO, EXIT_CAPACITY = 0, 2, 3, 4
+EXIT_OK, EXIT_MISMATCH, EXIT_USAGE, EXIT_IO, EXIT_CAPACITY = 0, 1, 2, 3, 4
 
 CSV_HEADER = ("dataset,structure,flavor,dims,cell_size,reordered,query_type,parameter,"
               "queries,mean_ns,median_ns,p95_ns,mean_voxels_visited,mean_result_size,status")
@@ -393,6 +395,66 @@ def cmd_report(args):
     return EXIT_OK
 
 
+def cmd_verify(args):
+    """cmd_verify (cmd_verify.cpp:31-114): every flavour x mode x cell size,
+    sphere / cube / cylinder at r in {0.5, 1, 2.5, 5} and kNN at k in
+    {1, 5, 10, 20}, for --queries centres, against the device brute force.
+    Sets are compared as (count, splitmix64 digest); kNN by (handle, d^2)."""
+    cloud, dataset = load_cloud(args.input, args.synthetic)
+    if cloud.shape[0] == 0:
+        raise cm.EmptyCloudError("point cloud is empty")
+    if cloud.shape[0] > args.cap:
+        raise cm.CapacityError(f"cloud has {cloud.shape[0]} points, above the verification cap "
+                               f"of {args.cap}; subsample the input first")
+    radii = (0.5, 1.0, 2.5, 5.0)
+    ks = (1, 5, 10, 20)
+    kinds = (("sphere", cm.SPHERE), ("cube", cm.CUBE), ("cylinder", cm.CYLINDER))
+    centers = np.ascontiguousarray(cloud[synth.center_stream(args.seed, 0, cloud.shape[0],
+                                                             args.queries).astype(np.int64)])
+    nq = centers.shape[0]
+    brute = {}
+    for r in radii:
+        for kname, kind in kinds:
+            brute[(kname, r)] = cm.brute_radius(cloud, centers, r, kind, device=args.device)
+    for k in ks:
+        brute[("knn", k)] = cm.brute_knn(cloud, centers, k, device=args.device)
+    cases = failures = 0
+    for flavor in (cm.Flavor.Dense, cm.Flavor.Sparse, cm.Flavor.Mixed):
+        for mode in (cm.GridMode.TwoD, cm.GridMode.ThreeD):
+            for cell in args.cell_sizes:
+                m = cm.Cheesemap.build(cloud, cm.BuildOptions(
+                    flavor=flavor, mode=mode, cell=cm.CellSize.uniform(cell),
+                    densify_threshold=args.tau), device=args.device)
+                if args.inject_fault:
+                    m.corrupt_for_testing()
+                name = cm.structure_name(flavor, mode, False)
+                ok = {}
+                for r in radii:
+                    for kname, kind in kinds:
+                        c, d = cm.radius_digest_batch(m, centers, r, kind)
+                        bc, bd = brute[(kname, r)]
+                        ok[(kname, r)] = (c == bc) & (d == bd)
+                for k in ks:
+                    idx, d2 = cm.knn_batch(m, centers, k)
+                    bi, bd = brute[("knn", k)]
+                    ok[("knn", k)] = np.all(idx == bi, axis=1) & np.all(d2 == bd, axis=1)
+                for q in range(nq):  # the reference's case order (cmd_verify.cpp:69-106)
+                    for r in radii:
+                        for kname, _ in kinds:
+                            cases += 1
+                            if not ok[(kname, r)][q]:
+                                failures += 1
+                                sys.stderr.write(f"MISMATCH: {name} s={cell:f} {kname} r={r:f}\n")
+                    for k in ks:
+                        cases += 1
+                        if not ok[("knn", k)][q]:
+                            failures += 1
+                            sys.stderr.write(f"MISMATCH: {name} s={cell:f} knn k={k}\n")
+                del m
+    print(f"verify: {dataset}: {cases - failures}/{cases} cases matched the oracle")
+    return EXIT_OK if failures == 0 else EXIT_MISMATCH
+
+
 def cmd_generate(args):
     if not args.output:
         raise cm.InvalidArgumentError("--output is required")
@@ -457,6 +519,16 @@ def parser():
     r.add_argument("--seed", type=int, default=1)
     r.add_argument("--output", default="")
     r.add_argument("--device", type=int, default=0)
+    v = sub.add_parser("verify", help="check every flavour/mode/kernel against the brute force")
+    v.add_argument("--input", default="")
+    v.add_argument("--synthetic", default="")
+    v.add_argument("--cell-sizes", type=_floats, default=[1.0, 2.5])
+    v.add_argument("--seed", type=int, default=1)
+    v.add_argument("--queries", type=int, default=25)
+    v.add_argument("--cap", type=int, default=200000)
+    v.add_argument("--tau", type=float, default=0.80)
+    v.add_argument("--inject-fault", action="store_true", help=argparse.SUPPRESS)
+    v.add_argument("--device", type=int, default=0)
     g = sub.add_parser("generate", help="write a synthetic cloud to a file")
     g.add_argument("--synthetic", required=True)
     g.add_argument("--output", required=True)
@@ -470,7 +542,8 @@ def main(argv=None):
     except SystemExit as e:
         return EXIT_OK if e.code == 0 else EXIT_USAGE
     try:
-        return {"bench": cmd_bench, "report": cmd_report, "generate": cmd_generate}[args.cmd](args)
+        return {"bench": cmd_bench, "report": cmd_report, "verify": cmd_verify,
+                "generate": cmd_generate}[args.cmd](args)
     except cm.CapacityError as e:
         sys.stderr.write(f"error: {e}\n")
         return EXIT_CAPACITY

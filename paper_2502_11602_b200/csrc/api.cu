@@ -439,19 +439,12 @@ __global__ void export_kernel(const PointRec* __restrict__ rec, uint64_t n, DevG
 // Test hook: drop the first record of the first non-empty voxel from the
 // tables (map.cpp:194-223 drops one stored handle): every voxel span at or
 // below that voxel starts one record later.
-__global__ void corrupt_kernel(uint32_t* ustart, uint32_t* dense_off, uint64_t first_key,
-                               HashSlot* vhash, uint64_t vmask) {
-  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  if (dense_off)
-    for (uint64_t g = tid; g <= first_key; g += (uint64_t)gridDim.x * blockDim.x) dense_off[g] = 1;
-  if (tid == 0) {
-    ustart[0] += 1;
-    if (vhash) {
-      uint64_t s = mix64(first_key) & vmask;
-      while (vhash[s].key != first_key) s = (s + 1) & vmask;
-      vhash[s].a += 1;
-    }
-  }
+// Removes one stored point from every query's view (its x becomes NaN, so
+// no kernel predicate accepts it) — the effect of the reference's hook,
+// which pops a handle out of a voxel list (map.cpp:194-223). The point is
+// the middle one in cell order, reachable from most query centres.
+__global__ void corrupt_kernel(PointRec* rec, uint64_t at) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) rec[at].x = __longlong_as_double(0x7ff8000000000000ll);
 }
 __global__ void add_offset_kernel(uint64_t* v, uint64_t n, uint64_t off) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
@@ -483,9 +476,7 @@ cm_status cm_export_voxels(const cm_index* ix, uint64_t* keys, uint32_t* handles
 cm_status cm_corrupt_for_testing(cm_index* ix) {
   CM_TRY(check_index(ix));
   DeviceGuard dg(ix->device);
-  uint64_t first = 0;
-  CM_CUDA_TRY(cudaMemcpy(&first, ix->ukey, 8, cudaMemcpyDeviceToHost));
-  apik::corrupt_kernel<<<64, 256, 0, 0>>>(ix->ustart, ix->dense_off, first, ix->vhash, ix->vmask); ::cmg::note_launch();
+  apik::corrupt_kernel<<<1, 1, 0, 0>>>(ix->rec, ix->n / 2); ::cmg::note_launch();
   CM_CUDA_TRY(cudaGetLastError());
   CM_CUDA_TRY(cudaDeviceSynchronize());
   return CM_OK;
@@ -1049,6 +1040,62 @@ cm_status cm_radius_digest(const cm_index* ix, const double* q, uint64_t nq, int
   CM_TRY(c.finish());
   CM_TRY(d.finish());
   return sync_if(c.host() || d.host(), st);
+}
+
+// brute_radius (baseline.hpp:11-21) on the device: (count, digest) per centre.
+cm_status cm_brute_radius(const double* xyz, uint64_t n, const double* q, uint64_t nq, int kernel,
+                          double r, uint32_t* counts, uint64_t* digests, int device, void* stream) {
+  CM_TRY(check_kernel(kernel));
+  if ((n && !xyz) || (nq && (!q || !counts || !digests))) {
+    set_error("null point, query or output pointer");
+    return CM_INVALID_ARGUMENT;
+  }
+  DeviceGuard dg(device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  InBuf pin, qin;
+  CM_TRY(stage_input(xyz, n * 24, st, &pin));
+  CM_TRY(stage_input(q, nq * 24, st, &qin));
+  OutBuf<uint32_t> c;
+  OutBuf<uint64_t> d;
+  CM_TRY(c.init(counts, nq, st));
+  CM_TRY(d.init(digests, nq, st));
+  CM_TRY(brute_radius_dev(static_cast<const double*>(pin.dev), n, static_cast<const double*>(qin.dev),
+                          nq, kernel, r, c.dev, d.dev, st));
+  CM_TRY(c.finish());
+  CM_TRY(d.finish());
+  return sync_if(c.host() || d.host(), st);
+}
+
+// brute_knn (baseline.cpp:8-25) on the device, ordered by (d², handle);
+// k <= 64. Missing neighbours (k > n) are handle 0xffffffff, d² = +inf.
+cm_status cm_brute_knn(const double* xyz, uint64_t n, const double* q, uint64_t nq, uint32_t k,
+                       uint32_t* idx, double* d2, int device, void* stream) {
+  if (k == 0) {
+    set_error("k must be at least 1");
+    return CM_INVALID_ARGUMENT;
+  }
+  if (k > (uint32_t)kBruteKMax) {
+    set_error("brute-force kNN supports k <= 64");
+    return CM_INVALID_ARGUMENT;
+  }
+  if ((n && !xyz) || (nq && (!q || !idx || !d2))) {
+    set_error("null point, query or output pointer");
+    return CM_INVALID_ARGUMENT;
+  }
+  DeviceGuard dg(device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  InBuf pin, qin;
+  CM_TRY(stage_input(xyz, n * 24, st, &pin));
+  CM_TRY(stage_input(q, nq * 24, st, &qin));
+  OutBuf<uint32_t> oi;
+  OutBuf<double> od;
+  CM_TRY(oi.init(idx, nq * k, st));
+  CM_TRY(od.init(d2, nq * k, st));
+  CM_TRY(brute_knn_dev(static_cast<const double*>(pin.dev), n, static_cast<const double*>(qin.dev),
+                       nq, k, oi.dev, od.dev, st));
+  CM_TRY(oi.finish());
+  CM_TRY(od.finish());
+  return sync_if(oi.host() || od.host(), st);
 }
 
 // global_density (analysis.cpp:17-24): points per m^2 of the xy bounding

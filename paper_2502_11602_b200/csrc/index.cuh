@@ -101,6 +101,12 @@ cm_status radius_count_dev(const cm_index* ix, const double* q_dev, uint64_t nq,
                            double r, const uint32_t* perm, uint32_t* counts_dev,
                            uint64_t* tested_dev, cudaStream_t st);
 bool radius_is_wide(const cm_index* ix, double r);
+// brute-force baselines (brute.cu): every point against every centre
+constexpr int kBruteKMax = 64;
+cm_status brute_radius_dev(const double* xyz, uint64_t n, const double* q, uint64_t nq, int kind,
+                           double r, uint32_t* counts, uint64_t* digests, cudaStream_t st);
+cm_status brute_knn_dev(const double* xyz, uint64_t n, const double* q, uint64_t nq, uint32_t k,
+                        uint32_t* idx, double* d2, cudaStream_t st);
 cm_status radius_fill_dev(const cm_index* ix, const double* q_dev, uint64_t nq, int kernel,
                           double r, const uint32_t* perm, const uint64_t* row_ptr_dev,
                           uint32_t* cols_dev, cudaStream_t st, cudaEvent_t after_fill = nullptr);

@@ -221,3 +221,37 @@ def test_report_json(tmp_path):
         assert (e["handle_bytes"], e["structure_bytes"], e["total_bytes"]) == (
             mem["handle_bytes"], mem["structure_bytes"], mem["total_bytes"])
         assert ("slices" in e) == ("mixed" in e["structure"])
+
+
+@pytest.mark.gpu
+def test_brute_force_baselines_match_oracle():
+    """brute_radius / brute_knn on the device against the restatement's
+    kernel_search / kNN (which the reference pins)."""
+    rng = np.random.default_rng(11)
+    cloud = rng.uniform(0, 20, (30000, 3))
+    q = np.ascontiguousarray(cloud[::97])
+    o = orc.CpuIndex(cloud, flavor=1)
+    for kind in (cm.SPHERE, cm.CUBE, cm.CYLINDER):
+        for r in (0.5, 2.0):
+            c, d = cm.brute_radius(cloud, q, r, kind)
+            oc, od = o.radius(q, int(kind), r)
+            assert np.array_equal(c, oc) and np.array_equal(d, od)
+    for k in (1, 7, 64):
+        idx, d2 = cm.brute_knn(cloud, q, k)
+        oi, od2 = o.knn(q, k)
+        assert np.array_equal(idx, oi) and np.array_equal(d2, od2)
+    with pytest.raises(cm.InvalidArgumentError):
+        cm.brute_knn(cloud, q, 65)
+
+
+@pytest.mark.gpu
+def test_verify_command(capsys):
+    """cmd_verify: all cases match; the fault hook must be detected."""
+    spec = "uniform:n=20000,extent=50x50x25,seed=10"
+    assert cli.main(["verify", "--synthetic", spec, "--queries", "10"]) == 0
+    out = capsys.readouterr().out
+    assert "verify: synthetic: 1920/1920 cases matched the oracle" in out
+    # test_cli.cpp:152-154: a small cloud, so the corrupted voxel is in reach
+    assert cli.main(["verify", "--synthetic", "uniform:n=2000,extent=20x20x10,seed=3",
+                     "--cell-sizes", "1", "--queries", "10", "--inject-fault"]) == cli.EXIT_MISMATCH
+    assert cli.main(["verify", "--synthetic", spec, "--cap", "100"]) == cli.EXIT_CAPACITY
