@@ -36,7 +36,7 @@ namespace {
 
 constexpr int kQThreads = 128;
 constexpr int kQWarps = kQThreads / 32;
-constexpr int kLaneRowCap = 96;                       // per-lane row buffer
+constexpr int kLaneRowCap = 128;                      // per-lane row buffer
 // Per warp: the tile path's per-lane rows (u16 hit keys, interleaved with
 // stride 33) followed by the cp.async staging double buffer; the one-query
 // path reuses the whole region as a u32 buffer.
@@ -990,6 +990,60 @@ __global__ void __launch_bounds__(1024) big_row_sort_kernel(uint32_t* __restrict
   }
 }
 
+// Rows of 97..1024 handles, one warp per row, blocked layout: lane l holds
+// handles [l * ITEMS, (l + 1) * ITEMS) of the row in registers, so the
+// bitonic network's exchanges at distance < ITEMS stay inside a lane (no
+// shuffles) and the row's loads and stores are contiguous per lane.
+constexpr int kBlockedMax = 1024;
+
+template <int ITEMS>
+__device__ __forceinline__ void warp_sort_blocked(uint32_t (&v)[ITEMS], int lane) {
+  constexpr int P = 32 * ITEMS;
+#pragma unroll
+  for (int k = 2; k <= P; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j < ITEMS) {
+#pragma unroll
+        for (int r = 0; r < ITEMS; ++r) {
+          const int p = r ^ j;
+          if (p > r) {
+            const bool asc = (((uint32_t)lane * ITEMS + r) & k) == 0;
+            const uint32_t a = v[r], b = v[p];
+            v[r] = asc ? min(a, b) : max(a, b);
+            v[p] = asc ? max(a, b) : min(a, b);
+          }
+        }
+      } else {
+        const int jl = j / ITEMS;
+        const bool lower = (lane & jl) == 0;
+#pragma unroll
+        for (int r = 0; r < ITEMS; ++r) {
+          const uint32_t o = __shfl_xor_sync(0xffffffffu, v[r], jl);
+          const bool asc = (((uint32_t)lane * ITEMS + r) & k) == 0;
+          v[r] = (lower == asc) ? min(v[r], o) : max(v[r], o);
+        }
+      }
+    }
+  }
+}
+
+template <int ITEMS>
+__device__ __forceinline__ void warp_sort_row_blocked(uint32_t* row, uint32_t n, int lane) {
+  uint32_t v[ITEMS];
+#pragma unroll
+  for (int r = 0; r < ITEMS; ++r) {
+    const uint32_t e = (uint32_t)lane * ITEMS + r;
+    v[r] = e < n ? row[e] : 0xffffffffu;
+  }
+  warp_sort_blocked<ITEMS>(v, lane);
+#pragma unroll
+  for (int r = 0; r < ITEMS; ++r) {
+    const uint32_t e = (uint32_t)lane * ITEMS + r;
+    if (e < n) row[e] = v[r];
+  }
+}
+
 // Arena rows -> CSR order, sorting them on the way. A warp takes 32
 // consecutive queries in the caller's order, so its output is one contiguous
 // stretch of cols (whole sectors, no partial-sector read-modify-write in L2);
@@ -997,8 +1051,10 @@ __global__ void __launch_bounds__(1024) big_row_sort_kernel(uint32_t* __restrict
 // handles are staged in shared memory (interleaved, stride 33); each lane
 // sorts its own row in registers with an unrolled bitonic network — rows
 // longer than 64 as two runs, [0, 64) and [64, len), merged by the warp
-// along the merge path (three outputs per lane). Rows longer than 96 come from the
-// one-query-per-warp path already sorted and are copied.
+// along the merge path (three outputs per lane). Rows of 97..128 (tile rows
+// past the staging width) are sorted by the warp (blocked register bitonic);
+// longer ones come from the one-query-per-warp path already sorted and are
+// copied.
 constexpr int kGatherRow = 96;
 constexpr int kGatherWarpWords = kGatherRow * 33 + 96;  // rows, sfin[32], srel[32] (u64)
 //
@@ -1138,6 +1194,22 @@ __global__ void __launch_bounds__(128) gather_rows_kernel(const uint32_t* temp,
             ib += !ta;
           }
         }
+      } else if (!SORT && ln <= (uint32_t)kLaneRowCap) {
+        // an unsorted tile row past the staging width: one warp, blocked
+        // register bitonic, straight from the arena to the CSR
+        const uint64_t o = __shfl_sync(0xffffffffu, so, l);
+        uint32_t v[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const uint32_t e = (uint32_t)lane * 4 + r;
+          v[r] = e < ln ? __ldg(temp + o + e) : 0xffffffffu;
+        }
+        warp_sort_blocked<4>(v, lane);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const uint32_t e = (uint32_t)lane * 4 + r;
+          if (e < ln) cols[d + e] = v[r];
+        }
       } else {
         const uint64_t o = __shfl_sync(0xffffffffu, so, l);
         for (uint32_t b0 = 0; b0 < ln; b0 += 256) {  // 8 loads in flight per lane
@@ -1156,60 +1228,6 @@ __global__ void __launch_bounds__(128) gather_rows_kernel(const uint32_t* temp,
       }
     }
     __syncwarp();
-  }
-}
-
-// Rows of 97..1024 handles, one warp per row, blocked layout: lane l holds
-// handles [l * ITEMS, (l + 1) * ITEMS) of the row in registers, so the
-// bitonic network's exchanges at distance < ITEMS stay inside a lane (no
-// shuffles) and the row's loads and stores are contiguous per lane.
-constexpr int kBlockedMax = 1024;
-
-template <int ITEMS>
-__device__ __forceinline__ void warp_sort_blocked(uint32_t (&v)[ITEMS], int lane) {
-  constexpr int P = 32 * ITEMS;
-#pragma unroll
-  for (int k = 2; k <= P; k <<= 1) {
-#pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      if (j < ITEMS) {
-#pragma unroll
-        for (int r = 0; r < ITEMS; ++r) {
-          const int p = r ^ j;
-          if (p > r) {
-            const bool asc = (((uint32_t)lane * ITEMS + r) & k) == 0;
-            const uint32_t a = v[r], b = v[p];
-            v[r] = asc ? min(a, b) : max(a, b);
-            v[p] = asc ? max(a, b) : min(a, b);
-          }
-        }
-      } else {
-        const int jl = j / ITEMS;
-        const bool lower = (lane & jl) == 0;
-#pragma unroll
-        for (int r = 0; r < ITEMS; ++r) {
-          const uint32_t o = __shfl_xor_sync(0xffffffffu, v[r], jl);
-          const bool asc = (((uint32_t)lane * ITEMS + r) & k) == 0;
-          v[r] = (lower == asc) ? min(v[r], o) : max(v[r], o);
-        }
-      }
-    }
-  }
-}
-
-template <int ITEMS>
-__device__ __forceinline__ void warp_sort_row_blocked(uint32_t* row, uint32_t n, int lane) {
-  uint32_t v[ITEMS];
-#pragma unroll
-  for (int r = 0; r < ITEMS; ++r) {
-    const uint32_t e = (uint32_t)lane * ITEMS + r;
-    v[r] = e < n ? row[e] : 0xffffffffu;
-  }
-  warp_sort_blocked<ITEMS>(v, lane);
-#pragma unroll
-  for (int r = 0; r < ITEMS; ++r) {
-    const uint32_t e = (uint32_t)lane * ITEMS + r;
-    if (e < n) row[e] = v[r];
   }
 }
 
