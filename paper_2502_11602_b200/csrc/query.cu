@@ -47,7 +47,11 @@ constexpr int kRowWarpBytes = kRowKeyBytes + kStageBytes;
 // (u32, kFillCap per lane, stride 33) — flushes then need no record lookups —
 // and still fits the compact tile's u16 key rows.
 constexpr int kFillCap = 64;
-constexpr int kFillRowBytes = kFillCap * 33 * 4 > kRowKeyBytes ? kFillCap * 33 * 4 : kRowKeyBytes;
+// + one scratch slot per lane: the walk stores every record's handle at the
+// lane's next slot unconditionally (no branch per hit) and advances on hits
+constexpr int kFillRowBytes = ((kFillCap + 1) * 33 * 4 + 15) / 16 * 16 > kRowKeyBytes
+                                  ? ((kFillCap + 1) * 33 * 4 + 15) / 16 * 16
+                                  : kRowKeyBytes;
 template <int MODE>
 __host__ __device__ constexpr int row_area_bytes() {
   return MODE == 1 /* MODE_FILL */ ? kFillRowBytes : kRowKeyBytes;
@@ -659,8 +663,10 @@ __device__ __forceinline__ void wide_tile(const Tables& t, const Range& R, bool 
           const bool in = need & (v[w].meta - kk0 <= kspan);
           const bool hit = in & pred<CUBE>(P, v[w].x, v[w].y, v[w].z);
           if (MODE == MODE_DIGEST && hit) dig += mix64(v[w].id);
-          if (FILL && hit) sid[nb * 33 + lane] = v[w].id;
-          if (FILL) nb += hit;
+          if (FILL) {
+            sid[nb * 33 + lane] = v[w].id;
+            nb += hit;
+          }
           cnt += hit;
           ntest += in;
         }
@@ -670,8 +676,10 @@ __device__ __forceinline__ void wide_tile(const Tables& t, const Range& R, bool 
         const bool in = need & (v.meta - kk0 <= kspan);
         const bool hit = in & pred<CUBE>(P, v.x, v.y, v.z);
         if (MODE == MODE_DIGEST && hit) dig += mix64(v.id);
-        if (FILL && hit) sid[nb * 33 + lane] = v.id;
-        if (FILL) nb += hit;
+        if (FILL) {
+          sid[nb * 33 + lane] = v.id;
+          nb += hit;
+        }
         cnt += hit;
         ntest += in;
       }
