@@ -499,7 +499,7 @@ cm_status cm_radius_count(const cm_index* ix, const double* q, uint64_t nq, int 
   CM_TRY(c.init(counts, nq, st));
   CM_TRY(t.init(tested, nq, st));
   QueryOrder ord;
-  CM_TRY(order_queries(ix, static_cast<const double*>(in.dev), nq, st, &ord));
+  CM_TRY(order_queries(ix, static_cast<const double*>(in.dev), nq, st, &ord, r, kernel));
   CM_TRY(radius_count_dev(ix, static_cast<const double*>(in.dev), nq, kernel, r, ord.perm, c.dev,
                           t.dev, st));
   CM_TRY(c.finish());
@@ -531,7 +531,7 @@ cm_status cm_radius_fill(const cm_index* ix, const double* q, uint64_t nq, int k
   OutBuf<uint32_t> c;
   CM_TRY(c.init(cols, nnz, st));
   QueryOrder ord;
-  CM_TRY(order_queries(ix, static_cast<const double*>(in.dev), nq, st, &ord));
+  CM_TRY(order_queries(ix, static_cast<const double*>(in.dev), nq, st, &ord, r, kernel));
   CM_TRY(radius_fill_dev(ix, static_cast<const double*>(in.dev), nq, kernel, r, ord.perm,
                          static_cast<const uint64_t*>(rp.dev), c.dev, st));
   CM_TRY(c.finish());
@@ -671,7 +671,7 @@ static cm_status radius_search_core(const cm_index* ix, const double* qd, uint64
   ev.valid = false;
   cudaEventRecord(ev.e[0], st);
   QueryOrder ord;
-  CM_TRY(order_queries(ix, qd, nq, st, &ord));
+  CM_TRY(order_queries(ix, qd, nq, st, &ord, r, kernel));
   cudaEventRecord(ev.e[1], st);
   uint32_t* counts = nullptr;
   uint64_t* toff = nullptr;
@@ -1034,7 +1034,7 @@ cm_status cm_radius_digest(const cm_index* ix, const double* q, uint64_t nq, int
   CM_TRY(c.init(counts, nq, st));
   CM_TRY(d.init(digests, nq, st));
   QueryOrder ord;
-  CM_TRY(order_queries(ix, static_cast<const double*>(in.dev), nq, st, &ord));
+  CM_TRY(order_queries(ix, static_cast<const double*>(in.dev), nq, st, &ord, r, kernel));
   CM_TRY(radius_digest_dev(ix, static_cast<const double*>(in.dev), nq, kernel, r, ord.perm, c.dev,
                            d.dev, st));
   CM_TRY(c.finish());
@@ -1190,7 +1190,7 @@ cm_status cm_weighted_density(const double* xyz, uint64_t n, uint64_t sample_siz
   CM_CUDA_TRY(dev_alloc_t(&bins, 256, st));
   cl.bufs.push_back(bins);
   QueryOrder ord;
-  CM_TRY(order_queries(ix, qd, nq, st, &ord));
+  CM_TRY(order_queries(ix, qd, nq, st, &ord, 1.0, CM_CYLINDER));
   CM_TRY(radius_count_dev(ix, qd, nq, CM_CYLINDER, 1.0, ord.perm, counts, nullptr, st));
   CM_TRY(density_histogram_dev(counts, nq, bins, st));
   unsigned long long hb[256];

@@ -96,7 +96,7 @@ struct QueryOrder {
   }
 };
 cm_status order_queries(const cm_index* ix, const double* q_dev, uint64_t nq, cudaStream_t st,
-                        QueryOrder* out);
+                        QueryOrder* out, double r = -1.0, int kind = 0);
 cm_status radius_count_dev(const cm_index* ix, const double* q_dev, uint64_t nq, int kernel,
                            double r, const uint32_t* perm, uint32_t* counts_dev,
                            uint64_t* tested_dev, cudaStream_t st);

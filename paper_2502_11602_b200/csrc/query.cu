@@ -92,15 +92,35 @@ struct Out {
   int no_wide;                    // diagnostics (CMGPU_NO_WIDE): wide tiles off
 };
 
-template <typename K>
+// Query order keys. RANGE = false: the centre's cell key, so a tile's 32
+// consecutive centres are spatial neighbours. RANGE = true (radii of at most
+// half a cell, where every clamped range spans 1 or 2 cells per axis): the
+// key of the range's low corner voxel, times 8, plus one bit per axis for a
+// 2-cell extent — centres with the same candidate voxels sort together, so
+// a tile's hull is the union of few distinct ranges (dense voxels holding
+// many centres, as near a TLS scanner, otherwise give every tile the whole
+// 3 x 3 x 3 neighbourhood).
+template <typename K, bool RANGE>
 __global__ void query_keys_kernel(const double* __restrict__ q, uint64_t nq, DevGrid g,
-                                  K* __restrict__ keys, uint32_t* __restrict__ vals) {
+                                  K* __restrict__ keys, uint32_t* __restrict__ vals, double r,
+                                  int kind) {
   for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < nq;
        p += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t i = axis_index(q[3 * p], g.ox, g.sx, g.nx);
-    const uint64_t j = axis_index(q[3 * p + 1], g.oy, g.sy, g.ny);
-    const uint64_t k = g.mode3d ? axis_index(q[3 * p + 2], g.oz, g.sz, g.nz) : 0;
-    keys[p] = (K)(i * (g.ny * g.nz) + j * g.nz + k);
+    const double cx = q[3 * p], cy = q[3 * p + 1], cz = q[3 * p + 2];
+    uint64_t i = axis_index(cx, g.ox, g.sx, g.nx);
+    uint64_t j = axis_index(cy, g.oy, g.sy, g.ny);
+    uint64_t k = g.mode3d ? axis_index(cz, g.oz, g.sz, g.nz) : 0;
+    uint64_t ext = 0;
+    if (RANGE) {
+      Range R;
+      if (clamped_range(g, cx, cy, cz, r, &R, kind)) {
+        i = R.i0, j = R.j0, k = R.k0;
+        ext = ((uint64_t)(R.i1 > R.i0) << 2) | ((uint64_t)(R.j1 > R.j0) << 1) |
+              (uint64_t)(R.k1 > R.k0);
+      }
+    }
+    const uint64_t cell = i * (g.ny * g.nz) + j * g.nz + k;
+    keys[p] = (K)(RANGE ? cell * 8 + ext : cell);
     vals[p] = (uint32_t)p;
   }
 }
@@ -1414,14 +1434,18 @@ __global__ void __launch_bounds__(kMidThreads) sort_mid_rows_kernel(
 
 template <typename K>
 cm_status order_typed(const cm_index* ix, const double* q, uint64_t nq, cudaStream_t st,
-                      uint32_t* perm) {
+                      uint32_t* perm, bool range, double r, int kind) {
   K* keys = nullptr;
   void* scratch = nullptr;
   CM_CUDA_TRY(dev_alloc_t(&keys, nq, st));
   CM_CUDA_TRY(dev_alloc(&scratch, radix_scratch_bytes<K>(nq), st));
   const unsigned grid = (unsigned)std::min<uint64_t>((nq + 255) / 256, (uint64_t)sm_count() * 16);
-  query_keys_kernel<K><<<std::max(1u, grid), 256, 0, st>>>(q, nq, ix->g, keys, perm); ::cmg::note_launch();
-  radix_sort_pairs<K>(keys, perm, nq, ix->key_bits, scratch, st);
+  if (range)
+    query_keys_kernel<K, true><<<std::max(1u, grid), 256, 0, st>>>(q, nq, ix->g, keys, perm, r, kind);
+  else
+    query_keys_kernel<K, false><<<std::max(1u, grid), 256, 0, st>>>(q, nq, ix->g, keys, perm, r, kind);
+  ::cmg::note_launch();
+  radix_sort_pairs<K>(keys, perm, nq, ix->key_bits + (range ? 3 : 0), scratch, st);
   dev_free(scratch, st);
   dev_free(keys, st);
   return CM_OK;
@@ -1505,13 +1529,21 @@ void query_stats(uint64_t* out, int reset) {
 }
 
 cm_status order_queries(const cm_index* ix, const double* q, uint64_t nq, cudaStream_t st,
-                        QueryOrder* out) {
+                        QueryOrder* out, double r, int kind) {
   out->nq = nq;
   out->st = st;
   if (nq == 0) return CM_OK;
   CM_CUDA_TRY(dev_alloc_t(&out->perm, nq, st));
-  return ix->V <= (1ull << 32) ? order_typed<uint32_t>(ix, q, nq, st, out->perm)
-                               : order_typed<uint64_t>(ix, q, nq, st, out->perm);
+  const DevGrid& g = ix->g;
+  auto fits = [&](double f) {  // f = 2: every clamped range spans at most 2 cells per axis
+    return r >= 0.0 && f * r <= g.sx && f * r <= g.sy &&
+           (!g.mode3d || kind == CM_CYLINDER || f * r <= g.sz);
+  };
+  // (2-bit extents for r <= cell, ranges of up to 3 cells, measured no gain at r = 1)
+  const bool range = fits(2.0);
+  const int bits = ix->key_bits + (range ? 3 : 0);
+  return bits <= 32 ? order_typed<uint32_t>(ix, q, nq, st, out->perm, range, r, kind)
+                    : order_typed<uint64_t>(ix, q, nq, st, out->perm, range, r, kind);
 }
 
 // Radii whose clamped ranges span more columns than a compact 32-column
