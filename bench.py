@@ -337,7 +337,7 @@ def main():
 
     phase = {k: round(mean_of(k), 4) for k in ("order_ms", "pass1_ms", "rowsort_ms", "scan_ms",
                                                 "pass2_ms")}
-    two_pass = any(k["two_pass"] for k in kern)
+    two_pass = any(k["two_pass"] == 1 for k in kern)
     phase["two_pass"] = bool(two_pass)
     dom = "pass1_ms"
     dom_ms = phase[dom]

@@ -124,7 +124,8 @@ typedef struct {
   double pass2_ms;    /* single pass: gather arena -> CSR; two-pass: fill */
   double total_ms;
   uint64_t nq, nnz;
-  int32_t two_pass;   /* 1 when the arena overflowed and count+fill ran */
+  int32_t two_pass;   /* 1: count + fill ran (large radius, or no arena); 2: the arena
+                         overflowed and the collect reran into one of the exact size */
 } cm_query_timing;
 
 typedef struct cm_index cm_index;

@@ -544,7 +544,7 @@ namespace {
 struct QueryEvents {
   cudaEvent_t e[6];
   uint64_t nq = 0, nnz = 0;
-  bool two_pass = false;
+  int two_pass = 0;  // 0 collect, 1 count + fill, 2 collect rerun (cm_query_timing)
   bool valid = false;
   QueryEvents() {
     for (auto& x : e) cudaEventCreate(&x);
@@ -578,7 +578,7 @@ cm_status cm_get_last_query_timing(cm_query_timing* o) {
   o->total_ms = tot;
   o->nq = ev.nq;
   o->nnz = ev.nnz;
-  o->two_pass = ev.two_pass ? 1 : 0;
+  o->two_pass = ev.two_pass;
   return CM_OK;
 }
 
@@ -702,7 +702,11 @@ static cm_status radius_search_core(const cm_index* ix, const double* qd, uint64
   // neighbours-per-query estimate; if the arena overflows, fall back to
   // count + scan + fill.
   // Large radii go count + scan + fill (wide tiles) + in-place row sort.
-  uint64_t cap = (uint64_t)((double)nq * ix->nnz_per_query * 1.05) + (1u << 20);
+  // An overflowing collect still counts every reservation, so the cursor
+  // then holds the exact arena size: the collect reruns once into an arena of
+  // that size (query subsets differ in density, e.g. the chunks of a
+  // host-buffer call over a cloud generated ground first, buildings last).
+  uint64_t cap = (uint64_t)((double)nq * ix->nnz_per_query * 1.25) + (1u << 20);
   bool two_pass = radius_is_wide(ix, r);
   if (!two_pass && dev_alloc_t(&temp, cap, st) != cudaSuccess) {
     two_pass = true;
@@ -710,6 +714,7 @@ static cm_status radius_search_core(const cm_index* ix, const double* qd, uint64
   }
   cm_status s = CM_OK;
   unsigned long long used = 0;
+  bool recollected = false;
   if (!two_pass) {
     s = radius_collect_dev(ix, qd, nq, kernel, r, ord.perm, temp, cap, toff, scnt, counts, cursor,
                            st, ev.e[2]);
@@ -719,9 +724,29 @@ static cm_status radius_search_core(const cm_index* ix, const double* qd, uint64
       set_error("arena cursor readback failed");
       return fail(CM_CUDA);
     }
-    if (nq) ix->nnz_per_query = std::max(1.0, (double)used / (double)nq);
-    two_pass = used > cap;
-    if (two_pass) {
+    // slow decay: alternating dense and sparse batches keep the larger size
+    if (nq)
+      ix->nnz_per_query = std::max({1.0, (double)used / (double)nq, 0.95 * ix->nnz_per_query});
+    if (used > cap && !std::getenv("CMGPU_NO_RECOLLECT")) {
+      dev_free(temp, st);
+      temp = nullptr;
+      cap = used;
+      if (dev_alloc_t(&temp, cap, st) == cudaSuccess) {
+        recollected = true;
+        s = radius_collect_dev(ix, qd, nq, kernel, r, ord.perm, temp, cap, toff, scnt, counts,
+                               cursor, st, ev.e[2]);
+        cudaEventRecord(ev.e[3], st);
+        if (s != CM_OK) return fail(s);
+        if (!read_u64_mapped(cursor, st, &used)) {
+          set_error("arena cursor readback failed");
+          return fail(CM_CUDA);
+        }
+      } else {
+        cudaGetLastError();
+      }
+    }
+    two_pass = used > cap || !temp;
+    if (two_pass && temp) {
       dev_free(temp, st);
       temp = nullptr;
     }
@@ -758,7 +783,7 @@ static cm_status radius_search_core(const cm_index* ix, const double* qd, uint64
   if (s != CM_OK) return fail(s);
   ev.nq = nq;
   ev.nnz = csr->nnz;
-  ev.two_pass = two_pass;
+  ev.two_pass = two_pass ? 1 : recollected ? 2 : 0;
   ev.valid = true;
   release();
   return CM_OK;
@@ -803,7 +828,9 @@ struct StreamingGather : GatherHook {
   cudaStream_t out = nullptr;
   uint64_t* row_ptr_host = nullptr;
   uint32_t* cols_host = nullptr;
-  uint64_t cap = 0;
+  uint64_t cap = 0;        // columns the host buffer still holds
+  bool rows_early = true;  // copy the row pointers before the columns (chunk 0 only:
+                           // later chunks' rows need the running offset first)
   bool copied = false, over = false;
   uint64_t nnz = 0;
   cm_status run(const uint32_t* temp, const uint64_t* toff, const uint32_t* scnt,
@@ -824,9 +851,11 @@ struct StreamingGather : GatherHook {
     }
     nnz = rp[G];
     over = nnz > cap;
-    cudaEventRecord(evs.e[G], st);
-    cudaStreamWaitEvent(out, evs.e[G], 0);
-    CM_CUDA_TRY(cudaMemcpyAsync(row_ptr_host + 1, row_ptr + 1, nq * 8, cudaMemcpyDeviceToHost, out));
+    if (rows_early) {
+      cudaEventRecord(evs.e[G], st);
+      cudaStreamWaitEvent(out, evs.e[G], 0);
+      CM_CUDA_TRY(cudaMemcpyAsync(row_ptr_host + 1, row_ptr + 1, nq * 8, cudaMemcpyDeviceToHost, out));
+    }
     for (int k = 0; k < G; ++k) {
       if (qb[k + 1] == qb[k]) continue;
       CM_TRY(gather_rows_dev(temp, toff + qb[k], scnt + qb[k], row_ptr + qb[k], perm, cols,
@@ -867,15 +896,22 @@ cm_status cm_radius_search_to_host(const cm_index* ix, const double* q_host, uin
     }
   };
   thread_local Streams ss;
-  // Chunks pay off only when consecutive queries are spatially coherent
-  // (e.g. scan-ordered LiDAR centres): the query tiles are formed within a
-  // chunk, so a chunk of a random-order batch is a sparse sample whose tiles
-  // fall back to one query per warp. Default: one chunk.
-  uint64_t nchunks = 1;
+  // Every chunk's CSR streams to the host while its gather runs, and chunk
+  // i+1's input copy and kernels overlap chunk i's columns on PCIe, which
+  // bounds the call (~54 GB/s device->host vs ~1 G queries/s of kernels).
+  // Query tiles form within a chunk, so a chunk is a sparser sample of the
+  // batch (config 1: 5M-query chunks run ~25 % slower per query, hidden
+  // behind the copy). 4 chunks of >= 4M queries measured best (config 1:
+  // 88 -> 74 ms per call); CMGPU_CHUNKS overrides.
+  uint64_t nchunks = std::min<uint64_t>(4, std::max<uint64_t>(1, nq / (4u << 20)));
   if (const char* ev = std::getenv("CMGPU_CHUNKS")) nchunks = std::max<uint64_t>(1, std::strtoull(ev, nullptr, 10));
   const uint64_t chunk = (nq + nchunks - 1) / std::max<uint64_t>(nchunks, 1);
   double* qbuf[2] = {nullptr, nullptr};
   cudaEvent_t in_done[2], comp_done[2], out_done[2];
+  // CMGPU_TRACE: device timeline per chunk (core start / core end on the
+  // compute stream, copies done on the output stream), relative to t_ev[0]
+  constexpr int kTraceChunks = 16;
+  cudaEvent_t t_ev[1 + 3 * kTraceChunks] = {};
   for (int i = 0; i < 2; ++i) {
     cudaEventCreateWithFlags(&in_done[i], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&comp_done[i], cudaEventDisableTiming);
@@ -895,8 +931,15 @@ cm_status cm_radius_search_to_host(const cm_index* ix, const double* q_host, uin
     cudaMemcpyAsync(qbuf[bi], q_host + 3 * q0, n * 24, cudaMemcpyHostToDevice, ss.in);
     cudaEventRecord(in_done[bi], ss.in);
   };
-  if (s == CM_OK && nq) issue_in(0);
   static const bool trace = std::getenv("CMGPU_TRACE") != nullptr;
+  if (trace) {
+    for (auto& e : t_ev) cudaEventCreate(&e);
+    cudaEventRecord(t_ev[0], st);
+  }
+  auto mark = [&](uint64_t c, int what, cudaStream_t on) {
+    if (trace && c < (uint64_t)kTraceChunks) cudaEventRecord(t_ev[1 + 3 * c + what], on);
+  };
+  if (s == CM_OK && nq) issue_in(0);
   auto t0 = std::chrono::steady_clock::now();
   auto tr = [&](const char* what, uint64_t c) {
     if (trace)
@@ -908,6 +951,7 @@ cm_status cm_radius_search_to_host(const cm_index* ix, const double* q_host, uin
     const uint64_t q0 = c * chunk, n = std::min(chunk, nq - q0);
     const int bi = (int)(c & 1);
     tr("start", c);
+    mark(c, 0, ss.in);  // after this chunk's input copy was issued
     if ((c + 1) * chunk < nq) issue_in(c + 1);
     cudaStreamWaitEvent(st, in_done[bi], 0);
     cudaStreamWaitEvent(st, out_done[bi], 0);  // csrs[bi] no longer being copied
@@ -920,11 +964,13 @@ cm_status cm_radius_search_to_host(const cm_index* ix, const double* q_host, uin
     csrs[bi].device = ix->device;
     StreamingGather sg;
     sg.out = ss.out;
-    sg.row_ptr_host = row_ptr_host;
-    sg.cols_host = cols_host;
-    sg.cap = cols_capacity;
-    s = radius_search_core(ix, qbuf[bi], n, kernel, r, st, &csrs[bi], nchunks == 1 ? &sg : nullptr);
+    sg.row_ptr_host = row_ptr_host + q0;
+    sg.cols_host = cols_host + (full ? 0 : base);
+    sg.cap = full || base > cols_capacity ? 0 : cols_capacity - base;
+    sg.rows_early = base == 0;
+    s = radius_search_core(ix, qbuf[bi], n, kernel, r, st, &csrs[bi], &sg);
     tr("core returned", c);
+    mark(c, 1, st);
     if (trace) {
       cm_query_timing qt;
       cm_get_last_query_timing(&qt);
@@ -937,22 +983,24 @@ cm_status cm_radius_search_to_host(const cm_index* ix, const double* q_host, uin
           csrs[bi].row_ptr + 1, n, base); ::cmg::note_launch();
     }
     cudaEventRecord(comp_done[bi], st);
-    if (sg.copied) {  // streamed during the gather
+    if (sg.copied) {  // columns streamed during the gather
       full = full || sg.over;
+      if (!sg.rows_early) {
+        cudaStreamWaitEvent(ss.out, comp_done[bi], 0);
+        cudaMemcpyAsync(row_ptr_host + q0 + 1, csrs[bi].row_ptr + 1, n * 8, cudaMemcpyDeviceToHost,
+                        ss.out);
+      }
       cudaEventRecord(out_done[bi], ss.out);
+      mark(c, 2, ss.out);
       base += csrs[bi].nnz;
       continue;
     }
-    if (full || base + csrs[bi].nnz > cols_capacity) {
-      base += csrs[bi].nnz;  // keep counting; report the size needed
-      full = true;
-      continue;
-    }
-    // rows of this chunk: shift by `base` on the host after the copy
+    full = full || base + csrs[bi].nnz > cols_capacity;  // keep counting: report the size needed
+    // rows of this chunk (already offset by `base` on the device)
     cudaStreamWaitEvent(ss.out, comp_done[bi], 0);
     cudaMemcpyAsync(row_ptr_host + q0 + 1, csrs[bi].row_ptr + 1, n * 8, cudaMemcpyDeviceToHost,
                     ss.out);
-    if (csrs[bi].nnz)
+    if (csrs[bi].nnz && !full)
       cudaMemcpyAsync(cols_host + base, csrs[bi].cols, csrs[bi].nnz * 4, cudaMemcpyDeviceToHost,
                       ss.out);
     cudaEventRecord(out_done[bi], ss.out);
@@ -961,6 +1009,18 @@ cm_status cm_radius_search_to_host(const cm_index* ix, const double* q_host, uin
   cudaStreamSynchronize(ss.out);
   cudaStreamSynchronize(st);
   tr("all done", 0);
+  if (trace) {
+    for (uint64_t c = 0; c < std::min<uint64_t>((nq + chunk - 1) / std::max<uint64_t>(chunk, 1), kTraceChunks); ++c) {
+      float a = -1, b = -1, d = -1;
+      cudaEventElapsedTime(&a, t_ev[0], t_ev[1 + 3 * c]);
+      cudaEventElapsedTime(&b, t_ev[0], t_ev[1 + 3 * c + 1]);
+      cudaEventElapsedTime(&d, t_ev[0], t_ev[1 + 3 * c + 2]);
+      std::fprintf(stderr, "[to_host dev] chunk %lu: input issued %.2f  core done %.2f  copies done %.2f ms\n",
+                   (unsigned long)c, a, b, d);
+    }
+    cudaGetLastError();
+    for (auto& e : t_ev) cudaEventDestroy(e);
+  }
   *nnz_out = base;
   if (s == CM_OK && full) s = CM_CAPACITY;
   if (s == CM_CAPACITY) {

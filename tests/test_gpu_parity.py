@@ -105,16 +105,21 @@ def test_corruption_detected(cfg0, cfg0_oracle):
         assert not (np.array_equal(cnt, ocnt) and np.array_equal(dig, odig))
 
 
-def test_arena_overflow_falls_back(cfg0, cfg0_oracle):
+@pytest.mark.parametrize("recollect", [True, False])
+def test_arena_overflow_falls_back(cfg0, cfg0_oracle, monkeypatch, recollect):
     """A small-radius call shrinks the arena estimate; the next, larger query
-    overflows it and must take the two-pass path with identical results."""
+    overflows it and must rerun the collect into an arena of the exact size
+    (or, with CMGPU_NO_RECOLLECT, take count + fill) with identical results."""
     from paper_2502_11602_b200 import _native
+    if not recollect:
+        monkeypatch.setenv("CMGPU_NO_RECOLLECT", "1")
     cloud, q = cfg0
     q = q[:60000]
     m = cm.Cheesemap.build(cloud, cm.BuildOptions(flavor=cm.Flavor.Mixed))
-    cm.radius_search_batch(m, q, 0.05, cm.SPHERE)
+    for _ in range(90):  # the estimate decays by 0.95 per call
+        cm.radius_search_batch(m, q[:1000], 0.05, cm.SPHERE)
     row, cols = cm.radius_search_batch(m, q, 1.4, cm.SPHERE)
-    assert _native.last_query_timing()["two_pass"] == 1
+    assert _native.last_query_timing()["two_pass"] == (2 if recollect else 1)
     orow, ocols = cfg0_oracle.radius_csr(q, 0, 1.4)
     assert np.array_equal(row, orow) and np.array_equal(cols, ocols)
     row, cols = cm.radius_search_batch(m, q, 1.4, cm.SPHERE)
@@ -188,22 +193,27 @@ def test_count_then_fill_api(cfg0, cfg0_oracle, flavor, r):
     assert np.array_equal(row, orow) and np.array_equal(cols, ocols)
 
 
-def test_search_to_host_pipeline(cfg0, cfg0_oracle):
-    """cm_radius_search_to_host (chunked host<->device overlap) returns the
-    same CSR; a too-small capacity reports CM_CAPACITY and the size needed."""
+@pytest.mark.parametrize("chunks,r", [(None, 1.0), ("3", 1.0), ("8", 1.0), ("3", 2.5)])
+def test_search_to_host_pipeline(cfg0, cfg0_oracle, monkeypatch, chunks, r):
+    """cm_radius_search_to_host (chunked host<->device overlap, every chunk's
+    CSR streamed during its gather) returns the same CSR; a too-small capacity
+    (before or in the middle of the chunks) reports CM_CAPACITY and the size
+    needed."""
     import ctypes
     import torch
     from paper_2502_11602_b200 import _native
+    if chunks:
+        monkeypatch.setenv("CMGPU_CHUNKS", chunks)
     cloud, _ = cfg0
-    q = np.ascontiguousarray(cloud[:600_000])  # 8 chunks
+    q = np.ascontiguousarray(cloud[:600_000 if r < 2 else 100_000])
     m = cm.Cheesemap.build(cloud, cm.BuildOptions(flavor=cm.Flavor.Mixed))
-    orow, ocols = cfg0_oracle.radius_csr(q, 0, 1.0)
+    orow, ocols = cfg0_oracle.radius_csr(q, 0, r)
     qh = torch.from_numpy(q).pin_memory()
     row = torch.zeros(q.shape[0] + 1, dtype=torch.int64).pin_memory()
     cols = torch.zeros(len(ocols), dtype=torch.int32).pin_memory()
     nnz = ctypes.c_uint64()
     L = _native.lib()
-    rc = L.cm_radius_search_to_host(m.handle, ctypes.c_void_p(qh.data_ptr()), q.shape[0], 0, 1.0,
+    rc = L.cm_radius_search_to_host(m.handle, ctypes.c_void_p(qh.data_ptr()), q.shape[0], 0, r,
                                     ctypes.c_void_p(row.data_ptr()),
                                     ctypes.c_void_p(cols.data_ptr()), cols.numel(),
                                     ctypes.byref(nnz), None)
@@ -212,7 +222,14 @@ def test_search_to_host_pipeline(cfg0, cfg0_oracle):
     assert np.array_equal(cols.numpy().astype(np.uint32), ocols)
     small = np.zeros(10, dtype=np.uint32)
     rc = L.cm_radius_search_to_host(m.handle, q.ctypes.data_as(ctypes.c_void_p), q.shape[0], 0,
-                                    1.0, ctypes.c_void_p(row.data_ptr()),
+                                    r, ctypes.c_void_p(row.data_ptr()),
                                     small.ctypes.data_as(ctypes.c_void_p), 10, ctypes.byref(nnz),
                                     None)
     assert rc == 3 and nnz.value == len(ocols)
+    half = torch.zeros(len(ocols) // 2, dtype=torch.int32).pin_memory()
+    rc = L.cm_radius_search_to_host(m.handle, ctypes.c_void_p(qh.data_ptr()), q.shape[0], 0, r,
+                                    ctypes.c_void_p(row.data_ptr()),
+                                    ctypes.c_void_p(half.data_ptr()), half.numel(),
+                                    ctypes.byref(nnz), None)
+    assert rc == 3 and nnz.value == len(ocols)
+    assert np.array_equal(row.numpy().astype(np.uint64), orow)  # row pointers still complete
