@@ -873,9 +873,9 @@ struct StreamingGather : GatherHook {
 };
 }  // namespace
 
-// Host-buffer pipeline: queries in chunks; chunk i+1's host->device copy and
-// chunk i-1's device->host copy of its CSR overlap chunk i's kernels (three
-// streams). row_ptr_host gets nq + 1 entries, cols_host up to cols_capacity.
+// Host-buffer pipeline: queries in chunks (three streams): all input copies
+// are issued up front, and chunk i's CSR copy to the host overlaps its own
+// gather and chunk i+1's kernels. row_ptr_host gets nq + 1 entries, cols_host up to cols_capacity.
 cm_status cm_radius_search_to_host(const cm_index* ix, const double* q_host, uint64_t nq,
                                    int kernel, double r, uint64_t* row_ptr_host,
                                    uint32_t* cols_host, uint64_t cols_capacity, uint64_t* nnz_out,
@@ -905,32 +905,30 @@ cm_status cm_radius_search_to_host(const cm_index* ix, const double* q_host, uin
   // 88 -> 74 ms per call); CMGPU_CHUNKS overrides.
   uint64_t nchunks = std::min<uint64_t>(4, std::max<uint64_t>(1, nq / (4u << 20)));
   if (const char* ev = std::getenv("CMGPU_CHUNKS")) nchunks = std::max<uint64_t>(1, std::strtoull(ev, nullptr, 10));
-  const uint64_t chunk = (nq + nchunks - 1) / std::max<uint64_t>(nchunks, 1);
-  double* qbuf[2] = {nullptr, nullptr};
-  cudaEvent_t in_done[2], comp_done[2], out_done[2];
+  // Chunk boundaries: the first chunk is half the size of the others, so the
+  // first columns reach PCIe sooner.
+  std::vector<uint64_t> qb(nchunks + 1);
+  for (uint64_t c = 0; c <= nchunks; ++c)
+    qb[c] = c == 0 ? 0 : (uint64_t)((double)nq * (2.0 * c - 1.0) / (2.0 * nchunks - 1.0));
+  qb[nchunks] = nq;
+  double* qdev = nullptr;  // every chunk's input copy is issued up front
+  std::vector<cudaEvent_t> in_done(nchunks);
+  cudaEvent_t comp_done[2], out_done[2];
   // CMGPU_TRACE: device timeline per chunk (core start / core end on the
   // compute stream, copies done on the output stream), relative to t_ev[0]
   constexpr int kTraceChunks = 16;
   cudaEvent_t t_ev[1 + 3 * kTraceChunks] = {};
+  for (auto& e : in_done) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
   for (int i = 0; i < 2; ++i) {
-    cudaEventCreateWithFlags(&in_done[i], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&comp_done[i], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&out_done[i], cudaEventDisableTiming);
   }
   cm_csr csrs[2];
   cm_status s = CM_OK;
-  for (int i = 0; i < 2 && nq; ++i)
-    if (dev_alloc_t(&qbuf[i], chunk * 3, ss.in) != cudaSuccess) s = CM_CUDA;
+  if (nq && dev_alloc_t(&qdev, nq * 3, ss.in) != cudaSuccess) s = CM_CUDA;
   uint64_t base = 0;
   bool full = false;
   row_ptr_host[0] = 0;
-  auto issue_in = [&](uint64_t c) {
-    const uint64_t q0 = c * chunk, n = std::min(chunk, nq - q0);
-    const int bi = (int)(c & 1);
-    cudaStreamWaitEvent(ss.in, comp_done[bi], 0);  // buffer reuse
-    cudaMemcpyAsync(qbuf[bi], q_host + 3 * q0, n * 24, cudaMemcpyHostToDevice, ss.in);
-    cudaEventRecord(in_done[bi], ss.in);
-  };
   static const bool trace = std::getenv("CMGPU_TRACE") != nullptr;
   if (trace) {
     for (auto& e : t_ev) cudaEventCreate(&e);
@@ -939,7 +937,13 @@ cm_status cm_radius_search_to_host(const cm_index* ix, const double* q_host, uin
   auto mark = [&](uint64_t c, int what, cudaStream_t on) {
     if (trace && c < (uint64_t)kTraceChunks) cudaEventRecord(t_ev[1 + 3 * c + what], on);
   };
-  if (s == CM_OK && nq) issue_in(0);
+  if (trace) cudaStreamWaitEvent(ss.in, t_ev[0], 0);
+  for (uint64_t c = 0; s == CM_OK && c < nchunks; ++c) {
+    cudaMemcpyAsync(qdev + 3 * qb[c], q_host + 3 * qb[c], (qb[c + 1] - qb[c]) * 24,
+                    cudaMemcpyHostToDevice, ss.in);
+    cudaEventRecord(in_done[c], ss.in);
+    mark(c, 0, ss.in);
+  }
   auto t0 = std::chrono::steady_clock::now();
   auto tr = [&](const char* what, uint64_t c) {
     if (trace)
@@ -947,13 +951,12 @@ cm_status cm_radius_search_to_host(const cm_index* ix, const double* q_host, uin
                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(),
                    (unsigned long)c, what);
   };
-  for (uint64_t c = 0; s == CM_OK && c * chunk < nq; ++c) {
-    const uint64_t q0 = c * chunk, n = std::min(chunk, nq - q0);
+  for (uint64_t c = 0; s == CM_OK && c < nchunks; ++c) {
+    const uint64_t q0 = qb[c], n = qb[c + 1] - qb[c];
     const int bi = (int)(c & 1);
+    if (n == 0) continue;
     tr("start", c);
-    mark(c, 0, ss.in);  // after this chunk's input copy was issued
-    if ((c + 1) * chunk < nq) issue_in(c + 1);
-    cudaStreamWaitEvent(st, in_done[bi], 0);
+    cudaStreamWaitEvent(st, in_done[c], 0);
     cudaStreamWaitEvent(st, out_done[bi], 0);  // csrs[bi] no longer being copied
     if (csrs[bi].row_ptr) {
       dev_free(csrs[bi].row_ptr, st);
@@ -968,7 +971,7 @@ cm_status cm_radius_search_to_host(const cm_index* ix, const double* q_host, uin
     sg.cols_host = cols_host + (full ? 0 : base);
     sg.cap = full || base > cols_capacity ? 0 : cols_capacity - base;
     sg.rows_early = base == 0;
-    s = radius_search_core(ix, qbuf[bi], n, kernel, r, st, &csrs[bi], &sg);
+    s = radius_search_core(ix, qdev + 3 * q0, n, kernel, r, st, &csrs[bi], &sg);
     tr("core returned", c);
     mark(c, 1, st);
     if (trace) {
@@ -1010,12 +1013,12 @@ cm_status cm_radius_search_to_host(const cm_index* ix, const double* q_host, uin
   cudaStreamSynchronize(st);
   tr("all done", 0);
   if (trace) {
-    for (uint64_t c = 0; c < std::min<uint64_t>((nq + chunk - 1) / std::max<uint64_t>(chunk, 1), kTraceChunks); ++c) {
+    for (uint64_t c = 0; c < std::min<uint64_t>(nchunks, kTraceChunks); ++c) {
       float a = -1, b = -1, d = -1;
       cudaEventElapsedTime(&a, t_ev[0], t_ev[1 + 3 * c]);
       cudaEventElapsedTime(&b, t_ev[0], t_ev[1 + 3 * c + 1]);
       cudaEventElapsedTime(&d, t_ev[0], t_ev[1 + 3 * c + 2]);
-      std::fprintf(stderr, "[to_host dev] chunk %lu: input issued %.2f  core done %.2f  copies done %.2f ms\n",
+      std::fprintf(stderr, "[to_host dev] chunk %lu: input copied %.2f  core done %.2f  copies done %.2f ms\n",
                    (unsigned long)c, a, b, d);
     }
     cudaGetLastError();
@@ -1026,11 +1029,14 @@ cm_status cm_radius_search_to_host(const cm_index* ix, const double* q_host, uin
   if (s == CM_CAPACITY) {
     set_error("cols_capacity too small; *nnz_out holds the size needed");
   }
+  for (auto& e : in_done) {
+    cudaStreamWaitEvent(st, e, 0);  // an early exit may leave input copies in flight
+    cudaEventDestroy(e);
+  }
+  if (qdev) dev_free(qdev, st);
   for (int i = 0; i < 2; ++i) {
     if (csrs[i].row_ptr) dev_free(csrs[i].row_ptr, st);
     if (csrs[i].cols) dev_free(csrs[i].cols, st);
-    if (qbuf[i]) dev_free(qbuf[i], st);
-    cudaEventDestroy(in_done[i]);
     cudaEventDestroy(comp_done[i]);
     cudaEventDestroy(out_done[i]);
   }
