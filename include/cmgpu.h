@@ -201,6 +201,13 @@ cm_status cm_csr_info(const cm_csr* csr, uint64_t* nq, uint64_t* nnz,
 cm_status cm_csr_download(const cm_csr* csr, uint64_t* row_ptr, uint32_t* cols,
                           void* stream);
 cm_status cm_csr_free(cm_csr* csr);
+/* Verification of a CSR in DEVICE memory: per-row count and digest exactly
+ * as cm_radius_digest reports them (either output may be null), and the
+ * number of rows that are not strictly ascending (host *unsorted_rows).
+ * Synchronous. */
+cm_status cm_csr_digest(const uint64_t* row_ptr, const uint32_t* cols, uint64_t nq,
+                        uint32_t* counts, uint64_t* digests, uint64_t* unsorted_rows,
+                        void* stream);
 /* Per-query count and set digest sum(mix64(handle)) mod 2^64 (splitmix64
  * finaliser) — verification of outputs too large to materialise. */
 cm_status cm_radius_digest(const cm_index* index, const double* q, uint64_t nq,

@@ -15,7 +15,7 @@ STATUS_NAMES = {0: "CM_OK", 1: "CM_EMPTY_CLOUD", 2: "CM_INVALID_ARGUMENT", 3: "C
 EXPORTS = [
     "cm_default_options", "cm_build", "cm_build_in_bounds", "cm_free", "cm_get_grid", "cm_get_occupancy",
     "cm_get_build_timing", "cm_export_voxels", "cm_size", "cm_radius_count", "cm_radius_fill",
-    "cm_radius_search", "cm_radius_search_to_host", "cm_csr_info", "cm_csr_download", "cm_csr_free", "cm_radius_digest",
+    "cm_radius_search", "cm_radius_search_to_host", "cm_csr_info", "cm_csr_download", "cm_csr_free", "cm_csr_digest", "cm_radius_digest",
     "cm_knn", "cm_corrupt_for_testing", "cm_last_error", "cm_status_name",
     "cm_get_last_query_timing", "cm_launch_count", "cm_debug_query_stats", "cm_debug_pool_bytes",
     "cm_global_density", "cm_weighted_density", "cm_las_parse_header", "cm_las_decode",
@@ -109,6 +109,7 @@ def lib():
                          ctypes.POINTER(p)], i32),
         "cm_csr_download": ([p, p, p, p], i32),
         "cm_csr_free": ([p], i32),
+        "cm_csr_digest": ([p, p, u64, p, p, ctypes.POINTER(u64), p], i32),
         "cm_radius_search_to_host": ([p, p, u64, i32, dbl, p, p, u64, ctypes.POINTER(u64), p], i32),
         "cm_radius_digest": ([p, p, u64, i32, dbl, p, p, p], i32),
         "cm_knn": ([p, p, u64, u32, p, p, p], i32),

@@ -1108,6 +1108,29 @@ cm_status cm_radius_digest(const cm_index* ix, const double* q, uint64_t nq, int
   return sync_if(c.host() || d.host(), st);
 }
 
+// Verification of a device CSR (row_ptr, cols in device memory): per-row
+// count and digest as cm_radius_digest reports them, and the number of rows
+// that are not strictly ascending (to *unsorted_rows, host memory).
+cm_status cm_csr_digest(const uint64_t* row_ptr, const uint32_t* cols, uint64_t nq,
+                        uint32_t* counts, uint64_t* digests, uint64_t* unsorted_rows,
+                        void* stream) {
+  if (!row_ptr || (nq && !cols) || !unsorted_rows) {
+    set_error("null CSR or output pointer");
+    return CM_INVALID_ARGUMENT;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  unsigned long long* dbad = nullptr;
+  CM_CUDA_TRY(cudaMallocAsync(&dbad, 8, st));
+  cm_status s = csr_digest_dev(row_ptr, cols, nq, counts, digests, dbad, st);
+  unsigned long long h = 0;
+  if (s == CM_OK && cudaMemcpyAsync(&h, dbad, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+    s = CM_CUDA;
+  cudaFreeAsync(dbad, st);
+  if (s == CM_OK && cudaStreamSynchronize(st) != cudaSuccess) s = CM_CUDA;
+  *unsorted_rows = h;
+  return s;
+}
+
 // brute_radius (baseline.hpp:11-21) on the device: (count, digest) per centre.
 cm_status cm_brute_radius(const double* xyz, uint64_t n, const double* q, uint64_t nq, int kernel,
                           double r, uint32_t* counts, uint64_t* digests, int device, void* stream) {

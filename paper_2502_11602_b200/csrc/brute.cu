@@ -128,7 +128,47 @@ __global__ void __launch_bounds__(kBruteThreads) brute_knn_kernel(
   }
 }
 
+// One warp per CSR row: count, Σ splitmix64(handle) (the cm_radius_digest
+// digest) and whether the row is strictly ascending.
+__global__ void __launch_bounds__(256) csr_digest_kernel(const uint64_t* __restrict__ row_ptr,
+                                                         const uint32_t* __restrict__ cols,
+                                                         uint64_t nq, uint32_t* __restrict__ counts,
+                                                         uint64_t* __restrict__ digests,
+                                                         unsigned long long* __restrict__ unsorted) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t W = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t q = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); q < nq; q += W) {
+    const uint64_t b = row_ptr[q], e = row_ptr[q + 1];
+    uint64_t dig = 0;
+    bool bad = e < b;
+    for (uint64_t i = b + lane; i < e; i += 32) {
+      const uint32_t v = cols[i];
+      dig += mix64(v);
+      if (i > b && cols[i - 1] >= v) bad = true;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dig += __shfl_xor_sync(0xffffffffu, dig, o);
+    bad = __any_sync(0xffffffffu, bad);
+    if (lane == 0) {
+      if (counts) counts[q] = (uint32_t)(e - b);
+      if (digests) digests[q] = dig;
+      if (bad) atomicAdd(unsorted, 1ull);
+    }
+  }
+}
+
 }  // namespace
+
+cm_status csr_digest_dev(const uint64_t* row_ptr, const uint32_t* cols, uint64_t nq,
+                         uint32_t* counts, uint64_t* digests, unsigned long long* unsorted,
+                         cudaStream_t st) {
+  CM_CUDA_TRY(cudaMemsetAsync(unsorted, 0, 8, st));
+  if (nq == 0) return CM_OK;
+  const unsigned grid = (unsigned)std::min<uint64_t>((nq + 7) / 8, (uint64_t)sm_count() * 16);
+  csr_digest_kernel<<<grid, 256, 0, st>>>(row_ptr, cols, nq, counts, digests, unsorted); note_launch();
+  CM_CUDA_TRY(cudaGetLastError());
+  return CM_OK;
+}
 
 cm_status brute_radius_dev(const double* xyz, uint64_t n, const double* q, uint64_t nq, int kind,
                            double r, uint32_t* counts, uint64_t* digests, cudaStream_t st) {

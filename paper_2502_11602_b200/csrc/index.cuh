@@ -103,6 +103,9 @@ cm_status radius_count_dev(const cm_index* ix, const double* q_dev, uint64_t nq,
 bool radius_is_wide(const cm_index* ix, double r);
 // brute-force baselines (brute.cu): every point against every centre
 constexpr int kBruteKMax = 64;
+cm_status csr_digest_dev(const uint64_t* row_ptr, const uint32_t* cols, uint64_t nq,
+                         uint32_t* counts, uint64_t* digests, unsigned long long* unsorted,
+                         cudaStream_t st);
 cm_status brute_radius_dev(const double* xyz, uint64_t n, const double* q, uint64_t nq, int kind,
                            double r, uint32_t* counts, uint64_t* digests, cudaStream_t st);
 cm_status brute_knn_dev(const double* xyz, uint64_t n, const double* q, uint64_t nq, uint32_t k,

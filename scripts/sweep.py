@@ -68,7 +68,7 @@ def digest_case(m, qd, qh_sample, oracle, kernel, r, n_sample):
                 verified_sample=n_sample, parity=ok)
 
 
-def radius_case(m, qd, qh_sample, oracle, kernel, r, n_sample):
+def radius_case(m, qd, qh_sample, oracle, kernel, r, n_sample, check_all=True):
     if r >= 5.0:
         qd = qd[: qd.shape[0] // 10]  # keep the CSR (4 B x ~1000-1800 x nq) in memory
     nq = qd.shape[0]
@@ -83,8 +83,28 @@ def radius_case(m, qd, qh_sample, oracle, kernel, r, n_sample):
     for _ in range(2):  # warm
         L.cm_csr_free(run())
     ms, csr = timed(run, release=L.cm_csr_free)
-    L.cm_csr_free(csr)
     t = _native.last_query_timing()
+    # the timed CSR itself, every row: sorted, and (count, digest) equal to
+    # the digest pass's (which the oracle checks on the sample below)
+    full_ok = None
+    if check_all:
+        rp, cp = ctypes.c_void_p(), ctypes.c_void_p()
+        cm._check(L.cm_csr_info(csr, None, None, ctypes.byref(rp), ctypes.byref(cp)))
+        c1 = torch.empty(nq, dtype=torch.int32, device="cuda")
+        d1 = torch.empty(nq, dtype=torch.int64, device="cuda")
+        bad = ctypes.c_uint64()
+        cm._check(L.cm_csr_digest(rp, cp, nq, ctypes.c_void_p(c1.data_ptr()),
+                                  ctypes.c_void_p(d1.data_ptr()), ctypes.byref(bad), None))
+        L.cm_csr_free(csr)
+        c2 = torch.empty_like(c1)
+        d2 = torch.empty_like(d1)
+        cm._check(L.cm_radius_digest(m.handle, ctypes.c_void_p(qd.data_ptr()), nq, kernel, r,
+                                     ctypes.c_void_p(c2.data_ptr()),
+                                     ctypes.c_void_p(d2.data_ptr()), None))
+        full_ok = bool(bad.value == 0 and torch.equal(c1, c2) and torch.equal(d1, d2))
+        del c1, d1, c2, d2
+    else:
+        L.cm_csr_free(csr)
     # verification on a sample: counts + digests vs the oracle
     cnt, dig = cm.radius_digest_batch(m, qh_sample, r, kernel)
     ocnt, odig = oracle.radius(qh_sample, kernel, r)
@@ -99,7 +119,7 @@ def radius_case(m, qd, qh_sample, oracle, kernel, r, n_sample):
                 qps=nq / (ms * 1e-3), nnz=int(t["nnz"]), two_pass=int(t["two_pass"]),
                 phases={k: round(t[k], 3) for k in ("order_ms", "pass1_ms", "scan_ms", "pass2_ms")},
                 alg_gb=round(alg / 1e9, 2), frac_pass1=round(alg / (t["pass1_ms"] * 1e-3) / 6542.1e9, 3),
-                verified_sample=n_sample, parity=ok)
+                verified_sample=n_sample, parity=ok, csr_all_rows_ok=full_ok)
 
 
 def knn_case(m, qd, qh_sample, oracle, k):
@@ -124,6 +144,9 @@ def main():
     ap.add_argument("--configs", default="0,1,2,3")
     ap.add_argument("--sample", type=int, default=1000)
     ap.add_argument("--scale", type=float, default=1.0)
+    ap.add_argument("--flavors", default=None, help="subset, e.g. mixed")
+    ap.add_argument("--radii", default=None, help="subset, e.g. 2.5,5")
+    ap.add_argument("--kernels", default=None, help="subset, e.g. 0")
     a = ap.parse_args()
     out = {"gpu": torch.cuda.get_device_name(0), "results": []}
     cfgs = [int(c) for c in a.configs.split(",")]
@@ -145,7 +168,13 @@ def main():
         q = synth.config_queries(c, cloud)
         log(f"config {c}: {cloud.shape[0]} points, {q.shape[0]} queries "
             f"({time.perf_counter() - t0:.1f}s)")
-        p = plan[c]
+        p = dict(plan[c])
+        if a.flavors:
+            p["flavors"] = [f for f in p["flavors"] if f in a.flavors.split(",")]
+        if a.radii:
+            p["radii"] = [r for r in p["radii"] if r in [float(x) for x in a.radii.split(",")]]
+        if a.kernels:
+            p["kernels"] = [k for k in p["kernels"] if k in [int(x) for x in a.kernels.split(",")]]
         dc = torch.from_numpy(cloud).cuda()
         qd = torch.from_numpy(np.ascontiguousarray(q)).cuda()
         rng = np.random.default_rng(c)
@@ -166,7 +195,7 @@ def main():
                           else radius_case)
                     res = fn(m, qd, samp, oracle, kern, r, samp.shape[0])
                     log(f"  cfg{c} {f} {res['kernel']} r={r}: {res['qps'] / 1e6:.1f} M q/s "
-                        f"parity={res['parity']} phases={res.get('phases', res.get('mode'))}")
+                        f"parity={res['parity']} all_rows={res.get('csr_all_rows_ok')} phases={res.get('phases', res.get('mode'))}")
                     entry["radius"].append(res)
             for k in p["ks"]:
                 res = knn_case(m, qd, samp, oracle, k)

@@ -233,3 +233,60 @@ def test_search_to_host_pipeline(cfg0, cfg0_oracle, monkeypatch, chunks, r):
                                     ctypes.byref(nnz), None)
     assert rc == 3 and nnz.value == len(ocols)
     assert np.array_equal(row.numpy().astype(np.uint64), orow)  # row pointers still complete
+
+
+@pytest.mark.parametrize("order", ["cells", "x"])
+def test_wide_radius_clustered_handles(cfg0, cfg0_oracle, order):
+    """Wide-fill rows whose handles are clustered (a cloud stored in cell or x
+    order): the bucket-rank row sort sees skewed buckets (rank scans over many
+    values, or the bitonic fallback) and must still equal the oracle."""
+    cloud, _ = cfg0
+    if order == "cells":
+        key = np.floor(cloud[:, 0]) * 1e4 + np.floor(cloud[:, 1])
+    else:
+        key = cloud[:, 0]
+    c2 = np.ascontiguousarray(cloud[np.argsort(key, kind="stable")][:300000])
+    q = c2[(c2[:, 0] < c2[:, 0].min() + 30) & (c2[:, 1] < c2[:, 1].min() + 30)]
+    q = np.ascontiguousarray(q[:6000])
+    o = CpuIndex(c2, flavor=1)
+    m = cm.Cheesemap.build(c2, cm.BuildOptions(flavor=cm.Flavor.Mixed))
+    for r in (2.5, 3.5):
+        row, cols = cm.radius_search_batch(m, q, r, cm.SPHERE)
+        orow, ocols = o.radius_csr(q, 0, r)
+        assert np.array_equal(row, orow) and np.array_equal(cols, ocols)
+
+
+def test_csr_digest_checker(cfg0, cfg0_oracle):
+    """cm_csr_digest (the full-size verification of a device CSR) reproduces
+    the digest pass and flags an unsorted row."""
+    import ctypes
+
+    import torch
+
+    from paper_2502_11602_b200 import _native
+    L = _native.lib()
+    cloud, q = cfg0
+    q = np.ascontiguousarray(q[:5000])
+    m = cm.Cheesemap.build(cloud, cm.BuildOptions(flavor=cm.Flavor.Mixed))
+    row, cols = cm.radius_search_batch(m, q, 2.5, cm.SPHERE, device_out=True)
+    nq = q.shape[0]
+    cnt = torch.empty(nq, dtype=torch.int32, device="cuda")
+    dig = torch.empty(nq, dtype=torch.int64, device="cuda")
+    bad = ctypes.c_uint64()
+
+    def check():
+        cm._check(L.cm_csr_digest(ctypes.c_void_p(row.data_ptr()), ctypes.c_void_p(cols.data_ptr()),
+                                  nq, ctypes.c_void_p(cnt.data_ptr()),
+                                  ctypes.c_void_p(dig.data_ptr()), ctypes.byref(bad), None))
+
+    check()
+    c2, d2 = cm.radius_digest_batch(m, q, 2.5, cm.SPHERE)
+    assert bad.value == 0
+    assert np.array_equal(cnt.cpu().numpy().astype(np.uint32), c2)
+    assert np.array_equal(dig.cpu().numpy().view(np.uint64), d2)
+    # swap two handles of a long row
+    r0 = int(torch.argmax(row[1:] - row[:-1]).item())
+    b = int(row[r0].item())
+    cols[b], cols[b + 1] = cols[b + 1].clone(), cols[b].clone()
+    check()
+    assert bad.value == 1
