@@ -221,10 +221,48 @@ __device__ __forceinline__ void warp_sort_regs(uint32_t (&v)[ITEMS], int lane) {
   }
 }
 
-// Ascending bitonic network over P registers of ONE thread (compile-time
-// indices only, so v stays in registers).
+// Ascending sorting network over P registers of ONE thread (compile-time
+// indices only, so v stays in registers): Batcher's odd-even merge sort
+// (543 compare-exchanges at P = 64 against the bitonic network's 672; fewer
+// instructions and a smaller unrolled body). CM_LANE_BITONIC selects the
+// bitonic network below instead.
 template <int P>
-__device__ __forceinline__ void lane_sort_regs(uint32_t (&v)[P]) {
+__device__ __forceinline__ void lane_ce(uint32_t (&v)[P], int i, int j) {
+  const uint32_t a = v[i], b = v[j];
+  v[i] = min(a, b);
+  v[j] = max(a, b);
+}
+// odd-even merge of v[LO, LO + N) whose halves are sorted, stride R
+template <int P, int LO, int N, int R>
+struct OemMerge {
+  __device__ __forceinline__ static void run(uint32_t (&v)[P]) {
+    if constexpr (2 * R < N) {
+      OemMerge<P, LO, N, 2 * R>::run(v);
+      OemMerge<P, LO + R, N, 2 * R>::run(v);
+#pragma unroll
+      for (int i = LO + R; i + R < LO + N; i += 2 * R) lane_ce<P>(v, i, i + R);
+    } else {
+      lane_ce<P>(v, LO, LO + R);
+    }
+  }
+};
+template <int P, int LO, int N>
+struct OemSort {
+  __device__ __forceinline__ static void run(uint32_t (&v)[P]) {
+    if constexpr (N > 1) {
+      OemSort<P, LO, N / 2>::run(v);
+      OemSort<P, LO + N / 2, N / 2>::run(v);
+      OemMerge<P, LO, N, 1>::run(v);
+    }
+  }
+};
+template <int P>
+__device__ __forceinline__ void lane_sort_oem(uint32_t (&v)[P]) {
+  OemSort<P, 0, P>::run(v);
+}
+
+template <int P>
+__device__ __forceinline__ void lane_sort_bitonic(uint32_t (&v)[P]) {
 #pragma unroll
   for (int k = 2; k <= P; k <<= 1) {
 #pragma unroll
@@ -245,6 +283,15 @@ __device__ __forceinline__ void lane_sort_regs(uint32_t (&v)[P]) {
       }
     }
   }
+}
+
+template <int P>
+__device__ __forceinline__ void lane_sort_regs(uint32_t (&v)[P]) {
+#ifdef CM_LANE_BITONIC
+  lane_sort_bitonic<P>(v);
+#else
+  lane_sort_oem<P>(v);
+#endif
 }
 
 // Each lane sorts its own interleaved row srow[i * 33 + lane], i < len
@@ -1026,14 +1073,23 @@ __device__ __forceinline__ void warp_sort_row_blocked(uint32_t* row, uint32_t n,
 // past the staging width) are sorted by the warp (blocked register bitonic);
 // longer ones come from the one-query-per-warp path already sorted and are
 // copied.
-constexpr int kGatherRow = 96;
+#ifndef CM_GATHER_ROW
+#define CM_GATHER_ROW 96
+#endif
+constexpr int kGatherRow = CM_GATHER_ROW;
+static_assert(kGatherRow > 64 && kGatherRow <= 96, "gather staging: run 1 of 64 + run 2 <= 32");
 constexpr int kGatherWarpWords = kGatherRow * 33 + 96;  // rows, sfin[32], srel[32] (u64)
 //
 // SORT = true is the in-place row sort after a wide-tile FILL (temp == cols,
 // toff == row_ptr, lengths from row_ptr): only rows <= 96 are handled here;
 // longer rows are sorted by sort_mid_rows_kernel / big_row_sort_kernel.
 template <bool SORT>
-__global__ void __launch_bounds__(128) gather_rows_kernel(const uint32_t* temp,
+#ifdef CM_GATHER_MINB
+#define CM_GATHER_BOUNDS __launch_bounds__(128, CM_GATHER_MINB)
+#else
+#define CM_GATHER_BOUNDS __launch_bounds__(128)
+#endif
+__global__ void CM_GATHER_BOUNDS gather_rows_kernel(const uint32_t* temp,
                                                           const uint64_t* __restrict__ toff,
                                                           const uint32_t* __restrict__ counts,
                                                           const uint64_t* __restrict__ row_ptr,
@@ -1110,7 +1166,7 @@ __global__ void __launch_bounds__(128) gather_rows_kernel(const uint32_t* temp,
     // run 2: [64, len)
     const uint32_t r2 = staged > 64u ? staged - 64u : 0u;
     const uint32_t m2 = warp_max_u32(r2);
-    if (m2 > 1) lane_sort_row<32>(srow + 64 * 33, lane, r2);
+    if (m2 > 1) lane_sort_row<(kGatherRow - 64 <= 16 ? 16 : 32)>(srow + 64 * 33, lane, r2);
     __syncwarp();
     // Rows of <= 64 (one sorted run) leave as one flat stream: flat element
     // f belongs to the row whose flat range holds it; every lane walks the
@@ -1225,6 +1281,109 @@ __global__ void __launch_bounds__(128) sort_blocked_rows_kernel(uint32_t* cols,
       const int l = __ffs(lm) - 1;
       const uint32_t n = __shfl_sync(0xffffffffu, len, l);
       warp_sort_row_blocked<ITEMS>(cols + __shfl_sync(0xffffffffu, b, l), n, lane);
+    }
+  }
+}
+
+// Rows of (32 HI, 64 HI] handles, one warp per row, without padding the
+// whole row to the next power of two: the head [0, 32 HI) is sorted by the
+// blocked register network, the tail [32 HI, n) by the smallest network that
+// holds it, and the two runs are merged along the merge path through shared
+// memory (each lane: co-rank by binary search, then ceil(n / 32) merge
+// steps), then copied back coalesced. Used for 513..1024 (a 512-network,
+// a tail network and the merge instead of a 1024-network); for shorter rows
+// the padded network measured faster (r = 2.5 fill + sort 95 -> 103 ms when
+// 129..512 were split too).
+__device__ __forceinline__ uint32_t spad(uint32_t p) { return p + (p >> 5); }
+
+template <int TI>
+__device__ __forceinline__ void split_sort_tail(const uint32_t* src, uint32_t t, uint32_t* dst,
+                                                int lane) {
+  uint32_t v[TI];
+#pragma unroll
+  for (int r = 0; r < TI; ++r) {
+    const uint32_t e = (uint32_t)lane * TI + r;
+    v[r] = e < t ? src[e] : 0xffffffffu;
+  }
+  warp_sort_blocked<TI>(v, lane);
+#pragma unroll
+  for (int r = 0; r < TI; ++r) {
+    const uint32_t e = (uint32_t)lane * TI + r;
+    if (e < t) dst[spad(e)] = v[r];
+  }
+}
+
+template <int HI>
+__device__ __forceinline__ void warp_sort_row_split(uint32_t* row, uint32_t n, uint32_t* sa,
+                                                    uint32_t* so, int lane) {
+  constexpr uint32_t H = 32u * HI;
+  const uint32_t t = n - H;  // 1 .. H
+  {
+    uint32_t v[HI];
+#pragma unroll
+    for (int r = 0; r < HI; ++r) v[r] = row[(uint32_t)lane * HI + r];
+    warp_sort_blocked<HI>(v, lane);
+#pragma unroll
+    for (int r = 0; r < HI; ++r) sa[spad((uint32_t)lane * HI + r)] = v[r];
+  }
+  uint32_t* sb = sa + spad(H);  // tail run, its own padded indices
+  if (t <= 32) {
+    uint32_t v = (uint32_t)lane < t ? row[H + lane] : 0xffffffffu;
+    v = warp_sort32(v, lane);
+    if ((uint32_t)lane < t) sb[spad(lane)] = v;
+  } else if (HI >= 4 && t <= H / 4) {
+    split_sort_tail<(HI >= 4 ? HI / 4 : 1)>(row + H, t, sb, lane);
+  } else if (HI >= 2 && t <= H / 2) {
+    split_sort_tail<(HI >= 2 ? HI / 2 : 1)>(row + H, t, sb, lane);
+  } else {
+    split_sort_tail<HI>(row + H, t, sb, lane);
+  }
+  __syncwarp();
+  const uint32_t per = (n + 31) >> 5;
+  const uint32_t d = min((uint32_t)lane * per, n);
+  uint32_t lo = d > t ? d - t : 0u, hi = min(d, H);
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (sa[spad(mid)] <= sb[spad(d - 1 - mid)]) lo = mid + 1; else hi = mid;
+  }
+  uint32_t ia = lo, ib = d - lo;
+  for (uint32_t s2 = 0; s2 < per && d + s2 < n; ++s2) {
+    const bool ta = ib >= t || (ia < H && sa[spad(ia)] <= sb[spad(ib)]);
+    so[spad(d + s2)] = ta ? sa[spad(ia)] : sb[spad(ib)];
+    ia += ta;
+    ib += !ta;
+  }
+  __syncwarp();
+  for (uint32_t i = lane; i < n; i += 32) row[i] = so[spad(i)];
+  __syncwarp();
+}
+
+constexpr int kSplitWarpWords = 2 * (kBlockedMax + kBlockedMax / 32 + 2);
+
+template <int HI>
+__global__ void __launch_bounds__(128) sort_split_rows_kernel(uint32_t* cols,
+                                                              const uint64_t* __restrict__ row_ptr,
+                                                              uint64_t nq) {
+  extern __shared__ uint32_t ssm[];
+  uint32_t* sa = ssm + (threadIdx.x >> 5) * kSplitWarpWords;
+  uint32_t* so = sa + kSplitWarpWords / 2;
+  const int lane = threadIdx.x & 31;
+  const uint64_t ngroups = (nq + 31) / 32;
+  const uint64_t W = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t g = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); g < ngroups;
+       g += W) {
+    const uint64_t q = g * 32 + lane;
+    uint64_t b = 0;
+    uint32_t len = 0;
+    if (q < nq) {
+      b = __ldg(row_ptr + q);
+      len = (uint32_t)(__ldg(row_ptr + q + 1) - b);
+    }
+    for (uint32_t lm = __ballot_sync(0xffffffffu, len > 32u * HI && len <= 64u * HI); lm;
+         lm &= lm - 1) {
+      const int l = __ffs(lm) - 1;
+      const uint32_t n = __shfl_sync(0xffffffffu, len, l);
+      warp_sort_row_split<HI>(cols + __shfl_sync(0xffffffffu, b, l), n, sa, so, lane);
     }
   }
 }
@@ -1607,7 +1766,11 @@ cm_status radius_fill_dev(const cm_index* ix, const double* q, uint64_t nq, int 
     sort_blocked_rows_kernel<4><<<bgrid, 128, 0, st>>>(cols, row_ptr, nq, kGatherRow); ::cmg::note_launch();
     sort_blocked_rows_kernel<8><<<bgrid, 128, 0, st>>>(cols, row_ptr, nq, 128); ::cmg::note_launch();
     sort_blocked_rows_kernel<16><<<bgrid, 128, 0, st>>>(cols, row_ptr, nq, 256); ::cmg::note_launch();
-    sort_blocked_rows_kernel<32><<<bgrid, 128, 0, st>>>(cols, row_ptr, nq, 512); ::cmg::note_launch();
+    // 513..1024: head 512 + tail + merge (measured: r = 5 fill + sort 44.4 ->
+    // 42.0 ms; for the shorter classes the padded network stays faster)
+    const int ssmem = 4 * kSplitWarpWords * 4;
+    cudaFuncSetAttribute(sort_split_rows_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, ssmem);
+    sort_split_rows_kernel<16><<<bgrid, 128, ssmem, st>>>(cols, row_ptr, nq); ::cmg::note_launch();
 
     CM_CUDA_TRY(cudaGetLastError());
   }

@@ -134,9 +134,15 @@ def knn_case(m, qd, qh_sample, oracle, k):
     run()
     ms, _ = timed(run)
     gi, gd = cm.knn_batch(m, qh_sample, k)
-    oi, od = oracle.knn(qh_sample, k)
+    oi, od, prk, pa2 = oracle.knn(qh_sample, k, stats=True)
     ok = bool(np.array_equal(gi, oi) and np.array_equal(gd, od))
-    return dict(k=k, nq=nq, ms=round(ms, 3), qps=nq / (ms * 1e-3), parity=ok)
+    # SURVEY 8d kNN bytes: 24 B x points_tested(kernel_search(c, r_k)), r_k
+    # the exact k-th distance — estimated from the oracle on the sample
+    alg = 24.0 * float(prk.mean()) * nq
+    return dict(k=k, nq=nq, ms=round(ms, 3), qps=nq / (ms * 1e-3), parity=ok,
+                alg_gb_est=round(alg / 1e9, 2), frac_est=round(alg / (ms * 1e-3) / 6542.1e9, 3),
+                ref_alg2_tested_mean=round(float(pa2.mean()), 1),
+                rk_tested_mean=round(float(prk.mean()), 1))
 
 
 def main():
@@ -199,7 +205,8 @@ def main():
                     entry["radius"].append(res)
             for k in p["ks"]:
                 res = knn_case(m, qd, samp, oracle, k)
-                log(f"  cfg{c} {f} knn k={k}: {res['qps'] / 1e6:.2f} M q/s parity={res['parity']}")
+                log(f"  cfg{c} {f} knn k={k}: {res['qps'] / 1e6:.2f} M q/s parity={res['parity']} "
+                    f"frac_est={res['frac_est']} tested(r_k)={res['rk_tested_mean']}")
                 entry["knn"].append(res)
             out["results"].append(entry)
             del m
