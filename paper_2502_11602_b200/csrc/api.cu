@@ -908,11 +908,28 @@ cm_status cm_radius_search_to_host(const cm_index* ix, const double* q_host, uin
   // Chunk boundaries: the first chunk is half the size of the others, so the
   // first columns reach PCIe sooner.
   std::vector<uint64_t> qb(nchunks + 1);
-  for (uint64_t c = 0; c <= nchunks; ++c)
-    qb[c] = c == 0 ? 0 : (uint64_t)((double)nq * (2.0 * c - 1.0) / (2.0 * nchunks - 1.0));
+  std::vector<double> w(nchunks, 2.0);
+  w[0] = 1.0;
+  if (const char* rv = std::getenv("CMGPU_CHUNK_W")) {  // e.g. "1,2,4,4,4" (probe)
+    w.clear();
+    for (const char* p = rv; *p;) {
+      char* e = nullptr;
+      w.push_back(std::strtod(p, &e));
+      p = *e ? e + 1 : e;
+    }
+    nchunks = w.size();
+    qb.assign(nchunks + 1, 0);
+  }
+  double wsum = 0.0;
+  for (double x : w) wsum += x;
+  double acc = 0.0;
+  for (uint64_t c = 0; c < nchunks; ++c) {
+    qb[c] = (uint64_t)((double)nq * acc / wsum);
+    acc += w[c];
+  }
   qb[nchunks] = nq;
   double* qdev = nullptr;  // every chunk's input copy is issued up front
-  std::vector<cudaEvent_t> in_done(nchunks);
+  std::vector<cudaEvent_t> in_done(nchunks);  // sized after the chunk plan
   cudaEvent_t comp_done[2], out_done[2];
   // CMGPU_TRACE: device timeline per chunk (core start / core end on the
   // compute stream, copies done on the output stream), relative to t_ev[0]

@@ -112,19 +112,23 @@ __global__ void __launch_bounds__(kKThreads) knn_warp_kernel(const Tables t,
     const double eps = 1e-12 * (fabs(cx) + fabs(cy) + fabs(cz) + fabs(g.ox) + fabs(g.oy) +
                                 fabs(g.oz) + g.sx + g.sy + g.sz);
     uint32_t cnt = 0;
-    for (int64_t L = 0;; ++L) {
+    // The first step visits the whole 3 x 3 x 3 block (shells 0 and 1 at
+    // once: the shell-0 stop test almost never holds for k >= 8 at
+    // cell-sized voxels, so testing it only cost a round of span lookups and
+    // a batch merge); later steps add one Chebyshev shell each.
+    for (int64_t L = 1;; ++L) {
       const int64_t i0 = imax64(0, ic - L), i1 = imin64(nx - 1, ic + L);
       const int64_t j0 = imax64(0, jc - L), j1 = imin64(ny - 1, jc + L);
-      const int64_t nj = j1 - j0 + 1;
-      const int64_t ncol = (i1 - i0 + 1) * nj;
-      for (int64_t cb = 0; cb < ncol; cb += 32) {
-        const int64_t c = cb + lane;
+      const uint32_t nj = (uint32_t)(j1 - j0 + 1);
+      const uint32_t ncol = (uint32_t)(i1 - i0 + 1) * nj;
+      for (uint32_t cb = 0; cb < ncol; cb += 32) {
+        const uint32_t c = cb + lane;
         uint32_t b1 = 0, e1 = 0, b2 = 0, e2 = 0;
         if (c < ncol) {
-          const int64_t i = i0 + c / nj, j = j0 + c % nj;
-          const bool ring = (i == ic - L) || (i == ic + L) || (j == jc - L) || (j == jc + L);
-          if (ring || L > 0)
-            shell_column_spans<FLAVOR>(t, i, j, ring, kc, L, (uint64_t)nzm, &b1, &e1, &b2, &e2);
+          const int64_t i = i0 + (int64_t)(c / nj), j = j0 + (int64_t)(c % nj);
+          const bool ring =
+              L == 1 || (i == ic - L) || (i == ic + L) || (j == jc - L) || (j == jc + L);
+          shell_column_spans<FLAVOR>(t, i, j, ring, kc, L, (uint64_t)nzm, &b1, &e1, &b2, &e2);
         }
         const uint32_t l1 = e1 - b1;
         const uint32_t len = l1 + (e2 - b2);
