@@ -46,11 +46,15 @@ static void configure_pool() {
   if (dev >= 0 && dev < 64 && !g_pool_configured[dev]) {
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      // keep up to half the device's memory cached across calls (steady
-      // state batches then allocate nothing), return the rest at syncs
+      // keep up to 3/4 of the device's memory cached across calls (steady
+      // state batches then allocate nothing; config 4's 200M-query calls need
+      // ~80 GB, and a pool trimmed back at every sync re-maps it inside the
+      // next call), return the rest at syncs; CMGPU_POOL_KEEP_FRAC overrides
       size_t fr = 0, tot = 0;
       cudaMemGetInfo(&fr, &tot);
-      uint64_t thr = tot / 2;
+      double keep = 0.75;
+      if (const char* kf = std::getenv("CMGPU_POOL_KEEP_FRAC")) keep = std::atof(kf);
+      uint64_t thr = (uint64_t)((double)tot * std::min(1.0, std::max(0.0, keep)));
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
       // Reserve one large block up front: the pool then carves later
       // requests out of it instead of mapping fresh physical memory for

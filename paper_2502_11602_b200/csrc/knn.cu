@@ -23,7 +23,10 @@ namespace {
 constexpr int kKThreads = 128;
 constexpr int kKWarps = kKThreads / 32;
 constexpr int kKMax = 256;
-constexpr uint32_t kKnnTileMax = 8;  // kNN query tiles for k <= this
+#ifndef CM_KNN_TILE_MAX
+#define CM_KNN_TILE_MAX 8
+#endif
+constexpr uint32_t kKnnTileMax = CM_KNN_TILE_MAX;  // kNN query tiles for k <= this
 
 __device__ __forceinline__ int64_t imax64(int64_t a, int64_t b) { return a < b ? b : a; }
 __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return b < a ? b : a; }

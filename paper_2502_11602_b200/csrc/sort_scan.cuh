@@ -243,8 +243,15 @@ template <typename K>
 inline int radix_sort_pairs(K* keys, uint32_t* vals, uint64_t n, int bits, void* scratch,
                             cudaStream_t st) {
   if (n <= 1 || bits <= 0) return 0;
-  // the fewest passes digits of 8..10 bits allow, with the narrowest such digit
-  const int passes_min = (bits + kRadixBitsMax - 1) / kRadixBitsMax;
+  // the fewest passes digits of 8..9 bits allow, with the narrowest such
+  // digit (10-bit digits double the downsweep's per-warp counters and cost
+  // occupancy: 200M 30-bit keys took 29 ms in 3 x 10-bit passes against
+  // 19 ms in 4 x 8-bit ones; CM_RADIX_MAX_BITS=10 restores them)
+#ifndef CM_RADIX_MAX_BITS
+#define CM_RADIX_MAX_BITS 9
+#endif
+  static_assert(CM_RADIX_MAX_BITS <= kRadixBitsMax, "digit wider than the kernels support");
+  const int passes_min = (bits + CM_RADIX_MAX_BITS - 1) / CM_RADIX_MAX_BITS;
   const int rb = (bits + passes_min - 1) / passes_min < 8 ? 8 : (bits + passes_min - 1) / passes_min;
   const uint32_t nb = (uint32_t)((n + kSortTile - 1) / kSortTile);
   const uint64_t h = (uint64_t)nb << rb;
