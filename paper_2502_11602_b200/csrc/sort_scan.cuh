@@ -164,19 +164,36 @@ __global__ void __launch_bounds__(kSortThreads) radix_upsweep(const K* __restric
 // Stable scatter. Warp w of block b owns keys [b*TILE + w*512, +512);
 // item `it` of lane l is key (it*32 + l) of that run, so processing items in
 // order with lanes in order visits keys in input order. Ranks inside a warp
-// come from __match_any_sync peer groups.
+// come from __match_any_sync peer groups. The block first reorders its tile
+// by digit in shared memory (stable: warp, then rank), then writes it out in
+// that order, so consecutive threads store consecutive positions of one
+// digit's run (a few sectors per digit) instead of one sector per key.
+template <typename K, int RB>
+struct DownsweepSmem {
+  static constexpr int kRadix = 1 << RB;
+  uint32_t wcount[kSortWarps][kRadix];
+  uint32_t lbase[kRadix];
+  uint32_t goff[kRadix];
+  uint32_t swarp[33];
+  K skeys[kSortTile];
+  uint32_t svals[kSortTile];
+};
+
 template <typename K, int RB>
 __global__ void __launch_bounds__(kSortThreads) radix_downsweep(
     const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, K* __restrict__ keys_out,
     uint32_t* __restrict__ vals_out, uint64_t n, int shift,
     const uint32_t* __restrict__ offs /* scanned hist [d][b] */, uint32_t nblocks) {
   constexpr int kRadix = 1 << RB;
-  __shared__ uint32_t wcount[kSortWarps][kRadix];
-  __shared__ uint32_t dbase[kRadix];
+  constexpr int kPer = kRadix / kSortThreads > 0 ? kRadix / kSortThreads : 1;
+  static_assert(kRadix % kSortThreads == 0, "digits per thread");
+  extern __shared__ __align__(16) unsigned char dsm_raw[];
+  DownsweepSmem<K, RB>& sm = *reinterpret_cast<DownsweepSmem<K, RB>*>(dsm_raw);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int d = lane; d < kRadix; d += 32) wcount[w][d] = 0;
+  for (int d = lane; d < kRadix; d += 32) sm.wcount[w][d] = 0;
   __syncwarp();
-  const uint64_t wbase = (uint64_t)blockIdx.x * kSortTile + (uint64_t)w * (32 * kSortItems);
+  const uint64_t bbase = (uint64_t)blockIdx.x * kSortTile;
+  const uint64_t wbase = bbase + (uint64_t)w * (32 * kSortItems);
   K kv[kSortItems];
   uint32_t vv[kSortItems];
   uint32_t rank[kSortItems];
@@ -199,21 +216,36 @@ __global__ void __launch_bounds__(kSortThreads) radix_downsweep(
     const uint32_t peers = __match_any_sync(0xffffffffu, d);
     const int leader = __ffs(peers) - 1;
     uint32_t old = 0;
-    if (valid && lane == leader) old = atomicAdd(&wcount[w][d], (uint32_t)__popc(peers));
+    if (valid && lane == leader) old = atomicAdd(&sm.wcount[w][d], (uint32_t)__popc(peers));
     old = __shfl_sync(0xffffffffu, old, leader);
     rank[it] = old + __popc(peers & lt);
   }
   __syncwarp();
   __syncthreads();
-  // per digit: global offset of this block + exclusive prefix over warps
-  for (int d = threadIdx.x; d < kRadix; d += blockDim.x) {
-    uint32_t s = offs[(uint64_t)d * nblocks + blockIdx.x];
+  // per digit: exclusive prefix over warps (in place), the block's total,
+  // its global offset; then the block-local digit starts (scan over digits)
+  uint32_t tsum = 0;
+#pragma unroll
+  for (int x = 0; x < kPer; ++x) {
+    const int d = threadIdx.x * kPer + x;
+    uint32_t s2 = 0;
     for (int ww = 0; ww < kSortWarps; ++ww) {
-      const uint32_t c = wcount[ww][d];
-      wcount[ww][d] = s;
-      s += c;
+      const uint32_t c = sm.wcount[ww][d];
+      sm.wcount[ww][d] = s2;
+      s2 += c;
     }
-    dbase[d] = 0;
+    sm.lbase[d] = s2;  // total for now
+    sm.goff[d] = offs[(uint64_t)d * nblocks + blockIdx.x];
+    tsum += s2;
+  }
+  uint32_t btot;
+  uint32_t run = block_excl_scan<uint32_t>(tsum, sm.swarp, &btot);
+#pragma unroll
+  for (int x = 0; x < kPer; ++x) {
+    const int d = threadIdx.x * kPer + x;
+    const uint32_t c = sm.lbase[d];
+    sm.lbase[d] = run;
+    run += c;
   }
   __syncthreads();
 #pragma unroll
@@ -221,11 +253,28 @@ __global__ void __launch_bounds__(kSortThreads) radix_downsweep(
     const uint64_t i = wbase + (uint64_t)it * 32 + lane;
     if (i < n) {
       const uint32_t d = (uint32_t)(kv[it] >> shift) & (kRadix - 1);
-      const uint32_t pos = wcount[w][d] + rank[it];
-      keys_out[pos] = kv[it];
-      vals_out[pos] = vv[it];
+      const uint32_t lpos = sm.lbase[d] + sm.wcount[w][d] + rank[it];
+      sm.skeys[lpos] = kv[it];
+      sm.svals[lpos] = vv[it];
     }
   }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < btot; i += kSortThreads) {
+    const K key = sm.skeys[i];
+    const uint32_t d = (uint32_t)(key >> shift) & (kRadix - 1);
+    const uint32_t pos = sm.goff[d] + (i - sm.lbase[d]);
+    keys_out[pos] = key;
+    vals_out[pos] = sm.svals[i];
+  }
+}
+
+template <typename K, int RB>
+inline void launch_downsweep(const K* ka, const uint32_t* va, K* kb, uint32_t* vb, uint64_t n,
+                             int shift, const uint32_t* hist, uint32_t nb, cudaStream_t st) {
+  const int smem = (int)sizeof(DownsweepSmem<K, RB>);
+  cudaFuncSetAttribute(radix_downsweep<K, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  radix_downsweep<K, RB><<<nb, kSortThreads, smem, st>>>(ka, va, kb, vb, n, shift, hist, nb);
+  ::cmg::note_launch();
 }
 
 // Scratch (bytes) for radix_sort_pairs over n keys.
@@ -277,13 +326,9 @@ inline int radix_sort_pairs(K* keys, uint32_t* vals, uint64_t n, int bits, void*
       radix_upsweep<K, 10><<<nb, kSortThreads, 0, st>>>(ka, n, shift, hist, nb); ::cmg::note_launch();
     }
     exclusive_scan<uint32_t, uint32_t>(hist, h, hist, part, 0, st);
-    if (rb == 8) {
-      radix_downsweep<K, 8><<<nb, kSortThreads, 0, st>>>(ka, va, kb, vb, n, shift, hist, nb); ::cmg::note_launch();
-    } else if (rb == 9) {
-      radix_downsweep<K, 9><<<nb, kSortThreads, 0, st>>>(ka, va, kb, vb, n, shift, hist, nb); ::cmg::note_launch();
-    } else {
-      radix_downsweep<K, 10><<<nb, kSortThreads, 0, st>>>(ka, va, kb, vb, n, shift, hist, nb); ::cmg::note_launch();
-    }
+    if (rb == 8) launch_downsweep<K, 8>(ka, va, kb, vb, n, shift, hist, nb, st);
+    else if (rb == 9) launch_downsweep<K, 9>(ka, va, kb, vb, n, shift, hist, nb, st);
+    else launch_downsweep<K, 10>(ka, va, kb, vb, n, shift, hist, nb, st);
     K* tk = ka; ka = kb; kb = tk;
     uint32_t* tv = va; va = vb; vb = tv;
   }
