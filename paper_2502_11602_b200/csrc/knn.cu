@@ -485,6 +485,21 @@ cm_status knn_dev(const cm_index* ix, const double* q, uint64_t nq, uint32_t k,
     };
     const size_t s8 = kKWarps * sizeof(KnnTileSmem<8>);
     cm_status ts;
+#if CM_KNN_TILE_MAX > 8
+    const size_t s16 = kKWarps * sizeof(KnnTileSmem<16>);
+    if (k > 8) {
+      switch (ix->opts.flavor) {
+        case CM_DENSE:
+          ts = tiles(knn_tile_kernel<CM_DENSE, 16>, s16);
+          break;
+        case CM_SPARSE:
+          ts = tiles(knn_tile_kernel<CM_SPARSE, 16>, s16);
+          break;
+        default:
+          ts = tiles(knn_tile_kernel<CM_MIXED, 16>, s16);
+      }
+    } else
+#endif
     switch (ix->opts.flavor) {
       case CM_DENSE:
         ts = tiles(knn_tile_kernel<CM_DENSE, 8>, s8);
