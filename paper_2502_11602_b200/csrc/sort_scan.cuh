@@ -213,7 +213,19 @@ __global__ void __launch_bounds__(kSortThreads) radix_downsweep(
     const uint64_t i = wbase + (uint64_t)it * 32 + lane;
     const bool valid = i < n;
     const uint32_t d = valid ? ((uint32_t)(kv[it] >> shift) & (kRadix - 1)) : kRadix;  // kRadix = invalid
+#ifdef CM_RADIX_BALLOT
+    // peer group by one ballot per digit bit (invalid lanes drop out first)
+    uint32_t peers = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+    for (int b = 0; b < RB; ++b) {
+      const bool bit = (d >> b) & 1u;
+      const uint32_t m = __ballot_sync(0xffffffffu, bit);
+      peers &= bit ? m : ~m;
+    }
+    if (!valid) peers = 1u << lane;
+#else
     const uint32_t peers = __match_any_sync(0xffffffffu, d);
+#endif
     const int leader = __ffs(peers) - 1;
     uint32_t old = 0;
     if (valid && lane == leader) old = atomicAdd(&sm.wcount[w][d], (uint32_t)__popc(peers));
