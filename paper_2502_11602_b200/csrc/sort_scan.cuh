@@ -213,8 +213,9 @@ __global__ void __launch_bounds__(kSortThreads) radix_downsweep(
     const uint64_t i = wbase + (uint64_t)it * 32 + lane;
     const bool valid = i < n;
     const uint32_t d = valid ? ((uint32_t)(kv[it] >> shift) & (kRadix - 1)) : kRadix;  // kRadix = invalid
-#ifdef CM_RADIX_BALLOT
-    // peer group by one ballot per digit bit (invalid lanes drop out first)
+#ifndef CM_RADIX_MATCH_ANY
+    // peer group by one ballot per digit bit (invalid lanes drop out first);
+    // measured faster than __match_any_sync (20M-key sort 0.83 -> 0.75 ms)
     uint32_t peers = __ballot_sync(0xffffffffu, valid);
 #pragma unroll
     for (int b = 0; b < RB; ++b) {
