@@ -1013,6 +1013,10 @@ __global__ void __launch_bounds__(1024) big_row_sort_kernel(uint32_t* __restrict
 // bitonic network's exchanges at distance < ITEMS stay inside a lane (no
 // shuffles) and the row's loads and stores are contiguous per lane.
 constexpr int kBlockedMax = 1024;
+#ifndef CM_MID_MIN
+#define CM_MID_MIN 1024
+#endif
+constexpr int kMidMin = CM_MID_MIN;  // rows above this go to sort_mid_rows_kernel
 
 template <int ITEMS>
 __device__ __forceinline__ void warp_sort_blocked(uint32_t (&v)[ITEMS], int lane) {
@@ -1430,7 +1434,7 @@ __global__ void __launch_bounds__(kMidThreads) sort_mid_rows_kernel(
         len = (uint32_t)(__ldg(row_ptr + ql + 1) - st);
       }
       const uint32_t runs =
-          (len > (uint32_t)kBlockedMax && len <= (uint32_t)kMidMax) ? (len + 63) >> 6 : 0u;
+          (len > (uint32_t)kMidMin && len <= (uint32_t)kMidMax) ? (len + 63) >> 6 : 0u;
       const uint32_t winc = warp_incl_scan(runs);
       // a group ends at the 128-run budget and before the first row past
       // kMidMax (which, when first, forms a group of its own: listed for the
@@ -1475,23 +1479,33 @@ __global__ void __launch_bounds__(kMidThreads) sort_mid_rows_kernel(
       const uint32_t nruns = s_rb[g - 1] + s_runs[g - 1];
       if (nruns) {
         uint32_t* b0 = msm;
-        const uint32_t span = s_off[g - 1] + s_len[g - 1];
-        {  // load the span flat, 8 loads in flight per thread
+        {  // load the group's rows by run slot (slot f = 64 * run + offset,
+           // the row's smem position), 8 loads in flight per thread; only the
+           // grouped rows' handles are read, not the shorter rows between
+           // them (which the earlier span load read and dropped: a second
+           // full pass over the CSR when long rows are sparse)
+          const uint32_t nslots = 64u * nruns;
           uint32_t r = 0;
-          for (uint32_t f0 = 0; f0 < span; f0 += 8 * kMidThreads) {
+          for (uint32_t f0 = 0; f0 < nslots; f0 += 8 * kMidThreads) {
             uint32_t v[8];
+            uint32_t ok = 0;
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
               const uint32_t f = f0 + k * kMidThreads + tid;
-              v[k] = f < span ? cols[g0 + f] : 0u;
+              v[k] = 0u;
+              if (f < nslots) {
+                while (r + 1 < g && 64u * s_rb[r + 1] <= f) ++r;
+                const uint32_t idx = f - 64u * s_rb[r];
+                if (idx < s_len[r]) {
+                  v[k] = cols[g0 + s_off[r] + idx];
+                  ok |= 1u << k;
+                }
+              }
             }
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
               const uint32_t f = f0 + k * kMidThreads + tid;
-              if (f < span) {
-                while (r + 1 < g && s_off[r + 1] <= f) ++r;
-                if (s_runs[r]) b0[mid_swz(64u * s_rb[r] + (f - s_off[r]))] = v[k];
-              }
+              if ((ok >> k) & 1u) b0[mid_swz(f)] = v[k];
             }
           }
         }
@@ -1575,12 +1589,13 @@ __global__ void __launch_bounds__(kMidThreads) sort_mid_rows_kernel(
         }
         {  // write back: a row with R runs ended in buffer (ceil(log2 R) & 1)
           uint32_t r = 0;
-          for (uint32_t f = tid; f < span; f += kMidThreads) {
-            while (r + 1 < g && s_off[r + 1] <= f) ++r;
-            const uint32_t rr = s_runs[r];
-            if (rr) {
+          for (uint32_t f = tid; f < 64u * nruns; f += kMidThreads) {
+            while (r + 1 < g && 64u * s_rb[r + 1] <= f) ++r;
+            const uint32_t idx = f - 64u * s_rb[r];
+            if (idx < s_len[r]) {
+              const uint32_t rr = s_runs[r];
               const int which = (32 - __clz((int)(rr - 1))) & 1;  // ceil(log2 rr) parity
-              cols[g0 + f] = msm[which * kMidBuf + mid_swz(64u * s_rb[r] + (f - s_off[r]))];
+              cols[g0 + s_off[r] + idx] = msm[which * kMidBuf + mid_swz(f)];
             }
           }
         }
@@ -1764,13 +1779,19 @@ cm_status radius_fill_dev(const cm_index* ix, const double* q, uint64_t nq, int 
   {
     const unsigned bgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((groups + 3) / 4, (uint64_t)sm_count() * 16));
     sort_blocked_rows_kernel<4><<<bgrid, 128, 0, st>>>(cols, row_ptr, nq, kGatherRow); ::cmg::note_launch();
-    sort_blocked_rows_kernel<8><<<bgrid, 128, 0, st>>>(cols, row_ptr, nq, 128); ::cmg::note_launch();
-    sort_blocked_rows_kernel<16><<<bgrid, 128, 0, st>>>(cols, row_ptr, nq, 256); ::cmg::note_launch();
+    if (kMidMin > 128) {
+      sort_blocked_rows_kernel<8><<<bgrid, 128, 0, st>>>(cols, row_ptr, nq, 128); ::cmg::note_launch();
+    }
+    if (kMidMin > 256) {
+      sort_blocked_rows_kernel<16><<<bgrid, 128, 0, st>>>(cols, row_ptr, nq, 256); ::cmg::note_launch();
+    }
     // 513..1024: head 512 + tail + merge (measured: r = 5 fill + sort 44.4 ->
     // 42.0 ms; for the shorter classes the padded network stays faster)
     const int ssmem = 4 * kSplitWarpWords * 4;
     cudaFuncSetAttribute(sort_split_rows_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, ssmem);
-    sort_split_rows_kernel<16><<<bgrid, 128, ssmem, st>>>(cols, row_ptr, nq); ::cmg::note_launch();
+    if (kMidMin > 512) {
+      sort_split_rows_kernel<16><<<bgrid, 128, ssmem, st>>>(cols, row_ptr, nq); ::cmg::note_launch();
+    }
 
     CM_CUDA_TRY(cudaGetLastError());
   }
