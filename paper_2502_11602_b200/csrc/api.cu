@@ -765,12 +765,28 @@ static cm_status radius_search_core(const cm_index* ix, const double* qd, uint64
   s = counts_to_row_ptr(counts, nq, csr->row_ptr, st);
   cudaEventRecord(ev.e[4], st);
   if (s != CM_OK) return fail(s);
+  // Row-sort plan of a wide FILL: rows of 513..1024 go to the merge-path
+  // block sort when they are short on average (config 1 cube r = 2.5, class
+  // mean 624: fill + sort 158 -> 142 ms), else to the 512-head split sort,
+  // which measured faster for longer class means (sphere / cube r = 5, 703 /
+  // 930: 37.7 / 50.0 -> 36.7 / 46.0 ms on 2M centres; sphere r = 2.5, 692:
+  // equal). The threshold sits between the measured cases.
+  uint32_t mid_min = 0;
   if (two_pass) {
+    unsigned long long cls_h[2] = {0, 0};
+    unsigned long long* cls_d = nullptr;
+    const bool cls = dev_alloc_t(&cls_d, 2, st) == cudaSuccess &&
+                     row_class_counts_dev(counts, nq, cls_d, st) == CM_OK &&
+                     cudaMemcpyAsync(cls_h, cls_d, 16, cudaMemcpyDeviceToHost, st) == cudaSuccess;
     if (cudaMemcpyAsync(&csr->nnz, csr->row_ptr + nq, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
         cudaStreamSynchronize(st) != cudaSuccess) {
       set_error("row pointer readback failed");
+      if (cls_d) dev_free(cls_d, st);
       return fail(CM_CUDA);
     }
+    if (cls_d) dev_free(cls_d, st);
+    cudaGetLastError();
+    if (cls && cls_h[0] > 0 && (double)cls_h[1] / (double)cls_h[0] < 660.0) mid_min = 512;
   } else {
     csr->nnz = used;
   }
@@ -779,7 +795,8 @@ static cm_status radius_search_core(const cm_index* ix, const double* qd, uint64
     return fail(CM_CUDA);
   }
   if (two_pass)
-    s = radius_fill_dev(ix, qd, nq, kernel, r, ord.perm, csr->row_ptr, csr->cols, st, nullptr);
+    s = radius_fill_dev(ix, qd, nq, kernel, r, ord.perm, csr->row_ptr, csr->cols, st, nullptr,
+                        mid_min);
   else
     s = hook ? hook->run(temp, toff, scnt, csr->row_ptr, ord.perm, csr->cols, nq, st)
              : gather_rows_dev(temp, toff, scnt, csr->row_ptr, ord.perm, csr->cols, nq, st);

@@ -112,7 +112,10 @@ cm_status brute_knn_dev(const double* xyz, uint64_t n, const double* q, uint64_t
                         uint32_t* idx, double* d2, cudaStream_t st);
 cm_status radius_fill_dev(const cm_index* ix, const double* q_dev, uint64_t nq, int kernel,
                           double r, const uint32_t* perm, const uint64_t* row_ptr_dev,
-                          uint32_t* cols_dev, cudaStream_t st, cudaEvent_t after_fill = nullptr);
+                          uint32_t* cols_dev, cudaStream_t st, cudaEvent_t after_fill = nullptr,
+                          uint32_t mid_min = 0);
+cm_status row_class_counts_dev(const uint32_t* counts, uint64_t nq, unsigned long long* out,
+                               cudaStream_t st);
 cm_status radius_digest_dev(const cm_index* ix, const double* q_dev, uint64_t nq, int kernel,
                             double r, const uint32_t* perm, uint32_t* counts_dev,
                             uint64_t* digest_dev, cudaStream_t st);

@@ -1413,7 +1413,7 @@ __device__ __forceinline__ uint32_t mid_swz(uint32_t p) { return p ^ ((p >> 6) &
 
 __global__ void __launch_bounds__(kMidThreads) sort_mid_rows_kernel(
     uint32_t* cols, const uint64_t* __restrict__ row_ptr, uint64_t nq, uint64_t* big_off,
-    uint32_t* big_len, uint32_t* n_big) {
+    uint32_t* big_len, uint32_t* n_big, uint32_t mid_min) {
   extern __shared__ uint32_t msm[];
   __shared__ uint32_t s_off[kMidThreads], s_len[kMidThreads], s_rb[kMidThreads],
       s_runs[kMidThreads];
@@ -1434,7 +1434,7 @@ __global__ void __launch_bounds__(kMidThreads) sort_mid_rows_kernel(
         len = (uint32_t)(__ldg(row_ptr + ql + 1) - st);
       }
       const uint32_t runs =
-          (len > (uint32_t)kMidMin && len <= (uint32_t)kMidMax) ? (len + 63) >> 6 : 0u;
+          (len > mid_min && len <= (uint32_t)kMidMax) ? (len + 63) >> 6 : 0u;
       const uint32_t winc = warp_incl_scan(runs);
       // a group ends at the 128-run budget and before the first row past
       // kMidMax (which, when first, forms a group of its own: listed for the
@@ -1748,10 +1748,44 @@ cm_status radius_digest_dev(const cm_index* ix, const double* q, uint64_t nq, in
   return launch_radius<MODE_DIGEST>(ix, q, nq, kernel, r, perm, o, st);
 }
 
+// Rows of 513..1024 handles, from the count pass: out[0] = how many,
+// out[1] = their total length (the row-sort plan of a wide FILL).
+__global__ void row_class_kernel(const uint32_t* __restrict__ counts, uint64_t nq,
+                                 unsigned long long* __restrict__ out) {
+  unsigned long long a = 0, b = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nq;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t c = __ldg(counts + i);
+    const bool in = c > 512u && c <= 1024u;
+    a += in;
+    b += in ? c : 0u;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (a) atomicAdd(out, a);
+    if (b) atomicAdd(out + 1, b);
+  }
+}
+
+cm_status row_class_counts_dev(const uint32_t* counts, uint64_t nq, unsigned long long* out,
+                               cudaStream_t st) {
+  CM_CUDA_TRY(cudaMemsetAsync(out, 0, 16, st));
+  if (nq == 0) return CM_OK;
+  const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nq + 255) / 256, (uint64_t)sm_count() * 8));
+  row_class_kernel<<<grid, 256, 0, st>>>(counts, nq, out); ::cmg::note_launch();
+  CM_CUDA_TRY(cudaGetLastError());
+  return CM_OK;
+}
+
 cm_status radius_fill_dev(const cm_index* ix, const double* q, uint64_t nq, int kernel, double r,
                           const uint32_t* perm, const uint64_t* row_ptr, uint32_t* cols,
-                          cudaStream_t st, cudaEvent_t after_fill) {
+                          cudaStream_t st, cudaEvent_t after_fill, uint32_t mid_min) {
   if (nq == 0) return CM_OK;
+  if (mid_min == 0) mid_min = (uint32_t)kMidMin;
   BigRows big;
   cm_status s = big.init(nq, st);
   if (s != CM_OK) return s;
@@ -1789,7 +1823,7 @@ cm_status radius_fill_dev(const cm_index* ix, const double* q, uint64_t nq, int 
     // 42.0 ms; for the shorter classes the padded network stays faster)
     const int ssmem = 4 * kSplitWarpWords * 4;
     cudaFuncSetAttribute(sort_split_rows_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, ssmem);
-    if (kMidMin > 512) {
+    if (mid_min > 512) {
       sort_split_rows_kernel<16><<<bgrid, 128, ssmem, st>>>(cols, row_ptr, nq); ::cmg::note_launch();
     }
 
@@ -1800,7 +1834,8 @@ cm_status radius_fill_dev(const cm_index* ix, const double* q, uint64_t nq, int 
     cudaFuncSetAttribute(sort_mid_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, msmem);
     const uint64_t tasks = (nq + 1023) / 1024;
     const unsigned mgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(tasks, (uint64_t)sm_count() * 3));
-    sort_mid_rows_kernel<<<mgrid, kMidThreads, msmem, st>>>(cols, row_ptr, nq, big2.off, big2.len, big2.n); ::cmg::note_launch();
+    sort_mid_rows_kernel<<<mgrid, kMidThreads, msmem, st>>>(cols, row_ptr, nq, big2.off, big2.len,
+                                                            big2.n, mid_min); ::cmg::note_launch();
   }
   CM_CUDA_TRY(cudaGetLastError());
   Out o2{};
