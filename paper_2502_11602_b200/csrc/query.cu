@@ -823,6 +823,13 @@ __global__ void __launch_bounds__(kQThreads, 5) radius_tile_kernel(
     P.init(cx, cy, cz, r, CUBE);
     uint32_t cnt = 0, ntest = 0;
     uint64_t dig = 0;
+    // ROWS: the lane's next key slot as a running shared-memory address
+    // (slot i of lane l at 2 * (33 i + l)); advancing it on a hit replaces the
+    // per-record slot-address arithmetic, and the row length is recovered
+    // from it after the walk
+    const uint32_t kaddr0 = ROWS ? (uint32_t)__cvta_generic_to_shared(skey + lane) : 0u;
+    const uint32_t klim = kaddr0 + 66u * (uint32_t)kLaneRowCap;
+    uint32_t kaddr = kaddr0;
     // Walk the hull: each needed column's span in chunks of <= 32 records,
     // staged into shared memory by cp.async one chunk ahead (double buffer),
     // then read warp-uniformly (LDS broadcast) by every lane.
@@ -857,8 +864,13 @@ __global__ void __launch_bounds__(kQThreads, 5) radius_tile_kernel(
           const bool in = need & (v[w].meta - kk0 <= kspan);
           const bool hit = in & pred<CUBE>(P, v[w].x, v[w].y, v[w].z);
           if (MODE == MODE_DIGEST && hit) dig += mix64(v[w].id);
-          if (ROWS && hit && cnt < (uint32_t)kLaneRowCap) skey[cnt * 33 + lane] = (uint16_t)(kbase + u + w);
-          cnt += hit;
+          if (ROWS) {
+            if (hit && kaddr < klim)
+              asm volatile("st.shared.u16 [%0], %1;" ::"r"(kaddr), "h"((unsigned short)(kbase + u + w)));
+            kaddr += hit ? 66u : 0u;
+          } else {
+            cnt += hit;
+          }
           ntest += in;
         }
       }
@@ -867,8 +879,13 @@ __global__ void __launch_bounds__(kQThreads, 5) radius_tile_kernel(
         const bool in = need & (v.meta - kk0 <= kspan);
         const bool hit = in & pred<CUBE>(P, v.x, v.y, v.z);
         if (MODE == MODE_DIGEST && hit) dig += mix64(v.id);
-        if (ROWS && hit && cnt < (uint32_t)kLaneRowCap) skey[cnt * 33 + lane] = (uint16_t)(kbase + u);
-        cnt += hit;
+        if (ROWS) {
+          if (hit && kaddr < klim)
+            asm volatile("st.shared.u16 [%0], %1;" ::"r"(kaddr), "h"((unsigned short)(kbase + u)));
+          kaddr += hit ? 66u : 0u;
+        } else {
+          cnt += hit;
+        }
         ntest += in;
       }
       __syncwarp();
@@ -877,6 +894,7 @@ __global__ void __launch_bounds__(kQThreads, 5) radius_tile_kernel(
       more = more2;
     }
     cp_async_wait<0>();
+    if (ROWS) cnt = (kaddr - kaddr0) / 66u;
     if (MODE == MODE_COUNT) {
       uint32_t sum = ntest;
 #pragma unroll
