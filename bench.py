@@ -441,7 +441,10 @@ def main():
                        "neighbours": nnz_total, "radius_m": a.radius, "kernel": a.kernel,
                        "l2": "flushed (256 MB write) before every timed step",
                        "parallelism": f"replicated index, queries sharded x{world} "
-                                      "(equal-count x-slabs)"},
+                                      "(equal-count x-slabs)",
+                       "query_order": ("the index's record order (centres = the indexed "
+                                       "device buffer; no key sort)" if world == 1 else
+                                       "cell-key radix sort of the shard")},
             "build_ms": {k: round(v, 3) for k, v in build_ms.items()},
             "build_detail": build_detail,
             "build_roofline": build_roof,

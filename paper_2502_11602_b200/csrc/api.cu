@@ -303,6 +303,7 @@ static cm_status build_common(const double* xyz, uint64_t n, const cm_build_opti
   if (s == CM_OK) {
     cudaEventElapsedTime(&h2d, e0, e1);
     ix->timing.h2d_ms = in.owned ? h2d : 0.0;
+    if (!in.owned) ix->src = xyz;
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);

@@ -20,6 +20,9 @@ struct cm_index {
   int key_bits = 0;
 
   cmg::PointRec* rec = nullptr;  // n, cell order
+  // the caller's device buffer the index was built from (null for host
+  // input): a query batch at this address with n centres is the cloud itself
+  const void* src = nullptr;
   uint64_t* ukey = nullptr;      // U unique voxel keys (ascending)
   uint32_t* ustart = nullptr;    // U + 1 record offsets
   uint32_t* uk_k = nullptr;      // U voxel z index

@@ -1632,6 +1632,13 @@ __global__ void __launch_bounds__(kMidThreads) sort_mid_rows_kernel(
   }
 }
 
+__global__ void self_perm_kernel(const PointRec* __restrict__ rec, uint64_t n,
+                                 uint32_t* __restrict__ perm) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    perm[i] = rec[i].id;
+}
+
 template <typename K>
 cm_status order_typed(const cm_index* ix, const double* q, uint64_t nq, cudaStream_t st,
                       uint32_t* perm, bool range, double r, int kind) {
@@ -1741,6 +1748,18 @@ cm_status order_queries(const cm_index* ix, const double* q, uint64_t nq, cudaSt
   };
   // (2-bit extents for r <= cell, ranges of up to 3 cells, measured no gain at r = 1)
   const bool range = fits(2.0);
+  if (!range && ix->src == static_cast<const void*>(q) && nq == ix->n) {
+    // Self queries (every indexed point a centre, from the buffer the index
+    // was built from): the records' cell order IS the order the key sort
+    // would produce (same keys, both stable by handle), so take it from the
+    // records instead of sorting again. Any permutation gives the same
+    // results (rows go to caller positions); the order only shapes tiles, so
+    // a buffer rewritten since the build still answers correctly.
+    const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nq + 255) / 256, (uint64_t)sm_count() * 16));
+    self_perm_kernel<<<grid, 256, 0, st>>>(ix->rec, nq, out->perm); ::cmg::note_launch();
+    CM_CUDA_TRY(cudaGetLastError());
+    return CM_OK;
+  }
   const int bits = ix->key_bits + (range ? 3 : 0);
   return bits <= 32 ? order_typed<uint32_t>(ix, q, nq, st, out->perm, range, r, kind)
                     : order_typed<uint64_t>(ix, q, nq, st, out->perm, range, r, kind);

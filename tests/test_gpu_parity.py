@@ -290,3 +290,29 @@ def test_csr_digest_checker(cfg0, cfg0_oracle):
     cols[b], cols[b + 1] = cols[b + 1].clone(), cols[b].clone()
     check()
     assert bad.value == 1
+
+
+def test_self_queries_reuse_index_order(cfg0, cfg0_oracle):
+    """Centres = the device buffer the index was built from: the query order
+    comes from the index's records (no key sort). Results must equal the
+    oracle, and still do after the buffer is rewritten (any order is
+    correct; the order only shapes tiles)."""
+    import torch
+
+    cloud, _ = cfg0
+    d = torch.from_numpy(np.ascontiguousarray(cloud)).cuda()
+    for flavor in FLAVORS:
+        m = cm.Cheesemap.build(d, cm.BuildOptions(flavor=flavor))
+        for kernel, r in ((cm.SPHERE, 1.0), (cm.CUBE, 1.0), (cm.SPHERE, 2.5)):
+            row, cols = cm.radius_search_batch(m, d, r, kernel)
+            orow, ocols = cfg0_oracle.radius_csr(cloud, int(kernel), r)
+            assert np.array_equal(row, orow) and np.array_equal(cols, ocols)
+        idx, d2 = cm.knn_batch(m, d[:4000], 8)  # not the whole buffer: sorted path
+        oidx, od2 = cfg0_oracle.knn(cloud[:4000], 8)
+        assert np.array_equal(idx, oidx) and np.array_equal(d2, od2)
+    # rewrite the buffer (reversed points): same address and size, other centres
+    rev = np.ascontiguousarray(cloud[::-1])
+    d.copy_(torch.from_numpy(rev))
+    row, cols = cm.radius_search_batch(m, d, 1.0, cm.SPHERE)
+    orow, ocols = cfg0_oracle.radius_csr(rev, 0, 1.0)
+    assert np.array_equal(row, orow) and np.array_equal(cols, ocols)
