@@ -39,7 +39,13 @@ using namespace ::cmg::tw;  // tile_walk.cuh
 
 constexpr int kQThreads = 128;
 constexpr int kQWarps = kQThreads / 32;
-constexpr int kLaneRowCap = 128;                      // per-lane row buffer
+#ifndef CM_LANE_ROW_CAP
+#define CM_LANE_ROW_CAP 128
+#endif
+#ifndef CM_QTILE_MINB
+#define CM_QTILE_MINB 5
+#endif
+constexpr int kLaneRowCap = CM_LANE_ROW_CAP;          // per-lane row buffer
 // Per warp: the tile path's per-lane rows (u16 hit keys, interleaved with
 // stride 33) followed by the cp.async staging double buffer; the one-query
 // path reuses the whole region as a u32 buffer.
@@ -730,7 +736,7 @@ __device__ __forceinline__ void wide_tile(const Tables& t, const Range& R, bool 
 
 // Query-tile kernel (see the file comment).
 template <int FLAVOR, int MODE, int CUBE>
-__global__ void __launch_bounds__(kQThreads, 5) radius_tile_kernel(
+__global__ void __launch_bounds__(kQThreads, CM_QTILE_MINB) radius_tile_kernel(
     const Tables t, const double* __restrict__ q, uint64_t nq, double r,
     const uint32_t* __restrict__ perm, const Out o) {
   extern __shared__ __align__(16) unsigned char smraw[];
