@@ -137,12 +137,13 @@ def cpu_reference_lib():
         return lib("oracle"), "port"
 
 
-def run_cpu(cloud, a, steps, warmup, threads=0):
+def run_cpu(cloud, a, steps, warmup, threads=0, flavor=None):
     """Times the CPU implementation on bounded query samples. Returns a dict."""
     from oracle.oracle import CpuIndex
     L, kind = cpu_reference_lib()
+    flavor = flavor or a.flavor
     t0 = time.perf_counter()
-    idx = CpuIndex(cloud, flavor=FLAVORS[a.flavor], which=kind)
+    idx = CpuIndex(cloud, flavor=FLAVORS[flavor], which=kind)
     build_s = time.perf_counter() - t0
     nthreads = threads or os.cpu_count() or 1
     stride = max(1, cloud.shape[0] // a.cpu_sample)
@@ -156,8 +157,9 @@ def run_cpu(cloud, a, steps, warmup, threads=0):
             rates.append(q.shape[0] / dt)
     return dict(value=statistics.median(rates), kind=kind, cores=nthreads, build_ms=build_s * 1e3,
                 sample=f"{min(a.cpu_sample, cloud.shape[0])} of the {cloud.shape[0]} queries "
-                       f"(every {stride}th point), {a.flavor} map, {nthreads} threads, "
-                       f"median of {steps} steps; build single-threaded")
+                       f"(every {stride}th point, a different offset per step), {flavor} map, "
+                       f"{nthreads} threads, median of {steps} steps after {warmup} warm-up; "
+                       f"build single-threaded")
 
 
 def reference_arm(a):
@@ -234,6 +236,12 @@ def main():
         return float(t.item())
 
     L = _native.lib()
+    # This process owns the GPU: let the library's private pool keep 3/4 of
+    # HBM cached and reserve 32 GiB up front (cm_pool_configure; the library
+    # default keeps 1/8 and reserves nothing)
+    total_mem = torch.cuda.get_device_properties(local).total_memory
+    pool_keep, pool_reserve = int(total_mem * 0.75), min(32 << 30, int(total_mem * 0.2))
+    cm.pool_configure(local, pool_keep, pool_reserve)
     t0 = time.perf_counter()
     cloud = synth.config_cloud(a.config, a.scale)
     log(f"[rank {rank}] generated {cloud.shape[0]} points in {time.perf_counter() - t0:.1f}s")
@@ -284,9 +292,12 @@ def main():
         q_dev = d_cloud[shard].contiguous()
         shard_host = shard.cpu().numpy()
     else:
-        q_dev = d_cloud
+        # centres in a buffer of their own: the general path (key sort of the
+        # centres); the headline at N = 1 is cm_radius_search_self
+        q_dev = d_cloud.clone()
         shard_host = None
     nq = hi - lo
+    self_q = world == 1
 
     # algorithmic bytes: 24 B x the reference's points_tested for these queries
     tested = torch.zeros(nq, dtype=torch.int64, device=dev)
@@ -302,11 +313,18 @@ def main():
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
-    def step_device():
+    def step_general():
         csr = ctypes.c_void_p()
         cm._check(L.cm_radius_search(index.handle, ctypes.c_void_p(q_dev.data_ptr()), nq, kernel,
                                      a.radius, sptr, ctypes.byref(csr)))
         return csr
+
+    def step_self():
+        csr = ctypes.c_void_p()
+        cm._check(L.cm_radius_search_self(index.handle, kernel, a.radius, sptr, ctypes.byref(csr)))
+        return csr
+
+    step_device = step_self if self_q else step_general
 
     for _ in range(a.warmup):
         csr = step_device()
@@ -344,6 +362,29 @@ def main():
     ms = allmax(ms_rank)
     value = nq_total / (ms * 1e-3)
 
+    # the same workload with the centres in a caller buffer (the general
+    # path: centre-key sort + the same kernels), reported beside the headline
+    general = None
+    if self_q:
+        for _ in range(2):
+            L.cm_csr_free(step_general())
+        g_ms = []
+        for _ in range(a.steps):
+            flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            csr = step_general()
+            e1.record(stream)
+            e1.synchronize()
+            g_ms.append(e0.elapsed_time(e1))
+            L.cm_csr_free(csr)
+        gm = sum(g_ms) / len(g_ms)
+        general = {"value": round(nq_total / (gm * 1e-3), 1), "unit": "queries/s",
+                   "ms_per_step": round(gm, 4),
+                   "call": "cm_radius_search with the centres in a separate device buffer "
+                           "(cell-key radix sort of the centres inside the step)"}
+
     def mean_of(key):
         return sum(k[key] for k in kern) / len(kern)
 
@@ -355,17 +396,21 @@ def main():
     dom_ms = phase[dom]
     peak, peak_src = read_peak()
     achieved = alg_bytes / (dom_ms * 1e-3) / 1e9
-    traffic = None
+    traffic, traffic_src = None, None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
             with open(tpath) as f:
                 tj = json.load(f)
             traffic = tj.get(f"{a.flavor}/collect/r{a.radius:g}")
+            traffic_src = ("not measured in this run: ncu dram__bytes_read.sum + "
+                           "dram__bytes_write.sum of this kernel from " +
+                           tj.get("_source", "profiles/traffic.json"))
         except Exception:
             traffic = None
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
+                "traffic_source": traffic_src,
                 "kernel": "radius_tile_kernel<" + a.flavor + ", " +
                           ("COUNT (two-pass fallback)" if two_pass else "COLLECT") + ">",
                 "kernel_ms": dom_ms, "alg_bytes_per_launch": alg_bytes,
@@ -420,10 +465,14 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         try:
-            r = run_cpu(cloud, a, steps=1, warmup=0)
+            r = run_cpu(cloud, a, steps=3, warmup=1)
             cpu = {"value": r["value"], "unit": "queries/s", "cores": r["cores"],
                    "kind": r["kind"], "sample": r["sample"],
                    "build_ms": {a.flavor: round(r["build_ms"], 1)}}
+            if a.flavor != "dense":  # the CPU's fastest flavour, for context
+                rd = run_cpu(cloud, a, steps=3, warmup=1, flavor="dense")
+                cpu["dense_map"] = {"value": rd["value"], "sample": rd["sample"],
+                                    "build_ms": round(rd["build_ms"], 1)}
         except Exception as ex:  # noqa: BLE001
             cpu = {"value": None, "unit": "queries/s", "cores": None, "kind": None,
                    "sample": f"unavailable: {ex}"}
@@ -442,13 +491,17 @@ def main():
                        "l2": "flushed (256 MB write) before every timed step",
                        "parallelism": f"replicated index, queries sharded x{world} "
                                       "(equal-count x-slabs)",
-                       "query_order": ("the index's record order (centres = the indexed "
-                                       "device buffer; no key sort)" if world == 1 else
-                                       "cell-key radix sort of the shard")},
+                       "call": ("cm_radius_search_self (every indexed point a centre; "
+                                "centres read in the index's cell order, no key sort)"
+                                if self_q else "cm_radius_search (cell-key radix sort of the "
+                                "shard's centres)"),
+                       "pool": f"cm_pool_configure(keep {pool_keep >> 30} GiB, "
+                               f"reserve {pool_reserve >> 30} GiB)"},
             "build_ms": {k: round(v, 3) for k, v in build_ms.items()},
             "build_detail": build_detail,
             "build_roofline": build_roof,
             "phases_ms": phase,
+            "general_centres": general,
             "tile_stats": step_stats,
             "roofline": roofline,
             "e2e": e2e,

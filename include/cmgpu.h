@@ -180,9 +180,16 @@ cm_status cm_radius_fill(const cm_index* index, const double* q, uint64_t nq,
                          int kernel, double r, const uint64_t* row_ptr,
                          uint32_t* cols, void* stream);
 /* count + scan + fill in one call; the CSR lives in device memory owned by
- * the returned cm_csr. */
+ * the returned cm_csr. The output size is data-dependent, so this call waits
+ * (host-side) for the neighbour total before it allocates the columns; the
+ * kernels themselves run in order on `stream`. */
 cm_status cm_radius_search(const cm_index* index, const double* q, uint64_t nq,
                            int kernel, double r, void* stream, cm_csr** out);
+/* cm_radius_search with every indexed point as a centre (row q = point q):
+ * the "every point is a query" workload. Centres are read from the index's
+ * own cell-ordered copy of the points, so no query sort runs. */
+cm_status cm_radius_search_self(const cm_index* index, int kernel, double r, void* stream,
+                                cm_csr** out);
 /* The same search with HOST buffers end to end: queries from host memory,
  * the sorted CSR to host memory (row_ptr: nq + 1 entries; cols: up to
  * cols_capacity). With CMGPU_CHUNKS=K in the environment, queries are
@@ -246,6 +253,12 @@ uint64_t cm_launch_count(void);
  * tiles, tiles answered one query per warp (fallback), hull points,
  * in-range candidates (count pass only). out8 has 8 entries. */
 cm_status cm_debug_query_stats(uint64_t* out8, int reset);
+/* The library allocates from a private stream-ordered pool per device.
+ * Defaults: nothing reserved, up to 1/8 of HBM kept cached across
+ * synchronisations. A process that owns the GPU may keep more cached
+ * (keep_bytes) and reserve a block up front (reserve_bytes), so later calls
+ * carve from it instead of mapping fresh memory. */
+cm_status cm_pool_configure(int device, uint64_t keep_bytes, uint64_t reserve_bytes);
 /* Device memory held by this library's stream-ordered pool on `device`:
  * reserved (cached + in use) and in use, in bytes; trim != 0 first returns
  * the cached part to the device. */

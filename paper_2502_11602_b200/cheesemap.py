@@ -152,14 +152,48 @@ def _is_torch(x):
     return type(x).__module__.startswith("torch")
 
 
-def _in_ptr(x, dtype=np.float64):
-    """Pointer to a host (numpy) or device (torch) buffer, plus a keepalive."""
+# torch dtypes the native code may read as each element type (same width;
+# torch has no unsigned 32/64-bit tensors in most builds, so the signed twins
+# are accepted and reinterpreted)
+_TORCH_DTYPES = {np.dtype(np.float64): ("float64",),
+                 np.dtype(np.uint32): ("int32", "uint32"),
+                 np.dtype(np.uint64): ("int64", "uint64")}
+
+
+def _in_ptr(x, dtype=np.float64, device=None, output=False):
+    """Pointer to a host (numpy) or device (torch) buffer, plus a keepalive.
+
+    Torch tensors are passed by address, so they must already have the
+    element type the C ABI reads (float64 points, u32 counts, u64 stats) and,
+    for points, 3 values per row; a CUDA tensor must live on the index's
+    device. Anything else raises InvalidArgumentError instead of letting the
+    native code read n*24 bytes out of a smaller buffer. Outputs must be
+    contiguous (a copy would not be written back)."""
     if x is None:
         return None, None
+    dt = np.dtype(dtype)
     if _is_torch(x):
-        x = x.contiguous()
+        tname = str(x.dtype).replace("torch.", "")
+        if tname not in _TORCH_DTYPES[dt]:
+            raise InvalidArgumentError(f"tensor dtype {x.dtype} where {dt.name} is expected")
+        if dt == np.float64 and not (x.dim() == 2 and x.shape[1] == 3) and \
+                not (x.dim() == 1 and x.shape[0] % 3 == 0):
+            raise InvalidArgumentError(f"points must be (n, 3) float64, got {tuple(x.shape)}")
+        if x.is_cuda and device is not None and x.device.index != device:
+            raise InvalidArgumentError(f"tensor on {x.device}, index on cuda:{device}")
+        if not x.is_contiguous():
+            if output:
+                raise InvalidArgumentError("output tensor must be contiguous")
+            x = x.contiguous()
         return ctypes.c_void_p(x.data_ptr()), x
+    if output:
+        if not (isinstance(x, np.ndarray) and x.dtype == dt and x.flags.c_contiguous):
+            raise InvalidArgumentError(f"output array must be contiguous {dt.name}")
+        return x.ctypes.data_as(ctypes.c_void_p), x
     a = np.ascontiguousarray(x, dtype=dtype)
+    if dt == np.float64 and not (a.ndim == 2 and a.shape[1] == 3) and \
+            not (a.ndim == 1 and a.shape[0] % 3 == 0):
+        raise InvalidArgumentError(f"points must be (n, 3) float64, got {a.shape}")
     return a.ctypes.data_as(ctypes.c_void_p), a
 
 
@@ -190,7 +224,7 @@ class Cheesemap:
     def build(cloud, opts=None, device=0, stream=None):
         opts = opts or BuildOptions()
         L = _native.lib()
-        p, keep = _in_ptr(cloud)
+        p, keep = _in_ptr(cloud, device=device)
         n = _nrows(keep) if keep is not None else 0
         h = ctypes.c_void_p()
         c = opts.to_c()
@@ -289,12 +323,16 @@ def _kernel_args(kernel):
 
 def radius_count(m, centers, r, kernel=SPHERE, counts=None, points_tested=None, stream=None):
     """Per-centre neighbour counts (and QueryStats::points_tested)."""
-    qp, qk = _in_ptr(centers)
+    qp, qk = _in_ptr(centers, device=m.device)
     nq = _nrows(qk)
     if counts is None:
         counts = np.zeros(nq, dtype=np.uint32)
-    cp, ck = _in_ptr(counts, np.uint32)
-    tp, tk = _in_ptr(points_tested, np.uint64) if points_tested is not None else (None, None)
+    cp, ck = _in_ptr(counts, np.uint32, device=m.device, output=True)
+    tp, tk = (_in_ptr(points_tested, np.uint64, device=m.device, output=True)
+              if points_tested is not None else (None, None))
+    for o in (ck, tk):
+        if o is not None and (o.numel() if _is_torch(o) else o.size) < nq:
+            raise InvalidArgumentError("output buffer holds fewer than one entry per centre")
     _check(_native.lib().cm_radius_count(m.handle, qp, nq, kernel, float(r), cp, tp,
                                          _stream_ptr(stream)))
     return counts if not isinstance(counts, np.ndarray) else ck
@@ -303,20 +341,41 @@ def radius_count(m, centers, r, kernel=SPHERE, counts=None, points_tested=None, 
 def radius_search_batch(m, centers, r, kernel=SPHERE, stream=None, device_out=False):
     """Sorted CSR of kernel_search over every centre: (row_ptr u64[nq+1],
     cols u32[nnz]) as numpy arrays, or as CUDA torch tensors when
-    device_out=True."""
-    qp, qk = _in_ptr(centers)
-    nq = _nrows(qk)
+    device_out=True. centers=None: every indexed point is a centre (row q =
+    point q, cm_radius_search_self)."""
     L = _native.lib()
     csr = ctypes.c_void_p()
-    _check(L.cm_radius_search(m.handle, qp, nq, kernel, float(r), _stream_ptr(stream),
-                              ctypes.byref(csr)))
+    if centers is None:
+        nq = m.size()
+        _check(L.cm_radius_search_self(m.handle, kernel, float(r), _stream_ptr(stream),
+                                       ctypes.byref(csr)))
+    else:
+        qp, qk = _in_ptr(centers, device=m.device)
+        nq = _nrows(qk)
+        _check(L.cm_radius_search(m.handle, qp, nq, kernel, float(r), _stream_ptr(stream),
+                                  ctypes.byref(csr)))
+    return _take_csr(L, csr, nq, m.device, stream, device_out)
+
+
+def radius_search_self(m, r, kernel=SPHERE, stream=None, device_out=False):
+    """Every indexed point as a centre: radius_search_batch(m, None, ...)."""
+    return radius_search_batch(m, None, r, kernel, stream, device_out)
+
+
+def pool_configure(device=0, keep_bytes=0, reserve_bytes=0):
+    """cm_pool_configure: how much device memory the library's private pool
+    keeps cached across synchronisations, and an up-front reservation."""
+    _check(_native.lib().cm_pool_configure(int(device), int(keep_bytes), int(reserve_bytes)))
+
+
+def _take_csr(L, csr, nq, device, stream, device_out):
     try:
         nnz = ctypes.c_uint64()
         _check(L.cm_csr_info(csr, None, ctypes.byref(nnz), None, None))
         if device_out:
             import torch
-            row = torch.empty(nq + 1, dtype=torch.int64, device=f"cuda:{m.device}")
-            cols = torch.empty(max(nnz.value, 1), dtype=torch.int32, device=f"cuda:{m.device}")
+            row = torch.empty(nq + 1, dtype=torch.int64, device=f"cuda:{device}")
+            cols = torch.empty(max(nnz.value, 1), dtype=torch.int32, device=f"cuda:{device}")
             _check(L.cm_csr_download(csr, ctypes.c_void_p(row.data_ptr()),
                                      ctypes.c_void_p(cols.data_ptr()), _stream_ptr(stream)))
             return row, cols[: nnz.value]
@@ -331,7 +390,7 @@ def radius_search_batch(m, centers, r, kernel=SPHERE, stream=None, device_out=Fa
 
 def radius_digest_batch(m, centers, r, kernel=SPHERE, stream=None):
     """Per-centre (count u32, digest u64 = sum(mix64(handle)))."""
-    qp, qk = _in_ptr(centers)
+    qp, qk = _in_ptr(centers, device=m.device)
     nq = _nrows(qk)
     counts = np.zeros(nq, dtype=np.uint32)
     dig = np.zeros(nq, dtype=np.uint64)
@@ -345,7 +404,7 @@ def radius_digest_batch(m, centers, r, kernel=SPHERE, stream=None):
 def knn_batch(m, centers, k, stream=None, device_out=False):
     """(idx u32[nq, k], d2 f64[nq, k]) ordered by (d^2, handle); with
     device_out=True, CUDA tensors (int32 / float64) that stay on the device."""
-    qp, qk = _in_ptr(centers)
+    qp, qk = _in_ptr(centers, device=m.device)
     nq = _nrows(qk)
     if device_out:
         import torch
@@ -462,7 +521,7 @@ def brute_radius(cloud, centers, r, kernel=SPHERE, device=0, stream=None):
     """brute_radius (baseline.hpp:11-21) on the device: every point tested
     against every centre -> (counts u32[nq], digests u64[nq])."""
     pp, pk = _in_ptr(cloud)
-    qp, qk = _in_ptr(centers)
+    qp, qk = _in_ptr(centers, device=device)
     nq = _nrows(qk)
     counts = np.zeros(nq, dtype=np.uint32)
     digests = np.zeros(nq, dtype=np.uint64)
@@ -477,7 +536,7 @@ def brute_knn(cloud, centers, k, device=0, stream=None):
     """brute_knn (baseline.cpp:8-25) on the device, ordered by (d^2, handle):
     (idx u32[nq, k], d2 f64[nq, k]); k <= 64."""
     pp, pk = _in_ptr(cloud)
-    qp, qk = _in_ptr(centers)
+    qp, qk = _in_ptr(centers, device=device)
     nq = _nrows(qk)
     idx = np.zeros((nq, k), dtype=np.uint32)
     d2 = np.zeros((nq, k), dtype=np.float64)

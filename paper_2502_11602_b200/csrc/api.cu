@@ -18,7 +18,6 @@ namespace cmg {
 namespace {
 thread_local std::string g_last_error;
 std::mutex g_pool_mu;
-bool g_pool_configured[64] = {};
 }  // namespace
 
 void set_error(const std::string& msg) { g_last_error = msg; }
@@ -39,55 +38,74 @@ int sm_count() {
   return cached[dev];
 }
 
-static void configure_pool() {
-  int dev = 0;
-  cudaGetDevice(&dev);
+// The library's device memory comes from a PRIVATE stream-ordered pool per
+// device (not the device's default pool), so torch or any other user of the
+// default pool is unaffected by what this pool caches. Defaults are
+// conservative: nothing is reserved up front, and at most 1/8 of HBM stays
+// cached across synchronisations. Serving processes that own the GPU opt in
+// to more with cm_pool_configure (the bench does: a reservation carved into
+// later requests avoids mapping fresh memory inside a call — measured 0.3-12
+// ms per cudaMallocAsync once the pool's chunks fragment) or with
+// CMGPU_POOL_KEEP_FRAC / CMGPU_POOL_RESERVE_GB in the environment.
+struct DevicePool {
+  cudaMemPool_t pool = nullptr;
+  bool tried = false;
+};
+DevicePool g_pools[kMaxDevices];
+
+static cudaError_t reserve_in_pool(cudaMemPool_t pool, uint64_t bytes) {
+  if (!bytes) return cudaSuccess;
+  void* p = nullptr;
+  cudaError_t e = cudaMallocFromPoolAsync(&p, bytes, pool, 0);
+  if (e == cudaSuccess) cudaFreeAsync(p, 0);
+  cudaStreamSynchronize(0);
+  cudaGetLastError();
+  return e;
+}
+
+static cudaMemPool_t device_pool(int dev) {
+  if (dev < 0 || dev >= kMaxDevices) return nullptr;
   std::lock_guard<std::mutex> lk(g_pool_mu);
-  if (dev >= 0 && dev < 64 && !g_pool_configured[dev]) {
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      // keep up to 3/4 of the device's memory cached across calls (steady
-      // state batches then allocate nothing; config 4's 200M-query calls need
-      // ~80 GB, and a pool trimmed back at every sync re-maps it inside the
-      // next call), return the rest at syncs; CMGPU_POOL_KEEP_FRAC overrides
-      size_t fr = 0, tot = 0;
-      cudaMemGetInfo(&fr, &tot);
-      double keep = 0.75;
-      if (const char* kf = std::getenv("CMGPU_POOL_KEEP_FRAC")) keep = std::atof(kf);
-      uint64_t thr = (uint64_t)((double)tot * std::min(1.0, std::max(0.0, keep)));
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-      // Reserve one large block up front: the pool then carves later
-      // requests out of it instead of mapping fresh physical memory for
-      // every new size (measured: 0.3-12 ms per cudaMallocAsync once the
-      // pool's chunks fragment; builds went 2.2 -> 3.9 ms). Default
-      // min(32 GiB, free / 4); CMGPU_POOL_RESERVE_GB overrides (0 = off).
-      double gb = std::min(32.0, (double)fr / 4.0 / (double)(1ull << 30));
-      if (const char* r = std::getenv("CMGPU_POOL_RESERVE_GB")) gb = std::atof(r);
-      if (gb > 0.0) {
-        void* p = nullptr;
-        if (cudaMallocAsync(&p, (size_t)(gb * (double)(1ull << 30)), 0) == cudaSuccess)
-          cudaFreeAsync(p, 0);
-        cudaStreamSynchronize(0);
-        cudaGetLastError();
-      }
+  DevicePool& dp = g_pools[dev];
+  if (!dp.tried) {
+    dp.tried = true;
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    if (cudaMemPoolCreate(&dp.pool, &props) != cudaSuccess) {
+      cudaGetLastError();
+      dp.pool = nullptr;
+      return nullptr;
     }
-    g_pool_configured[dev] = true;
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    double keep = 0.125;
+    if (const char* kf = std::getenv("CMGPU_POOL_KEEP_FRAC")) keep = std::atof(kf);
+    uint64_t thr = (uint64_t)((double)tot * std::min(1.0, std::max(0.0, keep)));
+    cudaMemPoolSetAttribute(dp.pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    if (const char* r = std::getenv("CMGPU_POOL_RESERVE_GB"))
+      reserve_in_pool(dp.pool, (uint64_t)(std::atof(r) * (double)(1ull << 30)));
   }
+  return dp.pool;
 }
 
 cudaError_t dev_alloc(void** p, size_t bytes, cudaStream_t st) {
-  configure_pool();
-  cudaError_t e = cudaMallocAsync(p, bytes == 0 ? 16 : bytes, st);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaMemPool_t pool = device_pool(dev);
+  auto alloc = [&]() {
+    return pool ? cudaMallocFromPoolAsync(p, bytes == 0 ? 16 : bytes, pool, st)
+                : cudaMallocAsync(p, bytes == 0 ? 16 : bytes, st);
+  };
+  cudaError_t e = alloc();
   if (e == cudaErrorMemoryAllocation) {
-    // the pool keeps freed blocks cached (release threshold = max): give
-    // them back to the device and retry once
+    // the pool keeps freed blocks cached: give them back to the device and
+    // retry once
     cudaGetLastError();
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaMemPool_t pool;
     cudaDeviceSynchronize();
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
-    e = cudaMallocAsync(p, bytes == 0 ? 16 : bytes, st);
+    if (pool) cudaMemPoolTrimTo(pool, 0);
+    e = alloc();
   }
   return e;
 }
@@ -230,8 +248,11 @@ cm_status cm_debug_pool_bytes(int device, int trim, uint64_t* reserved, uint64_t
     return CM_INVALID_ARGUMENT;
   }
   DeviceGuard dg(device);
-  cudaMemPool_t pool;
-  CM_CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, device));
+  cudaMemPool_t pool = device_pool(device);
+  if (!pool) {
+    set_error("no device pool");
+    return CM_CUDA;
+  }
   if (trim) {
     CM_CUDA_TRY(cudaDeviceSynchronize());
     CM_CUDA_TRY(cudaMemPoolTrimTo(pool, 0));
@@ -241,6 +262,27 @@ cm_status cm_debug_pool_bytes(int device, int trim, uint64_t* reserved, uint64_t
   CM_CUDA_TRY(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &u));
   *reserved = r;
   *used = u;
+  return CM_OK;
+}
+
+cm_status cm_pool_configure(int device, uint64_t keep_bytes, uint64_t reserve_bytes) {
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+    cudaGetLastError();
+    set_error("device ordinal out of range");
+    return CM_INVALID_ARGUMENT;
+  }
+  DeviceGuard dg(device);
+  cudaMemPool_t pool = device_pool(device);
+  if (!pool) {
+    set_error("no device pool");
+    return CM_CUDA;
+  }
+  CM_CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep_bytes));
+  if (reserve_in_pool(pool, reserve_bytes) != cudaSuccess) {
+    set_error("pool reservation failed");
+    return CM_CUDA;
+  }
   return CM_OK;
 }
 
@@ -303,7 +345,6 @@ static cm_status build_common(const double* xyz, uint64_t n, const cm_build_opti
   if (s == CM_OK) {
     cudaEventElapsedTime(&h2d, e0, e1);
     ix->timing.h2d_ms = in.owned ? h2d : 0.0;
-    if (!in.owned) ix->src = xyz;
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
@@ -548,17 +589,21 @@ cm_status cm_radius_fill(const cm_index* ix, const double* q, uint64_t nq, int k
 namespace {
 struct QueryEvents {
   cudaEvent_t e[6];
+  int device = 0;
   uint64_t nq = 0, nnz = 0;
   int two_pass = 0;  // 0 collect, 1 count + fill, 2 collect rerun (cm_query_timing)
   bool valid = false;
   QueryEvents() {
+    cudaGetDevice(&device);
     for (auto& x : e) cudaEventCreate(&x);
   }
 };
-thread_local QueryEvents* g_qev = nullptr;
+// the events of the last radius search on this thread (any device)
+thread_local QueryEvents* g_last_qev = nullptr;
 QueryEvents& qev() {
-  if (!g_qev) g_qev = new QueryEvents();
-  return *g_qev;
+  QueryEvents& ev = per_thread_device<QueryEvents>();
+  g_last_qev = &ev;
+  return ev;
 }
 }  // namespace
 
@@ -566,11 +611,12 @@ extern "C" {
 
 cm_status cm_get_last_query_timing(cm_query_timing* o) {
   if (!o) return CM_INVALID_ARGUMENT;
-  QueryEvents& ev = qev();
-  if (!ev.valid) {
+  if (!g_last_qev || !g_last_qev->valid) {
     set_error("no radius search has run on this thread");
     return CM_INVALID_ARGUMENT;
   }
+  QueryEvents& ev = *g_last_qev;
+  DeviceGuard dg(ev.device);
   CM_CUDA_TRY(cudaEventSynchronize(ev.e[5]));
   float ms[5], tot;
   for (int i = 0; i < 5; ++i) cudaEventElapsedTime(&ms[i], ev.e[i], ev.e[i + 1]);
@@ -623,12 +669,13 @@ struct MappedSlot {
   }
 };
 bool read_u64_mapped(const unsigned long long* dsrc, cudaStream_t st, unsigned long long* out) {
-  thread_local MappedSlot slot;  // per host thread (and device current at first use)
+  MappedSlot& slot = per_thread_device<MappedSlot>();
   if (!slot.ok) {
     if (cudaMemcpyAsync(out, dsrc, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess) return false;
     return cudaStreamSynchronize(st) == cudaSuccess;
   }
   cmg::apik::publish_u64_kernel<<<1, 1, 0, st>>>(dsrc, slot.dev); ::cmg::note_launch();
+  if (cudaGetLastError() != cudaSuccess) return false;
   if (cudaEventRecord(slot.ev, st) != cudaSuccess) return false;
   if (cudaEventSynchronize(slot.ev) != cudaSuccess) return false;
   *out = *reinterpret_cast<volatile unsigned long long*>(slot.host);
@@ -639,7 +686,8 @@ bool read_u64_mapped(const unsigned long long* dsrc, cudaStream_t st, unsigned l
 // idx is a host array; it travels in the mapped page too.
 bool read_row_ptrs_mapped(const uint64_t* row_ptr, const uint64_t* idx, int n, cudaStream_t st,
                           uint64_t* out) {
-  thread_local MappedSlot slot;
+  struct RowSlot : MappedSlot {};  // a second page per thread and device
+  MappedSlot& slot = per_thread_device<RowSlot>();
   if (!slot.ok || n > 256) {
     for (int k = 0; k < n; ++k)
       if (cudaMemcpyAsync(out + k, row_ptr + idx[k], 8, cudaMemcpyDeviceToHost, st) != cudaSuccess)
@@ -650,6 +698,7 @@ bool read_row_ptrs_mapped(const uint64_t* row_ptr, const uint64_t* idx, int n, c
   std::memcpy(hidx, idx, n * sizeof(uint64_t));
   const uint64_t* didx = reinterpret_cast<const uint64_t*>(slot.dev) + 256;
   cmg::apik::publish_gather_kernel<<<1, 256, 0, st>>>(row_ptr, didx, n, slot.dev); ::cmg::note_launch();
+  if (cudaGetLastError() != cudaSuccess) return false;
   if (cudaEventRecord(slot.ev, st) != cudaSuccess) return false;
   if (cudaEventSynchronize(slot.ev) != cudaSuccess) return false;
   for (int k = 0; k < n; ++k) out[k] = reinterpret_cast<volatile unsigned long long*>(slot.host)[k];
@@ -677,6 +726,7 @@ static cm_status radius_search_core(const cm_index* ix, const double* qd, uint64
   cudaEventRecord(ev.e[0], st);
   QueryOrder ord;
   CM_TRY(order_queries(ix, qd, nq, st, &ord, r, kernel));
+  qd = ord.q;  // null for self queries read from the records
   cudaEventRecord(ev.e[1], st);
   uint32_t* counts = nullptr;
   uint64_t* toff = nullptr;
@@ -711,7 +761,8 @@ static cm_status radius_search_core(const cm_index* ix, const double* qd, uint64
   // then holds the exact arena size: the collect reruns once into an arena of
   // that size (query subsets differ in density, e.g. the chunks of a
   // host-buffer call over a cloud generated ground first, buildings last).
-  uint64_t cap = (uint64_t)((double)nq * ix->nnz_per_query * 1.25) + (1u << 20);
+  const double est = ix->nnz_per_query.load(std::memory_order_relaxed);
+  uint64_t cap = (uint64_t)((double)nq * est * 1.25) + (1u << 20);
   bool two_pass = radius_is_wide(ix, r);
   if (!two_pass && dev_alloc_t(&temp, cap, st) != cudaSuccess) {
     two_pass = true;
@@ -731,7 +782,8 @@ static cm_status radius_search_core(const cm_index* ix, const double* qd, uint64
     }
     // slow decay: alternating dense and sparse batches keep the larger size
     if (nq)
-      ix->nnz_per_query = std::max({1.0, (double)used / (double)nq, 0.95 * ix->nnz_per_query});
+      ix->nnz_per_query.store(std::max({1.0, (double)used / (double)nq, 0.95 * est}),
+                              std::memory_order_relaxed);
     if (used > cap && !std::getenv("CMGPU_NO_RECOLLECT")) {
       dev_free(temp, st);
       temp = nullptr;
@@ -840,6 +892,33 @@ cm_status cm_radius_search(const cm_index* ix, const double* q, uint64_t nq, int
   return CM_OK;
 }
 
+// Every indexed point as a centre (the "every point is a query" workloads of
+// SURVEY.md §8d configs 1 and 4): row q is the result for point q. The
+// centres are read from the index's own cell-ordered records, so no query
+// sort runs and the caller passes no buffer.
+cm_status cm_radius_search_self(const cm_index* ix, int kernel, double r, void* stream,
+                                cm_csr** out) {
+  CM_TRY(check_index(ix));
+  CM_TRY(check_kernel(kernel));
+  if (!out) {
+    set_error("null output pointer");
+    return CM_INVALID_ARGUMENT;
+  }
+  *out = nullptr;
+  DeviceGuard dg(ix->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cm_csr* csr = new cm_csr();
+  csr->nq = ix->n;
+  csr->device = ix->device;
+  const cm_status s = radius_search_core(ix, nullptr, ix->n, kernel, r, st, csr);
+  if (s != CM_OK) {
+    cm_csr_free(csr);
+    return s;
+  }
+  *out = csr;
+  return CM_OK;
+}
+
 namespace {
 // One-chunk to_host: once the row pointers are scanned, the gather runs in G
 // query ranges and each range's columns start their device->host copy as
@@ -864,7 +943,7 @@ struct StreamingGather : GatherHook {
         for (auto& x : e) cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
       }
     };
-    thread_local Events evs;
+    Events& evs = per_thread_device<Events>();
     uint64_t qb[G + 1], rp[G + 1];
     for (int k = 0; k <= G; ++k) qb[k] = nq * (uint64_t)k / G;
     if (!read_row_ptrs_mapped(row_ptr, qb, G + 1, st, rp)) {
@@ -874,8 +953,8 @@ struct StreamingGather : GatherHook {
     nnz = rp[G];
     over = nnz > cap;
     if (rows_early) {
-      cudaEventRecord(evs.e[G], st);
-      cudaStreamWaitEvent(out, evs.e[G], 0);
+      CM_CUDA_TRY(cudaEventRecord(evs.e[G], st));
+      CM_CUDA_TRY(cudaStreamWaitEvent(out, evs.e[G], 0));
       CM_CUDA_TRY(cudaMemcpyAsync(row_ptr_host + 1, row_ptr + 1, nq * 8, cudaMemcpyDeviceToHost, out));
     }
     for (int k = 0; k < G; ++k) {
@@ -883,8 +962,8 @@ struct StreamingGather : GatherHook {
       CM_TRY(gather_rows_dev(temp, toff + qb[k], scnt + qb[k], row_ptr + qb[k], perm, cols,
                              qb[k + 1] - qb[k], st));
       if (!over && rp[k + 1] > rp[k]) {
-        cudaEventRecord(evs.e[k], st);
-        cudaStreamWaitEvent(out, evs.e[k], 0);
+        CM_CUDA_TRY(cudaEventRecord(evs.e[k], st));
+        CM_CUDA_TRY(cudaStreamWaitEvent(out, evs.e[k], 0));
         CM_CUDA_TRY(cudaMemcpyAsync(cols_host + rp[k], cols + rp[k], (rp[k + 1] - rp[k]) * 4,
                                     cudaMemcpyDeviceToHost, out));
       }
@@ -917,7 +996,7 @@ cm_status cm_radius_search_to_host(const cm_index* ix, const double* q_host, uin
       cudaStreamCreateWithFlags(&out, cudaStreamNonBlocking);
     }
   };
-  thread_local Streams ss;
+  Streams& ss = per_thread_device<Streams>();
   // Every chunk's CSR streams to the host while its gather runs, and chunk
   // i+1's input copy and kernels overlap chunk i's columns on PCIe, which
   // bounds the call (~54 GB/s device->host vs ~1 G queries/s of kernels).
@@ -1159,7 +1238,7 @@ cm_status cm_csr_digest(const uint64_t* row_ptr, const uint32_t* cols, uint64_t 
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   unsigned long long* dbad = nullptr;
-  CM_CUDA_TRY(cudaMallocAsync(&dbad, 8, st));
+  CM_CUDA_TRY(dev_alloc_t(&dbad, 1, st));
   cm_status s = csr_digest_dev(row_ptr, cols, nq, counts, digests, dbad, st);
   unsigned long long h = 0;
   if (s == CM_OK && cudaMemcpyAsync(&h, dbad, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess)

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <vector>
 
 #include "common.cuh"
@@ -20,9 +21,6 @@ struct cm_index {
   int key_bits = 0;
 
   cmg::PointRec* rec = nullptr;  // n, cell order
-  // the caller's device buffer the index was built from (null for host
-  // input): a query batch at this address with n centres is the cloud itself
-  const void* src = nullptr;
   uint64_t* ukey = nullptr;      // U unique voxel keys (ascending)
   uint32_t* ustart = nullptr;    // U + 1 record offsets
   uint32_t* uk_k = nullptr;      // U voxel z index
@@ -39,7 +37,9 @@ struct cm_index {
 
   std::vector<uint64_t> slice_ne;  // per z slice non-empty voxels (host)
   // Running estimate of neighbours per query, sizing the single-pass arena.
-  mutable double nnz_per_query = 64.0;
+  // Queries may run concurrently from many host threads (map.hpp:50-52), so
+  // it is an atomic; lost updates between threads only change arena sizing.
+  mutable std::atomic<double> nnz_per_query{64.0};
   cm_build_timing timing{};
 
   cmg::Tables tables() const {
@@ -62,6 +62,21 @@ struct cm_index {
 };
 
 namespace cmg {
+
+constexpr int kMaxDevices = 64;
+
+// One T per host thread AND per device: CUDA events and streams belong to
+// the device that was current when they were created, and an index may be
+// queried from any thread, one device after another. Callers have already
+// made the index's device current (DeviceGuard).
+template <typename T>
+T& per_thread_device() {
+  thread_local T* objs[kMaxDevices] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) dev = 0;
+  if (!objs[dev]) objs[dev] = new T();
+  return *objs[dev];
+}
 
 // Device-memory helpers (stream-ordered pool).
 cudaError_t dev_alloc(void** p, size_t bytes, cudaStream_t st);
@@ -92,12 +107,18 @@ cm_status build_index(const double* xyz_dev, uint64_t n, const cm_build_options&
 // Query pipeline pieces (query.cu)
 struct QueryOrder {
   uint32_t* perm = nullptr;  // sorted position -> query index
+  // the centres the kernels read: the caller's, a materialised copy
+  // (owned_q), or null = self queries read from the index's records
+  const double* q = nullptr;
+  double* owned_q = nullptr;
   uint64_t nq = 0;
   cudaStream_t st = nullptr;
   ~QueryOrder() {
     if (perm) dev_free(perm, st);
+    if (owned_q) dev_free(owned_q, st);
   }
 };
+// q_dev == nullptr: self queries (the index's own n points, row q = point q).
 cm_status order_queries(const cm_index* ix, const double* q_dev, uint64_t nq, cudaStream_t st,
                         QueryOrder* out, double r = -1.0, int kind = 0);
 cm_status radius_count_dev(const cm_index* ix, const double* q_dev, uint64_t nq, int kernel,

@@ -46,6 +46,9 @@ constexpr int kQWarps = kQThreads / 32;
 #define CM_QTILE_MINB 5
 #endif
 constexpr int kLaneRowCap = CM_LANE_ROW_CAP;          // per-lane row buffer
+// the FILL row translation and the gather's warp sort of 97..cap rows hold a
+// row in 4 registers per lane (4 x 32 = 128 handles)
+static_assert(kLaneRowCap >= 97 && kLaneRowCap <= 128, "CM_LANE_ROW_CAP must be in [97, 128]");
 // Per warp: the tile path's per-lane rows (u16 hit keys, interleaved with
 // stride 33) followed by the cp.async staging double buffer; the one-query
 // path reuses the whole region as a u32 buffer.
@@ -757,12 +760,21 @@ __global__ void __launch_bounds__(kQThreads, CM_QTILE_MINB) radius_tile_kernel(
   for (uint64_t tile = (uint64_t)blockIdx.x * kQWarps + wib; tile < ntiles; tile += W) {
     const uint64_t s = tile * 32 + lane;
     const bool active = s < nq;
-    const uint32_t qi = active ? __ldg(perm + s) : 0u;
+    uint32_t qi = 0u;
     double cx = 0.0, cy = 0.0, cz = 0.0;
     if (active) {
-      cx = __ldg(q + 3 * (uint64_t)qi);
-      cy = __ldg(q + 3 * (uint64_t)qi + 1);
-      cz = __ldg(q + 3 * (uint64_t)qi + 2);
+      if (q == nullptr) {
+        // self queries (cm_radius_search_self): centre s of the cell-ordered
+        // records, answered into row rec[s].id — the order the key sort
+        // would produce (same keys, both stable by handle)
+        const PointRec pr = rec[s];
+        qi = pr.id, cx = pr.x, cy = pr.y, cz = pr.z;
+      } else {
+        qi = __ldg(perm + s);
+        cx = __ldg(q + 3 * (uint64_t)qi);
+        cy = __ldg(q + 3 * (uint64_t)qi + 1);
+        cz = __ldg(q + 3 * (uint64_t)qi + 2);
+      }
     }
     Range R{};
     const bool ok = active && clamped_range(t.g, cx, cy, cz, r, &R, CUBE);
@@ -1638,11 +1650,17 @@ __global__ void __launch_bounds__(kMidThreads) sort_mid_rows_kernel(
   }
 }
 
-__global__ void self_perm_kernel(const PointRec* __restrict__ rec, uint64_t n,
-                                 uint32_t* __restrict__ perm) {
+// Centres of a self-query batch in handle order (q[id] = the record's
+// point), for the key sorts that need them (range-corner order).
+__global__ void self_centres_kernel(const PointRec* __restrict__ rec, uint64_t n,
+                                    double* __restrict__ q) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x)
-    perm[i] = rec[i].id;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const PointRec pr = rec[i];
+    q[3 * (uint64_t)pr.id] = pr.x;
+    q[3 * (uint64_t)pr.id + 1] = pr.y;
+    q[3 * (uint64_t)pr.id + 2] = pr.z;
+  }
 }
 
 template <typename K>
@@ -1745,8 +1763,8 @@ cm_status order_queries(const cm_index* ix, const double* q, uint64_t nq, cudaSt
                         QueryOrder* out, double r, int kind) {
   out->nq = nq;
   out->st = st;
+  out->q = q;
   if (nq == 0) return CM_OK;
-  CM_CUDA_TRY(dev_alloc_t(&out->perm, nq, st));
   const DevGrid& g = ix->g;
   auto fits = [&](double f) {  // f = 2: every clamped range spans at most 2 cells per axis
     return r >= 0.0 && f * r <= g.sx && f * r <= g.sy &&
@@ -1754,18 +1772,23 @@ cm_status order_queries(const cm_index* ix, const double* q, uint64_t nq, cudaSt
   };
   // (2-bit extents for r <= cell, ranges of up to 3 cells, measured no gain at r = 1)
   const bool range = fits(2.0);
-  if (!range && ix->src == static_cast<const void*>(q) && nq == ix->n) {
-    // Self queries (every indexed point a centre, from the buffer the index
-    // was built from): the records' cell order IS the order the key sort
-    // would produce (same keys, both stable by handle), so take it from the
-    // records instead of sorting again. Any permutation gives the same
-    // results (rows go to caller positions); the order only shapes tiles, so
-    // a buffer rewritten since the build still answers correctly.
+  if (q == nullptr) {
+    // Self queries (cm_radius_search_self: every indexed point a centre, row
+    // q = point q): the records' cell order IS the order the centre-key sort
+    // would produce, so the kernels read centres straight from the records
+    // (out->q stays null, no permutation). Range-corner order differs from
+    // cell order, so for those radii the centres are materialised in handle
+    // order and sorted like any batch.
+    if (!range) return CM_OK;
+    if (nq != ix->n) return CM_INVALID_ARGUMENT;
+    CM_CUDA_TRY(dev_alloc_t(&out->owned_q, nq * 3, st));
     const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nq + 255) / 256, (uint64_t)sm_count() * 16));
-    self_perm_kernel<<<grid, 256, 0, st>>>(ix->rec, nq, out->perm); ::cmg::note_launch();
+    self_centres_kernel<<<grid, 256, 0, st>>>(ix->rec, nq, out->owned_q); ::cmg::note_launch();
     CM_CUDA_TRY(cudaGetLastError());
-    return CM_OK;
+    q = out->owned_q;
   }
+  out->q = q;
+  CM_CUDA_TRY(dev_alloc_t(&out->perm, nq, st));
   const int bits = ix->key_bits + (range ? 3 : 0);
   return bits <= 32 ? order_typed<uint32_t>(ix, q, nq, st, out->perm, range, r, kind)
                     : order_typed<uint64_t>(ix, q, nq, st, out->perm, range, r, kind);

@@ -48,6 +48,9 @@ def test_gpu_arm_line():
     cb = d["cpu_baseline"]
     assert cb["value"] > 0 and cb["cores"] >= 1 and cb["kind"] in ("reference", "port")
     assert d["gpu_launches"] > 0
+    g = d["general_centres"]
+    assert g["value"] > 0 and g["unit"] == "queries/s"
+    assert "cm_radius_search_self" in d["config"]["call"]
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
     assert set(d["build_ms"]) == {"dense", "sparse", "mixed"}
     assert all(v["frac"] > 0 for v in d["build_roofline"].values())

@@ -292,27 +292,54 @@ def test_csr_digest_checker(cfg0, cfg0_oracle):
     assert bad.value == 1
 
 
-def test_self_queries_reuse_index_order(cfg0, cfg0_oracle):
-    """Centres = the device buffer the index was built from: the query order
-    comes from the index's records (no key sort). Results must equal the
-    oracle, and still do after the buffer is rewritten (any order is
-    correct; the order only shapes tiles)."""
+def test_self_queries_explicit(cfg0, cfg0_oracle):
+    """cm_radius_search_self: every indexed point a centre, row q = point q;
+    centres come from the index's records (no key sort; range-corner radii
+    materialise them). Results equal the oracle's with the cloud as centres.
+    A batch that merely shares the build buffer's address takes the general
+    path: rewriting that buffer changes the centres, not the index."""
     import torch
 
     cloud, _ = cfg0
     d = torch.from_numpy(np.ascontiguousarray(cloud)).cuda()
     for flavor in FLAVORS:
         m = cm.Cheesemap.build(d, cm.BuildOptions(flavor=flavor))
-        for kernel, r in ((cm.SPHERE, 1.0), (cm.CUBE, 1.0), (cm.SPHERE, 2.5)):
-            row, cols = cm.radius_search_batch(m, d, r, kernel)
+        for kernel, r in ((cm.SPHERE, 1.0), (cm.CUBE, 1.0), (cm.SPHERE, 2.5), (cm.SPHERE, 0.4)):
+            row, cols = cm.radius_search_self(m, r, kernel)
             orow, ocols = cfg0_oracle.radius_csr(cloud, int(kernel), r)
             assert np.array_equal(row, orow) and np.array_equal(cols, ocols)
-        idx, d2 = cm.knn_batch(m, d[:4000], 8)  # not the whole buffer: sorted path
+        idx, d2 = cm.knn_batch(m, d[:4000], 8)
         oidx, od2 = cfg0_oracle.knn(cloud[:4000], 8)
         assert np.array_equal(idx, oidx) and np.array_equal(d2, od2)
-    # rewrite the buffer (reversed points): same address and size, other centres
+    # rewrite the build buffer (reversed points): same address and size, other centres
     rev = np.ascontiguousarray(cloud[::-1])
     d.copy_(torch.from_numpy(rev))
     row, cols = cm.radius_search_batch(m, d, 1.0, cm.SPHERE)
     orow, ocols = cfg0_oracle.radius_csr(rev, 0, 1.0)
     assert np.array_equal(row, orow) and np.array_equal(cols, ocols)
+    # the index owns its points: self queries still answer the original cloud
+    row, cols = cm.radius_search_self(m, 1.0)
+    orow, ocols = cfg0_oracle.radius_csr(cloud, 0, 1.0)
+    assert np.array_equal(row, orow) and np.array_equal(cols, ocols)
+
+
+def test_torch_inputs_are_validated(cfg0):
+    """Torch buffers are passed by address, so a wrong dtype or width must be
+    refused before the native code reads it (float32 points, (n, 4) points,
+    int16 counts, a tensor on another device)."""
+    import torch
+
+    cloud, _ = cfg0
+    m = cm.Cheesemap.build(cloud[:5000], cm.BuildOptions(flavor=cm.Flavor.Sparse))
+    good = torch.from_numpy(np.ascontiguousarray(cloud[:100])).cuda()
+    with pytest.raises(cm.InvalidArgumentError):
+        cm.radius_search_batch(m, good.float(), 1.0)
+    with pytest.raises(cm.InvalidArgumentError):
+        cm.radius_search_batch(m, torch.zeros((10, 4), dtype=torch.float64, device="cuda"), 1.0)
+    with pytest.raises(cm.InvalidArgumentError):
+        cm.radius_count(m, good, 1.0, counts=torch.zeros(100, dtype=torch.int16, device="cuda"))
+    with pytest.raises(cm.InvalidArgumentError):
+        cm.radius_count(m, good, 1.0, counts=torch.zeros(10, dtype=torch.int32, device="cuda"))
+    c = torch.zeros(100, dtype=torch.int32, device="cuda")
+    cm.radius_count(m, good, 1.0, counts=c)
+    assert int(c.sum().item()) > 0
