@@ -300,6 +300,66 @@ cm_status cm_las_decode(const void* bytes, uint64_t nbytes, double* xyz, uint64_
 cm_status cm_las_read(const char* path, double* xyz, uint64_t xyz_capacity, cm_las_header* hdr,
                       int device, void* stream);
 
+/* ---- Multi-GPU: x-slabs with a halo ---------------------
+ * One rank per GPU (a process, or a host thread). Every rank of a cluster
+ * passes ITS share of the cloud (any partition of the points, each with a
+ * global id) to cm_build_slab; the ranks then all-reduce the global bounding
+ * box (the grid of grid.cpp:41-61 over the whole cloud), cut its x extent
+ * into nranks equal slabs, exchange the points so that every rank holds the
+ * points of its slab plus the points within `halo` of its faces, and index
+ * them on the global grid. A centre owned by a rank then has exactly the
+ * neighbour set the single global index gives it, for any r <= halo; rows
+ * and digests come out in GLOBAL ids. The map is immutable once built
+ * (map.hpp:50-52). Transports: NCCL (the ranks' GPUs, ncclUniqueId from
+ * rank 0 passed to every rank by the caller), or in-process (ranks are host
+ * threads of one process, e.g. several slabs on one GPU). */
+#define CM_CLUSTER_ID_BYTES 128
+typedef enum { CM_TRANSPORT_NCCL = 0, CM_TRANSPORT_IN_PROCESS = 1 } cm_transport;
+typedef struct cm_cluster cm_cluster;
+typedef struct cm_slab cm_slab;
+typedef struct {
+  double total_ms;    /* device time, device-resident points -> ready slab index,
+                         bbox all-reduce and point exchange included */
+  double wall_ms;     /* host wall time of the same call */
+  double index_ms;    /* of which the local index build */
+  uint64_t sent_points, received_points;  /* records packed / received (incl. own) */
+} cm_slab_timing;
+typedef struct {
+  int32_t nranks, rank;
+  uint64_t n_local, n_owned, n_halo;
+  double halo;
+  double bounds[6];   /* global box: min xyz, max xyz */
+  cm_slab_timing timing;
+} cm_slab_info_t;
+
+/* A fresh group id (CM_CLUSTER_ID_BYTES bytes) for `transport`; rank 0 makes
+ * it and the caller hands it to every rank. */
+cm_status cm_cluster_unique_id(int transport, void* id_out);
+cm_status cm_cluster_init(int transport, const void* id, int nranks, int rank, int device,
+                          cm_cluster** out);
+cm_status cm_cluster_free(cm_cluster* cluster);
+/* Collective over the cluster. xyz: n points (host or device); gids: their
+ * global ids (u32, host or device), or NULL for gid_base + i. */
+cm_status cm_build_slab(cm_cluster* cluster, const double* xyz, const uint32_t* gids,
+                        uint64_t gid_base, uint64_t n, const cm_build_options* opts, double halo,
+                        void* stream, cm_slab** out);
+cm_status cm_slab_free(cm_slab* slab);
+/* edges: nranks + 1 slab boundaries (slab s = [e_s, e_s+1), the last closed) */
+cm_status cm_slab_info(const cm_slab* slab, cm_slab_info_t* out, double* edges,
+                       uint64_t edges_capacity);
+/* The rank's local index (owned + halo points; handles are global ids). */
+const cm_index* cm_slab_index(const cm_slab* slab);
+/* Owned global ids (n_owned, ascending: the row order of q = NULL queries)
+ * and local ones (n_local, ascending); either may be NULL. */
+cm_status cm_slab_ids(const cm_slab* slab, uint32_t* owned_gids, uint32_t* local_gids,
+                      void* stream);
+/* kernel_search for centres inside this slab, r <= halo; q = NULL: every
+ * owned point (row i = owned point i). Columns are global ids. */
+cm_status cm_slab_radius_search(const cm_slab* slab, const double* q, uint64_t nq, int kernel,
+                                double r, void* stream, cm_csr** out);
+cm_status cm_slab_radius_digest(const cm_slab* slab, const double* q, uint64_t nq, int kernel,
+                                double r, uint32_t* counts, uint64_t* digests, void* stream);
+
 const char* cm_last_error(void);
 const char* cm_status_name(cm_status s);
 

@@ -81,6 +81,23 @@ class QueryTimingC(ctypes.Structure):
 _LIB = None
 
 
+class SlabTimingC(ctypes.Structure):  # cm_slab_timing
+    _fields_ = [("total_ms", ctypes.c_double), ("wall_ms", ctypes.c_double),
+                ("index_ms", ctypes.c_double), ("sent_points", ctypes.c_uint64),
+                ("received_points", ctypes.c_uint64)]
+
+
+class SlabInfoC(ctypes.Structure):  # cm_slab_info_t
+    _fields_ = [("nranks", ctypes.c_int32), ("rank", ctypes.c_int32),
+                ("n_local", ctypes.c_uint64), ("n_owned", ctypes.c_uint64),
+                ("n_halo", ctypes.c_uint64), ("halo", ctypes.c_double),
+                ("bounds", ctypes.c_double * 6), ("timing", SlabTimingC)]
+
+
+CLUSTER_ID_BYTES = 128
+TRANSPORT_NCCL, TRANSPORT_IN_PROCESS = 0, 1
+
+
 def lib():
     global _LIB
     if _LIB is not None:
@@ -130,6 +147,17 @@ def lib():
         "cm_brute_knn": ([p, u64, p, u64, u32, p, p, i32, p], i32),
         "cm_las_decode": ([p, u64, p, u64, ctypes.POINTER(LasHeaderC), i32, p], i32),
         "cm_las_read": ([ctypes.c_char_p, p, u64, ctypes.POINTER(LasHeaderC), i32, p], i32),
+        "cm_cluster_unique_id": ([i32, p], i32),
+        "cm_cluster_init": ([i32, p, i32, i32, i32, ctypes.POINTER(p)], i32),
+        "cm_cluster_free": ([p], i32),
+        "cm_build_slab": ([p, p, p, u64, u64, ctypes.POINTER(BuildOptionsC), dbl, p,
+                           ctypes.POINTER(p)], i32),
+        "cm_slab_free": ([p], i32),
+        "cm_slab_info": ([p, ctypes.POINTER(SlabInfoC), p, u64], i32),
+        "cm_slab_index": ([p], p),
+        "cm_slab_ids": ([p, p, p, p], i32),
+        "cm_slab_radius_search": ([p, p, u64, i32, dbl, p, ctypes.POINTER(p)], i32),
+        "cm_slab_radius_digest": ([p, p, u64, i32, dbl, p, p, p], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

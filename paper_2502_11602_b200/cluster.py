@@ -1,5 +1,12 @@
-"""Multi-GPU layouts: one process per GPU, torch.distributed
-for the plumbing (NCCL between GPUs; gloo works for the same code on CPU).
+"""Multi-GPU layouts: one process per GPU.
+
+The product path for x-slabs is the C ABI (include/cmgpu.h "Multi-GPU",
+csrc/cluster.cu): `Cluster` + `Slab` below wrap cm_cluster_init /
+cm_build_slab / cm_slab_radius_search — device bbox, NCCL MIN all-reduce,
+device classify + pack, NCCL grouped send/recv, local index on the global
+grid, results in global ids. The torch.distributed helpers further down
+restate the same partition rule on the host (SlabPartition) for the gloo
+multi-process tests and as the oracle-side reference of the partition.
 
 Two layouts:
 
@@ -19,9 +26,122 @@ Two layouts:
   global one. Local handles are assigned in ascending global-id order, so
   sorted local rows stay sorted after mapping back to global ids.
 """
+import ctypes
+
 import numpy as np
 import torch
 import torch.distributed as dist
+
+
+class Cluster:
+    """cm_cluster: this rank's membership of a group of `nranks` ranks.
+    transport: "nccl" (one GPU per rank; `uid` from Cluster.unique_id on rank
+    0, passed to every rank by the caller) or "in-process" (ranks are host
+    threads of this process)."""
+
+    TRANSPORTS = {"nccl": 0, "in-process": 1}
+
+    def __init__(self, uid, nranks, rank, device=0, transport="nccl"):
+        from . import _native
+        from . import cheesemap as cm
+        self._L = _native.lib()
+        self.nranks, self.rank, self.device = nranks, rank, device
+        h = ctypes.c_void_p()
+        buf = ctypes.create_string_buffer(bytes(uid), _native.CLUSTER_ID_BYTES)
+        cm._check(self._L.cm_cluster_init(self.TRANSPORTS[transport], buf, nranks, rank, device,
+                                          ctypes.byref(h)))
+        self._h = h
+
+    @staticmethod
+    def unique_id(transport="nccl"):
+        from . import _native
+        from . import cheesemap as cm
+        buf = ctypes.create_string_buffer(_native.CLUSTER_ID_BYTES)
+        cm._check(_native.lib().cm_cluster_unique_id(Cluster.TRANSPORTS[transport], buf))
+        return buf.raw
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            self._L.cm_cluster_free(h)
+            self._h = None
+
+
+class Slab:
+    """cm_slab: this rank's x-slab index (owned + halo points, global grid)."""
+
+    def __init__(self, cluster, xyz, gids=None, gid_base=0, opts=None, halo=5.0, stream=None):
+        from . import cheesemap as cm
+        opts = opts or cm.BuildOptions()
+        self.cluster = cluster
+        L = cluster._L
+        p, keep = cm._in_ptr(xyz, device=cluster.device)
+        n = cm._nrows(keep) if keep is not None else 0
+        gp, gkeep = cm._in_ptr(gids, np.uint32, device=cluster.device) if gids is not None \
+            else (None, None)
+        h = ctypes.c_void_p()
+        c = opts.to_c()
+        cm._check(L.cm_build_slab(cluster._h, p, gp, int(gid_base), n, ctypes.byref(c),
+                                  float(halo), cm._stream_ptr(stream), ctypes.byref(h)))
+        self._h = h
+        self._L = L
+        self.opts = opts
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            self._L.cm_slab_free(h)
+            self._h = None
+
+    def info(self):
+        from . import _native
+        from . import cheesemap as cm
+        o = _native.SlabInfoC()
+        e = np.zeros(self.cluster.nranks + 1)
+        cm._check(self._L.cm_slab_info(self._h, ctypes.byref(o), e.ctypes.data_as(ctypes.c_void_p),
+                                       e.size))
+        t = o.timing
+        return dict(nranks=o.nranks, rank=o.rank, n_local=o.n_local, n_owned=o.n_owned,
+                    n_halo=o.n_halo, halo=o.halo, bounds=list(o.bounds), edges=e,
+                    timing=dict(total_ms=t.total_ms, wall_ms=t.wall_ms, index_ms=t.index_ms,
+                                sent_points=t.sent_points, received_points=t.received_points))
+
+    def owned_ids(self):
+        from . import cheesemap as cm
+        n = int(self.info()["n_owned"])
+        out = np.zeros(n, dtype=np.uint32)
+        cm._check(self._L.cm_slab_ids(self._h, out.ctypes.data_as(ctypes.c_void_p), None, None))
+        return out
+
+    def radius_search(self, r, kernel=0, centers=None, stream=None, device_out=False):
+        """Sorted CSR in global ids; centers=None: every owned point (row i =
+        owned_ids()[i])."""
+        from . import cheesemap as cm
+        L = self._L
+        if centers is None:
+            qp, nq = None, int(self.info()["n_owned"])
+        else:
+            qp, qk = cm._in_ptr(centers, device=self.cluster.device)
+            nq = cm._nrows(qk)
+        csr = ctypes.c_void_p()
+        cm._check(L.cm_slab_radius_search(self._h, qp, nq, int(kernel), float(r),
+                                          cm._stream_ptr(stream), ctypes.byref(csr)))
+        return cm._take_csr(L, csr, nq, self.cluster.device, stream, device_out)
+
+    def radius_digest(self, r, kernel=0, centers=None, stream=None):
+        from . import cheesemap as cm
+        if centers is None:
+            qp, nq = None, int(self.info()["n_owned"])
+        else:
+            qp, qk = cm._in_ptr(centers, device=self.cluster.device)
+            nq = cm._nrows(qk)
+        cnt = np.zeros(nq, dtype=np.uint32)
+        dig = np.zeros(nq, dtype=np.uint64)
+        cm._check(self._L.cm_slab_radius_digest(self._h, qp, nq, int(kernel), float(r),
+                                                cnt.ctypes.data_as(ctypes.c_void_p),
+                                                dig.ctypes.data_as(ctypes.c_void_p),
+                                                cm._stream_ptr(stream)))
+        return cnt, dig
 
 
 def query_shard(n, rank, world):

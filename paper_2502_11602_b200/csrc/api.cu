@@ -905,6 +905,10 @@ cm_status cm_radius_search_self(const cm_index* ix, int kernel, double r, void* 
     return CM_INVALID_ARGUMENT;
   }
   *out = nullptr;
+  if (ix->global_ids) {
+    set_error("self queries of a slab index: use cm_slab_radius_search (owned centres)");
+    return CM_INVALID_ARGUMENT;
+  }
   DeviceGuard dg(ix->device);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cm_csr* csr = new cm_csr();

@@ -349,6 +349,31 @@ cm_status build_typed(const double* xyz, uint64_t n, cudaStream_t st, cm_index* 
 
 }  // namespace
 
+// aabb_of_points (geometry.cpp:7-21) of n device points -> host lo / hi
+// (+inf / -inf for n = 0). Synchronous; `after` (optional) is recorded once
+// the reduction is queued.
+cm_status bbox_dev(const double* xyz, uint64_t n, cudaStream_t st, double lo[3], double hi[3],
+                   cudaEvent_t after) {
+  unsigned long long* bb = nullptr;
+  CM_CUDA_TRY(dev_alloc_t(&bb, 6, st));
+  unsigned long long init[6] = {~0ull, ~0ull, ~0ull, 0ull, 0ull, 0ull};
+  CM_CUDA_TRY(cudaMemcpyAsync(bb, init, sizeof(init), cudaMemcpyHostToDevice, st));
+  if (n) {
+    bbox_kernel<<<grid_for(n), 256, 0, st>>>(xyz, n, bb); ::cmg::note_launch();
+    CM_CUDA_TRY(cudaGetLastError());
+  }
+  unsigned long long hb[6];
+  CM_CUDA_TRY(cudaMemcpyAsync(hb, bb, sizeof(hb), cudaMemcpyDeviceToHost, st));
+  if (after) cudaEventRecord(after, st);
+  CM_CUDA_TRY(cudaStreamSynchronize(st));
+  dev_free(bb, st);
+  for (int a = 0; a < 3; ++a) {
+    lo[a] = n ? double_of_ord(hb[a]) : __builtin_inf();
+    hi[a] = n ? double_of_ord(hb[3 + a]) : -__builtin_inf();
+  }
+  return CM_OK;
+}
+
 cm_status build_index(const double* xyz, uint64_t n, const cm_build_options& o, cudaStream_t st,
                       cm_index* ix, const double* bounds6) {
   // Check order follows map.cpp:23-39.
@@ -372,20 +397,10 @@ cm_status build_index(const double* xyz, uint64_t n, const cm_build_options& o, 
   ix->n = n;
   Events ev;
   cudaEventRecord(ev.e[0], st);
-  unsigned long long* bb = nullptr;
-  CM_CUDA_TRY(dev_alloc_t(&bb, 6, st));
-  unsigned long long init[6] = {~0ull, ~0ull, ~0ull, 0ull, 0ull, 0ull};
-  CM_CUDA_TRY(cudaMemcpyAsync(bb, init, sizeof(init), cudaMemcpyHostToDevice, st));
-  bbox_kernel<<<grid_for(n), 256, 0, st>>>(xyz, n, bb); ::cmg::note_launch();
-  unsigned long long hb[6];
-  CM_CUDA_TRY(cudaMemcpyAsync(hb, bb, sizeof(hb), cudaMemcpyDeviceToHost, st));
-  cudaEventRecord(ev.e[1], st);
-  CM_CUDA_TRY(cudaStreamSynchronize(st));
-  dev_free(bb, st);
   double lo[3], hi[3];
-  for (int a = 0; a < 3; ++a) {
-    lo[a] = double_of_ord(hb[a]);
-    hi[a] = double_of_ord(hb[3 + a]);
+  {
+    cm_status bs = bbox_dev(xyz, n, st, lo, hi, ev.e[1]);
+    if (bs != CM_OK) return bs;
   }
   if (bounds6) {
     // An explicit (e.g. global, all-reduced) bounding box: every point must

@@ -41,6 +41,9 @@ struct cm_index {
   // it is an atomic; lost updates between threads only change arena sizing.
   mutable std::atomic<double> nnz_per_query{64.0};
   cm_build_timing timing{};
+  // handles are global ids of a multi-GPU slab (cm_build_slab), not
+  // positions in the indexed points: self queries do not apply
+  bool global_ids = false;
 
   cmg::Tables tables() const {
     cmg::Tables t{};
@@ -101,6 +104,8 @@ struct InBuf {
 };
 cm_status stage_input(const void* p, size_t bytes, cudaStream_t st, InBuf* out);
 
+cm_status bbox_dev(const double* xyz, uint64_t n, cudaStream_t st, double lo[3], double hi[3],
+                   cudaEvent_t after = nullptr);
 cm_status build_index(const double* xyz_dev, uint64_t n, const cm_build_options& o,
                       cudaStream_t st, cm_index* ix, const double* bounds6 = nullptr);
 
