@@ -58,6 +58,10 @@ def parse():
     ap.add_argument("--flavor", default="mixed", choices=list(FLAVORS))
     ap.add_argument("--cpu-sample", type=int, default=1_000_000,
                     help="queries per CPU-baseline / reference step")
+    ap.add_argument("--layout", default="replicated", choices=["replicated", "slabs"],
+                    help="slabs: x-slab partition with halo exchange through cm_build_slab "
+                         "(config 4's layout)")
+    ap.add_argument("--halo", type=float, default=5.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -184,10 +188,131 @@ def reference_arm(a):
     print(json.dumps(line), flush=True)
 
 
+def slab_arm(a):
+    """x-slabs: every rank passes a contiguous 1/N
+    block of the cloud (global ids = handles) to cm_build_slab, which
+    all-reduces the global box, exchanges points into x-slabs + halos over
+    NCCL and indexes them on the global grid; each rank then answers every
+    point it owns (cm_slab_radius_search, q = NULL). value = all points /
+    max-over-ranks device time; build_ms = max over ranks of device-resident
+    points -> ready slab index, exchange included."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2502_11602_b200 import synth
+    from paper_2502_11602_b200 import cheesemap as cm
+    from paper_2502_11602_b200.cluster import Cluster, Slab
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    total_mem = torch.cuda.get_device_properties(local).total_memory
+    cm.pool_configure(local, int(total_mem * 0.75), min(32 << 30, int(total_mem * 0.2)))
+    uid = [Cluster.unique_id("nccl") if rank == 0 else None]
+    if world > 1:
+        dist.broadcast_object_list(uid, src=0)
+    cl = Cluster(uid[0], world, rank, local, "nccl")
+    cloud = synth.config_cloud(a.config, a.scale)
+    n = cloud.shape[0]
+    lo, hi = n * rank // world, n * (rank + 1) // world
+    share = torch.from_numpy(np.ascontiguousarray(cloud[lo:hi])).to(dev)
+    del cloud
+    stream = torch.cuda.current_stream(dev)
+    kernel = KERNELS[a.kernel]
+    opts = cm.BuildOptions(flavor=cm.Flavor(FLAVORS[a.flavor]))
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    def allred(x, op):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=op)
+        return float(t.item())
+
+    builds = []
+    slab = None
+    for _ in range(3):
+        barrier()
+        slab = None
+        slab = Slab(cl, share, gid_base=lo, opts=opts, halo=a.halo, stream=stream)
+        builds.append(slab.info()["timing"]["total_ms"])
+    inf = slab.info()
+    build_ms = allred(min(builds), dist.ReduceOp.MAX if world > 1 else None)
+    n_owned = inf["n_owned"]
+    L = cm._native.lib()
+    import ctypes
+
+    def step():
+        csr = ctypes.c_void_p()
+        cm._check(L.cm_slab_radius_search(slab._h, None, n_owned, kernel, a.radius,
+                                          ctypes.c_void_p(stream.cuda_stream), ctypes.byref(csr)))
+        return csr
+
+    for _ in range(a.warmup):
+        L.cm_csr_free(step())
+    nnz = ctypes.c_uint64()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    torch.cuda.synchronize(dev)
+    launches0 = cm._native.launch_count()
+    ms = []
+    for _ in range(a.steps):
+        flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        csr = step()
+        e1.record(stream)
+        e1.synchronize()
+        ms.append(e0.elapsed_time(e1))
+        L.cm_csr_info(csr, None, ctypes.byref(nnz), None, None)
+        L.cm_csr_free(csr)
+    launches = (cm._native.launch_count() - launches0) // a.steps
+    barrier()
+    clk = clocks.stop()
+    t = allred(sum(ms) / len(ms), dist.ReduceOp.MAX if world > 1 else None)
+    nnz_all = allred(float(nnz.value), dist.ReduceOp.SUM if world > 1 else None)
+    halo_all = allred(float(inf["n_halo"]), dist.ReduceOp.SUM if world > 1 else None)
+    if rank == 0:
+        print(json.dumps({
+            "metric": f"radius-search queries/sec (cfg{a.config} x-slabs, r={a.radius:g} m)",
+            "value": round(n / (t * 1e-3), 1), "unit": "queries/s", "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(t, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": f"synthetic (seeded config-{a.config} generator, DESIGN.md)",
+            "config": {"workload": f"cfg{a.config} ALS {n} pts, x-slabs x{world}, halo "
+                                   f"{a.halo:g} m, {a.kernel} r={a.radius:g} m, every point a "
+                                   "query (its owner rank), sorted CSR in global ids",
+                       "flavor": a.flavor, "layout": "slabs", "n_points": n,
+                       "neighbours": int(nnz_all), "halo_points": int(halo_all),
+                       "l2": "flushed (256 MB write) before every timed step",
+                       "call": "cm_build_slab + cm_slab_radius_search (q = NULL: owned points)"},
+            "build_ms": round(build_ms, 3),
+            "build_note": "max over ranks: device-resident share -> ready slab index, bbox "
+                          "all-reduce + point exchange included (host->device share copy "
+                          "excluded)",
+            "gpu_launches": int(launches), "clocks": clk}), flush=True)
+    del slab
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     a = parse()
     if a.impl == "reference":
         reference_arm(a)
+        return
+    if a.layout == "slabs":
+        slab_arm(a)
         return
     import ctypes
 

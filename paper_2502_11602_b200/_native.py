@@ -7,7 +7,9 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcmgpu.so")
+# CMGPU_LIB=libcmgpu_checked.so selects the build with device invariant
+# checks (make -C csrc checked); the default is the product library
+LIB_PATH = os.path.join(_HERE, os.environ.get("CMGPU_LIB", "libcmgpu.so"))
 
 STATUS_NAMES = {0: "CM_OK", 1: "CM_EMPTY_CLOUD", 2: "CM_INVALID_ARGUMENT", 3: "CM_CAPACITY",
                 4: "CM_OUT_OF_DOMAIN", 5: "CM_CUDA", 6: "CM_NCCL", 7: "CM_PARSE", 8: "CM_IO"}

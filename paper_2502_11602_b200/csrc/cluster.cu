@@ -283,7 +283,7 @@ __global__ void slab_count_kernel(const double* __restrict__ xyz, uint64_t n, Sl
 __global__ void slab_pack_kernel(const double* __restrict__ xyz, const uint32_t* __restrict__ gids,
                                  uint64_t gid_base, uint64_t n, SlabEdges E,
                                  unsigned long long* __restrict__ cursor,
-                                 PointRec* __restrict__ out) {
+                                 PointRec* __restrict__ out, uint64_t total) {
   for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n;
        p += (uint64_t)gridDim.x * blockDim.x) {
     PointRec r;
@@ -295,10 +295,20 @@ __global__ void slab_pack_kernel(const double* __restrict__ xyz, const uint32_t*
     bool dn, up;
     dests_of(E, r.x, &o, &dn, &up);
     r.k = 1;
-    out[atomicAdd(&cursor[o], 1ull)] = r;
+    const unsigned long long a = atomicAdd(&cursor[o], 1ull);
+    CM_DCHECK(a < total);
+    out[a] = r;
     r.k = 0;
-    if (dn) out[atomicAdd(&cursor[o - 1], 1ull)] = r;
-    if (up) out[atomicAdd(&cursor[o + 1], 1ull)] = r;
+    if (dn) {
+      const unsigned long long b = atomicAdd(&cursor[o - 1], 1ull);
+      CM_DCHECK(b < total);
+      out[b] = r;
+    }
+    if (up) {
+      const unsigned long long c = atomicAdd(&cursor[o + 1], 1ull);
+      CM_DCHECK(c < total);
+      out[c] = r;
+    }
   }
 }
 
@@ -596,7 +606,8 @@ cm_status cm_build_slab(cm_cluster* cl, const double* xyz, const uint32_t* gids,
     std::vector<unsigned long long> cur(soff.begin(), soff.end() - 1);
     CM_CUDA_TRY(cudaMemcpyAsync(dcount + P, cur.data(), 8 * P, cudaMemcpyHostToDevice, st));
     if (n) {
-      slab_pack_kernel<<<grid_of(n), 256, 0, st>>>(dx, dg_ids, gid_base, n, E, dcount + P, sendbuf);
+      slab_pack_kernel<<<grid_of(n), 256, 0, st>>>(dx, dg_ids, gid_base, n, E, dcount + P, sendbuf,
+                                                   soff[P]);
       ::cmg::note_launch();
     }
     CM_CUDA_TRY(cudaGetLastError());

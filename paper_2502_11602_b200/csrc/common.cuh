@@ -11,6 +11,25 @@
 
 #include "../../include/cmgpu.h"
 
+// Device-side invariant checks, compiled in only for the checked build
+// (make checked -> libcmgpu_checked.so, CMGPU_LIB selects it): a failed check
+// prints the condition and traps. The pool's GPUs have compute-sanitizer
+// closed, so these plus CPU-oracle parity are the out-of-bounds evidence.
+#ifdef CMGPU_CHECKED
+#include <cstdio>
+#define CM_DCHECK(cond)                                                            \
+  do {                                                                             \
+    if (!(cond)) {                                                                 \
+      printf("CM_DCHECK failed %s:%d: %s\n", __FILE__, __LINE__, #cond);           \
+      __trap();                                                                    \
+    }                                                                              \
+  } while (0)
+#else
+#define CM_DCHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
+
 namespace cmg {
 
 constexpr int kWarp = 32;

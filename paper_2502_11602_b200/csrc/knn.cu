@@ -171,6 +171,7 @@ __global__ void __launch_bounds__(kKThreads) knn_warp_kernel(const Tables t,
             uint32_t bi = acc ? id : 0xffffffffu;
             warp_sort_pairs32(bd, bi, lane);
             const uint32_t ncnt = min(k, cnt + nacc);
+            CM_DCHECK(ncnt <= (uint32_t)kKMax);
             for (uint32_t base = 0; base < cnt; base += 32) {
               const uint32_t x = base + lane;
               const bool valid = x < cnt;
@@ -387,6 +388,7 @@ __global__ void __launch_bounds__(kKThreads) knn_tile_kernel(
             const double d2 = sqdist(v.x, v.y, v.z, cx, cy, cz);
             if (cnt < k || pair_less(d2, v.id, kd, kid)) {
               uint32_t pos = cnt < k ? cnt : k - 1;
+              CM_DCHECK(pos < (uint32_t)KMAX);
               while (pos > 0) {
                 const double pd = ld[(pos - 1) * 33 + lane];
                 const uint32_t pi = li[(pos - 1) * 33 + lane];

@@ -636,6 +636,7 @@ __device__ __forceinline__ void wide_tile(const Tables& t, const Range& R, bool 
     for (int l = 0; l < 32; ++l) {
       const uint32_t n = __shfl_sync(0xffffffffu, nb, l);
       const uint64_t wp = __shfl_sync(0xffffffffu, wpos, l);
+      CM_DCHECK(n <= (uint32_t)kFillCap + 1u);
       const uint32_t a = (uint32_t)lane < n ? sid[lane * 33 + l] : 0u;
       const uint32_t b2 = lane + 32u < n ? sid[(lane + 32) * 33 + l] : 0u;
       if ((uint32_t)lane < n) o.cols[wp + lane] = a;
@@ -718,6 +719,7 @@ __device__ __forceinline__ void wide_tile(const Tables& t, const Range& R, bool 
     cp_async_wait<0>();
   }
   if (FILL) flush();
+  CM_DCHECK(!FILL || !active || wpos == __ldg(o.row_ptr + qi + 1));
   const uint32_t hsum = warp_incl_scan(hull);
   if (lane == 31) atomicAdd(&g_qstats[(FILL ? 4 : 0) + 2], (unsigned long long)hsum);
   if (MODE == MODE_COUNT) {
@@ -806,6 +808,7 @@ __global__ void __launch_bounds__(kQThreads, CM_QTILE_MINB) radius_tile_kernel(
         ncol = (uint32_t)nc;
         if ((uint32_t)lane < ncol)
           column_span<FLAVOR>(t, I0 + lane / nj, J0 + lane % nj, K0, K1, &b, &e);
+        CM_DCHECK(b <= e && e <= t.n);
         total = __shfl_sync(0xffffffffu, warp_incl_scan(e - b), 31);
         // row keys hold a 11-bit offset within a column span
         if (ROWS && warp_max_u32(e - b) > 2048u) use_tile = false;
@@ -943,6 +946,8 @@ __global__ void __launch_bounds__(kQThreads, CM_QTILE_MINB) radius_tile_kernel(
       bool write_ok = true;
       if (MODE == MODE_FILL) {
         dst = active ? __ldg(o.row_ptr + qi) : 0;
+        // the row the count pass sized must hold exactly this walk's hits
+        CM_DCHECK(!active || longrow || __ldg(o.row_ptr + qi + 1) - dst == (uint64_t)cnt);
       } else {
         const uint32_t inc = warp_incl_scan(mine);
         const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
@@ -951,6 +956,7 @@ __global__ void __launch_bounds__(kQThreads, CM_QTILE_MINB) radius_tile_kernel(
         base = __shfl_sync(0xffffffffu, base, 0);
         dst = base + (inc - mine);
         write_ok = base + tot <= o.cap;
+        CM_DCHECK(!write_ok || dst + mine <= o.cap);
         if (active && !longrow) {
           o.counts[qi] = cnt;
           o.toff[qi] = dst;
@@ -1165,6 +1171,7 @@ __global__ void CM_GATHER_BOUNDS gather_rows_kernel(const uint32_t* temp,
     const uint32_t len = nlen;
     const uint64_t so = nso;
     const uint64_t dof = act ? __ldg(row_ptr + q) : 0;
+    CM_DCHECK(!act || __ldg(row_ptr + q + 1) - dof == (uint64_t)len);
     // the next group's arena rows start moving into L2 while this one sorts
     {
       const uint64_t nq2 = (gidx + W) * 32 + lane;

@@ -1,16 +1,22 @@
-"""Every device code path once, on small inputs, for compute-sanitizer:
+"""Every device code path once, on small inputs, against the CPU oracle —
+run with the checked library (device invariant checks compiled in):
 
-    compute-sanitizer --tool memcheck  python scripts/sanitize_probe.py
-    compute-sanitizer --tool racecheck python scripts/sanitize_probe.py
-    compute-sanitizer --tool synccheck python scripts/sanitize_probe.py
-    compute-sanitizer --tool initcheck python scripts/sanitize_probe.py
+    make -C paper_2502_11602_b200/csrc checked
+    CMGPU_LIB=libcmgpu_checked.so python scripts/checked_probe.py
+
+compute-sanitizer is closed on this pool's GPUs (profiles/r02/
+sanitizer_unavailable.log), so out-of-bounds evidence is the CM_DCHECK
+invariants (common.cuh: span bounds, arena / row / flush bounds, count-pass
+vs fill-pass row lengths, gather row lengths, slab pack bounds, kNN list
+bounds) — a failed check traps and the process exits non-zero — plus the
+oracle comparisons below.
 
 Builds (dense / sparse / mixed, 3D and 2D), radius count / fill / single-pass
 collect + gather / digest / self queries / the large-radius count + fill +
 row-sort path / the one-query-per-warp path (sparse random centres), kNN
 (tile path k <= 8 and the shell walk), the brute-force baselines, the
-density metrics, LAS decode, and the host-buffer pipeline. Results are
-checked against the CPU oracle so a sanitizer run is also a parity run.
+density metrics, LAS decode, the host-buffer pipeline and a 2-rank x-slab
+build (in-process transport).
 """
 import os
 import struct
@@ -99,7 +105,34 @@ def main():
     recs[:, :3] = raw
     xyz, _ = cm.decode_las(bytes(hdr) + recs.tobytes())
     assert np.array_equal(xyz, raw.astype(np.float64) * 0.01 + 100.0)
-    print(f"sanitize probe ok ({checks} parity checks)")
+    # x-slabs: 2 ranks as threads (in-process transport), rows in global ids
+    import threading
+    from paper_2502_11602_b200.cluster import Cluster, Slab
+    uid = Cluster.unique_id("in-process")
+    res, errs = {}, []
+
+    def rank_main(rk):
+        try:
+            cl = Cluster(uid, 2, rk, 0, "in-process")
+            lo, hi = n * rk // 2, n * (rk + 1) // 2
+            sl = Slab(cl, cloud[lo:hi], gid_base=lo, halo=3.0,
+                      opts=cm.BuildOptions(flavor=cm.Flavor.Sparse))
+            res[rk] = (sl.owned_ids(), sl.radius_digest(2.0))
+        except Exception as ex:  # noqa: BLE001
+            errs.append(repr(ex))
+
+    th = [threading.Thread(target=rank_main, args=(i,)) for i in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    oc, od = o.radius(cloud, 0, 2.0)
+    for rk in range(2):
+        ids, (c, dg) = res[rk]
+        assert np.array_equal(c, oc[ids]) and np.array_equal(dg, od[ids])
+    checks += 1
+    print(f"checked probe ok ({checks} parity checks, library {cm._native.LIB_PATH})")
 
 
 if __name__ == "__main__":

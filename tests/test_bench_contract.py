@@ -54,3 +54,13 @@ def test_gpu_arm_line():
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
     assert set(d["build_ms"]) == {"dense", "sparse", "mixed"}
     assert all(v["frac"] > 0 for v in d["build_roofline"].values())
+
+
+@pytest.mark.gpu
+def test_gpu_slab_layout_line():
+    """bench.py --layout slabs (config 4's x-slab layout through cm_build_slab)."""
+    d = run_bench("--config", "4", "--layout", "slabs", "--flavor", "sparse", "--scale", "0.005",
+                  "--steps", "2", "--warmup", "1")
+    assert BASE_KEYS <= d.keys()
+    assert d["value"] > 0 and d["build_ms"] > 0 and d["config"]["layout"] == "slabs"
+    assert d["config"]["neighbours"] > 0 and d["gpu_launches"] > 0
