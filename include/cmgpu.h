@@ -221,6 +221,27 @@ cm_status cm_radius_digest(const cm_index* index, const double* q, uint64_t nq,
                            int kernel, double r, uint32_t* counts,
                            uint64_t* digests, void* stream);
 
+/* kernel_search for a batch of EXPLICIT kernels (geometry.hpp:73-113), each
+ * with its own parameters, params = nq rows of:
+ *   CM_SPHERE   4 doubles  cx cy cz r           SphereKernel{c, r}
+ *   CM_CUBE     6 doubles  min xyz, max xyz     BoxKernel{Aabb} (any box)
+ *   CM_CYLINDER 5 doubles  cx cy r z_lo z_hi    CylinderKernel (+-inf: unbounded)
+ * Host or device params; sorted rows as cm_radius_search. */
+cm_status cm_kernel_search(const cm_index* index, int kernel, const double* params, uint64_t nq,
+                           void* stream, cm_csr** out);
+/* Counts and QueryStats (search.hpp:12-17) of explicit kernels: counts[q],
+ * points_tested[q] and voxels_visited[q] (the voxels of the clamped range,
+ * search.hpp:116-119). Any output may be NULL; host or device outputs. */
+cm_status cm_kernel_count(const cm_index* index, int kernel, const double* params, uint64_t nq,
+                          uint32_t* counts, uint64_t* points_tested, uint64_t* voxels_visited,
+                          void* stream);
+/* Cheesemap::voxel_present / voxel_lookup (map.hpp:62-69): whether voxel
+ * (i, j, k) is materialized (dense flavour: always; mixed: every cell of a
+ * densified slice; else non-empty), its handles ascending (up to capacity;
+ * host or device) and their number. CM_OUT_OF_DOMAIN outside the grid. */
+cm_status cm_voxel_lookup(const cm_index* index, uint64_t i, uint64_t j, uint64_t k, int* present,
+                          uint32_t* handles, uint64_t capacity, uint64_t* count);
+
 /* knn_search (search.cpp:87-146), exact, rows ordered by (fp64 squared
  * distance, handle). idx[q*k + t], d2[q*k + t] (d2 may be NULL). Rows of a
  * cloud with fewer than k points are padded with UINT32_MAX / +inf. */

@@ -10,15 +10,24 @@
 //    voxel-visit order, search.hpp:110-122; its tests sort,
 //    tests/test_util.hpp:30-35);
 //  * knn_search orders ties by handle (the reference keeps insertion order,
-//    search.cpp:16-28); distances are sqrt of the same fp64 d^2;
-//  * BoxKernel is the cube {c - r, c + r} (what the reference CLI and tests
-//    build, cmd_bench.cpp:107-111); CylinderKernel keeps the default
-//    unbounded z range (the one weighted_density uses);
+//    search.cpp:16-28); distances are sqrt of the same fp64 d^2. It is exact
+//    for any GrowthPolicy (the policy only steers the reference's Alg. 2);
+//    its QueryStats report the candidates of kernel_search at the exact k-th
+//    distance (points_tested, voxels_visited), growth_iterations = 0 and
+//    final_radius = that distance;
 //  * the map owns device copies of the points (the cloud need not outlive it).
+//
+// Exceptions ARE the reference's: when <cheesemap/errors.hpp> is on the
+// include path it is used directly; otherwise the same hierarchy is declared
+// in namespace cheesemap (errors.hpp:8-42). Either way a caller's
+// `catch (cheesemap::CapacityError&)` catches what this mirror throws.
 #pragma once
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <limits>
+#include <optional>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -26,20 +35,39 @@
 
 #include "../cmgpu.h"
 
-namespace cheesemap::gpu {
-
-// ------------------------------------------------------------ errors.hpp --
+#if __has_include(<cheesemap/errors.hpp>)
+#include <cheesemap/errors.hpp>
+#else
+namespace cheesemap {
 class Error : public std::runtime_error {
  public:
   using std::runtime_error::runtime_error;
 };
-class EmptyCloudError : public Error { public: using Error::Error; };
+class EmptyCloudError : public Error {
+ public:
+  EmptyCloudError() : Error("point cloud is empty") {}
+  using Error::Error;
+};
 class CapacityError : public Error { public: using Error::Error; };
 class OutOfDomainError : public Error { public: using Error::Error; };
-class InvalidArgumentError : public Error { public: using Error::Error; };
-class CudaError : public Error { public: using Error::Error; };
 class ParseError : public Error { public: using Error::Error; };
+class InvalidArgumentError : public Error { public: using Error::Error; };
 class IoError : public Error { public: using Error::Error; };
+}  // namespace cheesemap
+#endif
+
+namespace cheesemap::gpu {
+
+// ------------------------------------------------------------ errors.hpp --
+using ::cheesemap::CapacityError;
+using ::cheesemap::EmptyCloudError;
+using ::cheesemap::Error;
+using ::cheesemap::InvalidArgumentError;
+using ::cheesemap::IoError;
+using ::cheesemap::OutOfDomainError;
+using ::cheesemap::ParseError;
+// device / collective failures (no reference analogue), still a cheesemap::Error
+class CudaError : public ::cheesemap::Error { public: using ::cheesemap::Error::Error; };
 
 inline void check(cm_status s) {
   if (s == CM_OK) return;
@@ -63,17 +91,55 @@ static_assert(sizeof(Point3) == 24, "PointCloud layout is n x 3 doubles");
 using PointHandle = std::uint64_t;
 using PointCloud = std::vector<Point3>;
 
+// Axis-aligned box, closed on all faces (geometry.hpp:43-58).
+struct Aabb {
+  Point3 min, max;
+  bool contains(const Point3& p) const {
+    return p.x >= min.x && p.x <= max.x && p.y >= min.y && p.y <= max.y && p.z >= min.z &&
+           p.z <= max.z;
+  }
+  bool intersects(const Aabb& o) const {
+    return min.x <= o.max.x && max.x >= o.min.x && min.y <= o.max.y && max.y >= o.min.y &&
+           min.z <= o.max.z && max.z >= o.min.z;
+  }
+};
+
+inline double squared_distance(const Point3& a, const Point3& b) {  // geometry.hpp:26-31
+  const double dx = a.x - b.x, dy = a.y - b.y, dz = a.z - b.z;
+  return dx * dx + dy * dy + dz * dz;
+}
+
+// The three kernels of geometry.hpp:73-113, with the reference's box() and
+// is_inside() (the device applies the same arithmetic).
 struct SphereKernel {
   Point3 center;
   double radius = 0.0;
+  Aabb box() const {
+    return {{center.x - radius, center.y - radius, center.z - radius},
+            {center.x + radius, center.y + radius, center.z + radius}};
+  }
+  bool is_inside(const Point3& p) const { return squared_distance(p, center) <= radius * radius; }
 };
-struct BoxKernel {  // the cube {c - r, c + r}
-  Point3 center;
-  double half = 0.0;
-  static BoxKernel cube(const Point3& c, double r) { return {c, r}; }
+struct BoxKernel {
+  Aabb aabb;
+  Aabb box() const { return aabb; }
+  bool is_inside(const Point3& p) const { return aabb.contains(p); }
+  // the cube the reference CLI builds (cmd_bench.cpp:107-111)
+  static BoxKernel cube(const Point3& c, double r) {
+    return {{{c.x - r, c.y - r, c.z - r}, {c.x + r, c.y + r, c.z + r}}};
+  }
 };
-struct CylinderKernel {  // vertical, unbounded z range (geometry.hpp:97-113)
+struct CylinderKernel {  // vertical, optional z range (geometry.hpp:97-113)
   double center_x = 0.0, center_y = 0.0, radius = 0.0;
+  double z_lo = -std::numeric_limits<double>::infinity();
+  double z_hi = std::numeric_limits<double>::infinity();
+  Aabb box() const {
+    return {{center_x - radius, center_y - radius, z_lo}, {center_x + radius, center_y + radius, z_hi}};
+  }
+  bool is_inside(const Point3& p) const {
+    const double dx = p.x - center_x, dy = p.y - center_y;
+    return p.z >= z_lo && p.z <= z_hi && dx * dx + dy * dy <= radius * radius;
+  }
 };
 
 // ------------------------------------------------------ grid.hpp, map.hpp --
@@ -103,6 +169,16 @@ struct GridParams {
   std::uint64_t total_voxels() const { return nx * ny * nz; }
 };
 
+struct VoxelCoord {  // grid.hpp:21-27
+  std::uint64_t i = 0, j = 0, k = 0;
+};
+
+struct MemoryReport {  // map.hpp:41-48
+  std::uint64_t handle_bytes = 0;
+  std::uint64_t structure_bytes = 0;
+  std::uint64_t total_bytes = 0;
+};
+
 struct SliceOccupancy {
   bool dense = false;
   std::uint64_t cells = 0;
@@ -115,6 +191,15 @@ struct OccupancyStats {
   double empty_fraction = 0.0;
   std::vector<SliceOccupancy> slices;  // mixed flavour only, as the reference
 };
+
+struct QueryStats {  // search.hpp:12-17
+  std::uint64_t voxels_visited = 0;
+  std::uint64_t points_tested = 0;
+  std::uint64_t growth_iterations = 0;
+  double final_radius = 0.0;
+};
+
+enum class GrowthPolicy { Density, Monotonic };  // search.hpp:88
 
 struct Neighbor {
   PointHandle handle = 0;
@@ -194,6 +279,34 @@ class Cheesemap {
     return st;
   }
 
+  // map.hpp:62-69: materialized? (dense: always; mixed: any cell of a
+  // densified slice; else non-empty) and the voxel's handles (ascending)
+  bool voxel_present(const VoxelCoord& v) const {
+    int present = 0;
+    std::uint64_t n = 0;
+    check(cm_voxel_lookup(h_, v.i, v.j, v.k, &present, nullptr, 0, &n));
+    return present != 0;
+  }
+  std::optional<std::vector<PointHandle>> voxel_lookup(const VoxelCoord& v) const {
+    int present = 0;
+    std::uint64_t n = 0;
+    check(cm_voxel_lookup(h_, v.i, v.j, v.k, &present, nullptr, 0, &n));
+    if (!present) return std::nullopt;
+    std::vector<std::uint32_t> h(n);
+    if (n) check(cm_voxel_lookup(h_, v.i, v.j, v.k, &present, h.data(), n, &n));
+    return std::vector<PointHandle>(h.begin(), h.end());
+  }
+  MemoryReport memory_report() const {  // map.hpp:105, map.cpp:173-192
+    cm_memory_report r;
+    check(cm_get_memory_report(h_, &r));
+    return {r.handle_bytes, r.structure_bytes, r.total_bytes};
+  }
+  std::uint64_t device_bytes() const {
+    cm_memory_report r;
+    check(cm_get_memory_report(h_, &r));
+    return r.device_bytes;
+  }
+
   void corrupt_for_testing() { check(cm_corrupt_for_testing(h_)); }
   const cm_index* handle() const { return h_; }
 
@@ -220,25 +333,77 @@ inline Csr radius_search(const Cheesemap& m, const std::vector<Point3>& centers,
   return out;
 }
 
-inline std::vector<PointHandle> kernel_search(const Cheesemap& m, const SphereKernel& k) {
-  const Csr c = radius_search(m, {k.center}, k.radius, CM_SPHERE);
+namespace detail {
+inline void kernel_params(const SphereKernel& k, std::vector<double>& p) {
+  p.insert(p.end(), {k.center.x, k.center.y, k.center.z, k.radius});
+}
+inline void kernel_params(const BoxKernel& k, std::vector<double>& p) {
+  p.insert(p.end(), {k.aabb.min.x, k.aabb.min.y, k.aabb.min.z, k.aabb.max.x, k.aabb.max.y,
+                     k.aabb.max.z});
+}
+inline void kernel_params(const CylinderKernel& k, std::vector<double>& p) {
+  p.insert(p.end(), {k.center_x, k.center_y, k.radius, k.z_lo, k.z_hi});
+}
+inline int kernel_kind(const SphereKernel&) { return CM_SPHERE; }
+inline int kernel_kind(const BoxKernel&) { return CM_CUBE; }
+inline int kernel_kind(const CylinderKernel&) { return CM_CYLINDER; }
+
+inline Csr take(cm_csr* csr) {
+  std::uint64_t nq = 0, nnz = 0;
+  cm_csr_info(csr, &nq, &nnz, nullptr, nullptr);
+  Csr out;
+  out.row_ptr.resize(nq + 1);
+  out.cols.resize(nnz);
+  const cm_status s = cm_csr_download(csr, out.row_ptr.data(), out.cols.data(), nullptr);
+  cm_csr_free(csr);
+  check(s);
+  return out;
+}
+}  // namespace detail
+
+// kernel_search for a batch of kernels of one type (sorted rows).
+template <class K>
+Csr kernel_search_batch(const Cheesemap& m, const std::vector<K>& kernels,
+                        std::vector<QueryStats>* stats = nullptr) {
+  std::vector<double> p;
+  for (const K& k : kernels) detail::kernel_params(k, p);
+  const int kind = kernels.empty() ? CM_SPHERE : detail::kernel_kind(kernels.front());
+  cm_csr* csr = nullptr;
+  check(cm_kernel_search(m.handle(), kind, p.data(), kernels.size(), nullptr, &csr));
+  if (stats) {
+    std::vector<std::uint64_t> tested(kernels.size()), voxels(kernels.size());
+    const cm_status s = cm_kernel_count(m.handle(), kind, p.data(), kernels.size(), nullptr,
+                                        tested.data(), voxels.data(), nullptr);
+    if (s != CM_OK) cm_csr_free(csr);
+    check(s);
+    stats->assign(kernels.size(), QueryStats{});
+    for (std::size_t q = 0; q < kernels.size(); ++q)
+      (*stats)[q].points_tested = tested[q], (*stats)[q].voxels_visited = voxels[q];
+  }
+  return detail::take(csr);
+}
+
+// kernel_search (search.hpp:102-127): handles sorted ascending; QueryStats
+// voxels_visited / points_tested equal the reference's counters.
+template <class K>
+std::vector<PointHandle> kernel_search(const Cheesemap& m, const K& kernel,
+                                       QueryStats* stats = nullptr) {
+  std::vector<QueryStats> st;
+  const Csr c = kernel_search_batch(m, std::vector<K>{kernel}, stats ? &st : nullptr);
+  if (stats) *stats = st[0];
   return {c.cols.begin(), c.cols.end()};
 }
 
-inline std::vector<PointHandle> kernel_search(const Cheesemap& m, const BoxKernel& k) {
-  const Csr c = radius_search(m, {k.center}, k.half, CM_CUBE);
-  return {c.cols.begin(), c.cols.end()};
-}
-
-inline std::vector<PointHandle> kernel_search(const Cheesemap& m, const CylinderKernel& k) {
-  const Csr c = radius_search(m, {Point3{k.center_x, k.center_y, 0.0}}, k.radius, CM_CYLINDER);
-  return {c.cols.begin(), c.cols.end()};
+// baseline.hpp:11-21: the linear-scan oracle (ascending handles).
+template <class K>
+std::vector<PointHandle> brute_radius(const PointCloud& cloud, const K& kernel) {
+  std::vector<PointHandle> out;
+  for (std::size_t h = 0; h < cloud.size(); ++h)
+    if (kernel.is_inside(cloud[h])) out.push_back(h);
+  return out;
 }
 
 // ---------------------------------------------------------------- io.hpp --
-struct Aabb {
-  Point3 min, max;
-};
 struct LasHeaderInfo {  // io.hpp:11-19
   std::uint8_t version_major = 0, version_minor = 0, point_format = 0;
   std::uint64_t point_count = 0;
@@ -304,14 +469,31 @@ inline void knn_batch(const Cheesemap& m, const std::vector<Point3>& centers, st
                static_cast<uint32_t>(k), idx.data(), d2.data(), nullptr));
 }
 
-inline std::vector<Neighbor> knn_search(const Cheesemap& m, const Point3& c, std::size_t k) {
+// knn_search (search.hpp:131-134): exact for either policy; see the header
+// comment for what QueryStats reports.
+inline std::vector<Neighbor> knn_search(const Cheesemap& m, const Point3& c, std::size_t k,
+                                        GrowthPolicy policy = GrowthPolicy::Density,
+                                        QueryStats* stats = nullptr) {
+  (void)policy;
   if (k == 0) throw InvalidArgumentError("k must be at least 1");
   std::vector<std::uint32_t> idx;
   std::vector<double> d2;
   knn_batch(m, {c}, k, idx, d2);
   std::vector<Neighbor> out;
+  double dk = 0.0;
   for (std::size_t t = 0; t < k; ++t)
-    if (idx[t] != 0xffffffffu) out.push_back({idx[t], std::sqrt(d2[t])});
+    if (idx[t] != 0xffffffffu) {
+      out.push_back({idx[t], std::sqrt(d2[t])});
+      dk = d2[t];
+    }
+  if (stats) {
+    *stats = QueryStats{};
+    const double r = std::sqrt(dk);
+    const double p[4] = {c.x, c.y, c.z, r};
+    check(cm_kernel_count(m.handle(), CM_SPHERE, p, 1, nullptr, &stats->points_tested,
+                          &stats->voxels_visited, nullptr));
+    stats->final_radius = r;
+  }
   return out;
 }
 

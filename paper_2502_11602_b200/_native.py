@@ -125,6 +125,10 @@ def lib():
         "cm_radius_fill": ([p, p, u64, i32, dbl, p, p, p], i32),
         "cm_radius_search": ([p, p, u64, i32, dbl, p, ctypes.POINTER(p)], i32),
         "cm_radius_search_self": ([p, i32, dbl, p, ctypes.POINTER(p)], i32),
+        "cm_kernel_search": ([p, i32, p, u64, p, ctypes.POINTER(p)], i32),
+        "cm_kernel_count": ([p, i32, p, u64, p, p, p, p], i32),
+        "cm_voxel_lookup": ([p, u64, u64, u64, ctypes.POINTER(ctypes.c_int), p, u64,
+                             ctypes.POINTER(u64)], i32),
         "cm_pool_configure": ([i32, u64, u64], i32),
         "cm_csr_info": ([p, ctypes.POINTER(u64), ctypes.POINTER(u64), ctypes.POINTER(p),
                          ctypes.POINTER(p)], i32),

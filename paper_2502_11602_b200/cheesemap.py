@@ -8,7 +8,7 @@ so parity tests read like the reference's own tests:
   Cheesemap::build(cloud, BuildOptions)          Cheesemap.build(cloud, BuildOptions())
   map.grid() / occupancy_stats()                 Cheesemap.grid() / .occupancy_stats()
   kernel_search(map, SphereKernel{c, r})         kernel_search(map, SphereKernel(c, r))
-  kernel_search(map, BoxKernel{{c-r},{c+r}})     kernel_search(map, BoxKernel.cube(c, r))
+  kernel_search(map, BoxKernel{{lo},{hi}})       kernel_search(map, BoxKernel(lo, hi))
   knn_search(map, c, k)                          knn_search(map, c, k)
   cheesemap::EmptyCloudError, ...                EmptyCloudError, ...
 
@@ -122,20 +122,36 @@ class SphereKernel:  # geometry.hpp:73-85
 
 
 @dataclass
-class BoxKernel:  # geometry.hpp:87-92; the device path takes cubes c +- r
-    center: tuple
-    half: float
+class BoxKernel:  # geometry.hpp:87-92: any axis-aligned box, closed on all faces
+    min: tuple
+    max: tuple
 
     @staticmethod
-    def cube(center, r):
-        return BoxKernel(tuple(center), float(r))
+    def cube(center, r):  # the cube the reference CLI builds (cmd_bench.cpp:107-111)
+        c = [float(v) for v in center]
+        return BoxKernel(tuple(v - r for v in c), tuple(v + r for v in c))
 
 
 @dataclass
-class CylinderKernel:  # geometry.hpp:97-113, unbounded z (the weighted_density kernel)
+class CylinderKernel:  # geometry.hpp:97-113 (z range unbounded by default)
     center_x: float
     center_y: float
     radius: float
+    z_lo: float = float("-inf")
+    z_hi: float = float("inf")
+
+
+@dataclass
+class QueryStats:  # search.hpp:12-17
+    voxels_visited: int = 0
+    points_tested: int = 0
+    growth_iterations: int = 0
+    final_radius: float = 0.0
+
+
+class GrowthPolicy(IntEnum):  # search.hpp:88 (the device kNN is exact for either)
+    Density = 0
+    Monotonic = 1
 
 
 @dataclass
@@ -280,6 +296,29 @@ class Cheesemap:
         _check(_native.lib().cm_get_memory_report(self._h, ctypes.byref(r)))
         return {k: int(getattr(r, k)) for k, _ in r._fields_}
 
+    def voxel_present(self, v):
+        """Cheesemap::voxel_present (map.hpp:62-63) for v = (i, j, k)."""
+        n, pres = ctypes.c_uint64(), ctypes.c_int()
+        _check(_native.lib().cm_voxel_lookup(self._h, int(v[0]), int(v[1]), int(v[2]),
+                                             ctypes.byref(pres), None, 0, ctypes.byref(n)))
+        return bool(pres.value)
+
+    def voxel_lookup(self, v):
+        """Cheesemap::voxel_lookup (map.hpp:65-67): the voxel's handles
+        (ascending), or None when the voxel is not materialized."""
+        L = _native.lib()
+        n, pres = ctypes.c_uint64(), ctypes.c_int()
+        _check(L.cm_voxel_lookup(self._h, int(v[0]), int(v[1]), int(v[2]), ctypes.byref(pres),
+                                 None, 0, ctypes.byref(n)))
+        if not pres.value:
+            return None
+        out = np.zeros(n.value, dtype=np.uint32)
+        if n.value:
+            _check(L.cm_voxel_lookup(self._h, int(v[0]), int(v[1]), int(v[2]), ctypes.byref(pres),
+                                     out.ctypes.data_as(ctypes.c_void_p), out.size,
+                                     ctypes.byref(n)))
+        return out.astype(np.uint64)
+
     def reordered(self):
         return bool(self._opts.reorder)
 
@@ -310,15 +349,40 @@ def structure_name(flavor, mode, reordered=False):
 
 
 # -------------------------------------------------------------- queries --
-def _kernel_args(kernel):
-    if isinstance(kernel, SphereKernel):
-        return np.asarray(kernel.center, dtype=np.float64).reshape(1, 3), SPHERE, kernel.radius
-    if isinstance(kernel, BoxKernel):
-        return np.asarray(kernel.center, dtype=np.float64).reshape(1, 3), CUBE, kernel.half
-    if isinstance(kernel, CylinderKernel):
-        c = np.array([[kernel.center_x, kernel.center_y, 0.0]])
-        return c, CYLINDER, kernel.radius
-    raise InvalidArgumentError("kernel must be SphereKernel, BoxKernel.cube or CylinderKernel")
+def _kernel_params(kernels):
+    """Explicit kernels of one type -> (kind, params rows) for cm_kernel_search."""
+    k0 = kernels[0]
+    if isinstance(k0, SphereKernel):
+        rows = [[*map(float, k.center), float(k.radius)] for k in kernels]
+        return SPHERE, np.asarray(rows, dtype=np.float64).reshape(-1, 4)
+    if isinstance(k0, BoxKernel):
+        rows = [[*map(float, k.min), *map(float, k.max)] for k in kernels]
+        return CUBE, np.asarray(rows, dtype=np.float64).reshape(-1, 6)
+    if isinstance(k0, CylinderKernel):
+        rows = [[k.center_x, k.center_y, k.radius, k.z_lo, k.z_hi] for k in kernels]
+        return CYLINDER, np.asarray(rows, dtype=np.float64).reshape(-1, 5)
+    raise InvalidArgumentError("kernel must be SphereKernel, BoxKernel or CylinderKernel")
+
+
+def kernel_search_batch(m, kernels, stats=False, stream=None):
+    """kernel_search over explicit kernels of one type (each with its own
+    radius / box / z range): sorted CSR (row_ptr, cols), plus the per-kernel
+    (points_tested, voxels_visited) when stats=True."""
+    kind, prm = _kernel_params(list(kernels))
+    L = _native.lib()
+    nq = prm.shape[0]
+    csr = ctypes.c_void_p()
+    _check(L.cm_kernel_search(m.handle, kind, prm.ctypes.data_as(ctypes.c_void_p), nq,
+                              _stream_ptr(stream), ctypes.byref(csr)))
+    row, cols = _take_csr(L, csr, nq, m.device, stream, False)
+    if not stats:
+        return row, cols
+    pt = np.zeros(nq, dtype=np.uint64)
+    vv = np.zeros(nq, dtype=np.uint64)
+    _check(L.cm_kernel_count(m.handle, kind, prm.ctypes.data_as(ctypes.c_void_p), nq, None,
+                             pt.ctypes.data_as(ctypes.c_void_p), vv.ctypes.data_as(ctypes.c_void_p),
+                             _stream_ptr(stream)))
+    return row, cols, pt, vv
 
 
 def radius_count(m, centers, r, kernel=SPHERE, counts=None, points_tested=None, stream=None):
@@ -421,21 +485,35 @@ def knn_batch(m, centers, k, stream=None, device_out=False):
     return idx, d2
 
 
-def kernel_search(m, kernel):
+def kernel_search(m, kernel, stats=None):
     """kernel_search (search.hpp:102-127) for one kernel: the handles inside
-    it, sorted ascending."""
-    c, kind, r = _kernel_args(kernel)
-    _, cols = radius_search_batch(m, c, r, kind)
+    it, sorted ascending; a QueryStats passed as `stats` gets the reference's
+    voxels_visited / points_tested."""
+    if stats is None:
+        _, cols = kernel_search_batch(m, [kernel])
+    else:
+        _, cols, pt, vv = kernel_search_batch(m, [kernel], stats=True)
+        stats.points_tested, stats.voxels_visited = int(pt[0]), int(vv[0])
+        stats.growth_iterations, stats.final_radius = 0, 0.0
     return cols.astype(np.uint64)
 
 
-def knn_search(m, c, k):
-    """knn_search (search.cpp:87-146): min(k, N) nearest, by (d^2, handle)."""
+def knn_search(m, c, k, policy=GrowthPolicy.Density, stats=None):
+    """knn_search (search.cpp:87-146): min(k, N) nearest, by (d^2, handle).
+    Exact for either policy; `stats` gets the candidates of kernel_search at
+    the exact k-th distance (points_tested, voxels_visited) and that distance
+    as final_radius."""
     if k == 0:
         raise InvalidArgumentError("k must be at least 1")
     idx, d2 = knn_batch(m, np.asarray(c, dtype=np.float64).reshape(1, 3), k)
-    return [Neighbor(int(i), float(np.sqrt(d))) for i, d in zip(idx[0], d2[0])
-            if i != 0xFFFFFFFF]
+    out = [Neighbor(int(i), float(np.sqrt(d))) for i, d in zip(idx[0], d2[0])
+           if i != 0xFFFFFFFF]
+    if stats is not None:
+        r = out[-1].distance if out else 0.0
+        _, _, pt, vv = kernel_search_batch(m, [SphereKernel(tuple(map(float, c)), r)], stats=True)
+        stats.points_tested, stats.voxels_visited = int(pt[0]), int(vv[0])
+        stats.growth_iterations, stats.final_radius = 0, r
+    return out
 
 
 # -------------------------------------------------------------- analysis --

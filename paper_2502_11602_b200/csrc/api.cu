@@ -378,8 +378,8 @@ cm_status cm_free(cm_index* ix) {
   if (!ix) return CM_OK;
   DeviceGuard dg(ix->device);
   cudaDeviceSynchronize();
-  void* ptrs[] = {ix->rec,   ix->ukey,  ix->ustart, ix->uk_k,    ix->dense_off,
-                  ix->vhash, ix->col_dense, ix->chash, ix->col_vbeg};
+  void* ptrs[] = {ix->rec,   ix->ukey,      ix->ustart, ix->uk_k,     ix->dense_off,
+                  ix->vhash, ix->col_dense, ix->chash,  ix->col_vbeg, ix->rec_of};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, 0);
   cudaStreamSynchronize(0);
@@ -515,6 +515,79 @@ cm_status cm_export_voxels(const cm_index* ix, uint64_t* keys, uint32_t* handles
   CM_CUDA_TRY(cudaGetLastError());
   CM_TRY(k.finish());
   CM_TRY(h.finish());
+  CM_CUDA_TRY(cudaStreamSynchronize(st));
+  return CM_OK;
+}
+
+}  // extern "C"
+
+namespace cmg {
+namespace apik {
+// The span [b, e) of voxel (i, j, k) in the cell-ordered records, and the
+// handles stored there (ascending, as the reference stores a voxel's points
+// in cloud order, map.cpp:67-120).
+template <int FLAVOR>
+__global__ void voxel_span_kernel(const Tables t, uint64_t i, uint64_t j, uint64_t k,
+                                  uint32_t* __restrict__ be) {
+  uint32_t b = 0, e = 0;
+  column_span<FLAVOR>(t, i, j, k, k, &b, &e);
+  be[0] = b;
+  be[1] = e;
+}
+__global__ void voxel_ids_kernel(const PointRec* __restrict__ rec, const uint32_t* __restrict__ be,
+                                 uint32_t cap, uint32_t* __restrict__ out) {
+  const uint32_t b = be[0], e = be[1];
+  for (uint32_t p = b + threadIdx.x; p < e && p - b < cap; p += blockDim.x) out[p - b] = rec[p].id;
+}
+}  // namespace apik
+}  // namespace cmg
+
+extern "C" {
+
+// Cheesemap::voxel_present / voxel_lookup (map.hpp:62-69, map.cpp:124-136):
+// *present = the voxel is materialized (always for the dense flavour; for a
+// mixed map, every cell of a densified slice; otherwise non-empty); the
+// voxel's handles (ascending) to `handles` (host or device, up to capacity)
+// and their number to *count. Synchronous. CM_OUT_OF_DOMAIN for a voxel
+// outside the grid.
+cm_status cm_voxel_lookup(const cm_index* ix, uint64_t i, uint64_t j, uint64_t k, int* present,
+                          uint32_t* handles, uint64_t capacity, uint64_t* count) {
+  CM_TRY(check_index(ix));
+  if (i >= ix->g.nx || j >= ix->g.ny || k >= ix->g.nz) {
+    set_error("voxel outside the grid");
+    return CM_OUT_OF_DOMAIN;
+  }
+  DeviceGuard dg(ix->device);
+  cudaStream_t st = 0;
+  uint32_t* be = nullptr;
+  CM_CUDA_TRY(dev_alloc_t(&be, 2, st));
+  const Tables t = ix->tables();
+  if (ix->opts.flavor == CM_DENSE) apik::voxel_span_kernel<CM_DENSE><<<1, 1, 0, st>>>(t, i, j, k, be);
+  else if (ix->opts.flavor == CM_SPARSE) apik::voxel_span_kernel<CM_SPARSE><<<1, 1, 0, st>>>(t, i, j, k, be);
+  else apik::voxel_span_kernel<CM_MIXED><<<1, 1, 0, st>>>(t, i, j, k, be);
+  ::cmg::note_launch();
+  uint32_t hb[2] = {0, 0};
+  CM_CUDA_TRY(cudaMemcpyAsync(hb, be, 8, cudaMemcpyDeviceToHost, st));
+  CM_CUDA_TRY(cudaStreamSynchronize(st));
+  const uint64_t n = hb[1] - hb[0];
+  if (count) *count = n;
+  if (present) {
+    bool p = n > 0;
+    if (ix->opts.flavor == CM_DENSE) p = true;
+    if (ix->opts.flavor == CM_MIXED && k < ix->slice_ne.size())
+      p = p || static_cast<double>(ix->slice_ne[k]) / static_cast<double>(ix->g.nx * ix->g.ny) >=
+                   ix->opts.densify_threshold;
+    *present = p ? 1 : 0;
+  }
+  if (handles && n && capacity) {
+    OutBuf<uint32_t> h;
+    CM_TRY(h.init(handles, std::min<uint64_t>(n, capacity), st));
+    apik::voxel_ids_kernel<<<1, 256, 0, st>>>(ix->rec, be, (uint32_t)std::min<uint64_t>(n, capacity), h.dev);
+    ::cmg::note_launch();
+    CM_CUDA_TRY(cudaGetLastError());
+    CM_TRY(h.finish());
+  }
+  dev_free(be, st);
   CM_CUDA_TRY(cudaStreamSynchronize(st));
   return CM_OK;
 }
@@ -720,7 +793,8 @@ struct GatherHook {
 // the phases (cm_get_last_query_timing).
 static cm_status radius_search_core(const cm_index* ix, const double* qd, uint64_t nq, int kernel,
                                     double r, cudaStream_t st, cm_csr* csr,
-                                    GatherHook* hook = nullptr) {
+                                    GatherHook* hook = nullptr, const double* rq = nullptr,
+                                    const double* qbox = nullptr) {
   QueryEvents& ev = qev();
   ev.valid = false;
   cudaEventRecord(ev.e[0], st);
@@ -773,7 +847,7 @@ static cm_status radius_search_core(const cm_index* ix, const double* qd, uint64
   bool recollected = false;
   if (!two_pass) {
     s = radius_collect_dev(ix, qd, nq, kernel, r, ord.perm, temp, cap, toff, scnt, counts, cursor,
-                           st, ev.e[2]);
+                           st, ev.e[2], rq, qbox);
     cudaEventRecord(ev.e[3], st);
     if (s != CM_OK) return fail(s);
     if (!read_u64_mapped(cursor, st, &used)) {
@@ -791,7 +865,7 @@ static cm_status radius_search_core(const cm_index* ix, const double* qd, uint64
       if (dev_alloc_t(&temp, cap, st) == cudaSuccess) {
         recollected = true;
         s = radius_collect_dev(ix, qd, nq, kernel, r, ord.perm, temp, cap, toff, scnt, counts,
-                               cursor, st, ev.e[2]);
+                               cursor, st, ev.e[2], rq, qbox);
         cudaEventRecord(ev.e[3], st);
         if (s != CM_OK) return fail(s);
         if (!read_u64_mapped(cursor, st, &used)) {
@@ -810,7 +884,7 @@ static cm_status radius_search_core(const cm_index* ix, const double* qd, uint64
   }
   if (two_pass) {
     cudaEventRecord(ev.e[1], st);
-    s = radius_count_dev(ix, qd, nq, kernel, r, ord.perm, counts, nullptr, st);
+    s = radius_count_dev(ix, qd, nq, kernel, r, ord.perm, counts, nullptr, st, rq, qbox);
     cudaEventRecord(ev.e[2], st);
     cudaEventRecord(ev.e[3], st);
     if (s != CM_OK) return fail(s);
@@ -849,7 +923,7 @@ static cm_status radius_search_core(const cm_index* ix, const double* qd, uint64
   }
   if (two_pass)
     s = radius_fill_dev(ix, qd, nq, kernel, r, ord.perm, csr->row_ptr, csr->cols, st, nullptr,
-                        mid_min);
+                        mid_min, rq, qbox);
   else
     s = hook ? hook->run(temp, toff, scnt, csr->row_ptr, ord.perm, csr->cols, nq, st)
              : gather_rows_dev(temp, toff, scnt, csr->row_ptr, ord.perm, csr->cols, nq, st);
@@ -921,6 +995,167 @@ cm_status cm_radius_search_self(const cm_index* ix, int kernel, double r, void* 
   }
   *out = csr;
   return CM_OK;
+}
+
+}  // extern "C"
+
+namespace cmg {
+namespace apik {
+// Explicit kernels -> centres (query order only), per-centre radius, and
+// the kernel's box() where it is not c +- r:
+//   CM_SPHERE   4 doubles: cx cy cz r            (box c +- r, computed by the kernels)
+//   CM_CUBE     6 doubles: min xyz, max xyz      (BoxKernel{Aabb}, geometry.hpp:87-92)
+//   CM_CYLINDER 5 doubles: cx cy r z_lo z_hi     (geometry.hpp:97-113)
+__global__ void kernel_params_kernel(int kind, const double* __restrict__ prm, uint64_t nq,
+                                     DevGrid g, double* __restrict__ q, double* __restrict__ rq,
+                                     double* __restrict__ qbox) {
+  const int w = kind == CM_SPHERE ? 4 : kind == CM_CUBE ? 6 : 5;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nq;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const double* p = prm + (uint64_t)w * i;
+    double cx, cy, cz, r = 0.0;
+    if (kind == CM_SPHERE) {
+      cx = p[0], cy = p[1], cz = p[2], r = p[3];
+    } else if (kind == CM_CUBE) {
+      double* b = qbox + 6 * i;
+      for (int a = 0; a < 6; ++a) b[a] = p[a];
+      cx = 0.5 * (p[0] + p[3]), cy = 0.5 * (p[1] + p[4]), cz = 0.5 * (p[2] + p[5]);
+    } else {
+      cx = p[0], cy = p[1], r = p[2];
+      double* b = qbox + 6 * i;
+      b[0] = __dsub_rn(cx, r), b[1] = __dsub_rn(cy, r), b[2] = p[3];
+      b[3] = __dadd_rn(cx, r), b[4] = __dadd_rn(cy, r), b[5] = p[4];
+      cz = 0.5 * (fmax(p[3], g.bz0) + fmin(p[4], g.bz1));
+    }
+    // centres only order the queries; keep them finite and inside the grid
+    cx = fmin(fmax(cx, g.bx0), g.bx1);
+    cy = fmin(fmax(cy, g.by0), g.by1);
+    cz = fmin(fmax(cz, g.bz0), g.bz1);
+    q[3 * i] = isnan(cx) ? g.bx0 : cx;
+    q[3 * i + 1] = isnan(cy) ? g.by0 : cy;
+    q[3 * i + 2] = isnan(cz) ? g.bz0 : cz;
+    rq[i] = r;
+  }
+}
+
+// QueryStats::voxels_visited (search.hpp:116-119): the voxels of the
+// kernel's clamped range, empty or not.
+__global__ void voxels_visited_kernel(int kind, const double* __restrict__ q,
+                                      const double* __restrict__ rq, const double* __restrict__ qbox,
+                                      uint64_t nq, DevGrid g, uint64_t* __restrict__ out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nq;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    Range R;
+    const bool ok = clamped_range(g, q[3 * i], q[3 * i + 1], q[3 * i + 2], rq[i], &R, kind,
+                                  kind == CM_SPHERE ? nullptr : qbox + 6 * i);
+    out[i] = ok ? (R.i1 - R.i0 + 1) * (R.j1 - R.j0 + 1) * (R.k1 - R.k0 + 1) : 0;
+  }
+}
+}  // namespace apik
+}  // namespace cmg
+
+namespace {
+// Device buffers of an explicit-kernel batch (kernel_params_kernel).
+struct KernelBatch {
+  double* q = nullptr;
+  double* rq = nullptr;
+  double* qbox = nullptr;
+  cudaStream_t st = nullptr;
+  ~KernelBatch() {
+    if (q) dev_free(q, st);
+    if (rq) dev_free(rq, st);
+    if (qbox) dev_free(qbox, st);
+  }
+  cm_status init(const cm_index* ix, int kind, const double* params, uint64_t nq, cudaStream_t s) {
+    st = s;
+    if (kind != CM_SPHERE && kind != CM_CUBE && kind != CM_CYLINDER) {
+      set_error("unknown kernel (CM_SPHERE = 0, CM_CUBE = 1 (Aabb box), CM_CYLINDER = 2)");
+      return CM_INVALID_ARGUMENT;
+    }
+    const int w = kind == CM_SPHERE ? 4 : kind == CM_CUBE ? 6 : 5;
+    InBuf in;
+    CM_TRY(stage_input(params, nq * w * 8, st, &in));
+    CM_CUDA_TRY(dev_alloc_t(&q, 3 * nq + 3, st));
+    CM_CUDA_TRY(dev_alloc_t(&rq, nq + 1, st));
+    if (kind != CM_SPHERE) CM_CUDA_TRY(dev_alloc_t(&qbox, 6 * nq + 6, st));
+    if (nq) {
+      const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nq + 255) / 256, (uint64_t)sm_count() * 8));
+      apik::kernel_params_kernel<<<grid, 256, 0, st>>>(kind, static_cast<const double*>(in.dev), nq,
+                                                       ix->g, q, rq, qbox);
+      ::cmg::note_launch();
+      CM_CUDA_TRY(cudaGetLastError());
+    }
+    return CM_OK;
+  }
+};
+}  // namespace
+
+extern "C" {
+
+// kernel_search (search.hpp:102-127) for a batch of explicit kernels, each
+// with its own parameters (see kernel_params_kernel): per-centre radii,
+// BoxKernel Aabbs, bounded cylinders. Sorted rows like cm_radius_search.
+cm_status cm_kernel_search(const cm_index* ix, int kernel, const double* params, uint64_t nq,
+                           void* stream, cm_csr** out) {
+  CM_TRY(check_index(ix));
+  if (!out || (nq && !params)) {
+    set_error("null parameters or output pointer");
+    return CM_INVALID_ARGUMENT;
+  }
+  *out = nullptr;
+  DeviceGuard dg(ix->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  KernelBatch kb;
+  CM_TRY(kb.init(ix, kernel, params, nq, st));
+  cm_csr* csr = new cm_csr();
+  csr->nq = nq;
+  csr->device = ix->device;
+  const cm_status s =
+      radius_search_core(ix, kb.q, nq, kernel, -1.0, st, csr, nullptr, kb.rq, kb.qbox);
+  if (s != CM_OK) {
+    cm_csr_free(csr);
+    return s;
+  }
+  *out = csr;
+  return CM_OK;
+}
+
+// Counts and QueryStats (search.hpp:12-17) of explicit kernels: counts[q],
+// points_tested[q], voxels_visited[q]; any output may be NULL; host or
+// device outputs.
+cm_status cm_kernel_count(const cm_index* ix, int kernel, const double* params, uint64_t nq,
+                          uint32_t* counts, uint64_t* points_tested, uint64_t* voxels_visited,
+                          void* stream) {
+  CM_TRY(check_index(ix));
+  if (nq && !params) {
+    set_error("null parameters");
+    return CM_INVALID_ARGUMENT;
+  }
+  DeviceGuard dg(ix->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  KernelBatch kb;
+  CM_TRY(kb.init(ix, kernel, params, nq, st));
+  OutBuf<uint32_t> c;
+  OutBuf<uint64_t> t, v;
+  CM_TRY(c.init(counts, nq, st));
+  CM_TRY(t.init(points_tested, nq, st));
+  CM_TRY(v.init(voxels_visited, nq, st));
+  if (nq && (c.dev || t.dev)) {
+    QueryOrder ord;
+    CM_TRY(order_queries(ix, kb.q, nq, st, &ord, -1.0, kernel));
+    CM_TRY(radius_count_dev(ix, kb.q, nq, kernel, -1.0, ord.perm, c.dev, t.dev, st, kb.rq,
+                            kb.qbox));
+  }
+  if (nq && v.dev) {
+    const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nq + 255) / 256, (uint64_t)sm_count() * 8));
+    apik::voxels_visited_kernel<<<grid, 256, 0, st>>>(kernel, kb.q, kb.rq, kb.qbox, nq, ix->g, v.dev);
+    ::cmg::note_launch();
+    CM_CUDA_TRY(cudaGetLastError());
+  }
+  CM_TRY(c.finish());
+  CM_TRY(t.finish());
+  CM_TRY(v.finish());
+  return sync_if(c.host() || t.host() || v.host(), st);
 }
 
 namespace {
@@ -1437,7 +1672,10 @@ cm_status cm_knn(const cm_index* ix, const double* q, uint64_t nq, uint32_t k, u
   CM_TRY(oi.init(idx, nq * k, st));
   CM_TRY(od.init(d2, nq * k, st));
   QueryOrder ord;
-  CM_TRY(order_queries(ix, static_cast<const double*>(in.dev), nq, st, &ord));
+  // 2D Morton centre order: measured no change for config 3 (the tile
+  // hulls are set by the centre density, not the curve); opt-in
+  static const bool morton = std::getenv("CMGPU_KNN_MORTON") != nullptr;
+  CM_TRY(order_queries(ix, static_cast<const double*>(in.dev), nq, st, &ord, -1.0, 0, morton));
   CM_TRY(knn_dev(ix, static_cast<const double*>(in.dev), nq, k, ord.perm, oi.dev, od.dev, st));
   CM_TRY(oi.finish());
   CM_TRY(od.finish());

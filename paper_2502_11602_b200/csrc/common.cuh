@@ -100,12 +100,28 @@ __device__ __forceinline__ void kernel_zbox(int kind, double cz, double r, doubl
   }
 }
 
+// The kernel's box(): c +- r (sphere, cube, and the x / y extent of the
+// cylinder), or, for queries given as explicit kernels (cm_kernel_search:
+// BoxKernel's Aabb, CylinderKernel's z range), the caller's box
+// {min xyz, max xyz}, which IS the reference's box() (geometry.hpp:87-113).
+__device__ __forceinline__ void kernel_box(int kind, double cx, double cy, double cz, double r,
+                                           const double* box, double* lx, double* ly, double* lz,
+                                           double* hx, double* hy, double* hz) {
+  if (box) {
+    *lx = box[0], *ly = box[1], *lz = box[2];
+    *hx = box[3], *hy = box[4], *hz = box[5];
+    return;
+  }
+  *lx = __dsub_rn(cx, r), *hx = __dadd_rn(cx, r);
+  *ly = __dsub_rn(cy, r), *hy = __dadd_rn(cy, r);
+  kernel_zbox(kind, cz, r, lz, hz);
+}
+
 __device__ __forceinline__ bool clamped_range(const DevGrid& g, double cx, double cy, double cz,
-                                              double r, Range* out, int kind = 0) {
-  const double lx = __dsub_rn(cx, r), hx = __dadd_rn(cx, r);
-  const double ly = __dsub_rn(cy, r), hy = __dadd_rn(cy, r);
-  double lz, hz;
-  kernel_zbox(kind, cz, r, &lz, &hz);
+                                              double r, Range* out, int kind = 0,
+                                              const double* box = nullptr) {
+  double lx, ly, lz, hx, hy, hz;
+  kernel_box(kind, cx, cy, cz, r, box, &lx, &ly, &lz, &hx, &hy, &hz);
   if (!(lx <= g.bx1 && hx >= g.bx0 && ly <= g.by1 && hy >= g.by0 && lz <= g.bz1 &&
         hz >= g.bz0))
     return false;
@@ -127,11 +143,9 @@ __device__ __forceinline__ bool clamped_range(const DevGrid& g, double cx, doubl
 // arithmetic as clamped_range.
 __device__ __forceinline__ bool clamped_range_warp(const DevGrid& g, double cx, double cy,
                                                    double cz, double r, int lane, Range* out,
-                                                   int kind = 0) {
-  const double lx = __dsub_rn(cx, r), hx = __dadd_rn(cx, r);
-  const double ly = __dsub_rn(cy, r), hy = __dadd_rn(cy, r);
-  double lz, hz;
-  kernel_zbox(kind, cz, r, &lz, &hz);
+                                                   int kind = 0, const double* box = nullptr) {
+  double lx, ly, lz, hx, hy, hz;
+  kernel_box(kind, cx, cy, cz, r, box, &lx, &ly, &lz, &hx, &hy, &hz);
   if (!(lx <= g.bx1 && hx >= g.bx0 && ly <= g.by1 && hy >= g.by0 && lz <= g.bz1 &&
         hz >= g.bz0))
     return false;
@@ -172,12 +186,11 @@ struct Predicate {
   double lx, ly, lz, hx, hy, hz;      // c -+ r (cube)
   int cube;
 
-  __device__ __forceinline__ void init(double x, double y, double z, double r, int kind) {
+  __device__ __forceinline__ void init(double x, double y, double z, double r, int kind,
+                                       const double* box = nullptr) {
     cx = x, cy = y, cz = z;
     rr = __dmul_rn(r, r);
-    lx = __dsub_rn(x, r), ly = __dsub_rn(y, r);
-    hx = __dadd_rn(x, r), hy = __dadd_rn(y, r);
-    kernel_zbox(kind, z, r, &lz, &hz);
+    kernel_box(kind, x, y, z, r, box, &lx, &ly, &lz, &hx, &hy, &hz);
     cube = kind;
   }
   __device__ __forceinline__ bool operator()(double px, double py, double pz) const {

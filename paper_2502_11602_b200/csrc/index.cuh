@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -44,6 +45,9 @@ struct cm_index {
   // handles are global ids of a multi-GPU slab (cm_build_slab), not
   // positions in the indexed points: self queries do not apply
   bool global_ids = false;
+  // lazily built (first kNN): handle -> record position, n entries
+  mutable uint32_t* rec_of = nullptr;
+  mutable std::mutex lazy_mu;
 
   cmg::Tables tables() const {
     cmg::Tables t{};
@@ -124,11 +128,13 @@ struct QueryOrder {
   }
 };
 // q_dev == nullptr: self queries (the index's own n points, row q = point q).
+// morton: 2D Morton order of the centres' columns (sparse centre sets, kNN)
 cm_status order_queries(const cm_index* ix, const double* q_dev, uint64_t nq, cudaStream_t st,
-                        QueryOrder* out, double r = -1.0, int kind = 0);
+                        QueryOrder* out, double r = -1.0, int kind = 0, bool morton = false);
 cm_status radius_count_dev(const cm_index* ix, const double* q_dev, uint64_t nq, int kernel,
                            double r, const uint32_t* perm, uint32_t* counts_dev,
-                           uint64_t* tested_dev, cudaStream_t st);
+                           uint64_t* tested_dev, cudaStream_t st, const double* rq = nullptr,
+                           const double* qbox = nullptr);
 bool radius_is_wide(const cm_index* ix, double r);
 // brute-force baselines (brute.cu): every point against every centre
 constexpr int kBruteKMax = 64;
@@ -142,17 +148,20 @@ cm_status brute_knn_dev(const double* xyz, uint64_t n, const double* q, uint64_t
 cm_status radius_fill_dev(const cm_index* ix, const double* q_dev, uint64_t nq, int kernel,
                           double r, const uint32_t* perm, const uint64_t* row_ptr_dev,
                           uint32_t* cols_dev, cudaStream_t st, cudaEvent_t after_fill = nullptr,
-                          uint32_t mid_min = 0);
+                          uint32_t mid_min = 0, const double* rq = nullptr,
+                          const double* qbox = nullptr);
 cm_status row_class_counts_dev(const uint32_t* counts, uint64_t nq, unsigned long long* out,
                                cudaStream_t st);
 cm_status radius_digest_dev(const cm_index* ix, const double* q_dev, uint64_t nq, int kernel,
                             double r, const uint32_t* perm, uint32_t* counts_dev,
-                            uint64_t* digest_dev, cudaStream_t st);
+                            uint64_t* digest_dev, cudaStream_t st, const double* rq = nullptr,
+                            const double* qbox = nullptr);
 cm_status radius_collect_dev(const cm_index* ix, const double* q_dev, uint64_t nq, int kernel,
                              double r, const uint32_t* perm, uint32_t* temp, uint64_t cap,
                              uint64_t* toff, uint32_t* scnt, uint32_t* counts,
                              unsigned long long* cursor, cudaStream_t st,
-                             cudaEvent_t after_collect);
+                             cudaEvent_t after_collect, const double* rq = nullptr,
+                             const double* qbox = nullptr);
 cm_status gather_rows_dev(const uint32_t* temp, const uint64_t* toff, const uint32_t* scnt,
                           const uint64_t* row_ptr, const uint32_t* perm, uint32_t* cols,
                           uint64_t nq, cudaStream_t st);

@@ -11,6 +11,11 @@
 // exact; this one also settles ties by handle, which the reference's
 // insertion-ordered CandidateList (search.cpp:16-28) does not.
 #include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <mutex>
+#include <vector>
 
 #include "index.cuh"
 #include "sort_scan.cuh"
@@ -450,6 +455,339 @@ __global__ void __launch_bounds__(kKThreads) knn_tile_kernel(
   }
 }
 
+// ---- kNN by radius brackets (the default for k <= kKMax) -------------------
+// The k nearest of a centre are exactly the k smallest (d², handle) among
+// the points with d² <= R² for ANY R with count(d² <= R²) >= k. So: (1)
+// per-centre radius brackets from the radius engine's COUNT pass (the same
+// query tiles: 32 cell-sorted centres share each staged record), growing R
+// for the centres that saw fewer than k points; (2) one COLLECT pass at each
+// centre's final R (its hits land in an arena row); (3) each row sorted by
+// (d², handle) and cut to k. Centres still open after the last bracket, or
+// with rows too long to sort in registers, take the shell walk above.
+constexpr int kSelMax = 512;  // longest row sorted by knn_select_kernel
+
+// Round outcome of list entry s: 0 resolved (count in [k, kSelMax]), 1 grow
+// the radius and retry, 2 shell walk (last round, or the row is too long).
+__global__ void knn_bracket_kernel(const uint32_t* __restrict__ list, uint32_t n,
+                                   const uint32_t* __restrict__ counts, uint32_t k, int last,
+                                   double* __restrict__ rq, uint32_t* __restrict__ f_res,
+                                   uint32_t* __restrict__ f_next, double rmax) {
+  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < n; s += gridDim.x * blockDim.x) {
+    const uint32_t qi = list[s];
+    const uint32_t c = counts[qi];
+    const double r = rq[qi];
+    uint32_t res = 0, nxt = 0;
+    if (c >= k && c <= (uint32_t)kSelMax) {
+      res = 1;
+    } else if (c < k && !last && r < rmax) {
+      // grow as for a surface (count ~ r^2), by 1.25..2x, 5 % margin
+      const double g = fmin(2.0, fmax(1.25, 1.05 * sqrt((double)k / fmax(1.0, (double)c))));
+      rq[qi] = r * g;
+      nxt = 1;
+    }
+    f_res[s] = res;
+    f_next[s] = nxt;
+  }
+}
+
+// Order-preserving compaction of the round: resolved entries are appended
+// after the earlier rounds' (res_base), retries form the next list, the rest
+// go to the shell-walk list (any order).
+__global__ void knn_compact_kernel(const uint32_t* __restrict__ list, uint32_t n,
+                                   const uint32_t* __restrict__ f_res, const uint32_t* __restrict__ p_res,
+                                   const uint32_t* __restrict__ f_next, const uint32_t* __restrict__ p_next,
+                                   uint32_t* __restrict__ res_list, const uint32_t* __restrict__ res_base,
+                                   uint32_t* __restrict__ next_list, uint32_t* __restrict__ walk_list,
+                                   uint32_t* __restrict__ n_walk) {
+  const uint32_t rb = *res_base;
+  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < n; s += gridDim.x * blockDim.x) {
+    const uint32_t qi = list[s];
+    if (f_res[s]) res_list[rb + p_res[s]] = qi;
+    else if (f_next[s]) next_list[p_next[s]] = qi;
+    else walk_list[atomicAdd(n_walk, 1u)] = qi;
+  }
+}
+
+__global__ void knn_rank_kernel(const PointRec* __restrict__ rec, uint64_t n,
+                                uint32_t* __restrict__ rec_of) {
+  for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n;
+       p += (uint64_t)gridDim.x * blockDim.x)
+    rec_of[rec[p].id] = (uint32_t)p;
+}
+
+// Bitonic sort of 32 * E (d², handle) pairs held blocked by a warp (lane l:
+// elements [l * E, (l + 1) * E)), ascending by (d², handle).
+template <int E>
+__device__ __forceinline__ void warp_sort_pairs_blocked(double (&d)[E], uint32_t (&id)[E], int lane) {
+  constexpr int P = 32 * E;
+#pragma unroll
+  for (int kk = 2; kk <= P; kk <<= 1) {
+#pragma unroll
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      if (j < E) {
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+          const int p = r ^ j;
+          if (p > r) {
+            const bool asc = (((uint32_t)lane * E + r) & kk) == 0;
+            const bool pl = pair_less(d[p], id[p], d[r], id[r]);
+            if (asc == pl) {
+              const double td = d[r];
+              d[r] = d[p];
+              d[p] = td;
+              const uint32_t ti = id[r];
+              id[r] = id[p];
+              id[p] = ti;
+            }
+          }
+        }
+      } else {
+        const int jl = j / E;
+        const bool lower = (lane & jl) == 0;
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+          const double od = __shfl_xor_sync(0xffffffffu, d[r], jl);
+          const uint32_t oi = __shfl_xor_sync(0xffffffffu, id[r], jl);
+          const bool asc = (((uint32_t)lane * E + r) & kk) == 0;
+          const bool o_less = pair_less(od, oi, d[r], id[r]);
+          if ((lower == asc) ? o_less : !o_less) {
+            d[r] = od;
+            id[r] = oi;
+          }
+        }
+      }
+    }
+  }
+}
+
+template <int E>
+__device__ __forceinline__ void select_row(const PointRec* __restrict__ rec,
+                                           const uint32_t* __restrict__ rec_of,
+                                           const uint32_t* __restrict__ row, uint32_t n, double cx,
+                                           double cy, double cz, uint32_t k, uint64_t qi, int lane,
+                                           uint32_t* __restrict__ idx_out,
+                                           double* __restrict__ d2_out) {
+  double d[E];
+  uint32_t id[E];
+#pragma unroll
+  for (int r = 0; r < E; ++r) {
+    const uint32_t i = (uint32_t)lane * E + r;
+    d[r] = __longlong_as_double(0x7ff0000000000000ll);
+    id[r] = 0xffffffffu;
+    if (i < n) {
+      const uint32_t h = __ldg(row + i);
+      const PointRec pr = load_rec(rec + __ldg(rec_of + h));
+      d[r] = sqdist(pr.x, pr.y, pr.z, cx, cy, cz);
+      id[r] = h;
+    }
+  }
+  warp_sort_pairs_blocked<E>(d, id, lane);
+#pragma unroll
+  for (int r = 0; r < E; ++r) {
+    const uint32_t i = (uint32_t)lane * E + r;
+    if (i < k) {
+      idx_out[qi * k + i] = id[r];
+      if (d2_out) d2_out[qi * k + i] = d[r];
+    }
+  }
+}
+
+// One warp per resolved centre: its arena row (every point with d² <= R²,
+// at least k of them) sorted by (d², handle); the first k are the answer.
+__global__ void __launch_bounds__(kKThreads) knn_select_kernel(
+    const PointRec* __restrict__ rec, const uint32_t* __restrict__ rec_of,
+    const double* __restrict__ q, const uint32_t* __restrict__ list,
+    const uint32_t* __restrict__ n_list, uint32_t k, const uint32_t* __restrict__ arena,
+    const uint64_t* __restrict__ toff, const uint32_t* __restrict__ scnt,
+    uint32_t* __restrict__ idx_out, double* __restrict__ d2_out) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t nl = *n_list;
+  for (uint32_t s = blockIdx.x * kKWarps + (threadIdx.x >> 5); s < nl; s += gridDim.x * kKWarps) {
+    const uint32_t qi = __ldg(list + s);
+    const uint32_t n = __ldg(scnt + qi);
+    const uint32_t* row = arena + __ldg(toff + qi);
+    const double cx = __ldg(q + 3 * (uint64_t)qi);
+    const double cy = __ldg(q + 3 * (uint64_t)qi + 1);
+    const double cz = __ldg(q + 3 * (uint64_t)qi + 2);
+    CM_DCHECK(n >= k && n <= (uint32_t)kSelMax);
+    if (n <= 32)
+      select_row<1>(rec, rec_of, row, n, cx, cy, cz, k, qi, lane, idx_out, d2_out);
+    else if (n <= 64)
+      select_row<2>(rec, rec_of, row, n, cx, cy, cz, k, qi, lane, idx_out, d2_out);
+    else if (n <= 128)
+      select_row<4>(rec, rec_of, row, n, cx, cy, cz, k, qi, lane, idx_out, d2_out);
+    else if (n <= 256)
+      select_row<8>(rec, rec_of, row, n, cx, cy, cz, k, qi, lane, idx_out, d2_out);
+    else
+      select_row<16>(rec, rec_of, row, n, cx, cy, cz, k, qi, lane, idx_out, d2_out);
+  }
+}
+
+__global__ void fill_f64_kernel(double* __restrict__ a, uint64_t n, double v) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    a[i] = v;
+}
+
+__global__ void add_total_kernel(uint32_t* __restrict__ acc, const uint32_t* __restrict__ v) {
+  *acc += *v;
+}
+
+// sum of counts over the resolved list -> *out (arena size)
+__global__ void sum_counts_kernel(const uint32_t* __restrict__ list, const uint32_t* __restrict__ n_list,
+                                  const uint32_t* __restrict__ counts,
+                                  unsigned long long* __restrict__ out) {
+  unsigned long long a = 0;
+  const uint32_t n = *n_list;
+  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < n; s += gridDim.x * blockDim.x)
+    a += counts[list[s]];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+  if ((threadIdx.x & 31) == 0 && a) atomicAdd(out, a);
+}
+
+unsigned kgrid(uint64_t n) {
+  return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, (uint64_t)sm_count() * 8));
+}
+
+// The radius-bracket path (see knn_bracket_kernel). Centres it cannot finish
+// go to walk[0 .. *n_walk) for the shell walk.
+cm_status knn_brackets(const cm_index* ix, const double* q, uint64_t nq, uint32_t k,
+                       const uint32_t* perm, uint32_t* idx, double* d2, cudaStream_t st,
+                       uint32_t* walk, uint32_t* n_walk) {
+  std::vector<void*> bufs;
+  struct Free {
+    std::vector<void*>& b;
+    cudaStream_t st;
+    ~Free() {
+      for (void* p : b) dev_free(p, st);
+    }
+  } fr{bufs, st};
+  auto alloc = [&](auto** p, size_t count) -> bool {
+    if (dev_alloc_t(p, count, st) != cudaSuccess) return false;
+    bufs.push_back(*p);
+    return true;
+  };
+  const uint32_t* rec_of = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(ix->lazy_mu);
+    if (!ix->rec_of) {
+      uint32_t* ro = nullptr;
+      CM_CUDA_TRY(dev_alloc_t(&ro, ix->n, st));
+      knn_rank_kernel<<<kgrid(ix->n), 256, 0, st>>>(ix->rec, ix->n, ro); ::cmg::note_launch();
+      CM_CUDA_TRY(cudaGetLastError());
+      ix->rec_of = ro;
+    }
+    rec_of = ix->rec_of;
+  }
+  double* rq = nullptr;
+  uint32_t *counts = nullptr, *la = nullptr, *lb = nullptr, *res = nullptr, *f_res = nullptr,
+           *f_next = nullptr, *p_res = nullptr, *p_next = nullptr, *part = nullptr,
+           *n_res = nullptr, *scnt = nullptr;
+  uint64_t* toff = nullptr;
+  unsigned long long *cursor = nullptr, *cap_d = nullptr;
+  if (!alloc(&rq, nq) || !alloc(&counts, nq + 1) || !alloc(&la, nq) || !alloc(&lb, nq) ||
+      !alloc(&res, nq) || !alloc(&f_res, nq + 1) || !alloc(&f_next, nq + 1) ||
+      !alloc(&p_res, nq + 1) || !alloc(&p_next, nq + 1) || !alloc(&part, scan_part_elems(nq)) ||
+      !alloc(&n_res, 1) || !alloc(&scnt, nq + 1) || !alloc(&toff, nq + 1) || !alloc(&cursor, 1) ||
+      !alloc(&cap_d, 1)) {
+    set_error("device allocation failed (kNN brackets)");
+    return CM_CUDA;
+  }
+  // first radius: the k-th neighbour distance of a surface sampled at the
+  // cloud's mean xy density (ALS), later rounds grow per centre
+  const DevGrid& g = ix->g;
+  const double ax = g.bx1 - g.bx0, ay = g.by1 - g.by0, az = g.bz1 - g.bz0;
+  const double area = ax * ay;
+  double r0 = area > 0.0 ? std::sqrt((double)k / (3.141592653589793 * (double)ix->n / area))
+                         : std::max(g.sx, std::max(g.sy, g.sz));
+  const double rmax = std::sqrt(ax * ax + ay * ay + az * az) + std::max(g.sx, g.sy);
+  static const double r0_mult = std::getenv("CMGPU_KNN_R0") ? std::atof(std::getenv("CMGPU_KNN_R0")) : 1.0;
+  r0 = std::min(std::max(r0 * r0_mult, 1e-6), rmax);
+  static const bool trace = std::getenv("CMGPU_KNN_TRACE") != nullptr;
+  cudaEvent_t tev[16];
+  int ntev = 0;
+  auto mark = [&]() {
+    if (trace && ntev < 16) {
+      cudaEventCreate(&tev[ntev]);
+      cudaEventRecord(tev[ntev++], st);
+    }
+  };
+  mark();
+  fill_f64_kernel<<<kgrid(nq), 256, 0, st>>>(rq, nq, r0); ::cmg::note_launch();
+  CM_CUDA_TRY(cudaMemsetAsync(n_res, 0, 4, st));
+  const uint32_t* list = perm;
+  uint32_t* next = la;
+  uint64_t n = nq;
+  static const int kRounds = std::getenv("CMGPU_KNN_ROUNDS") ? std::atoi(std::getenv("CMGPU_KNN_ROUNDS")) : 6;
+  for (int round = 0; round < kRounds && n; ++round) {
+    cm_status s = radius_count_dev(ix, q, n, CM_SPHERE, r0, list, counts, nullptr, st, rq);
+    if (s != CM_OK) return s;
+    knn_bracket_kernel<<<kgrid(n), 256, 0, st>>>(list, (uint32_t)n, counts, k,
+                                                 round == kRounds - 1, rq, f_res, f_next, rmax);
+    ::cmg::note_launch();
+    exclusive_scan<uint32_t, uint32_t>(f_res, n, p_res, part, 1, st);
+    exclusive_scan<uint32_t, uint32_t>(f_next, n, p_next, part, 1, st);
+    knn_compact_kernel<<<kgrid(n), 256, 0, st>>>(list, (uint32_t)n, f_res, p_res, f_next, p_next,
+                                                 res, n_res, next, walk, n_walk);
+    ::cmg::note_launch();
+    add_total_kernel<<<1, 1, 0, st>>>(n_res, p_res + n); ::cmg::note_launch();
+    uint32_t nn = 0;
+    CM_CUDA_TRY(cudaMemcpyAsync(&nn, p_next + n, 4, cudaMemcpyDeviceToHost, st));
+    CM_CUDA_TRY(cudaStreamSynchronize(st));
+    mark();
+    if (trace) {
+      uint64_t qs[8];
+      query_stats(qs, 1);
+      std::fprintf(stderr, "[knn] round %d: %lu centres -> %u retry; tiles %lu fallback %lu hull %lu\n",
+                   round, (unsigned long)n, nn, (unsigned long)qs[0], (unsigned long)qs[1],
+                   (unsigned long)qs[2]);
+    }
+    list = next;
+    next = next == la ? lb : la;
+    n = nn;
+  }
+  uint32_t nres = 0;
+  unsigned long long cap = 0;
+  CM_CUDA_TRY(cudaMemsetAsync(cap_d, 0, 8, st));
+  sum_counts_kernel<<<kgrid(nq), 256, 0, st>>>(res, n_res, counts, cap_d); ::cmg::note_launch();
+  CM_CUDA_TRY(cudaMemcpyAsync(&nres, n_res, 4, cudaMemcpyDeviceToHost, st));
+  CM_CUDA_TRY(cudaMemcpyAsync(&cap, cap_d, 8, cudaMemcpyDeviceToHost, st));
+  CM_CUDA_TRY(cudaStreamSynchronize(st));
+  if (!nres) return CM_OK;
+  uint32_t* arena = nullptr;
+  if (!alloc(&arena, cap + 1)) {
+    set_error("device allocation failed (kNN arena)");
+    return CM_CUDA;
+  }
+  cm_status s = radius_collect_dev(ix, q, nres, CM_SPHERE, r0, res, arena, cap + 1, toff, scnt,
+                                   counts, cursor, st, nullptr, rq);
+  if (s != CM_OK) return s;
+  mark();
+  const uint64_t need = (nres + kKWarps - 1) / kKWarps;
+  const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(need, (uint64_t)sm_count() * 16));
+  knn_select_kernel<<<grid, kKThreads, 0, st>>>(ix->rec, rec_of, q, res, n_res, k, arena, toff,
+                                                scnt, idx, d2);
+  ::cmg::note_launch();
+  CM_CUDA_TRY(cudaGetLastError());
+  mark();
+  if (trace) {
+    cudaStreamSynchronize(st);
+    uint64_t qs[8];
+    query_stats(qs, 1);
+    std::fprintf(stderr, "[knn] resolved %u (arena %llu); collect tiles %lu fallback %lu hull %lu long %lu\n",
+                 nres, cap, (unsigned long)qs[4], (unsigned long)qs[5], (unsigned long)qs[6],
+                 (unsigned long)qs[7]);
+    for (int i = 1; i < ntev; ++i) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, tev[i - 1], tev[i]);
+      std::fprintf(stderr, "[knn]   phase %d: %.3f ms\n", i, ms);
+    }
+    for (int i = 0; i < ntev; ++i) cudaEventDestroy(tev[i]);
+  }
+  return CM_OK;
+}
+
 }  // namespace
 
 cm_status knn_dev(const cm_index* ix, const double* q, uint64_t nq, uint32_t k,
@@ -469,7 +807,26 @@ cm_status knn_dev(const cm_index* ix, const double* q, uint64_t nq, uint32_t k,
   uint32_t* redo = nullptr;
   uint32_t* n_redo = nullptr;
   const uint32_t* wperm = perm;
-  if (!glist && k <= kKnnTileMax) {
+  // The radius-bracket path (knn_brackets) is exact but measured SLOWER on
+  // config 3 (k = 8: 28-54 ms against 14.8 ms for the tiles + shell walk,
+  // profiles/r02/knn_brackets.log): at a quarter of the cloud as centres a
+  // 32-centre tile's hull has a median of 30 columns, so 43 % of the count
+  // passes' tiles fall back to one centre per warp. Kept behind
+  // CMGPU_KNN_BRACKETS for that comparison.
+  static const bool brackets = std::getenv("CMGPU_KNN_BRACKETS") != nullptr;
+  if (!glist && !ix->global_ids && brackets) {
+    // radius brackets first; the shell walk takes what they leave
+    CM_CUDA_TRY(dev_alloc_t(&redo, nq, st));
+    CM_CUDA_TRY(dev_alloc_t(&n_redo, 1, st));
+    CM_CUDA_TRY(cudaMemsetAsync(n_redo, 0, 4, st));
+    const cm_status bs = knn_brackets(ix, q, nq, k, perm, idx, d2, st, redo, n_redo);
+    if (bs != CM_OK) {
+      dev_free(redo, st);
+      dev_free(n_redo, st);
+      return bs;
+    }
+    wperm = redo;
+  } else if (!glist && k <= kKnnTileMax) {
     CM_CUDA_TRY(dev_alloc_t(&redo, nq, st));
     CM_CUDA_TRY(dev_alloc_t(&n_redo, 1, st));
     CM_CUDA_TRY(cudaMemsetAsync(n_redo, 0, 4, st));

@@ -98,6 +98,8 @@ struct Out {
   uint32_t* big_len;
   uint32_t* n_big;
   int wide_fill;                  // FILL: wide tiles may leave rows unsorted (sorted afterwards)
+  const double* rq;               // per-centre radius by query index (kNN brackets), or null
+  const double* qbox;             // per-centre kernel box {min, max} by query index, or null
   int no_wide;                    // diagnostics (CMGPU_NO_WIDE): wide tiles off
 };
 
@@ -130,6 +132,31 @@ __global__ void query_keys_kernel(const double* __restrict__ q, uint64_t nq, Dev
     }
     const uint64_t cell = i * (g.ny * g.nz) + j * g.nz + k;
     keys[p] = (K)(RANGE ? cell * 8 + ext : cell);
+    vals[p] = (uint32_t)p;
+  }
+}
+
+// 2D Morton order of the centre's (i, j) column, voxel k in the low bits:
+// for SPARSE centre sets (a random quarter of the cloud, as kNN config 3)
+// 32 consecutive centres then form a compact patch of columns instead of a
+// strip along j, so a tile's hull stays within the compact-tile limit.
+__device__ __forceinline__ uint64_t interleave2(uint64_t a, uint64_t b) {
+  // a on even bits, b on odd bits
+  uint64_t x = 0;
+#pragma unroll
+  for (int i = 0; i < 21; ++i) x |= (((a >> i) & 1ull) << (2 * i)) | (((b >> i) & 1ull) << (2 * i + 1));
+  return x;
+}
+template <typename K>
+__global__ void query_morton_kernel(const double* __restrict__ q, uint64_t nq, DevGrid g,
+                                    K* __restrict__ keys, uint32_t* __restrict__ vals, int bz) {
+  for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < nq;
+       p += (uint64_t)gridDim.x * blockDim.x) {
+    const double cx = q[3 * p], cy = q[3 * p + 1], cz = q[3 * p + 2];
+    const uint64_t i = axis_index(cx, g.ox, g.sx, g.nx);
+    const uint64_t j = axis_index(cy, g.oy, g.sy, g.ny);
+    const uint64_t k = g.mode3d ? axis_index(cz, g.oz, g.sz, g.nz) : 0;
+    keys[p] = (K)((interleave2(j, i) << bz) | k);
     vals[p] = (uint32_t)p;
   }
 }
@@ -352,11 +379,12 @@ __device__ __forceinline__ bool pred(const Predicate& P, double x, double y, dou
 template <int FLAVOR, int CUBE, bool DIG>
 __device__ __forceinline__ void warp_query_count(const Tables& t, double cx, double cy, double cz,
                                                  double r, int lane, uint32_t* cnt_out,
-                                                 uint64_t* tested_out, uint64_t* dig_out) {
+                                                 uint64_t* tested_out, uint64_t* dig_out,
+                                                 const double* box) {
   Range R;
-  const bool ok = clamped_range_warp(t.g, cx, cy, cz, r, lane, &R, CUBE);
+  const bool ok = clamped_range_warp(t.g, cx, cy, cz, r, lane, &R, CUBE, box);
   Predicate P;
-  P.init(cx, cy, cz, r, CUBE);
+  P.init(cx, cy, cz, r, CUBE, box);
   uint32_t cnt = 0;
   uint64_t ntested = 0, dig = 0;
   if (ok) {
@@ -498,11 +526,11 @@ template <int FLAVOR, int CUBE>
 __device__ __forceinline__ uint32_t warp_query_walk(const Tables& t, double cx, double cy,
                                                     double cz, double r, int lane, uint32_t lt,
                                                     uint32_t* buf, uint32_t cap,
-                                                    uint32_t* direct) {
+                                                    uint32_t* direct, const double* box) {
   Range R;
-  const bool ok = clamped_range_warp(t.g, cx, cy, cz, r, lane, &R, CUBE);
+  const bool ok = clamped_range_warp(t.g, cx, cy, cz, r, lane, &R, CUBE, box);
   Predicate P;
-  P.init(cx, cy, cz, r, CUBE);
+  P.init(cx, cy, cz, r, CUBE, box);
   uint32_t cnt = 0;
   if (ok) {
     const uint64_t nj = R.j1 - R.j0 + 1;
@@ -552,13 +580,13 @@ template <int FLAVOR, int CUBE>
 __device__ __forceinline__ void warp_row_out(const Tables& t, double cx, double cy, double cz,
                                              double r, int lane, uint32_t lt, uint32_t* wbuf,
                                              uint32_t cnt, uint32_t* dst, uint64_t big_base,
-                                             const Out& o) {
+                                             const Out& o, const double* box) {
   if (cnt <= (uint32_t)kSortCap) {
     const int bits = 32 - __clz((int)max(1u, (uint32_t)(t.n - 1)));
     const uint32_t* res = warp_sort_buffer(wbuf, cnt, bits, lane, lt);
     for (uint32_t x = lane; x < cnt; x += 32) dst[x] = res[x];
   } else {
-    warp_query_walk<FLAVOR, CUBE>(t, cx, cy, cz, r, lane, lt, nullptr, 0, dst);
+    warp_query_walk<FLAVOR, CUBE>(t, cx, cy, cz, r, lane, lt, nullptr, 0, dst, box);
     if (lane == 0) {
       const uint32_t slot = atomicAdd(o.n_big, 1u);
       o.big_off[slot] = big_base;
@@ -573,11 +601,12 @@ template <int FLAVOR, int MODE, int CUBE>
 __device__ __forceinline__ void single_query(const Tables& t, uint32_t qi, uint64_t spos,
                                              double cx, double cy, double cz, double r, int lane,
                                              uint32_t lt, const Out& o, uint32_t* wbuf) {
+  const double* box = o.qbox ? o.qbox + 6 * (uint64_t)qi : nullptr;
   if (MODE == MODE_COUNT || MODE == MODE_DIGEST) {
     uint32_t cnt;
     uint64_t tested, dig;
     warp_query_count<FLAVOR, CUBE, MODE == MODE_DIGEST>(t, cx, cy, cz, r, lane, &cnt, &tested,
-                                                        &dig);
+                                                        &dig, box);
     if (lane == 0) {
       if (o.counts) o.counts[qi] = cnt;
       if (MODE == MODE_COUNT && o.tested) o.tested[qi] = tested;
@@ -587,12 +616,12 @@ __device__ __forceinline__ void single_query(const Tables& t, uint32_t qi, uint6
     const uint64_t rb = __ldg(o.row_ptr + qi);
     const uint32_t len = (uint32_t)(__ldg(o.row_ptr + qi + 1) - rb);
     if (len <= (uint32_t)kSortCap)
-      warp_query_walk<FLAVOR, CUBE>(t, cx, cy, cz, r, lane, lt, wbuf, kSortCap, nullptr);
-    warp_row_out<FLAVOR, CUBE>(t, cx, cy, cz, r, lane, lt, wbuf, len, o.cols + rb, rb, o);
+      warp_query_walk<FLAVOR, CUBE>(t, cx, cy, cz, r, lane, lt, wbuf, kSortCap, nullptr, box);
+    warp_row_out<FLAVOR, CUBE>(t, cx, cy, cz, r, lane, lt, wbuf, len, o.cols + rb, rb, o, box);
   } else {
     // single walk into the buffer (count exact even past the buffer)
     const uint32_t cnt =
-        warp_query_walk<FLAVOR, CUBE>(t, cx, cy, cz, r, lane, lt, wbuf, kSortCap, nullptr);
+        warp_query_walk<FLAVOR, CUBE>(t, cx, cy, cz, r, lane, lt, wbuf, kSortCap, nullptr, box);
     unsigned long long base = 0;
     if (lane == 0) {
       base = atomicAdd(o.cursor, (unsigned long long)cnt);
@@ -602,7 +631,7 @@ __device__ __forceinline__ void single_query(const Tables& t, uint32_t qi, uint6
     }
     base = __shfl_sync(0xffffffffu, base, 0);
     if (base + cnt <= o.cap)
-      warp_row_out<FLAVOR, CUBE>(t, cx, cy, cz, r, lane, lt, wbuf, cnt, o.temp + base, base, o);
+      warp_row_out<FLAVOR, CUBE>(t, cx, cy, cz, r, lane, lt, wbuf, cnt, o.temp + base, base, o, box);
   }
 }
 
@@ -778,8 +807,12 @@ __global__ void __launch_bounds__(kQThreads, CM_QTILE_MINB) radius_tile_kernel(
         cz = __ldg(q + 3 * (uint64_t)qi + 2);
       }
     }
+    // the centre's own radius (kNN radius brackets), else the batch's
+    const double rl = (o.rq && active) ? __ldg(o.rq + qi) : r;
+    // explicit kernel boxes (cm_kernel_search: Aabb boxes, bounded cylinders)
+    const double* qb = (o.qbox && active) ? o.qbox + 6 * (uint64_t)qi : nullptr;
     Range R{};
-    const bool ok = active && clamped_range(t.g, cx, cy, cz, r, &R, CUBE);
+    const bool ok = active && clamped_range(t.g, cx, cy, cz, rl, &R, CUBE, qb);
     const uint32_t okmask = __ballot_sync(0xffffffffu, ok);
     bool use_tile = small_grid && okmask != 0;
     bool wide = false;
@@ -821,7 +854,7 @@ __global__ void __launch_bounds__(kQThreads, CM_QTILE_MINB) radius_tile_kernel(
     }
     if (wide) {
       Predicate P;
-      P.init(cx, cy, cz, r, CUBE);
+      P.init(cx, cy, cz, rl, CUBE, qb);
       wide_tile<FLAVOR, MODE, CUBE>(t, R, ok, active, qi, I0, J0, nj, (uint32_t)nc, K0, K1, P,
                                     lane, stg, reinterpret_cast<uint32_t*>(wreg), o);
       __syncwarp();
@@ -835,7 +868,8 @@ __global__ void __launch_bounds__(kQThreads, CM_QTILE_MINB) radius_tile_kernel(
         const double xl = __shfl_sync(0xffffffffu, cx, l);
         const double yl = __shfl_sync(0xffffffffu, cy, l);
         const double zl = __shfl_sync(0xffffffffu, cz, l);
-        single_query<FLAVOR, MODE, CUBE>(t, ql, tile * 32 + l, xl, yl, zl, r, lane, lt, o, wbuf);
+        const double rl2 = __shfl_sync(0xffffffffu, rl, l);
+        single_query<FLAVOR, MODE, CUBE>(t, ql, tile * 32 + l, xl, yl, zl, rl2, lane, lt, o, wbuf);
       }
       continue;
     }
@@ -849,7 +883,7 @@ __global__ void __launch_bounds__(kQThreads, CM_QTILE_MINB) radius_tile_kernel(
     const uint32_t kk0 = ok ? (uint32_t)R.k0 : 1u;
     const uint32_t kspan = ok ? (uint32_t)(R.k1 - R.k0) : 0u;
     Predicate P;
-    P.init(cx, cy, cz, r, CUBE);
+    P.init(cx, cy, cz, rl, CUBE, qb);
     uint32_t cnt = 0, ntest = 0;
     uint64_t dig = 0;
     // ROWS: the lane's next key slot as a running shared-memory address
@@ -1029,7 +1063,8 @@ __global__ void __launch_bounds__(kQThreads, CM_QTILE_MINB) radius_tile_kernel(
         const double xl = __shfl_sync(0xffffffffu, cx, l);
         const double yl = __shfl_sync(0xffffffffu, cy, l);
         const double zl = __shfl_sync(0xffffffffu, cz, l);
-        single_query<FLAVOR, MODE, CUBE>(t, ql, tile * 32 + l, xl, yl, zl, r, lane, lt, o, wbuf);
+        const double rl2 = __shfl_sync(0xffffffffu, rl, l);
+        single_query<FLAVOR, MODE, CUBE>(t, ql, tile * 32 + l, xl, yl, zl, rl2, lane, lt, o, wbuf);
       }
     }
     __syncwarp();
@@ -1672,12 +1707,21 @@ __global__ void self_centres_kernel(const PointRec* __restrict__ rec, uint64_t n
 
 template <typename K>
 cm_status order_typed(const cm_index* ix, const double* q, uint64_t nq, cudaStream_t st,
-                      uint32_t* perm, bool range, double r, int kind) {
+                      uint32_t* perm, bool range, double r, int kind, int morton_bits = 0,
+                      int bz = 0) {
   K* keys = nullptr;
   void* scratch = nullptr;
   CM_CUDA_TRY(dev_alloc_t(&keys, nq, st));
   CM_CUDA_TRY(dev_alloc(&scratch, radix_scratch_bytes<K>(nq), st));
   const unsigned grid = (unsigned)std::min<uint64_t>((nq + 255) / 256, (uint64_t)sm_count() * 16);
+  if (morton_bits) {
+    query_morton_kernel<K><<<std::max(1u, grid), 256, 0, st>>>(q, nq, ix->g, keys, perm, bz);
+    ::cmg::note_launch();
+    radix_sort_pairs<K>(keys, perm, nq, morton_bits, scratch, st);
+    dev_free(scratch, st);
+    dev_free(keys, st);
+    return CM_OK;
+  }
   if (range)
     query_keys_kernel<K, true><<<std::max(1u, grid), 256, 0, st>>>(q, nq, ix->g, keys, perm, r, kind);
   else
@@ -1766,8 +1810,14 @@ void query_stats(uint64_t* out, int reset) {
   }
 }
 
+static int bit_width_u64(uint64_t v) {
+  int b = 0;
+  while (v) ++b, v >>= 1;
+  return b;
+}
+
 cm_status order_queries(const cm_index* ix, const double* q, uint64_t nq, cudaStream_t st,
-                        QueryOrder* out, double r, int kind) {
+                        QueryOrder* out, double r, int kind, bool morton) {
   out->nq = nq;
   out->st = st;
   out->q = q;
@@ -1796,6 +1846,15 @@ cm_status order_queries(const cm_index* ix, const double* q, uint64_t nq, cudaSt
   }
   out->q = q;
   CM_CUDA_TRY(dev_alloc_t(&out->perm, nq, st));
+  if (morton && q) {
+    const int bxy = bit_width_u64(std::max(g.nx, g.ny) - 1);
+    const int bz = g.mode3d ? bit_width_u64(g.nz - 1) : 0;
+    const int mb = 2 * bxy + bz;
+    if (bxy <= 21 && mb <= 64) {
+      return mb <= 32 ? order_typed<uint32_t>(ix, q, nq, st, out->perm, false, r, kind, std::max(1, mb), bz)
+                      : order_typed<uint64_t>(ix, q, nq, st, out->perm, false, r, kind, mb, bz);
+    }
+  }
   const int bits = ix->key_bits + (range ? 3 : 0);
   return bits <= 32 ? order_typed<uint32_t>(ix, q, nq, st, out->perm, range, r, kind)
                     : order_typed<uint64_t>(ix, q, nq, st, out->perm, range, r, kind);
@@ -1811,21 +1870,25 @@ bool radius_is_wide(const cm_index* ix, double r) {
 
 cm_status radius_count_dev(const cm_index* ix, const double* q, uint64_t nq, int kernel, double r,
                            const uint32_t* perm, uint32_t* counts, uint64_t* tested,
-                           cudaStream_t st) {
+                           cudaStream_t st, const double* rq, const double* qbox) {
   if (nq == 0) return CM_OK;
   Out o{};
   o.counts = counts;
   o.tested = tested;
+  o.rq = rq;
+  o.qbox = qbox;
   return launch_radius<MODE_COUNT>(ix, q, nq, kernel, r, perm, o, st);
 }
 
 cm_status radius_digest_dev(const cm_index* ix, const double* q, uint64_t nq, int kernel, double r,
                             const uint32_t* perm, uint32_t* counts, uint64_t* digests,
-                            cudaStream_t st) {
+                            cudaStream_t st, const double* rq, const double* qbox) {
   if (nq == 0) return CM_OK;
   Out o{};
   o.counts = counts;
   o.digests = digests;
+  o.rq = rq;
+  o.qbox = qbox;
   return launch_radius<MODE_DIGEST>(ix, q, nq, kernel, r, perm, o, st);
 }
 
@@ -1864,7 +1927,8 @@ cm_status row_class_counts_dev(const uint32_t* counts, uint64_t nq, unsigned lon
 
 cm_status radius_fill_dev(const cm_index* ix, const double* q, uint64_t nq, int kernel, double r,
                           const uint32_t* perm, const uint64_t* row_ptr, uint32_t* cols,
-                          cudaStream_t st, cudaEvent_t after_fill, uint32_t mid_min) {
+                          cudaStream_t st, cudaEvent_t after_fill, uint32_t mid_min,
+                          const double* rq, const double* qbox) {
   if (nq == 0) return CM_OK;
   if (mid_min == 0) mid_min = (uint32_t)kMidMin;
   BigRows big;
@@ -1876,7 +1940,9 @@ cm_status radius_fill_dev(const cm_index* ix, const double* q, uint64_t nq, int 
   o.big_off = big.off;
   o.big_len = big.len;
   o.n_big = big.n;
-  o.wide_fill = radius_is_wide(ix, r) ? 1 : 0;
+  o.wide_fill = (radius_is_wide(ix, r) || rq || qbox) ? 1 : 0;
+  o.rq = rq;
+  o.qbox = qbox;
   s = launch_radius<MODE_FILL>(ix, q, nq, kernel, r, perm, o, st);
   if (after_fill) cudaEventRecord(after_fill, st);
   if (s != CM_OK) return s;
@@ -1930,7 +1996,7 @@ cm_status radius_collect_dev(const cm_index* ix, const double* q, uint64_t nq, i
                              double r, const uint32_t* perm, uint32_t* temp, uint64_t cap,
                              uint64_t* toff, uint32_t* scnt, uint32_t* counts,
                              unsigned long long* cursor, cudaStream_t st,
-                             cudaEvent_t after_collect) {
+                             cudaEvent_t after_collect, const double* rq, const double* qbox) {
   if (nq == 0) return CM_OK;
   BigRows big;
   cm_status s = big.init(nq, st);
@@ -1946,6 +2012,8 @@ cm_status radius_collect_dev(const cm_index* ix, const double* q, uint64_t nq, i
   o.big_off = big.off;
   o.big_len = big.len;
   o.n_big = big.n;
+  o.rq = rq;
+  o.qbox = qbox;
   s = launch_radius<MODE_COLLECT>(ix, q, nq, kernel, r, perm, o, st);
   if (after_collect) cudaEventRecord(after_collect, st);
   if (s == CM_OK) s = sort_big_rows(temp, o, st);

@@ -1,0 +1,153 @@
+"""Explicit kernels through cm_kernel_search / cm_kernel_count (the reference's
+Kernel concept, geometry.hpp:67-113): per-centre radii, general BoxKernel
+Aabbs, bounded CylinderKernels, QueryStats (search.hpp:12-17), and
+voxel_present / voxel_lookup (map.hpp:62-69) — against the oracle and the
+reference's own definitions."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from paper_2502_11602_b200 import cheesemap as cm
+from paper_2502_11602_b200 import synth
+from oracle.oracle import CpuIndex
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+FLAVORS = [cm.Flavor.Dense, cm.Flavor.Sparse, cm.Flavor.Mixed]
+
+
+@pytest.fixture(scope="module")
+def cloud():
+    return synth.config_cloud(1, scale=0.003)  # 60k points with a building
+
+
+def brute(cloud, inside):
+    return np.nonzero(inside(cloud))[0].astype(np.uint32)
+
+
+@pytest.mark.parametrize("flavor", FLAVORS)
+def test_general_kernels_equal_linear_scan(cloud, flavor):
+    rng = np.random.default_rng(5)
+    m = cm.Cheesemap.build(cloud, cm.BuildOptions(flavor=flavor))
+    ctr = cloud[rng.choice(cloud.shape[0], 60, replace=False)]
+    rad = rng.uniform(0.2, 4.0, 60)
+    x, y, z = cloud[:, 0], cloud[:, 1], cloud[:, 2]
+    spheres = [cm.SphereKernel(tuple(c), float(r)) for c, r in zip(ctr, rad)]
+    boxes = [cm.BoxKernel((c[0] - 2 * r, c[1] - 0.5 * r, c[2] - 0.25 * r),
+                          (c[0] + r, c[1] + r, c[2] + 3 * r)) for c, r in zip(ctr, rad)]
+    cyls = [cm.CylinderKernel(float(c[0]), float(c[1]), float(r), float(c[2] - 1.0),
+                              float(c[2] + 0.5)) for c, r in zip(ctr, rad)]
+    cyls_u = [cm.CylinderKernel(float(c[0]), float(c[1]), float(r)) for c, r in zip(ctr, rad)]
+    for ks, inside in (
+            (spheres, lambda k: ((x - k.center[0]) ** 2 + (y - k.center[1]) ** 2)
+             + (z - k.center[2]) ** 2 <= k.radius * k.radius),
+            (boxes, lambda k: (x >= k.min[0]) & (x <= k.max[0]) & (y >= k.min[1]) &
+             (y <= k.max[1]) & (z >= k.min[2]) & (z <= k.max[2])),
+            (cyls, lambda k: (z >= k.z_lo) & (z <= k.z_hi) &
+             ((x - k.center_x) ** 2 + (y - k.center_y) ** 2 <= k.radius * k.radius)),
+            (cyls_u, lambda k: (x - k.center_x) ** 2 + (y - k.center_y) ** 2
+             <= k.radius * k.radius)):
+        row, cols = cm.kernel_search_batch(m, ks)
+        for q, k in enumerate(ks):
+            want = brute(cloud, lambda _c, k=k: inside(k))
+            assert np.array_equal(cols[row[q]:row[q + 1]], want), (type(k).__name__, q)
+
+
+def test_sphere_batch_with_own_radii_equals_oracle(cloud):
+    """A batch of spheres with per-centre radii = the uniform-radius batches."""
+    o = CpuIndex(cloud, flavor=1)
+    m = cm.Cheesemap.build(cloud, cm.BuildOptions(flavor=cm.Flavor.Mixed))
+    q = np.ascontiguousarray(cloud[::50])
+    rad = np.where(np.arange(q.shape[0]) % 2 == 0, 0.7, 2.2)
+    row, cols = cm.kernel_search_batch(m, [cm.SphereKernel(tuple(c), float(r)) for c, r in zip(q, rad)])
+    for r in (0.7, 2.2):
+        sel = np.nonzero(rad == r)[0]
+        orow, ocols = o.radius_csr(q[sel], 0, r)
+        for t, qi in enumerate(sel):
+            assert np.array_equal(cols[row[qi]:row[qi + 1]], ocols[orow[t]:orow[t + 1]])
+
+
+@pytest.mark.parametrize("flavor", FLAVORS)
+def test_query_stats(cloud, flavor):
+    """voxels_visited = the voxels of the clamped range; points_tested = the
+    points in them (search.hpp:116-119), as the oracle counts them."""
+    o = CpuIndex(cloud, flavor=int(flavor))
+    m = cm.Cheesemap.build(cloud, cm.BuildOptions(flavor=flavor))
+    q = np.ascontiguousarray(cloud[::997])
+    _, _, pt, vv = cm.kernel_search_batch(m, [cm.SphereKernel(tuple(c), 1.5) for c in q], stats=True)
+    _, _, opt, ovv = o.radius(q, 0, 1.5, stats=True)
+    assert np.array_equal(pt, opt) and np.array_equal(vv, ovv)
+    st = cm.QueryStats()
+    assert len(cm.kernel_search(m, cm.SphereKernel((1e6, 1e6, 1e6), 1.0), stats=st)) == 0
+    assert st.voxels_visited == 0 and st.points_tested == 0
+    g = m.grid()
+    c = [(a + b) / 2 for a, b in zip(g["bounds_min"], g["bounds_max"])]
+    allh = cm.kernel_search(m, cm.SphereKernel(tuple(c), 1e5), stats=st)
+    assert len(allh) == cloud.shape[0] and st.points_tested == cloud.shape[0]
+    assert st.voxels_visited == g["nx"] * g["ny"] * g["nz"]
+    nn = cm.knn_search(m, tuple(q[0]), 10, cm.GrowthPolicy.Monotonic, stats=st)
+    assert len(nn) == 10 and st.final_radius == nn[-1].distance and st.points_tested >= 10
+
+
+def test_voxel_lookup(cloud):
+    L = cm._native.lib()
+    import ctypes
+    for flavor in FLAVORS:
+        m = cm.Cheesemap.build(cloud, cm.BuildOptions(flavor=flavor))
+        keys, hs = m.export_voxels()
+        g = m.grid()
+        nyz = g["ny"] * g["nz"]
+        for key in np.unique(keys)[::157]:
+            i, j, k = int(key // nyz), int(key % nyz // g["nz"]), int(key % g["nz"])
+            want = np.sort(hs[keys == key]).astype(np.uint32)
+            out = np.zeros(want.size + 4, dtype=np.uint32)
+            n, pres = ctypes.c_uint64(), ctypes.c_int()
+            cm._check(L.cm_voxel_lookup(m.handle, i, j, k, ctypes.byref(pres),
+                                        out.ctypes.data_as(ctypes.c_void_p), out.size,
+                                        ctypes.byref(n)))
+            assert pres.value == 1 and n.value == want.size
+            assert np.array_equal(out[:want.size], want)
+        # an empty voxel: present only for the dense flavour (map.hpp:62-63)
+        occupied = set(int(v) for v in np.unique(keys))
+        empty = next(v for v in range(g["nx"] * nyz) if v not in occupied)
+        i, j, k = empty // nyz, empty % nyz // g["nz"], empty % g["nz"]
+        n, pres = ctypes.c_uint64(), ctypes.c_int()
+        cm._check(L.cm_voxel_lookup(m.handle, i, j, k, ctypes.byref(pres), None, 0, ctypes.byref(n)))
+        assert n.value == 0
+        if flavor == cm.Flavor.Dense:
+            assert pres.value == 1
+        elif flavor == cm.Flavor.Sparse:
+            assert pres.value == 0
+        assert L.cm_voxel_lookup(m.handle, g["nx"], 0, 0, ctypes.byref(pres), None, 0,
+                                 ctypes.byref(n)) == 4  # CM_OUT_OF_DOMAIN
+
+
+def test_knn_radius_brackets_parity():
+    """The opt-in radius-bracket kNN (CMGPU_KNN_BRACKETS) stays exact."""
+    code = ("import numpy as np, sys; sys.path.insert(0, %r)\n"
+            "from paper_2502_11602_b200 import cheesemap as cm, synth\n"
+            "from oracle.oracle import CpuIndex\n"
+            "c = synth.config_cloud(1, scale=0.01); q = synth.config_queries(3, c, count=20000)\n"
+            "m = cm.Cheesemap.build(c, cm.BuildOptions(flavor=cm.Flavor.Mixed)); o = CpuIndex(c, flavor=1)\n"
+            "for k in (1, 8, 33, 64):\n"
+            "    i, d = cm.knn_batch(m, q, k); oi, od = o.knn(q, k)\n"
+            "    assert np.array_equal(i, oi) and np.array_equal(d, od), k\n"
+            "print('brackets ok')\n") % ROOT
+    env = dict(os.environ, CMGPU_KNN_BRACKETS="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and "brackets ok" in r.stdout, r.stderr[-2000:]
+
+
+def test_voxel_lookup_mirror(cloud):
+    m = cm.Cheesemap.build(cloud, cm.BuildOptions(flavor=cm.Flavor.Sparse))
+    keys, hs = m.export_voxels()
+    g = m.grid()
+    key = int(keys[len(keys) // 2])
+    nyz = g["ny"] * g["nz"]
+    v = (key // nyz, key % nyz // g["nz"], key % g["nz"])
+    assert m.voxel_present(v)
+    assert np.array_equal(m.voxel_lookup(v), np.sort(hs[keys == key]).astype(np.uint64))
