@@ -781,6 +781,7 @@ bool read_row_ptrs_mapped(const uint64_t* row_ptr, const uint64_t* idx, int n, c
 // Replaces the single gather launch of radius_search_core (to_host uses it to
 // stream the CSR to the host while the gather still runs).
 struct GatherHook {
+  uint32_t skip_above = 0xffffffffu;  // rows longer than this were merged already
   virtual cm_status run(const uint32_t* temp, const uint64_t* toff, const uint32_t* scnt,
                         const uint64_t* row_ptr, const uint32_t* perm, uint32_t* cols, uint64_t nq,
                         cudaStream_t st) = 0;
@@ -820,7 +821,12 @@ static cm_status radius_search_core(const cm_index* ix, const double* qd, uint64
     cudaStreamSynchronize(st);
     return s;
   };
+  MergeList ml;
+  ml.st = st;
   if (dev_alloc_t(&counts, nq + 1, st) != cudaSuccess ||
+      dev_alloc_t(&ml.off, nq + 1, st) != cudaSuccess ||
+      dev_alloc_t(&ml.len, nq + 1, st) != cudaSuccess ||
+      dev_alloc_t(&ml.q, nq + 1, st) != cudaSuccess || dev_alloc_t(&ml.n, 1, st) != cudaSuccess ||
       dev_alloc_t(&csr->row_ptr, nq + 1, st) != cudaSuccess ||
       dev_alloc_t(&toff, nq + 1, st) != cudaSuccess || dev_alloc_t(&scnt, nq + 1, st) != cudaSuccess ||
       dev_alloc_t(&cursor, 1, st) != cudaSuccess) {
@@ -847,7 +853,7 @@ static cm_status radius_search_core(const cm_index* ix, const double* qd, uint64
   bool recollected = false;
   if (!two_pass) {
     s = radius_collect_dev(ix, qd, nq, kernel, r, ord.perm, temp, cap, toff, scnt, counts, cursor,
-                           st, ev.e[2], rq, qbox);
+                           st, ev.e[2], rq, qbox, &ml);
     cudaEventRecord(ev.e[3], st);
     if (s != CM_OK) return fail(s);
     if (!read_u64_mapped(cursor, st, &used)) {
@@ -865,7 +871,7 @@ static cm_status radius_search_core(const cm_index* ix, const double* qd, uint64
       if (dev_alloc_t(&temp, cap, st) == cudaSuccess) {
         recollected = true;
         s = radius_collect_dev(ix, qd, nq, kernel, r, ord.perm, temp, cap, toff, scnt, counts,
-                               cursor, st, ev.e[2], rq, qbox);
+                               cursor, st, ev.e[2], rq, qbox, &ml);
         cudaEventRecord(ev.e[3], st);
         if (s != CM_OK) return fail(s);
         if (!read_u64_mapped(cursor, st, &used)) {
@@ -924,9 +930,20 @@ static cm_status radius_search_core(const cm_index* ix, const double* qd, uint64
   if (two_pass)
     s = radius_fill_dev(ix, qd, nq, kernel, r, ord.perm, csr->row_ptr, csr->cols, st, nullptr,
                         mid_min, rq, qbox);
-  else
-    s = hook ? hook->run(temp, toff, scnt, csr->row_ptr, ord.perm, csr->cols, nq, st)
-             : gather_rows_dev(temp, toff, scnt, csr->row_ptr, ord.perm, csr->cols, nq, st);
+  else {
+    // long rows: merged from their sorted voxel runs straight into the CSR
+    // (before the gather, so a streaming hook copies finished rows)
+    s = merge_big_rows(ml, temp, csr->row_ptr, csr->cols, st);
+    if (s == CM_OK) {
+      if (hook) {
+        hook->skip_above = long_row_min() - 1;
+        s = hook->run(temp, toff, scnt, csr->row_ptr, ord.perm, csr->cols, nq, st);
+      } else {
+        s = gather_rows_dev(temp, toff, scnt, csr->row_ptr, ord.perm, csr->cols, nq, st,
+                            long_row_min() - 1);
+      }
+    }
+  }
   cudaEventRecord(ev.e[5], st);
   if (s != CM_OK) return fail(s);
   ev.nq = nq;
@@ -1027,13 +1044,22 @@ __global__ void kernel_params_kernel(int kind, const double* __restrict__ prm, u
       b[3] = __dadd_rn(cx, r), b[4] = __dadd_rn(cy, r), b[5] = p[4];
       cz = 0.5 * (fmax(p[3], g.bz0) + fmin(p[4], g.bz1));
     }
-    // centres only order the queries; keep them finite and inside the grid
-    cx = fmin(fmax(cx, g.bx0), g.bx1);
-    cy = fmin(fmax(cy, g.by0), g.by1);
-    cz = fmin(fmax(cz, g.bz0), g.bz1);
-    q[3 * i] = isnan(cx) ? g.bx0 : cx;
-    q[3 * i + 1] = isnan(cy) ? g.by0 : cy;
-    q[3 * i + 2] = isnan(cz) ? g.bz0 : cz;
+    // A box's centre only orders the queries (its predicate reads the box),
+    // so it is kept finite and inside the grid; sphere centres and the
+    // cylinder's axis are the predicates' own and pass unchanged.
+    if (kind == CM_CUBE) {
+      cx = fmin(fmax(cx, g.bx0), g.bx1);
+      cy = fmin(fmax(cy, g.by0), g.by1);
+      cx = isnan(cx) ? g.bx0 : cx;
+      cy = isnan(cy) ? g.by0 : cy;
+    }
+    if (kind != CM_SPHERE) {
+      cz = fmin(fmax(cz, g.bz0), g.bz1);
+      cz = isnan(cz) ? g.bz0 : cz;
+    }
+    q[3 * i] = cx;
+    q[3 * i + 1] = cy;
+    q[3 * i + 2] = cz;
     rq[i] = r;
   }
 }
@@ -1199,7 +1225,7 @@ struct StreamingGather : GatherHook {
     for (int k = 0; k < G; ++k) {
       if (qb[k + 1] == qb[k]) continue;
       CM_TRY(gather_rows_dev(temp, toff + qb[k], scnt + qb[k], row_ptr + qb[k], perm, cols,
-                             qb[k + 1] - qb[k], st));
+                             qb[k + 1] - qb[k], st, skip_above));
       if (!over && rp[k + 1] > rp[k]) {
         CM_CUDA_TRY(cudaEventRecord(evs.e[k], st));
         CM_CUDA_TRY(cudaStreamWaitEvent(out, evs.e[k], 0));

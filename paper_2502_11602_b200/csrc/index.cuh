@@ -156,15 +156,33 @@ cm_status radius_digest_dev(const cm_index* ix, const double* q_dev, uint64_t nq
                             double r, const uint32_t* perm, uint32_t* counts_dev,
                             uint64_t* digest_dev, cudaStream_t st, const double* rq = nullptr,
                             const double* qbox = nullptr);
+// Long COLLECT rows (one query per warp, > kSortCap handles), left in visit
+// order for merge_big_rows: arena offset, length and query of each.
+struct MergeList {
+  uint64_t* off = nullptr;
+  uint32_t* len = nullptr;
+  uint32_t* q = nullptr;
+  uint32_t* n = nullptr;
+  cudaStream_t st = nullptr;
+  ~MergeList() {
+    if (off) dev_free(off, st);
+    if (len) dev_free(len, st);
+    if (q) dev_free(q, st);
+    if (n) dev_free(n, st);
+  }
+};
+uint32_t long_row_min();
+cm_status merge_big_rows(const MergeList& ml, uint32_t* arena, const uint64_t* row_ptr,
+                         uint32_t* cols, cudaStream_t st);
 cm_status radius_collect_dev(const cm_index* ix, const double* q_dev, uint64_t nq, int kernel,
                              double r, const uint32_t* perm, uint32_t* temp, uint64_t cap,
                              uint64_t* toff, uint32_t* scnt, uint32_t* counts,
                              unsigned long long* cursor, cudaStream_t st,
                              cudaEvent_t after_collect, const double* rq = nullptr,
-                             const double* qbox = nullptr);
+                             const double* qbox = nullptr, const MergeList* ml = nullptr);
 cm_status gather_rows_dev(const uint32_t* temp, const uint64_t* toff, const uint32_t* scnt,
                           const uint64_t* row_ptr, const uint32_t* perm, uint32_t* cols,
-                          uint64_t nq, cudaStream_t st);
+                          uint64_t nq, cudaStream_t st, uint32_t skip_above = 0xffffffffu);
 cm_status counts_to_row_ptr(const uint32_t* counts_dev, uint64_t nq, uint64_t* row_ptr_dev,
                             cudaStream_t st);
 cm_status knn_dev(const cm_index* ix, const double* q_dev, uint64_t nq, uint32_t k,

@@ -96,8 +96,10 @@ struct Out {
   unsigned long long* cursor;     // COLLECT arena bump pointer
   uint64_t* big_off;              // rows sorted afterwards: offset into `rows`
   uint32_t* big_len;
+  uint32_t* big_q;                // COLLECT with a merge list: the row's query (or null)
   uint32_t* n_big;
   int wide_fill;                  // FILL: wide tiles may leave rows unsorted (sorted afterwards)
+  uint32_t cur_q;                 // (set per call of single_query for big-row registration)
   const double* rq;               // per-centre radius by query index (kNN brackets), or null
   const double* qbox;             // per-centre kernel box {min, max} by query index, or null
   int no_wide;                    // diagnostics (CMGPU_NO_WIDE): wide tiles off
@@ -591,6 +593,7 @@ __device__ __forceinline__ void warp_row_out(const Tables& t, double cx, double 
       const uint32_t slot = atomicAdd(o.n_big, 1u);
       o.big_off[slot] = big_base;
       o.big_len[slot] = cnt;
+      if (o.big_q) o.big_q[slot] = o.cur_q;
     }
   }
   __syncwarp();
@@ -630,8 +633,11 @@ __device__ __forceinline__ void single_query(const Tables& t, uint32_t qi, uint6
       o.scnt[qi] = cnt;
     }
     base = __shfl_sync(0xffffffffu, base, 0);
-    if (base + cnt <= o.cap)
-      warp_row_out<FLAVOR, CUBE>(t, cx, cy, cz, r, lane, lt, wbuf, cnt, o.temp + base, base, o, box);
+    if (base + cnt <= o.cap) {
+      Out o2 = o;
+      o2.cur_q = qi;
+      warp_row_out<FLAVOR, CUBE>(t, cx, cy, cz, r, lane, lt, wbuf, cnt, o.temp + base, base, o2, box);
+    }
   }
 }
 
@@ -1182,7 +1188,8 @@ __global__ void CM_GATHER_BOUNDS gather_rows_kernel(const uint32_t* temp,
                                                           const uint64_t* __restrict__ toff,
                                                           const uint32_t* __restrict__ counts,
                                                           const uint64_t* __restrict__ row_ptr,
-                                                          uint32_t* cols, uint64_t nq) {
+                                                          uint32_t* cols, uint64_t nq,
+                                                          uint32_t skip_above = 0xffffffffu) {
   extern __shared__ uint32_t gsm[];
   const int lane = threadIdx.x & 31;
   uint32_t* srow = gsm + (threadIdx.x >> 5) * kGatherWarpWords;
@@ -1327,7 +1334,7 @@ __global__ void CM_GATHER_BOUNDS gather_rows_kernel(const uint32_t* temp,
           const uint32_t e = (uint32_t)lane * 4 + r;
           if (e < ln) cols[d + e] = v[r];
         }
-      } else {
+      } else if (ln <= skip_above) {  // longer rows: merge_big_rows_kernel wrote them
         const uint64_t o = __shfl_sync(0xffffffffu, so, l);
         for (uint32_t b0 = 0; b0 < ln; b0 += 256) {  // 8 loads in flight per lane
           uint32_t v[8];
@@ -1770,6 +1777,204 @@ cm_status launch_radius(const cm_index* ix, const double* q, uint64_t nq, int ke
   }
 }
 
+// Rows longer than a warp buffer (kSortCap), from the one-query-per-warp
+// path in COLLECT: written in visit order, i.e. one ascending run per voxel
+// (records of a voxel are in handle order), so a row is a few long sorted
+// runs (TLS, config 2: up to ~64 voxels per row, thousands of handles each).
+// One block per row: find the runs, then merge them pairwise (merge path,
+// every thread a fixed slice of the output) — log2(runs) passes instead of
+// a bitonic network's log^2(n) stages. Rows that fit go through shared
+// memory (two buffers); longer ones ping-pong between their arena row and
+// their CSR row, ending in the CSR. More runs than kMergeRunsMax (short
+// voxel runs): fixed chunks are bitonic-sorted first and merged the same way.
+constexpr int kMergeThreads = 1024;
+constexpr uint32_t kMergeSmemElems = 27 * 1024;  // per buffer (two buffers)
+constexpr int kMergeRunsMax = 1024;
+constexpr uint32_t kMergeChunk = 4096;           // bitonic chunk when runs are short
+
+struct MergeSmem {
+  uint32_t buf[2][kMergeSmemElems];
+  uint32_t starts[kMergeRunsMax + 2];
+  uint32_t swarp[33];
+  uint32_t nruns;
+};
+
+// One merge pass: runs [starts[r], starts[r + 1]) of `in`, pairs (2p, 2p + 1)
+// merged into `out` (same positions); thread t writes outputs
+// [t * per, (t + 1) * per). Distinct values: no ties.
+__device__ __forceinline__ void merge_pass(const uint32_t* in, uint32_t* out,
+                                           const uint32_t* starts, int R, uint32_t n) {
+  const uint32_t per = (n + blockDim.x - 1) / blockDim.x;
+  uint32_t o = threadIdx.x * per;
+  const uint32_t o1 = min(n, o + per);
+  if (o >= o1) return;
+  // the pair holding output o: the largest p with starts[2p] <= o
+  int lo = 0, hi = (R + 1) / 2 - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (starts[2 * mid] <= o) lo = mid; else hi = mid - 1;
+  }
+  int p = lo;
+  while (o < o1) {
+    const uint32_t a0 = starts[2 * p];
+    const uint32_t a1 = starts[min(2 * p + 1, R)];
+    const uint32_t b1 = starts[min(2 * p + 2, R)];
+    const uint32_t la = a1 - a0, lb = b1 - a1;
+    const uint32_t* A = in + a0;
+    const uint32_t* B = in + a1;
+    // co-rank of diagonal o - a0
+    const uint32_t dg = o - a0;
+    uint32_t i0 = dg > lb ? dg - lb : 0u, i1 = min(dg, la);
+    while (i0 < i1) {
+      const uint32_t mid = (i0 + i1) >> 1;
+      if (A[mid] < B[dg - 1 - mid]) i0 = mid + 1; else i1 = mid;
+    }
+    uint32_t ia = i0, ib = dg - i0;
+    const uint32_t oe = min(o1, b1);
+    for (; o < oe; ++o) {
+      const uint32_t av = ia < la ? A[ia] : 0xffffffffu;
+      const uint32_t bv = ib < lb ? B[ib] : 0xffffffffu;
+      const bool ta = ib >= lb || (ia < la && av < bv);
+      out[o] = ta ? av : bv;
+      ia += ta;
+      ib += !ta;
+    }
+    ++p;
+  }
+}
+
+// starts[] of the ascending runs of a[0..n) (block-wide); returns the run
+// count, or kMergeRunsMax + 1 when there are more runs than fit.
+__device__ __forceinline__ int find_runs(const uint32_t* a, uint32_t n, MergeSmem& sm) {
+  const uint32_t per = (n + blockDim.x - 1) / blockDim.x;
+  const uint32_t b = min(n, threadIdx.x * per), e = min(n, b + per);
+  uint32_t c = 0;
+  for (uint32_t i = b; i < e; ++i) c += (i == 0 || a[i] < a[i - 1]);
+  uint32_t tot;
+  const uint32_t pos = block_excl_scan<uint32_t>(c, sm.swarp, &tot);
+  if (tot <= (uint32_t)kMergeRunsMax) {
+    uint32_t w = pos;
+    for (uint32_t i = b; i < e; ++i)
+      if (i == 0 || a[i] < a[i - 1]) sm.starts[w++] = i;
+    if (threadIdx.x == 0) sm.starts[tot] = n;
+  }
+  __syncthreads();
+  return tot <= (uint32_t)kMergeRunsMax ? (int)tot : kMergeRunsMax + 1;
+}
+
+// Fixed runs of `chunk` (power of two): each chunk bitonic-sorted through
+// shared memory (buf = one smem buffer of >= chunk elements).
+__device__ __forceinline__ int chunk_runs(uint32_t* a, uint32_t n, uint32_t chunk, uint32_t* buf,
+                                          MergeSmem& sm) {
+  for (uint32_t c0 = 0; c0 < n; c0 += chunk) {
+    const uint32_t len = min(chunk, n - c0);
+    for (uint32_t x = threadIdx.x; x < len; x += blockDim.x) buf[x] = a[c0 + x];
+    __syncthreads();
+    bitonic_sort(buf, len, threadIdx.x, blockDim.x, [] { __syncthreads(); });
+    for (uint32_t x = threadIdx.x; x < len; x += blockDim.x) a[c0 + x] = buf[x];
+    __syncthreads();
+  }
+  const int R = (int)((n + chunk - 1) / chunk);
+  for (int r = threadIdx.x; r <= R; r += blockDim.x) sm.starts[r] = r < R ? (uint32_t)r * chunk : n;
+  __syncthreads();
+  return R;
+}
+
+// starts of the merged runs: every other start
+__device__ __forceinline__ int halve_runs(MergeSmem& sm, int R, uint32_t n) {
+  __syncthreads();
+  const int R2 = (R + 1) / 2;
+  uint32_t v = 0;
+  if ((int)threadIdx.x < R2) v = sm.starts[2 * threadIdx.x];
+  __syncthreads();
+  if ((int)threadIdx.x < R2) sm.starts[threadIdx.x] = v;
+  if (threadIdx.x == 0) sm.starts[R2] = n;
+  __syncthreads();
+  return R2;
+}
+
+__global__ void __launch_bounds__(kMergeThreads) merge_big_rows_kernel(
+    uint32_t* __restrict__ arena, const uint64_t* __restrict__ big_off,
+    const uint32_t* __restrict__ big_len, const uint32_t* __restrict__ big_q,
+    const uint32_t* __restrict__ n_big, const uint64_t* __restrict__ row_ptr,
+    uint32_t* __restrict__ cols) {
+  extern __shared__ __align__(16) unsigned char msm_raw[];
+  MergeSmem& sm = *reinterpret_cast<MergeSmem*>(msm_raw);
+  const uint32_t nb = *n_big;
+  for (uint32_t bi = blockIdx.x; bi < nb; bi += gridDim.x) {
+    const uint32_t n = big_len[bi];
+    uint32_t* src = arena + big_off[bi];
+    uint32_t* dst = cols + row_ptr[big_q[bi]];
+    CM_DCHECK(row_ptr[big_q[bi] + 1] - row_ptr[big_q[bi]] == (uint64_t)n);
+    if (n <= kMergeSmemElems) {
+      uint32_t* a = sm.buf[0];
+      uint32_t* b = sm.buf[1];
+      for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) a[x] = src[x];
+      __syncthreads();
+      int R = find_runs(a, n, sm);
+      if (R > kMergeRunsMax) {
+        R = chunk_runs(a, n, kMergeChunk, b, sm);
+      }
+      while (R > 1) {
+        merge_pass(a, b, sm.starts, R, n);
+        R = halve_runs(sm, R, n);
+        uint32_t* t = a;
+        a = b;
+        b = t;
+      }
+      for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) dst[x] = a[x];
+    } else {
+      int R = find_runs(src, n, sm);
+      if (R > kMergeRunsMax) {
+        // chunk size: a power of two with at most kMergeRunsMax chunks
+        uint32_t ch = kMergeChunk;
+        while ((n + ch - 1) / ch > (uint32_t)kMergeRunsMax && ch < 16384u) ch <<= 1;
+        R = chunk_runs(src, n, ch, sm.buf[0], sm);
+      }
+      // ping-pong src <-> dst; an even number of passes ends in src
+      uint32_t* a = src;
+      uint32_t* b = dst;
+      while (R > 1) {
+        merge_pass(a, b, sm.starts, R, n);
+        R = halve_runs(sm, R, n);
+        uint32_t* t = a;
+        a = b;
+        b = t;
+      }
+      if (a != dst)
+        for (uint32_t x = threadIdx.x; x < n; x += blockDim.x) dst[x] = a[x];
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+uint32_t long_row_min() { return (uint32_t)kSortCap + 1u; }
+
+namespace {
+
+cm_status merge_big_rows_impl(uint32_t* arena, const uint64_t* big_off, const uint32_t* big_len,
+                         const uint32_t* big_q, const uint32_t* n_big, const uint64_t* row_ptr,
+                         uint32_t* cols, cudaStream_t st) {
+  const int smem = (int)sizeof(MergeSmem);
+  cudaFuncSetAttribute(merge_big_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  merge_big_rows_kernel<<<sm_count(), kMergeThreads, smem, st>>>(arena, big_off, big_len, big_q,
+                                                                 n_big, row_ptr, cols);
+  ::cmg::note_launch();
+  CM_CUDA_TRY(cudaGetLastError());
+  return CM_OK;
+}
+
+}  // namespace
+
+cm_status merge_big_rows(const MergeList& ml, uint32_t* arena, const uint64_t* row_ptr,
+                         uint32_t* cols, cudaStream_t st) {
+  return merge_big_rows_impl(arena, ml.off, ml.len, ml.q, ml.n, row_ptr, cols, st);
+}
+
+namespace {
+
 cm_status sort_big_rows(uint32_t* rows, const Out& o, cudaStream_t st) {
   const int smem = kBigSmemCap * 4;
   cudaFuncSetAttribute(big_row_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1996,11 +2201,13 @@ cm_status radius_collect_dev(const cm_index* ix, const double* q, uint64_t nq, i
                              double r, const uint32_t* perm, uint32_t* temp, uint64_t cap,
                              uint64_t* toff, uint32_t* scnt, uint32_t* counts,
                              unsigned long long* cursor, cudaStream_t st,
-                             cudaEvent_t after_collect, const double* rq, const double* qbox) {
+                             cudaEvent_t after_collect, const double* rq, const double* qbox,
+                             const MergeList* ml) {
   if (nq == 0) return CM_OK;
   BigRows big;
-  cm_status s = big.init(nq, st);
+  cm_status s = ml ? CM_OK : big.init(nq, st);
   if (s != CM_OK) return s;
+  if (ml) CM_CUDA_TRY(cudaMemsetAsync(ml->n, 0, 4, st));
   CM_CUDA_TRY(cudaMemsetAsync(cursor, 0, 8, st));
   Out o{};
   o.counts = counts;
@@ -2009,27 +2216,32 @@ cm_status radius_collect_dev(const cm_index* ix, const double* q, uint64_t nq, i
   o.toff = toff;
   o.scnt = scnt;
   o.cursor = cursor;
-  o.big_off = big.off;
-  o.big_len = big.len;
-  o.n_big = big.n;
+  o.big_off = ml ? ml->off : big.off;
+  o.big_len = ml ? ml->len : big.len;
+  o.big_q = ml ? ml->q : nullptr;
+  o.n_big = ml ? ml->n : big.n;
   o.rq = rq;
   o.qbox = qbox;
   s = launch_radius<MODE_COLLECT>(ix, q, nq, kernel, r, perm, o, st);
   if (after_collect) cudaEventRecord(after_collect, st);
-  if (s == CM_OK) s = sort_big_rows(temp, o, st);
+  // with a merge list the long rows stay in visit order (sorted runs) for
+  // merge_big_rows after the scan; otherwise they are sorted here in place
+  if (s == CM_OK && !ml) s = sort_big_rows(temp, o, st);
   return s;
 }
 
 cm_status gather_rows_dev(const uint32_t* temp, const uint64_t* toff, const uint32_t* counts,
                           const uint64_t* row_ptr, const uint32_t* perm, uint32_t* cols,
-                          uint64_t nq, cudaStream_t st) {
+                          uint64_t nq, cudaStream_t st, uint32_t skip_above) {
   if (nq == 0) return CM_OK;
   const uint64_t groups = (nq + 31) / 32;
   const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((groups + 3) / 4, (uint64_t)sm_count() * 8));
   const int smem = 4 * kGatherWarpWords * 4;
   (void)perm;
   cudaFuncSetAttribute(gather_rows_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  gather_rows_kernel<false><<<grid, 128, smem, st>>>(temp, toff, counts, row_ptr, cols, nq); ::cmg::note_launch();
+  gather_rows_kernel<false><<<grid, 128, smem, st>>>(temp, toff, counts, row_ptr, cols, nq,
+                                                     skip_above);
+  ::cmg::note_launch();
   CM_CUDA_TRY(cudaGetLastError());
   return CM_OK;
 }
