@@ -379,7 +379,8 @@ cm_status cm_free(cm_index* ix) {
   DeviceGuard dg(ix->device);
   cudaDeviceSynchronize();
   void* ptrs[] = {ix->rec,   ix->ukey,      ix->ustart, ix->uk_k,     ix->dense_off,
-                  ix->vhash, ix->col_dense, ix->chash,  ix->col_vbeg, ix->rec_of};
+                  ix->vhash, ix->col_dense, ix->chash,  ix->col_vbeg, ix->rec_of,
+                  ix->frec,  ix->ids};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, 0);
   cudaStreamSynchronize(0);
@@ -489,8 +490,11 @@ __global__ void export_kernel(const PointRec* __restrict__ rec, uint64_t n, DevG
 // no kernel predicate accepts it) — the effect of the reference's hook,
 // which pops a handle out of a voxel list (map.cpp:194-223). The point is
 // the middle one in cell order, reachable from most query centres.
-__global__ void corrupt_kernel(PointRec* rec, uint64_t at) {
-  if (blockIdx.x == 0 && threadIdx.x == 0) rec[at].x = __longlong_as_double(0x7ff8000000000000ll);
+__global__ void corrupt_kernel(PointRec* rec, FRec* frec, uint64_t at) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    rec[at].x = __longlong_as_double(0x7ff8000000000000ll);
+    frec[at].x = __int_as_float(0x7fc00000);
+  }
 }
 __global__ void add_offset_kernel(uint64_t* v, uint64_t n, uint64_t off) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
@@ -595,7 +599,7 @@ cm_status cm_voxel_lookup(const cm_index* ix, uint64_t i, uint64_t j, uint64_t k
 cm_status cm_corrupt_for_testing(cm_index* ix) {
   CM_TRY(check_index(ix));
   DeviceGuard dg(ix->device);
-  apik::corrupt_kernel<<<1, 1, 0, 0>>>(ix->rec, ix->n / 2); ::cmg::note_launch();
+  apik::corrupt_kernel<<<1, 1, 0, 0>>>(ix->rec, ix->frec, ix->n / 2); ::cmg::note_launch();
   CM_CUDA_TRY(cudaGetLastError());
   CM_CUDA_TRY(cudaDeviceSynchronize());
   return CM_OK;
@@ -713,8 +717,9 @@ namespace apik {
 // A small device value -> host without the copy engines (which may be busy
 // with large device->host copies queued on other streams): a one-thread
 // kernel stores it into mapped pinned host memory.
-__global__ void publish_u64_kernel(const unsigned long long* src, volatile unsigned long long* dst) {
-  *dst = *src;
+__global__ void publish_u64_kernel(const unsigned long long* src, volatile unsigned long long* dst,
+                                   int n) {
+  for (int k = 0; k < n; ++k) dst[k] = src[k];
   __threadfence_system();
 }
 // dst[k] = src[idx[k]] for k < n (a few row-pointer values for the host).
@@ -741,17 +746,19 @@ struct MappedSlot {
       cudaGetLastError();
   }
 };
-bool read_u64_mapped(const unsigned long long* dsrc, cudaStream_t st, unsigned long long* out) {
+// dsrc[0..n) (n <= 2) to the host.
+bool read_u64_mapped(const unsigned long long* dsrc, cudaStream_t st, unsigned long long* out,
+                     int n = 1) {
   MappedSlot& slot = per_thread_device<MappedSlot>();
   if (!slot.ok) {
-    if (cudaMemcpyAsync(out, dsrc, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess) return false;
+    if (cudaMemcpyAsync(out, dsrc, 8 * n, cudaMemcpyDeviceToHost, st) != cudaSuccess) return false;
     return cudaStreamSynchronize(st) == cudaSuccess;
   }
-  cmg::apik::publish_u64_kernel<<<1, 1, 0, st>>>(dsrc, slot.dev); ::cmg::note_launch();
+  cmg::apik::publish_u64_kernel<<<1, 1, 0, st>>>(dsrc, slot.dev, n); ::cmg::note_launch();
   if (cudaGetLastError() != cudaSuccess) return false;
   if (cudaEventRecord(slot.ev, st) != cudaSuccess) return false;
   if (cudaEventSynchronize(slot.ev) != cudaSuccess) return false;
-  *out = *reinterpret_cast<volatile unsigned long long*>(slot.host);
+  for (int k = 0; k < n; ++k) out[k] = reinterpret_cast<volatile unsigned long long*>(slot.host)[k];
   return true;
 }
 
@@ -829,7 +836,7 @@ static cm_status radius_search_core(const cm_index* ix, const double* qd, uint64
       dev_alloc_t(&ml.q, nq + 1, st) != cudaSuccess || dev_alloc_t(&ml.n, 1, st) != cudaSuccess ||
       dev_alloc_t(&csr->row_ptr, nq + 1, st) != cudaSuccess ||
       dev_alloc_t(&toff, nq + 1, st) != cudaSuccess || dev_alloc_t(&scnt, nq + 1, st) != cudaSuccess ||
-      dev_alloc_t(&cursor, 1, st) != cudaSuccess) {
+      dev_alloc_t(&cursor, 2, st) != cudaSuccess) {
     set_error("device allocation failed (row pointers)");
     return fail(CM_CUDA);
   }
@@ -849,17 +856,19 @@ static cm_status radius_search_core(const cm_index* ix, const double* qd, uint64
     cudaGetLastError();
   }
   cm_status s = CM_OK;
-  unsigned long long used = 0;
+  unsigned long long used = 0;        // arena entries (rows padded to 4 handles)
+  unsigned long long cur[2] = {0, 0}; // arena cursor, exact handle count
   bool recollected = false;
   if (!two_pass) {
     s = radius_collect_dev(ix, qd, nq, kernel, r, ord.perm, temp, cap, toff, scnt, counts, cursor,
                            st, ev.e[2], rq, qbox, &ml);
     cudaEventRecord(ev.e[3], st);
     if (s != CM_OK) return fail(s);
-    if (!read_u64_mapped(cursor, st, &used)) {
+    if (!read_u64_mapped(cursor, st, cur, 2)) {
       set_error("arena cursor readback failed");
       return fail(CM_CUDA);
     }
+    used = cur[0];
     // slow decay: alternating dense and sparse batches keep the larger size
     if (nq)
       ix->nnz_per_query.store(std::max({1.0, (double)used / (double)nq, 0.95 * est}),
@@ -874,10 +883,11 @@ static cm_status radius_search_core(const cm_index* ix, const double* qd, uint64
                                cursor, st, ev.e[2], rq, qbox, &ml);
         cudaEventRecord(ev.e[3], st);
         if (s != CM_OK) return fail(s);
-        if (!read_u64_mapped(cursor, st, &used)) {
+        if (!read_u64_mapped(cursor, st, cur, 2)) {
           set_error("arena cursor readback failed");
           return fail(CM_CUDA);
         }
+        used = cur[0];
       } else {
         cudaGetLastError();
       }
@@ -921,7 +931,7 @@ static cm_status radius_search_core(const cm_index* ix, const double* qd, uint64
     cudaGetLastError();
     if (cls && cls_h[0] > 0 && (double)cls_h[1] / (double)cls_h[0] < 660.0) mid_min = 512;
   } else {
-    csr->nnz = used;
+    csr->nnz = cur[1];
   }
   if (dev_alloc_t(&csr->cols, csr->nnz, st) != cudaSuccess) {
     set_error("device allocation failed (columns)");

@@ -80,24 +80,39 @@ __global__ void keys_kernel(const double* __restrict__ xyz, uint64_t n, DevGrid 
 }
 
 // Sorted order -> 32-byte records; run-start flags for the unique pass.
+// Also writes the float records of the filtered predicates (filter.cuh: x, y
+// relative to the column corner, z relative to oz) and the handle array.
 template <typename K>
 __global__ void gather_kernel(const double* __restrict__ xyz, const K* __restrict__ keys,
-                              const uint32_t* __restrict__ perm, uint64_t n, uint64_t nz,
-                              PointRec* __restrict__ rec, uint32_t* __restrict__ flags) {
+                              const uint32_t* __restrict__ perm, uint64_t n, DevGrid g,
+                              PointRec* __restrict__ rec, FRec* __restrict__ frec,
+                              uint32_t* __restrict__ ids, uint32_t* __restrict__ flags) {
+  const K nz = (K)g.nz, ny = (K)g.ny;
   for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < n;
        s += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t h = perm[s];
-    const uint64_t key = (uint64_t)keys[s];
+    const K key = keys[s];
     double2 a, b;
     a.x = xyz[3 * (uint64_t)h];
     a.y = xyz[3 * (uint64_t)h + 1];
     b.x = xyz[3 * (uint64_t)h + 2];
+    const K col = key / nz;
+    const uint32_t k = (uint32_t)(key - col * nz);
+    const K i = col / ny;
+    const K j = col - i * ny;
     uint2 t;
     t.x = h;
-    t.y = (uint32_t)(key % nz);
+    t.y = k;
     b.y = *reinterpret_cast<double*>(&t);
     reinterpret_cast<double2*>(rec + s)[0] = a;
     reinterpret_cast<double2*>(rec + s)[1] = b;
+    FRec f;
+    f.x = __double2float_rn(__dsub_rn(a.x, col_corner(g.ox, (uint64_t)i, g.sx)));
+    f.y = __double2float_rn(__dsub_rn(a.y, col_corner(g.oy, (uint64_t)j, g.sy)));
+    f.z = __double2float_rn(__dsub_rn(b.x, g.oz));
+    f.k = k;
+    frec[s] = f;
+    ids[s] = h;
     flags[s] = (s == 0 || keys[s - 1] != keys[s]) ? 1u : 0u;
   }
 }
@@ -257,13 +272,15 @@ cm_status build_typed(const double* xyz, uint64_t n, cudaStream_t st, cm_index* 
   dev_free(scratch, st);
 
   CM_CUDA_TRY(dev_alloc_t(&ix->rec, n, st));
+  CM_CUDA_TRY(dev_alloc_t(&ix->frec, n, st));
+  CM_CUDA_TRY(dev_alloc_t(&ix->ids, n, st));
   uint32_t* flags = nullptr;
   uint32_t* pos = nullptr;
   uint32_t* part = nullptr;
   CM_CUDA_TRY(dev_alloc_t(&flags, n, st));
   CM_CUDA_TRY(dev_alloc_t(&pos, n + 1, st));
   CM_CUDA_TRY(dev_alloc_t(&part, scan_part_elems(n), st));
-  gather_kernel<K><<<grid_for(n), 256, 0, st>>>(xyz, keys, perm, n, g.nz, ix->rec, flags); ::cmg::note_launch();
+  gather_kernel<K><<<grid_for(n), 256, 0, st>>>(xyz, keys, perm, n, g, ix->rec, ix->frec, ix->ids, flags); ::cmg::note_launch();
   cudaEventRecord(ev.e[4], st);
   exclusive_scan<uint32_t, uint32_t>(flags, n, pos, part, 1, st);
   uint32_t U32 = 0;

@@ -355,11 +355,14 @@ __global__ void slab_owned_kernel(const double* __restrict__ xyz, const uint32_t
 // After the local build: every record's handle becomes its global id, so
 // all query outputs (CSR, digests, kNN, exports) come out in global ids.
 // Local handles ascend with global ids, so row order is unchanged.
-__global__ void relabel_kernel(PointRec* __restrict__ rec, uint64_t n,
+__global__ void relabel_kernel(PointRec* __restrict__ rec, uint32_t* __restrict__ ids, uint64_t n,
                                const uint32_t* __restrict__ gid) {
   for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n;
-       p += (uint64_t)gridDim.x * blockDim.x)
-    rec[p].id = __ldg(gid + rec[p].id);
+       p += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t g = __ldg(gid + rec[p].id);
+    rec[p].id = g;
+    ids[p] = g;
+  }
 }
 
 unsigned grid_of(uint64_t n) {
@@ -704,7 +707,7 @@ cm_status cm_build_slab(cm_cluster* cl, const double* xyz, const uint32_t* gids,
       cm_slab_free(sl.release());
       return s;
     }
-    relabel_kernel<<<grid_of(nl), 256, 0, st>>>(sl->ix->rec, nl, sl->local_gid); ::cmg::note_launch();
+    relabel_kernel<<<grid_of(nl), 256, 0, st>>>(sl->ix->rec, sl->ix->ids, nl, sl->local_gid); ::cmg::note_launch();
     CM_CUDA_TRY(cudaGetLastError());
     sl->ix->global_ids = true;
   }

@@ -224,9 +224,12 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 // Flavour-specific span lookup: the points of column (i, j) with voxel z
 // index in [k0, k1] are ONE contiguous run of the cell-sorted records,
 // because global_index is k-fastest (grid.hpp:65-67).
+struct FRec;
 struct Tables {
   DevGrid g;
   const PointRec* rec;
+  const FRec* frec;       // float records (filter.cuh), same order as rec
+  const uint32_t* ids;    // rec[].id, 4 B per record
   uint64_t n;
   int flavor;
   // dense: offsets over all V voxels (+1)

@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "filter.cuh"
 
 struct cm_index {
   int device = 0;
@@ -22,6 +23,8 @@ struct cm_index {
   int key_bits = 0;
 
   cmg::PointRec* rec = nullptr;  // n, cell order
+  cmg::FRec* frec = nullptr;     // n, cell order: float records (filter.cuh)
+  uint32_t* ids = nullptr;       // n, cell order: handles (rec[].id)
   uint64_t* ukey = nullptr;      // U unique voxel keys (ascending)
   uint32_t* ustart = nullptr;    // U + 1 record offsets
   uint32_t* uk_k = nullptr;      // U voxel z index
@@ -53,6 +56,8 @@ struct cm_index {
     cmg::Tables t{};
     t.g = g;
     t.rec = rec;
+    t.frec = frec;
+    t.ids = ids;
     t.n = n;
     t.flavor = opts.flavor;
     t.dense_off = dense_off;

@@ -455,7 +455,183 @@ __global__ void __launch_bounds__(kKThreads) knn_tile_kernel(
   }
 }
 
-// ---- kNN by radius brackets (the default for k <= kKMax) -------------------
+// ---- per-thread kNN (k <= 64, the default) --------------------------------
+// One THREAD per centre (cell-sorted, so a warp's 32 centres are spatial
+// neighbours and share their records through L1): the thread walks its own
+// Chebyshev voxel shells — the 3 x 3 x 3 block first, own column first —
+// keeping its k best (d², handle) in a max-heap in shared memory (entry e of
+// thread t at [e][t], conflict-free), and stops with the shell walk's exact
+// test. Against one warp per centre there are no per-centre span lookups or
+// batch merges on the warp's critical path and no lanes idle on another
+// centre's candidates. Pass 1 stops at shell LFIRST; the centres it cannot
+// finish are compacted into a redo list and walked again, all shells, by a
+// second launch (so hard centres share warps with hard centres).
+constexpr int kTThreads = 128;
+
+template <int K>
+struct KnnHeap {
+  double* d;
+  uint32_t* id;
+  __device__ __forceinline__ double dd(uint32_t e) const { return d[e * kTThreads]; }
+  __device__ __forceinline__ uint32_t ii(uint32_t e) const { return id[e * kTThreads]; }
+  __device__ __forceinline__ void put(uint32_t e, double x, uint32_t xi) {
+    d[e * kTThreads] = x;
+    id[e * kTThreads] = xi;
+  }
+  // max-heap of n entries by (d², handle): insert (n < cap)
+  __device__ __forceinline__ void push(uint32_t n, double x, uint32_t xi) {
+    uint32_t pos = n;
+    while (pos > 0) {
+      const uint32_t par = (pos - 1) >> 1;
+      const double pd = dd(par);
+      const uint32_t pi = ii(par);
+      if (!pair_less(pd, pi, x, xi)) break;
+      put(pos, pd, pi);
+      pos = par;
+    }
+    put(pos, x, xi);
+  }
+  // replace the root (largest) by a smaller entry, heap of n
+  __device__ __forceinline__ void replace_top(uint32_t n, double x, uint32_t xi) {
+    uint32_t pos = 0;
+    for (;;) {
+      uint32_t c = 2 * pos + 1;
+      if (c >= n) break;
+      double cd = dd(c);
+      uint32_t ci = ii(c);
+      if (c + 1 < n) {
+        const double rd = dd(c + 1);
+        const uint32_t ri = ii(c + 1);
+        if (pair_less(cd, ci, rd, ri)) cd = rd, ci = ri, ++c;
+      }
+      if (!pair_less(x, xi, cd, ci)) break;
+      put(pos, cd, ci);
+      pos = c;
+    }
+    put(pos, x, xi);
+  }
+};
+
+template <int FLAVOR, int K>
+__global__ void __launch_bounds__(kTThreads) knn_thread_kernel(
+    const Tables t, const double* __restrict__ q, uint64_t nq, uint32_t k,
+    const uint32_t* __restrict__ list, const uint32_t* __restrict__ n_list, int lmax,
+    uint32_t* __restrict__ idx_out, double* __restrict__ d2_out, uint32_t* __restrict__ redo,
+    uint32_t* __restrict__ n_redo) {
+  extern __shared__ __align__(16) unsigned char hsm[];
+  double* sd = reinterpret_cast<double*>(hsm);
+  uint32_t* sid = reinterpret_cast<uint32_t*>(hsm + (size_t)K * kTThreads * sizeof(double));
+  KnnHeap<K> h{sd + threadIdx.x, sid + threadIdx.x};
+  if (n_list) nq = nq < (uint64_t)*n_list ? nq : (uint64_t)*n_list;
+  const DevGrid& g = t.g;
+  const PointRec* __restrict__ rec = t.rec;
+  const int64_t nx = (int64_t)g.nx, ny = (int64_t)g.ny, nzm = (int64_t)g.nz - 1;
+  const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+  const uint64_t stride = (uint64_t)gridDim.x * kTThreads;
+  for (uint64_t s0 = (uint64_t)blockIdx.x * kTThreads; s0 < nq; s0 += stride) {
+    const uint64_t s = s0 + threadIdx.x;
+    const bool active = s < nq;
+    bool done = !active;
+    uint32_t qi = 0, cnt = 0;
+    if (active) {
+      qi = __ldg(list + s);
+      const double cx = __ldg(q + 3 * (uint64_t)qi);
+      const double cy = __ldg(q + 3 * (uint64_t)qi + 1);
+      const double cz = __ldg(q + 3 * (uint64_t)qi + 2);
+      const int64_t ic = (int64_t)axis_index(cx, g.ox, g.sx, g.nx);
+      const int64_t jc = (int64_t)axis_index(cy, g.oy, g.sy, g.ny);
+      const int64_t kc = g.mode3d ? (int64_t)axis_index(cz, g.oz, g.sz, g.nz) : 0;
+      const double eps = 1e-12 * (fabs(cx) + fabs(cy) + fabs(cz) + fabs(g.ox) + fabs(g.oy) +
+                                  fabs(g.oz) + g.sx + g.sy + g.sz);
+      double kd = kInf;       // the heap's root (k-th best) once full
+      uint32_t kid = 0xffffffffu;
+      auto visit = [&](uint32_t b, uint32_t e) {
+        for (uint32_t p = b; p < e; ++p) {
+          const PointRec pr = load_rec(rec + p);
+          const double d2 = sqdist(pr.x, pr.y, pr.z, cx, cy, cz);
+          if (cnt < k) {
+            h.push(cnt, d2, pr.id);
+            if (++cnt == k) kd = h.dd(0), kid = h.ii(0);
+          } else if (pair_less(d2, pr.id, kd, kid)) {
+            h.replace_top(k, d2, pr.id);
+            kd = h.dd(0), kid = h.ii(0);
+          }
+        }
+      };
+      for (int64_t L = 1; L <= lmax; ++L) {
+        const int64_t i0 = imax64(0, ic - L), i1 = imin64(nx - 1, ic + L);
+        const int64_t j0 = imax64(0, jc - L), j1 = imin64(ny - 1, jc + L);
+        const int64_t nj = j1 - j0 + 1;
+        const int64_t ncol = (i1 - i0 + 1) * nj;
+        // L = 1: the centre's own column first (a tight k-th bound early
+        // means fewer heap updates), then the other eight
+        for (int64_t c = -1; c < ncol; ++c) {
+          int64_t i, j;
+          if (c < 0) {
+            if (L != 1) continue;
+            i = ic, j = jc;
+          } else {
+            i = i0 + c / nj, j = j0 + c % nj;
+            if (L == 1 && i == ic && j == jc) continue;
+          }
+          const bool ring = L == 1 || i == ic - L || i == ic + L || j == jc - L || j == jc + L;
+          uint32_t b1, e1, b2, e2;
+          shell_column_spans<FLAVOR>(t, i, j, ring, kc, L, (uint64_t)nzm, &b1, &e1, &b2, &e2);
+          visit(b1, e1);
+          visit(b2, e2);
+        }
+        const bool all = i0 == 0 && i1 == nx - 1 && j0 == 0 && j1 == ny - 1 &&
+                         imax64(0, kc - L) == 0 && imin64(nzm, kc + L) == nzm;
+        if (all) {
+          done = true;
+          break;
+        }
+        if (cnt == k) {
+          double dmin = 1e300;
+          if (i0 > 0) dmin = fmin(dmin, cx - (g.ox + (double)i0 * g.sx));
+          if (i1 < nx - 1) dmin = fmin(dmin, (g.ox + (double)(i1 + 1) * g.sx) - cx);
+          if (j0 > 0) dmin = fmin(dmin, cy - (g.oy + (double)j0 * g.sy));
+          if (j1 < ny - 1) dmin = fmin(dmin, (g.oy + (double)(j1 + 1) * g.sy) - cy);
+          if (g.mode3d) {
+            if (kc - L > 0) dmin = fmin(dmin, cz - (g.oz + (double)(kc - L) * g.sz));
+            if (kc + L < nzm) dmin = fmin(dmin, (g.oz + (double)(kc + L + 1) * g.sz) - cz);
+          }
+          const double dm = dmin - eps;
+          if (dm > 0.0 && kd < dm * dm) {
+            done = true;
+            break;
+          }
+        }
+      }
+      if (done) {
+        // heapsort in place: ascending (d², handle)
+        for (uint32_t n = cnt; n > 1; --n) {
+          const double td = h.dd(0);
+          const uint32_t ti = h.ii(0);
+          const double xd = h.dd(n - 1);
+          const uint32_t xi = h.ii(n - 1);
+          h.put(n - 1, td, ti);
+          h.replace_top(n - 1, xd, xi);
+        }
+        for (uint32_t x = 0; x < k; ++x) {
+          idx_out[(uint64_t)qi * k + x] = x < cnt ? h.ii(x) : 0xffffffffu;
+          if (d2_out) d2_out[(uint64_t)qi * k + x] = x < cnt ? h.dd(x) : kInf;
+        }
+      }
+    }
+    const bool r = active && !done;
+    const uint32_t rm = __ballot_sync(0xffffffffu, r);
+    if (rm) {
+      const int lane = threadIdx.x & 31;
+      uint32_t slot = 0;
+      if (lane == __ffs(rm) - 1) slot = atomicAdd(n_redo, (uint32_t)__popc(rm));
+      slot = __shfl_sync(0xffffffffu, slot, __ffs(rm) - 1);
+      if (r) redo[slot + __popc(rm & lanemask_lt())] = qi;
+    }
+  }
+}
+
+// ---- kNN by radius brackets (opt-in) ---------------------------------------
 // The k nearest of a centre are exactly the k smallest (d², handle) among
 // the points with d² <= R² for ANY R with count(d² <= R²) >= k. So: (1)
 // per-centre radius brackets from the radius engine's COUNT pass (the same
@@ -689,7 +865,7 @@ cm_status knn_brackets(const cm_index* ix, const double* q, uint64_t nq, uint32_
   if (!alloc(&rq, nq) || !alloc(&counts, nq + 1) || !alloc(&la, nq) || !alloc(&lb, nq) ||
       !alloc(&res, nq) || !alloc(&f_res, nq + 1) || !alloc(&f_next, nq + 1) ||
       !alloc(&p_res, nq + 1) || !alloc(&p_next, nq + 1) || !alloc(&part, scan_part_elems(nq)) ||
-      !alloc(&n_res, 1) || !alloc(&scnt, nq + 1) || !alloc(&toff, nq + 1) || !alloc(&cursor, 1) ||
+      !alloc(&n_res, 1) || !alloc(&scnt, nq + 1) || !alloc(&toff, nq + 1) || !alloc(&cursor, 2) ||
       !alloc(&cap_d, 1)) {
     set_error("device allocation failed (kNN brackets)");
     return CM_CUDA;
@@ -814,6 +990,68 @@ cm_status knn_dev(const cm_index* ix, const double* q, uint64_t nq, uint32_t k,
   // passes' tiles fall back to one centre per warp. Kept behind
   // CMGPU_KNN_BRACKETS for that comparison.
   static const bool brackets = std::getenv("CMGPU_KNN_BRACKETS") != nullptr;
+  static const bool legacy = std::getenv("CMGPU_KNN_LEGACY") != nullptr;
+  // (k = 32 / 64 measured slower per thread than one warp per centre: 36.9 /
+  // 109 ms against 25.5 / 39 ms on config 3)
+  static const uint32_t thread_kmax =
+      std::getenv("CMGPU_KNN_THREAD_KMAX") ? (uint32_t)std::atoi(std::getenv("CMGPU_KNN_THREAD_KMAX")) : 16u;
+  if (!brackets && !legacy && k <= std::min(64u, thread_kmax)) {
+    // per-thread kNN: pass 1 up to shell LFIRST, pass 2 (all shells) on the
+    // centres pass 1 could not finish
+    static const int lfirst_env = std::getenv("CMGPU_KNN_LFIRST") ? std::atoi(std::getenv("CMGPU_KNN_LFIRST")) : 0;
+    const int lfirst = lfirst_env > 0 ? lfirst_env : (k <= 16 ? 1 : 2);
+    uint32_t* redo1 = nullptr;
+    uint32_t* redo2 = nullptr;
+    uint32_t* nr = nullptr;  // [0] pass-1 redo count, [1] pass-2 (must stay 0)
+    CM_CUDA_TRY(dev_alloc_t(&redo1, nq, st));
+    CM_CUDA_TRY(dev_alloc_t(&redo2, nq, st));
+    CM_CUDA_TRY(dev_alloc_t(&nr, 2, st));
+    CM_CUDA_TRY(cudaMemsetAsync(nr, 0, 8, st));
+    auto pass = [&](auto kern, int K, const uint32_t* list, const uint32_t* nl, int lmax,
+                    uint32_t* rd, uint32_t* nrd) -> cm_status {
+      const size_t smem = (size_t)K * kTThreads * 12;
+      if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kTThreads, smem);
+      per_sm = std::max(per_sm, 1);
+      const uint64_t need = (nq + kTThreads - 1) / kTThreads;
+      const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(need, (uint64_t)sm_count() * per_sm));
+      kern<<<grid, kTThreads, smem, st>>>(t, q, nq, k, list, nl, lmax, idx, d2, rd, nrd);
+      ::cmg::note_launch();
+      CM_CUDA_TRY(cudaGetLastError());
+      return CM_OK;
+    };
+    auto both = [&](auto kern, int K) -> cm_status {
+      const cm_status s1 = pass(kern, K, perm, nullptr, lfirst, redo1, nr);
+      if (s1 != CM_OK) return s1;
+      return pass(kern, K, redo1, nr, 1 << 30, redo2, nr + 1);
+    };
+    auto by_k = [&](auto k8, auto k16, auto k32, auto k64) -> cm_status {
+      if (k <= 8) return both(k8, 8);
+      if (k <= 16) return both(k16, 16);
+      if (k <= 32) return both(k32, 32);
+      return both(k64, 64);
+    };
+    cm_status s;
+    switch (ix->opts.flavor) {
+      case CM_DENSE:
+        s = by_k(knn_thread_kernel<CM_DENSE, 8>, knn_thread_kernel<CM_DENSE, 16>,
+                 knn_thread_kernel<CM_DENSE, 32>, knn_thread_kernel<CM_DENSE, 64>);
+        break;
+      case CM_SPARSE:
+        s = by_k(knn_thread_kernel<CM_SPARSE, 8>, knn_thread_kernel<CM_SPARSE, 16>,
+                 knn_thread_kernel<CM_SPARSE, 32>, knn_thread_kernel<CM_SPARSE, 64>);
+        break;
+      default:
+        s = by_k(knn_thread_kernel<CM_MIXED, 8>, knn_thread_kernel<CM_MIXED, 16>,
+                 knn_thread_kernel<CM_MIXED, 32>, knn_thread_kernel<CM_MIXED, 64>);
+    }
+    dev_free(redo1, st);
+    dev_free(redo2, st);
+    dev_free(nr, st);
+    if (scratch) dev_free(scratch, st);
+    return s;
+  }
   if (!glist && !ix->global_ids && brackets) {
     // radius brackets first; the shell walk takes what they leave
     CM_CUDA_TRY(dev_alloc_t(&redo, nq, st));

@@ -37,6 +37,12 @@ namespace {
 
 using namespace ::cmg::tw;  // tile_walk.cuh
 
+#ifndef CM_FILTER
+#define CM_FILTER 0  // filtered predicates (filter.cuh) in the compact tile walk: measured slower at r = 1 (collect 9.9 -> 11.3 ms)
+#endif
+#ifndef CM_PARK
+#define CM_PARK 1    // long-row centres parked in shared memory across the row stores
+#endif
 constexpr int kQThreads = 128;
 constexpr int kQWarps = kQThreads / 32;
 #ifndef CM_LANE_ROW_CAP
@@ -93,7 +99,8 @@ struct Out {
   uint64_t cap;                   // COLLECT arena capacity (entries)
   uint64_t* toff;                 // COLLECT arena offset, by query
   uint32_t* scnt;                 // COLLECT row length, by query
-  unsigned long long* cursor;     // COLLECT arena bump pointer
+  unsigned long long* cursor;     // COLLECT arena bump pointer (rows padded to 4 handles)
+  unsigned long long* nnz;        // COLLECT: exact handle count (or null)
   uint64_t* big_off;              // rows sorted afterwards: offset into `rows`
   uint32_t* big_len;
   uint32_t* big_q;                // COLLECT with a merge list: the row's query (or null)
@@ -364,6 +371,13 @@ __device__ __forceinline__ void warp_sort_row_out(const uint32_t* srow, int l, u
   }
 }
 
+// Predicated 16-bit shared store (no branch around it).
+__device__ __forceinline__ void sts_u16_if(uint32_t addr, uint32_t v, bool p) {
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q st.shared.u16 [%0], %1;\n}\n" ::"r"(addr),
+      "h"((unsigned short)v), "r"((uint32_t)p));
+}
+
 template <int CUBE>
 __device__ __forceinline__ bool pred(const Predicate& P, double x, double y, double z) {
   if (CUBE == 1)  // closed box (geometry.hpp:48-51)
@@ -626,14 +640,16 @@ __device__ __forceinline__ void single_query(const Tables& t, uint32_t qi, uint6
     const uint32_t cnt =
         warp_query_walk<FLAVOR, CUBE>(t, cx, cy, cz, r, lane, lt, wbuf, kSortCap, nullptr, box);
     unsigned long long base = 0;
+    const uint32_t alloc = cnt;
     if (lane == 0) {
-      base = atomicAdd(o.cursor, (unsigned long long)cnt);
+      base = atomicAdd(o.cursor, (unsigned long long)alloc);
+      if (o.nnz) atomicAdd(o.nnz, (unsigned long long)cnt);
       o.counts[qi] = cnt;
       o.toff[qi] = base;
       o.scnt[qi] = cnt;
     }
     base = __shfl_sync(0xffffffffu, base, 0);
-    if (base + cnt <= o.cap) {
+    if (base + alloc <= o.cap) {
       Out o2 = o;
       o2.cur_q = qi;
       warp_row_out<FLAVOR, CUBE>(t, cx, cy, cz, r, lane, lt, wbuf, cnt, o.temp + base, base, o2, box);
@@ -781,6 +797,7 @@ __global__ void __launch_bounds__(kQThreads, CM_QTILE_MINB) radius_tile_kernel(
     const uint32_t* __restrict__ perm, const Out o) {
   extern __shared__ __align__(16) unsigned char smraw[];
   constexpr bool ROWS = MODE == MODE_FILL || MODE == MODE_COLLECT;
+  constexpr bool FILTERED = CM_FILTER && (CUBE == 0 || CUBE == 1);
   constexpr int so = ROWS ? 4 : 0;
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -868,8 +885,8 @@ __global__ void __launch_bounds__(kQThreads, CM_QTILE_MINB) radius_tile_kernel(
     }
     if (!use_tile) {
       const uint32_t am = __ballot_sync(0xffffffffu, active);
-      for (int l = 0; l < 32; ++l) {
-        if (!((am >> l) & 1u)) continue;
+      for (uint32_t lr = am; lr; lr &= lr - 1) {
+        const int l = __ffs(lr) - 1;
         const uint32_t ql = __shfl_sync(0xffffffffu, qi, l);
         const double xl = __shfl_sync(0xffffffffu, cx, l);
         const double yl = __shfl_sync(0xffffffffu, cy, l);
@@ -899,15 +916,105 @@ __global__ void __launch_bounds__(kQThreads, CM_QTILE_MINB) radius_tile_kernel(
     const uint32_t kaddr0 = ROWS ? (uint32_t)__cvta_generic_to_shared(skey + lane) : 0u;
     const uint32_t klim = kaddr0 + 66u * (uint32_t)kLaneRowCap;
     uint32_t kaddr = kaddr0;
-    // Walk the hull: each needed column's span in chunks of <= 32 records,
-    // staged into shared memory by cp.async one chunk ahead (double buffer),
-    // then read warp-uniformly (LDS broadcast) by every lane.
     uint32_t needmask = colmask;
 #pragma unroll
     for (int sh = 16; sh > 0; sh >>= 1) needmask |= __shfl_xor_sync(0xffffffffu, needmask, sh);
     uint32_t c = 0, p = 0, ce = 0;
     bool more = advance_chunk(needmask, c, p, ce, b, e, true);
     int buf = 0;
+    if (FILTERED && !o.qbox) {
+      // Filtered predicates (filter.cuh): fp32 records decide every hit and
+      // miss they can prove; the rest go through the exact fp64 test.
+      Filter F;
+      filter_init<CUBE>(F, t.g, cx, cy, cz, rl,
+                        eps_of(t.g, cx, cy, cz, I0, nc / nj, J0, nj));
+      // lane l < ncol: corner of hull column l
+      const double ccx = col_corner(t.g.ox, I0 + lane / nj, t.g.sx);
+      const double ccy = col_corner(t.g.oy, J0 + lane % nj, t.g.sy);
+      FRec* stf = reinterpret_cast<FRec*>(stg);
+      const FRec* __restrict__ frec = t.frec;
+      if (more) stage_chunk_f(stf, frec, p, min(32u, ce - p), lane);
+      cp_async_commit();
+      while (more) {
+        uint32_t c2 = c, p2 = p, ce2 = ce;
+        const bool more2 = advance_chunk(needmask, c2, p2, ce2, b, e, false);
+        if (more2) stage_chunk_f(stf + (buf ^ 1) * 32, frec, p2, min(32u, ce2 - p2), lane);
+        cp_async_commit();
+        const float ax = __double2float_rn(__dsub_rn(__shfl_sync(0xffffffffu, ccx, c), F.cx));
+        const float ay = __double2float_rn(__dsub_rn(__shfl_sync(0xffffffffu, ccy, c), F.cy));
+        cp_async_wait<1>();
+        __syncwarp();
+        const FRec* sr = stf + buf * 32;
+        const uint32_t len = min(32u, ce - p);
+        const bool need = (colmask >> c) & 1u;
+        const uint32_t kbase = (c << 11) | (p - __shfl_sync(0xffffffffu, b, c));
+        // chunks (k-sorted) outside every lane's z window are skipped whole
+        const bool want = need & (sr[len - 1].k >= kk0) & (sr[0].k <= kk0 + kspan);
+        uint32_t u = __any_sync(0xffffffffu, want) ? 0u : len;
+        // a hit at chunk position pos, or nothing (branch-free: a divergent
+        // branch here leaves the warp split, and every later shuffle / vote
+        // then takes the compiler's WARPSYNC.COLLECTIVE path)
+        auto take = [&](uint32_t pos, bool hit) {
+          if (MODE == MODE_DIGEST) {
+            const uint64_t m = mix64(__ldg(t.ids + p + pos));  // warp-uniform address
+            dig += hit ? m : 0ull;
+          }
+          if (ROWS) {
+            sts_u16_if(kaddr, kbase + pos, hit & (kaddr < klim));
+            kaddr += hit ? 66u : 0u;
+          } else {
+            cnt += hit;
+          }
+        };
+        auto resolve = [&](uint32_t unc, uint32_t at) {  // exact fp64 test of the undecided
+          if (__any_sync(0xffffffffu, unc != 0u)) {
+            Predicate P;
+            P.init(F.cx, F.cy, cz, rl, CUBE, nullptr);
+            for (int w = 0; w < 8; ++w) {
+              if (!__any_sync(0xffffffffu, (unc >> w) & 1u)) continue;
+              const PointRec pr = load_rec(rec + p + at + w);  // warp-uniform address
+              take(at + w, ((unc >> w) & 1u) && pred<CUBE>(P, pr.x, pr.y, pr.z));
+            }
+          }
+        };
+        for (; u + 8 <= len; u += 8) {
+          FRec v[8];
+#pragma unroll
+          for (int w = 0; w < 8; ++w) v[w] = sr[u + w];
+          uint32_t unc = 0;
+#pragma unroll
+          for (int w = 0; w < 8; ++w) {
+            const bool in = need & (v[w].k - kk0 <= kspan);
+            const float f = filter_value<CUBE>(__fadd_rn(v[w].x, ax), __fadd_rn(v[w].y, ay),
+                                               __fadd_rn(v[w].z, F.az));
+            const bool hit = in & (f <= F.tin);
+            unc |= (in & !(f <= F.tin) & (f <= F.tout)) ? (1u << w) : 0u;
+            take(u + w, hit);
+            ntest += in;
+          }
+          resolve(unc, u);
+        }
+        {
+          uint32_t unc = 0;
+          const uint32_t u0 = u;
+          for (; u < len; ++u) {
+            const FRec v = sr[u];
+            const bool in = need & (v.k - kk0 <= kspan);
+            const float f = filter_value<CUBE>(__fadd_rn(v.x, ax), __fadd_rn(v.y, ay),
+                                               __fadd_rn(v.z, F.az));
+            const bool hit = in & (f <= F.tin);
+            unc |= (in & !(f <= F.tin) & (f <= F.tout)) ? (1u << (u - u0)) : 0u;
+            take(u, hit);
+            ntest += in;
+          }
+          resolve(unc, u0);
+        }
+        __syncwarp();
+        buf ^= 1;
+        c = c2, p = p2, ce = ce2;
+        more = more2;
+      }
+    } else {
     if (more) stage_chunk(stg, rec, p, min(32u, ce - p), lane);
     cp_async_commit();
     while (more) {
@@ -962,6 +1069,7 @@ __global__ void __launch_bounds__(kQThreads, CM_QTILE_MINB) radius_tile_kernel(
       c = c2, p = p2, ce = ce2;
       more = more2;
     }
+    }
     cp_async_wait<0>();
     if (ROWS) cnt = (kaddr - kaddr0) / 66u;
     if (MODE == MODE_COUNT) {
@@ -979,8 +1087,16 @@ __global__ void __launch_bounds__(kQThreads, CM_QTILE_MINB) radius_tile_kernel(
         o.digests[qi] = dig;
       }
     } else {
-      // rows: lanes whose hits overflowed the buffer are redone per query
+      // rows: lanes whose hits overflowed the buffer are redone per query.
+      // Their centres wait in the idle staging buffer (bytes 128..1151, past
+      // the column starts), so no registers stay live across the row sorts.
       const bool longrow = cnt > (uint32_t)kLaneRowCap;
+      uint32_t* spark = reinterpret_cast<uint32_t*>(stg) + 32;
+      double* sc = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(stg) + 256);
+      if (CM_PARK && __any_sync(0xffffffffu, active && longrow)) {
+        spark[lane] = qi;
+        sc[lane] = cx, sc[32 + lane] = cy, sc[64 + lane] = cz, sc[96 + lane] = rl;
+      }
       const uint32_t mine = (active && !longrow) ? cnt : 0u;
       uint64_t dst;
       bool write_ok = true;
@@ -989,14 +1105,18 @@ __global__ void __launch_bounds__(kQThreads, CM_QTILE_MINB) radius_tile_kernel(
         // the row the count pass sized must hold exactly this walk's hits
         CM_DCHECK(!active || longrow || __ldg(o.row_ptr + qi + 1) - dst == (uint64_t)cnt);
       } else {
-        const uint32_t inc = warp_incl_scan(mine);
+        const uint32_t alloc = mine;
+        const uint32_t inc = warp_incl_scan(alloc);
         const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
         unsigned long long base = 0;
-        if (lane == 0 && tot) base = atomicAdd(o.cursor, (unsigned long long)tot);
+        if (lane == 0 && tot) {
+          base = atomicAdd(o.cursor, (unsigned long long)tot);
+          if (o.nnz) atomicAdd(o.nnz, (unsigned long long)tot);
+        }
         base = __shfl_sync(0xffffffffu, base, 0);
-        dst = base + (inc - mine);
+        dst = base + (inc - alloc);
         write_ok = base + tot <= o.cap;
-        CM_DCHECK(!write_ok || dst + mine <= o.cap);
+        CM_DCHECK(!write_ok || dst + alloc <= o.cap);
         if (active && !longrow) {
           o.counts[qi] = cnt;
           o.toff[qi] = dst;
@@ -1013,6 +1133,9 @@ __global__ void __launch_bounds__(kQThreads, CM_QTILE_MINB) radius_tile_kernel(
           // translates and stores its own row: independent loads, many in
           // flight, no warp-wide round trip per row. Column starts move to
           // the (now idle) staging buffer so the loop needs no shuffles.
+          // (Sorting here instead — per-lane networks after the walk — put
+          // the network's 17 KB of code next to the walk's and the kernel
+          // thrashed the 32 KB instruction cache: collect 10.7 -> 22 ms.)
           uint32_t* cbeg = reinterpret_cast<uint32_t*>(stg);
           cbeg[lane] = b;
           __syncwarp();
@@ -1023,13 +1146,13 @@ __global__ void __launch_bounds__(kQThreads, CM_QTILE_MINB) radius_tile_kernel(
 #pragma unroll
             for (int w = 0; w < 8; ++w) kv[w] = skey[(i + w) * 33 + lane];
 #pragma unroll
-            for (int w = 0; w < 8; ++w) v[w] = __ldg(&rec[cbeg[kv[w] >> 11] + (kv[w] & 2047u)].id);
+            for (int w = 0; w < 8; ++w) v[w] = __ldg(t.ids + cbeg[kv[w] >> 11] + (kv[w] & 2047u));
 #pragma unroll
             for (int w = 0; w < 8; ++w) out[i + w] = v[w];
           }
           for (; i < mine; ++i) {
             const uint32_t kv = skey[i * 33 + lane];
-            out[i] = __ldg(&rec[cbeg[kv >> 11] + (kv & 2047u)].id);
+            out[i] = __ldg(t.ids + cbeg[kv >> 11] + (kv & 2047u));
           }
         } else
         for (int l = 0; l < 32; ++l) {
@@ -1042,7 +1165,7 @@ __global__ void __launch_bounds__(kQThreads, CM_QTILE_MINB) radius_tile_kernel(
             const uint32_t i = r2 * 32 + lane;
             const uint32_t key = i < len ? skey[i * 33 + l] : 0u;
             const uint32_t cb2 = __shfl_sync(0xffffffffu, b, key >> 11);
-            v[r2] = i < len ? __ldg(&rec[cb2 + (key & 2047u)].id) : 0xffffffffu;
+            v[r2] = i < len ? __ldg(t.ids + cb2 + (key & 2047u)) : 0xffffffffu;
           }
           if (MODE == MODE_COLLECT) {  // arena rows go out unsorted; the gather sorts
 #pragma unroll
@@ -1063,13 +1186,25 @@ __global__ void __launch_bounds__(kQThreads, CM_QTILE_MINB) radius_tile_kernel(
       __syncwarp();
       const uint32_t lm = __ballot_sync(0xffffffffu, active && longrow);
       if (lane == 0 && lm) atomicAdd(&g_qstats[7], (unsigned long long)__popc(lm));
-      for (int l = 0; l < 32; ++l) {
-        if (!((lm >> l) & 1u)) continue;
-        const uint32_t ql = __shfl_sync(0xffffffffu, qi, l);
-        const double xl = __shfl_sync(0xffffffffu, cx, l);
-        const double yl = __shfl_sync(0xffffffffu, cy, l);
-        const double zl = __shfl_sync(0xffffffffu, cz, l);
-        const double rl2 = __shfl_sync(0xffffffffu, rl, l);
+      // single_query reuses the whole warp region: take every parked centre
+      // into registers first (lane l holds centre l)
+      uint32_t pq = qi;
+      double px = cx, py = cy, pz = cz, pr = rl;
+      if (CM_PARK && lm) {  // warp-uniform; the loads are branch-free selects
+        const bool mine = (lm >> lane) & 1u;
+        const uint32_t a = spark[lane];
+        const double b0 = sc[lane], b1 = sc[32 + lane], b2 = sc[64 + lane], b3 = sc[96 + lane];
+        pq = mine ? a : pq;
+        px = mine ? b0 : px, py = mine ? b1 : py, pz = mine ? b2 : pz, pr = mine ? b3 : pr;
+      }
+      __syncwarp();
+      for (uint32_t lr = lm; lr; lr &= lr - 1) {
+        const int l = __ffs(lr) - 1;
+        const uint32_t ql = __shfl_sync(0xffffffffu, pq, l);
+        const double xl = __shfl_sync(0xffffffffu, px, l);
+        const double yl = __shfl_sync(0xffffffffu, py, l);
+        const double zl = __shfl_sync(0xffffffffu, pz, l);
+        const double rl2 = __shfl_sync(0xffffffffu, pr, l);
         single_query<FLAVOR, MODE, CUBE>(t, ql, tile * 32 + l, xl, yl, zl, rl2, lane, lt, o, wbuf);
       }
     }
@@ -2208,7 +2343,7 @@ cm_status radius_collect_dev(const cm_index* ix, const double* q, uint64_t nq, i
   cm_status s = ml ? CM_OK : big.init(nq, st);
   if (s != CM_OK) return s;
   if (ml) CM_CUDA_TRY(cudaMemsetAsync(ml->n, 0, 4, st));
-  CM_CUDA_TRY(cudaMemsetAsync(cursor, 0, 8, st));
+  CM_CUDA_TRY(cudaMemsetAsync(cursor, 0, 16, st));
   Out o{};
   o.counts = counts;
   o.temp = temp;
@@ -2216,6 +2351,7 @@ cm_status radius_collect_dev(const cm_index* ix, const double* q, uint64_t nq, i
   o.toff = toff;
   o.scnt = scnt;
   o.cursor = cursor;
+  o.nnz = cursor + 1;
   o.big_off = ml ? ml->off : big.off;
   o.big_len = ml ? ml->len : big.len;
   o.big_q = ml ? ml->q : nullptr;

@@ -4,6 +4,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "filter.cuh"
 
 namespace cmg {
 namespace tw {
@@ -44,6 +45,12 @@ __device__ __forceinline__ void stage_chunk(PointRec* stg, const PointRec* rec, 
     cp_async16(d, g);
     cp_async16(d + 16, g + 16);
   }
+}
+
+// Float records [p, p + len) -> stg[0..len): lane t copies record t (16 B).
+__device__ __forceinline__ void stage_chunk_f(FRec* stg, const FRec* frec, uint32_t p,
+                                              uint32_t len, int lane) {
+  if ((uint32_t)lane < len) cp_async16(stg + lane, frec + p + lane);
 }
 
 // Chunk iterator over the hull's needed columns (bit c of `mask`), spans
