@@ -76,6 +76,11 @@ __device__ __forceinline__ void shell_column_spans(const Tables& t, int64_t i, i
   }
 }
 
+#ifndef CM_KNN_BALL
+#define CM_KNN_BALL 0  // measured slower on config 3 (k = 64: 39.3 -> 47.8 ms): opt-in
+#endif
+constexpr bool kBallWarp = CM_KNN_BALL;  // ball completion in the shell walk
+
 // GLIST = false: the sorted (d2, handle) list of one query lives in shared
 // memory (k <= kKMax). GLIST = true (any k): it lives in the outputs
 // themselves (idx_out row, and d2_out row or a chunk-local d2 scratch).
@@ -124,20 +129,13 @@ __global__ void __launch_bounds__(kKThreads) knn_warp_kernel(const Tables t,
     // once: the shell-0 stop test almost never holds for k >= 8 at
     // cell-sized voxels, so testing it only cost a round of span lookups and
     // a batch merge); later steps add one Chebyshev shell each.
-    for (int64_t L = 1;; ++L) {
-      const int64_t i0 = imax64(0, ic - L), i1 = imin64(nx - 1, ic + L);
-      const int64_t j0 = imax64(0, jc - L), j1 = imin64(ny - 1, jc + L);
-      const uint32_t nj = (uint32_t)(j1 - j0 + 1);
-      const uint32_t ncol = (uint32_t)(i1 - i0 + 1) * nj;
+    // Columns [0, ncol) of a visit set, 32 per step: spans(c, ...) gives
+    // column c's (at most two) record spans.
+    auto walk_cols = [&](uint32_t ncol, auto spans) {
       for (uint32_t cb = 0; cb < ncol; cb += 32) {
         const uint32_t c = cb + lane;
         uint32_t b1 = 0, e1 = 0, b2 = 0, e2 = 0;
-        if (c < ncol) {
-          const int64_t i = i0 + (int64_t)(c / nj), j = j0 + (int64_t)(c % nj);
-          const bool ring =
-              L == 1 || (i == ic - L) || (i == ic + L) || (j == jc - L) || (j == jc + L);
-          shell_column_spans<FLAVOR>(t, i, j, ring, kc, L, (uint64_t)nzm, &b1, &e1, &b2, &e2);
-        }
+        if (c < ncol) spans(c, &b1, &e1, &b2, &e2);
         const uint32_t l1 = e1 - b1;
         const uint32_t len = l1 + (e2 - b2);
         const uint32_t incl = warp_incl_scan(len);
@@ -259,6 +257,17 @@ __global__ void __launch_bounds__(kKThreads) knn_warp_kernel(const Tables t,
           }
         }
       }
+    };
+    for (int64_t L = 1;; ++L) {
+      const int64_t i0 = imax64(0, ic - L), i1 = imin64(nx - 1, ic + L);
+      const int64_t j0 = imax64(0, jc - L), j1 = imin64(ny - 1, jc + L);
+      const uint32_t nj = (uint32_t)(j1 - j0 + 1);
+      const uint32_t ncol = (uint32_t)(i1 - i0 + 1) * nj;
+      walk_cols(ncol, [&](uint32_t c, uint32_t* b1, uint32_t* e1, uint32_t* b2, uint32_t* e2) {
+        const int64_t i = i0 + (int64_t)(c / nj), j = j0 + (int64_t)(c % nj);
+        const bool ring = L == 1 || (i == ic - L) || (i == ic + L) || (j == jc - L) || (j == jc + L);
+        shell_column_spans<FLAVOR>(t, i, j, ring, kc, L, (uint64_t)nzm, b1, e1, b2, e2);
+      });
       // distance from c to the nearest unvisited voxel face
       const bool all = i0 == 0 && i1 == nx - 1 && j0 == 0 && j1 == ny - 1 &&
                        imax64(0, kc - L) == 0 && imin64(nzm, kc + L) == nzm;
@@ -275,6 +284,34 @@ __global__ void __launch_bounds__(kKThreads) knn_warp_kernel(const Tables t,
         }
         const double dm = dmin - eps;
         if (dm > 0.0 && ld[k - 1] < dm * dm) break;
+        // Ball completion instead of the next whole shell: every voxel of
+        // clamped_range(c +- R) outside the visited block, R = the current
+        // k-th distance rounded up (a point that beats the final k-th has
+        // fp64 d² <= kd, true distance <= sqrt(kd)(1 + 2^-51) <= R, and
+        // axis_index is monotone): exact, and the walk ends here.
+        if (kBallWarp) {
+          const double R = sqrt(ld[k - 1]) * (1.0 + 1e-12) + eps;
+          Range B;
+          if (clamped_range(g, cx, cy, cz, R, &B, 0)) {
+            const uint32_t bnj = (uint32_t)(B.j1 - B.j0 + 1);
+            const uint32_t bnc = (uint32_t)(B.i1 - B.i0 + 1) * bnj;
+            walk_cols(bnc, [&](uint32_t c, uint32_t* b1, uint32_t* e1, uint32_t* b2, uint32_t* e2) {
+              const int64_t i = (int64_t)B.i0 + (int64_t)(c / bnj), j = (int64_t)B.j0 + (int64_t)(c % bnj);
+              const bool inblock = i >= ic - L && i <= ic + L && j >= jc - L && j <= jc + L;
+              int64_t lo1 = (int64_t)B.k0, hi1 = (int64_t)B.k1, lo2 = 1, hi2 = 0;
+              if (inblock) {  // only the parts below and above the block
+                hi1 = imin64(hi1, kc - L - 1);
+                lo2 = imax64((int64_t)B.k0, kc + L + 1);
+                hi2 = (int64_t)B.k1;
+              }
+              if (lo1 <= hi1)
+                column_span<FLAVOR>(t, (uint64_t)i, (uint64_t)j, (uint64_t)lo1, (uint64_t)hi1, b1, e1);
+              if (lo2 <= hi2)
+                column_span<FLAVOR>(t, (uint64_t)i, (uint64_t)j, (uint64_t)lo2, (uint64_t)hi2, b2, e2);
+            });
+          }
+          break;
+        }
       }
     }
     if (GLIST) {
@@ -512,8 +549,11 @@ struct KnnHeap {
   }
 };
 
-template <int FLAVOR, int K>
-__global__ void __launch_bounds__(kTThreads) knn_thread_kernel(
+// BALL: ball completion after the first full block (k > 16); otherwise
+// whole shells with the stop test after each (fewer registers: measured
+// faster at k = 8 / 16, 8.6 / 12.5 ms against 11.2 / 16.2 ms on config 3).
+template <int FLAVOR, int K, bool BALL = (K > 16)>
+__global__ void __launch_bounds__(kTThreads, (K > 16 ? 4 : 6)) knn_thread_kernel(
     const Tables t, const double* __restrict__ q, uint64_t nq, uint32_t k,
     const uint32_t* __restrict__ list, const uint32_t* __restrict__ n_list, int lmax,
     uint32_t* __restrict__ idx_out, double* __restrict__ d2_out, uint32_t* __restrict__ redo,
@@ -545,26 +585,53 @@ __global__ void __launch_bounds__(kTThreads) knn_thread_kernel(
                                   fabs(g.oz) + g.sx + g.sy + g.sz);
       double kd = kInf;       // the heap's root (k-th best) once full
       uint32_t kid = 0xffffffffu;
-      auto visit = [&](uint32_t b, uint32_t e) {
-        for (uint32_t p = b; p < e; ++p) {
-          const PointRec pr = load_rec(rec + p);
-          const double d2 = sqdist(pr.x, pr.y, pr.z, cx, cy, cz);
-          if (cnt < k) {
-            h.push(cnt, d2, pr.id);
-            if (++cnt == k) kd = h.dd(0), kid = h.ii(0);
-          } else if (pair_less(d2, pr.id, kd, kid)) {
-            h.replace_top(k, d2, pr.id);
-            kd = h.dd(0), kid = h.ii(0);
-          }
+      auto offer = [&](double d2, uint32_t id) {
+        if (cnt < k) {
+          h.push(cnt, d2, id);
+          if (++cnt == k) kd = h.dd(0), kid = h.ii(0);
+        } else if (pair_less(d2, id, kd, kid)) {
+          h.replace_top(k, d2, id);
+          kd = h.dd(0), kid = h.ii(0);
         }
       };
-      for (int64_t L = 1; L <= lmax; ++L) {
+      // records in groups of four: all four loads in flight before the
+      // first distance is needed (the walk is load-latency bound otherwise).
+      // (Screening candidates on the fp32 records first — filter.cuh — and
+      // loading the fp64 record only for possible improvements measured
+      // slower: config 3 k = 8 9.6 -> 13.2 ms.)
+      auto visit = [&](uint32_t b, uint32_t e, int64_t, int64_t) {
+        uint32_t p = b;
+        for (; p + 4 <= e; p += 4) {
+          PointRec pr[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) pr[u] = load_rec(rec + p + u);
+          double d2[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) d2[u] = sqdist(pr[u].x, pr[u].y, pr[u].z, cx, cy, cz);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) offer(d2[u], pr[u].id);
+        }
+        for (; p < e; ++p) {
+          const PointRec pr = load_rec(rec + p);
+          offer(sqdist(pr.x, pr.y, pr.z, cx, cy, cz), pr.id);
+        }
+      };
+      // (1) the 3 x 3 x 3 block, own column first; (2) further Chebyshev
+      // shells only while fewer than k points are known; (3) the shell
+      // walk's stop test, and where it fails, ball completion: every voxel
+      // of clamped_range(c +- R) outside the visited block, R = the current
+      // k-th distance rounded up. A point that beats the final k-th has fp64
+      // d² <= kd, so its true distance is <= sqrt(kd)(1 + 2^-51) <= R and it
+      // lies in that voxel range (axis_index is monotone): exact, and a
+      // centre visits only the voxels its k-th neighbour ball touches
+      // instead of whole shells.
+      int64_t L = 1;
+      bool all = false;
+      for (;; ++L) {
         const int64_t i0 = imax64(0, ic - L), i1 = imin64(nx - 1, ic + L);
         const int64_t j0 = imax64(0, jc - L), j1 = imin64(ny - 1, jc + L);
         const int64_t nj = j1 - j0 + 1;
         const int64_t ncol = (i1 - i0 + 1) * nj;
-        // L = 1: the centre's own column first (a tight k-th bound early
-        // means fewer heap updates), then the other eight
         for (int64_t c = -1; c < ncol; ++c) {
           int64_t i, j;
           if (c < 0) {
@@ -577,31 +644,76 @@ __global__ void __launch_bounds__(kTThreads) knn_thread_kernel(
           const bool ring = L == 1 || i == ic - L || i == ic + L || j == jc - L || j == jc + L;
           uint32_t b1, e1, b2, e2;
           shell_column_spans<FLAVOR>(t, i, j, ring, kc, L, (uint64_t)nzm, &b1, &e1, &b2, &e2);
-          visit(b1, e1);
-          visit(b2, e2);
+          visit(b1, e1, i, j);
+          visit(b2, e2, i, j);
         }
-        const bool all = i0 == 0 && i1 == nx - 1 && j0 == 0 && j1 == ny - 1 &&
-                         imax64(0, kc - L) == 0 && imin64(nzm, kc + L) == nzm;
-        if (all) {
-          done = true;
-          break;
-        }
+        all = i0 == 0 && i1 == nx - 1 && j0 == 0 && j1 == ny - 1 && imax64(0, kc - L) == 0 &&
+              imin64(nzm, kc + L) == nzm;
+        if (all) break;
         if (cnt == k) {
+          if (BALL) break;  // the stop test and ball completion follow
+          // without ball completion: the shell walk's stop test, every shell
+          const int64_t si0 = imax64(0, ic - L), si1 = imin64(nx - 1, ic + L);
+          const int64_t sj0 = imax64(0, jc - L), sj1 = imin64(ny - 1, jc + L);
           double dmin = 1e300;
-          if (i0 > 0) dmin = fmin(dmin, cx - (g.ox + (double)i0 * g.sx));
-          if (i1 < nx - 1) dmin = fmin(dmin, (g.ox + (double)(i1 + 1) * g.sx) - cx);
-          if (j0 > 0) dmin = fmin(dmin, cy - (g.oy + (double)j0 * g.sy));
-          if (j1 < ny - 1) dmin = fmin(dmin, (g.oy + (double)(j1 + 1) * g.sy) - cy);
+          if (si0 > 0) dmin = fmin(dmin, cx - (g.ox + (double)si0 * g.sx));
+          if (si1 < nx - 1) dmin = fmin(dmin, (g.ox + (double)(si1 + 1) * g.sx) - cx);
+          if (sj0 > 0) dmin = fmin(dmin, cy - (g.oy + (double)sj0 * g.sy));
+          if (sj1 < ny - 1) dmin = fmin(dmin, (g.oy + (double)(sj1 + 1) * g.sy) - cy);
           if (g.mode3d) {
             if (kc - L > 0) dmin = fmin(dmin, cz - (g.oz + (double)(kc - L) * g.sz));
             if (kc + L < nzm) dmin = fmin(dmin, (g.oz + (double)(kc + L + 1) * g.sz) - cz);
           }
           const double dm = dmin - eps;
           if (dm > 0.0 && kd < dm * dm) {
-            done = true;
+            all = true;
             break;
           }
         }
+        if (L >= lmax) break;
+      }
+      if (BALL && cnt == k && !all) {
+        const int64_t i0 = imax64(0, ic - L), i1 = imin64(nx - 1, ic + L);
+        const int64_t j0 = imax64(0, jc - L), j1 = imin64(ny - 1, jc + L);
+        double dmin = 1e300;
+        if (i0 > 0) dmin = fmin(dmin, cx - (g.ox + (double)i0 * g.sx));
+        if (i1 < nx - 1) dmin = fmin(dmin, (g.ox + (double)(i1 + 1) * g.sx) - cx);
+        if (j0 > 0) dmin = fmin(dmin, cy - (g.oy + (double)j0 * g.sy));
+        if (j1 < ny - 1) dmin = fmin(dmin, (g.oy + (double)(j1 + 1) * g.sy) - cy);
+        if (g.mode3d) {
+          if (kc - L > 0) dmin = fmin(dmin, cz - (g.oz + (double)(kc - L) * g.sz));
+          if (kc + L < nzm) dmin = fmin(dmin, (g.oz + (double)(kc + L + 1) * g.sz) - cz);
+        }
+        const double dm = dmin - eps;
+        if (dm > 0.0 && kd < dm * dm) all = true;  // nothing unvisited can beat the k-th
+      }
+      if (BALL && cnt == k && !all) {
+        const double R = sqrt(kd) * (1.0 + 1e-12) + eps;
+        Range B;
+        if (clamped_range(g, cx, cy, cz, R, &B, 0)) {
+          for (int64_t i = (int64_t)B.i0; i <= (int64_t)B.i1; ++i)
+            for (int64_t j = (int64_t)B.j0; j <= (int64_t)B.j1; ++j) {
+              const bool inblock = i >= ic - L && i <= ic + L && j >= jc - L && j <= jc + L;
+              int64_t lo1 = (int64_t)B.k0, hi1 = (int64_t)B.k1, lo2 = 1, hi2 = 0;
+              if (inblock) {  // only the parts below and above the block
+                hi1 = imin64(hi1, kc - L - 1);
+                lo2 = imax64((int64_t)B.k0, kc + L + 1);
+                hi2 = (int64_t)B.k1;
+              }
+              uint32_t b, e;
+              if (lo1 <= hi1) {
+                column_span<FLAVOR>(t, (uint64_t)i, (uint64_t)j, (uint64_t)lo1, (uint64_t)hi1, &b, &e);
+                visit(b, e, i, j);
+              }
+              if (lo2 <= hi2) {
+                column_span<FLAVOR>(t, (uint64_t)i, (uint64_t)j, (uint64_t)lo2, (uint64_t)hi2, &b, &e);
+                visit(b, e, i, j);
+              }
+            }
+        }
+        done = true;
+      } else if (all) {
+        done = true;  // fewer than k points in the whole grid, or the stop test holds
       }
       if (done) {
         // heapsort in place: ascending (d², handle)
@@ -999,7 +1111,7 @@ cm_status knn_dev(const cm_index* ix, const double* q, uint64_t nq, uint32_t k,
     // per-thread kNN: pass 1 up to shell LFIRST, pass 2 (all shells) on the
     // centres pass 1 could not finish
     static const int lfirst_env = std::getenv("CMGPU_KNN_LFIRST") ? std::atoi(std::getenv("CMGPU_KNN_LFIRST")) : 0;
-    const int lfirst = lfirst_env > 0 ? lfirst_env : (k <= 16 ? 1 : 2);
+    const int lfirst = lfirst_env > 0 ? lfirst_env : 1;
     uint32_t* redo1 = nullptr;
     uint32_t* redo2 = nullptr;
     uint32_t* nr = nullptr;  // [0] pass-1 redo count, [1] pass-2 (must stay 0)
