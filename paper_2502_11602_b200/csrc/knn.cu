@@ -76,6 +76,12 @@ __device__ __forceinline__ void shell_column_spans(const Tables& t, int64_t i, i
   }
 }
 
+// Radius-box walk in the per-thread kernel (CMGPU_KNN_R0MULT > 0 at run
+// time): exact, measured slower than the shells on config 3 (k = 8: 10.4 ->
+// 13.4 ms at 1.3 x the expected k-th distance); compiled in only on request.
+#ifndef CM_KNN_BOX
+#define CM_KNN_BOX 0
+#endif
 #ifndef CM_KNN_BALL
 #define CM_KNN_BALL 0  // measured slower on config 3 (k = 64: 39.3 -> 47.8 ms): opt-in
 #endif
@@ -557,7 +563,7 @@ __global__ void __launch_bounds__(kTThreads, (K > 16 ? 4 : 6)) knn_thread_kernel
     const Tables t, const double* __restrict__ q, uint64_t nq, uint32_t k,
     const uint32_t* __restrict__ list, const uint32_t* __restrict__ n_list, int lmax,
     uint32_t* __restrict__ idx_out, double* __restrict__ d2_out, uint32_t* __restrict__ redo,
-    uint32_t* __restrict__ n_redo) {
+    uint32_t* __restrict__ n_redo, double r0) {
   extern __shared__ __align__(16) unsigned char hsm[];
   double* sd = reinterpret_cast<double*>(hsm);
   uint32_t* sid = reinterpret_cast<uint32_t*>(hsm + (size_t)K * kTThreads * sizeof(double));
@@ -625,6 +631,79 @@ __global__ void __launch_bounds__(kTThreads, (K > 16 ? 4 : 6)) knn_thread_kernel
       // lies in that voxel range (axis_index is monotone): exact, and a
       // centre visits only the voxels its k-th neighbour ball touches
       // instead of whole shells.
+      if (CM_KNN_BOX && r0 > 0.0) {
+        // Radius boxes: visit every voxel of clamped_range(c +- R) for R =
+        // r0 (the expected k-th distance, from the cloud's mean density),
+        // doubling R while fewer than k points are known; then ball
+        // completion at the k-th distance. The visited set is always the
+        // last box (boxes grow monotonically), so each step visits only the
+        // new box minus the old one: per column the k ranges below and
+        // above the old box, or the whole k range outside its (i, j) range.
+        Range V{};
+        bool hasV = false;
+        auto visit_new = [&](const Range& B) {
+          const int64_t bi0 = (int64_t)B.i0, bi1 = (int64_t)B.i1, bj0 = (int64_t)B.j0,
+                        bj1 = (int64_t)B.j1;
+          const int64_t nbj = bj1 - bj0 + 1, nbc = (bi1 - bi0 + 1) * nbj;
+          const bool own = ic >= bi0 && ic <= bi1 && jc >= bj0 && jc <= bj1;
+          for (int64_t c = -1; c < nbc; ++c) {
+            int64_t i, j;
+            if (c < 0) {  // the centre's own column first: a tight k-th early
+              if (!own) continue;
+              i = ic, j = jc;
+            } else {
+              i = bi0 + c / nbj, j = bj0 + c % nbj;
+              if (own && i == ic && j == jc) continue;
+            }
+            const bool inV = hasV && i >= (int64_t)V.i0 && i <= (int64_t)V.i1 &&
+                             j >= (int64_t)V.j0 && j <= (int64_t)V.j1;
+            int64_t lo1 = (int64_t)B.k0, hi1 = (int64_t)B.k1, lo2 = 1, hi2 = 0;
+            if (inV) {
+              hi1 = imin64(hi1, (int64_t)V.k0 - 1);
+              lo2 = imax64((int64_t)B.k0, (int64_t)V.k1 + 1);
+              hi2 = (int64_t)B.k1;
+            }
+            uint32_t b, e;
+            if (lo1 <= hi1) {
+              column_span<FLAVOR>(t, (uint64_t)i, (uint64_t)j, (uint64_t)lo1, (uint64_t)hi1, &b, &e);
+              visit(b, e, i, j);
+            }
+            if (lo2 <= hi2) {
+              column_span<FLAVOR>(t, (uint64_t)i, (uint64_t)j, (uint64_t)lo2, (uint64_t)hi2, &b, &e);
+              visit(b, e, i, j);
+            }
+          }
+        };
+        auto merge_box = [&](const Range& B) {
+          if (!hasV) {
+            V = B;
+            hasV = true;
+            return;
+          }
+          V.i0 = min(V.i0, B.i0), V.i1 = max(V.i1, B.i1);
+          V.j0 = min(V.j0, B.j0), V.j1 = max(V.j1, B.j1);
+          V.k0 = min(V.k0, B.k0), V.k1 = max(V.k1, B.k1);
+        };
+        double R = r0;
+        for (;;) {
+          Range B;
+          if (clamped_range(g, cx, cy, cz, R, &B, 0)) {
+            visit_new(B);
+            merge_box(B);
+          }
+          if (cnt >= k) break;
+          if (hasV && V.i0 == 0 && V.i1 == (uint64_t)(nx - 1) && V.j0 == 0 &&
+              V.j1 == (uint64_t)(ny - 1) && V.k0 == 0 && V.k1 == (uint64_t)nzm)
+            break;  // the whole grid: fewer than k points
+          R *= 2.0;
+        }
+        if (cnt == k) {
+          Range B;
+          const double Rk = sqrt(kd) * (1.0 + 1e-12) + eps;
+          if (clamped_range(g, cx, cy, cz, Rk, &B, 0)) visit_new(B);
+        }
+        done = true;
+      } else {
       int64_t L = 1;
       bool all = false;
       for (;; ++L) {
@@ -714,6 +793,7 @@ __global__ void __launch_bounds__(kTThreads, (K > 16 ? 4 : 6)) knn_thread_kernel
         done = true;
       } else if (all) {
         done = true;  // fewer than k points in the whole grid, or the stop test holds
+      }
       }
       if (done) {
         // heapsort in place: ascending (d², handle)
@@ -1112,6 +1192,18 @@ cm_status knn_dev(const cm_index* ix, const double* q, uint64_t nq, uint32_t k,
     // centres pass 1 could not finish
     static const int lfirst_env = std::getenv("CMGPU_KNN_LFIRST") ? std::atoi(std::getenv("CMGPU_KNN_LFIRST")) : 0;
     const int lfirst = lfirst_env > 0 ? lfirst_env : 1;
+    // first box radius: the k-th neighbour distance of a surface sampled at
+    // the cloud's mean xy density (ALS), times a margin; 0 = Chebyshev shells
+    static const double r0_mult =
+        std::getenv("CMGPU_KNN_R0MULT") ? std::atof(std::getenv("CMGPU_KNN_R0MULT")) : 0.0;
+    double r0 = 0.0;
+    {
+      const DevGrid& gg = ix->g;
+      const double area = (gg.bx1 - gg.bx0) * (gg.by1 - gg.by0);
+      if (r0_mult > 0.0)
+        r0 = area > 0.0 ? r0_mult * std::sqrt((double)k / (3.141592653589793 * (double)ix->n / area))
+                        : std::max(gg.sx, std::max(gg.sy, gg.sz));
+    }
     uint32_t* redo1 = nullptr;
     uint32_t* redo2 = nullptr;
     uint32_t* nr = nullptr;  // [0] pass-1 redo count, [1] pass-2 (must stay 0)
@@ -1128,7 +1220,7 @@ cm_status knn_dev(const cm_index* ix, const double* q, uint64_t nq, uint32_t k,
       per_sm = std::max(per_sm, 1);
       const uint64_t need = (nq + kTThreads - 1) / kTThreads;
       const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(need, (uint64_t)sm_count() * per_sm));
-      kern<<<grid, kTThreads, smem, st>>>(t, q, nq, k, list, nl, lmax, idx, d2, rd, nrd);
+      kern<<<grid, kTThreads, smem, st>>>(t, q, nq, k, list, nl, lmax, idx, d2, rd, nrd, r0);
       ::cmg::note_launch();
       CM_CUDA_TRY(cudaGetLastError());
       return CM_OK;
