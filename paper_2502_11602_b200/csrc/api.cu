@@ -493,7 +493,7 @@ __global__ void export_kernel(const PointRec* __restrict__ rec, uint64_t n, DevG
 __global__ void corrupt_kernel(PointRec* rec, FRec* frec, uint64_t at) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     rec[at].x = __longlong_as_double(0x7ff8000000000000ll);
-    frec[at].x = __int_as_float(0x7fc00000);
+    if (frec) frec[at].x = __int_as_float(0x7fc00000);
   }
 }
 __global__ void add_offset_kernel(uint64_t* v, uint64_t n, uint64_t off) {

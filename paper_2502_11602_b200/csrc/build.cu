@@ -98,20 +98,22 @@ __global__ void gather_kernel(const double* __restrict__ xyz, const K* __restric
     b.x = xyz[3 * (uint64_t)h + 2];
     const K col = key / nz;
     const uint32_t k = (uint32_t)(key - col * nz);
-    const K i = col / ny;
-    const K j = col - i * ny;
     uint2 t;
     t.x = h;
     t.y = k;
     b.y = *reinterpret_cast<double*>(&t);
     reinterpret_cast<double2*>(rec + s)[0] = a;
     reinterpret_cast<double2*>(rec + s)[1] = b;
-    FRec f;
-    f.x = __double2float_rn(__dsub_rn(a.x, col_corner(g.ox, (uint64_t)i, g.sx)));
-    f.y = __double2float_rn(__dsub_rn(a.y, col_corner(g.oy, (uint64_t)j, g.sy)));
-    f.z = __double2float_rn(__dsub_rn(b.x, g.oz));
-    f.k = k;
-    frec[s] = f;
+    if (CM_FILTER) {
+      const K i = col / ny;
+      const K j = col - i * ny;
+      FRec f;
+      f.x = __double2float_rn(__dsub_rn(a.x, col_corner(g.ox, (uint64_t)i, g.sx)));
+      f.y = __double2float_rn(__dsub_rn(a.y, col_corner(g.oy, (uint64_t)j, g.sy)));
+      f.z = __double2float_rn(__dsub_rn(b.x, g.oz));
+      f.k = k;
+      frec[s] = f;
+    }
     ids[s] = h;
     flags[s] = (s == 0 || keys[s - 1] != keys[s]) ? 1u : 0u;
   }
@@ -272,7 +274,7 @@ cm_status build_typed(const double* xyz, uint64_t n, cudaStream_t st, cm_index* 
   dev_free(scratch, st);
 
   CM_CUDA_TRY(dev_alloc_t(&ix->rec, n, st));
-  CM_CUDA_TRY(dev_alloc_t(&ix->frec, n, st));
+  if (CM_FILTER) CM_CUDA_TRY(dev_alloc_t(&ix->frec, n, st));
   CM_CUDA_TRY(dev_alloc_t(&ix->ids, n, st));
   uint32_t* flags = nullptr;
   uint32_t* pos = nullptr;

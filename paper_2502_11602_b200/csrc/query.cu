@@ -37,9 +37,6 @@ namespace {
 
 using namespace ::cmg::tw;  // tile_walk.cuh
 
-#ifndef CM_FILTER
-#define CM_FILTER 0  // filtered predicates (filter.cuh) in the compact tile walk: measured slower at r = 1 (collect 9.9 -> 11.3 ms)
-#endif
 #ifndef CM_PARK
 #define CM_PARK 1    // long-row centres parked in shared memory across the row stores
 #endif
@@ -1307,6 +1304,9 @@ __device__ __forceinline__ void warp_sort_row_blocked(uint32_t* row, uint32_t n,
 #define CM_GATHER_ROW 96
 #endif
 constexpr int kGatherRow = CM_GATHER_ROW;
+#ifndef CM_GATHER_NET16
+#define CM_GATHER_NET16 0  // 16-wide network for short groups: one more network in the i-cache (gather 5.99 -> 6.08 ms)
+#endif
 static_assert(kGatherRow > 64 && kGatherRow <= 96, "gather staging: run 1 of 64 + run 2 <= 32");
 constexpr int kGatherWarpWords = kGatherRow * 33 + 96;  // rows, sfin[32], srel[32] (u64)
 //
@@ -1393,8 +1393,12 @@ __global__ void CM_GATHER_BOUNDS gather_rows_kernel(const uint32_t* temp,
     const uint32_t r1 = staged < 64u ? staged : 64u;
     const uint32_t m1 = warp_max_u32(r1);
     if (m1 > 32) lane_sort_row<64>(srow, lane, r1);
+#if CM_GATHER_NET16
     else if (m1 > 16) lane_sort_row<32>(srow, lane, r1);
     else if (m1 > 1) lane_sort_row<16>(srow, lane, r1);
+#else
+    else if (m1 > 1) lane_sort_row<32>(srow, lane, r1);  // one network less in the i-cache
+#endif
     // run 2: [64, len)
     const uint32_t r2 = staged > 64u ? staged - 64u : 0u;
     const uint32_t m2 = warp_max_u32(r2);
@@ -2338,12 +2342,13 @@ cm_status radius_collect_dev(const cm_index* ix, const double* q, uint64_t nq, i
                              unsigned long long* cursor, cudaStream_t st,
                              cudaEvent_t after_collect, const double* rq, const double* qbox,
                              const MergeList* ml) {
+  // the caller reads the cursor and the merge list even for nq = 0
+  CM_CUDA_TRY(cudaMemsetAsync(cursor, 0, 16, st));
+  if (ml) CM_CUDA_TRY(cudaMemsetAsync(ml->n, 0, 4, st));
   if (nq == 0) return CM_OK;
   BigRows big;
   cm_status s = ml ? CM_OK : big.init(nq, st);
   if (s != CM_OK) return s;
-  if (ml) CM_CUDA_TRY(cudaMemsetAsync(ml->n, 0, 4, st));
-  CM_CUDA_TRY(cudaMemsetAsync(cursor, 0, 16, st));
   Out o{};
   o.counts = counts;
   o.temp = temp;
