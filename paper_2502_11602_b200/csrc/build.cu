@@ -88,14 +88,36 @@ __global__ void gather_kernel(const double* __restrict__ xyz, const K* __restric
                               PointRec* __restrict__ rec, FRec* __restrict__ frec,
                               uint32_t* __restrict__ ids, uint32_t* __restrict__ flags) {
   const K nz = (K)g.nz, ny = (K)g.ny;
-  for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < n;
-       s += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t h = perm[s];
+  // four records per thread per step, every random xyz read in flight first
+  constexpr int kG = 4;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t s0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s0 < n; s0 += kG * stride) {
+    uint32_t hh[kG];
+    double xx[kG], yy[kG], zz[kG];
+#pragma unroll
+    for (int u = 0; u < kG; ++u) {
+      const uint64_t s = s0 + u * stride;
+      hh[u] = s < n ? perm[s] : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < kG; ++u) {
+      const uint64_t s = s0 + u * stride;
+      if (s < n) {
+        xx[u] = xyz[3 * (uint64_t)hh[u]];
+        yy[u] = xyz[3 * (uint64_t)hh[u] + 1];
+        zz[u] = xyz[3 * (uint64_t)hh[u] + 2];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kG; ++u) {
+    const uint64_t s = s0 + u * stride;
+    if (s >= n) break;
+    const uint32_t h = hh[u];
     const K key = keys[s];
     double2 a, b;
-    a.x = xyz[3 * (uint64_t)h];
-    a.y = xyz[3 * (uint64_t)h + 1];
-    b.x = xyz[3 * (uint64_t)h + 2];
+    a.x = xx[u];
+    a.y = yy[u];
+    b.x = zz[u];
     const K col = key / nz;
     const uint32_t k = (uint32_t)(key - col * nz);
     uint2 t;
@@ -116,6 +138,7 @@ __global__ void gather_kernel(const double* __restrict__ xyz, const K* __restric
     }
     ids[s] = h;
     flags[s] = (s == 0 || keys[s - 1] != keys[s]) ? 1u : 0u;
+    }
   }
 }
 
@@ -269,9 +292,12 @@ cm_status build_typed(const double* xyz, uint64_t n, cudaStream_t st, cm_index* 
   keys_kernel<K><<<grid_for(n), 256, 0, st>>>(xyz, n, g, keys, perm); ::cmg::note_launch();
   cudaEventRecord(ev.e[2], st);
   ix->key_bits = bit_width(ix->V - 1);
-  ix->timing.sort_passes = (uint32_t)radix_sort_pairs<K>(keys, perm, n, ix->key_bits, scratch, st);
+  // the sorted pairs stay where the last pass left them (no copy back)
+  K* skeys = keys;
+  uint32_t* sperm = perm;
+  ix->timing.sort_passes =
+      (uint32_t)radix_sort_pairs<K>(keys, perm, n, ix->key_bits, scratch, st, &skeys, &sperm);
   cudaEventRecord(ev.e[3], st);
-  dev_free(scratch, st);
 
   CM_CUDA_TRY(dev_alloc_t(&ix->rec, n, st));
   if (CM_FILTER) CM_CUDA_TRY(dev_alloc_t(&ix->frec, n, st));
@@ -282,7 +308,7 @@ cm_status build_typed(const double* xyz, uint64_t n, cudaStream_t st, cm_index* 
   CM_CUDA_TRY(dev_alloc_t(&flags, n, st));
   CM_CUDA_TRY(dev_alloc_t(&pos, n + 1, st));
   CM_CUDA_TRY(dev_alloc_t(&part, scan_part_elems(n), st));
-  gather_kernel<K><<<grid_for(n), 256, 0, st>>>(xyz, keys, perm, n, g, ix->rec, ix->frec, ix->ids, flags); ::cmg::note_launch();
+  gather_kernel<K><<<grid_for(n), 256, 0, st>>>(xyz, skeys, sperm, n, g, ix->rec, ix->frec, ix->ids, flags); ::cmg::note_launch();
   cudaEventRecord(ev.e[4], st);
   exclusive_scan<uint32_t, uint32_t>(flags, n, pos, part, 1, st);
   uint32_t U32 = 0;
@@ -300,12 +326,13 @@ cm_status build_typed(const double* xyz, uint64_t n, cudaStream_t st, cm_index* 
   const uint32_t n32 = (uint32_t)n;
   CM_CUDA_TRY(cudaMemcpyAsync(ix->ustart + U, &n32, 4, cudaMemcpyHostToDevice, st));
   const size_t hsmem = g.nz <= kSliceSmem ? g.nz * 4 : 0;
-  unique_kernel<K><<<grid_for(n), 256, hsmem, st>>>(keys, flags, pos, n, g.nz, ix->ukey, ix->ustart,
+  unique_kernel<K><<<grid_for(n), 256, hsmem, st>>>(skeys, flags, pos, n, g.nz, ix->ukey, ix->ustart,
                                                  ix->uk_k, slice_ne); ::cmg::note_launch();
   ix->slice_ne.assign(g.nz, 0);
   CM_CUDA_TRY(cudaMemcpyAsync(ix->slice_ne.data(), slice_ne, g.nz * 8, cudaMemcpyDeviceToHost, st));
   dev_free(keys, st);
   dev_free(perm, st);
+  dev_free(scratch, st);
 
   if (flavor == CM_DENSE) {
     CM_CUDA_TRY(dev_alloc_t(&ix->dense_off, ix->V + 1, st));

@@ -514,9 +514,13 @@ inline size_t radix_scratch_bytes(uint64_t n) {
 // Sorts (keys, vals) by the low `bits` bits of the keys, stably. n < 2^32.
 // Result ends in (keys, vals) (the function ping-pongs through scratch).
 // Returns the number of passes.
+// kres / vres (optional): receive where the sorted pairs are (keys / vals or
+// the scratch copy) instead of copying an odd pass count's result back.
 template <typename K>
 inline int radix_sort_pairs(K* keys, uint32_t* vals, uint64_t n, int bits, void* scratch,
-                            cudaStream_t st) {
+                            cudaStream_t st, K** kres = nullptr, uint32_t** vres = nullptr) {
+  if (kres) *kres = keys;
+  if (vres) *vres = vals;
   if (n <= 1 || bits <= 0) return 0;
   // the fewest passes digits of 8..9 bits allow, with the narrowest such
   // digit (10-bit digits double the downsweep's per-warp counters and cost
@@ -605,7 +609,10 @@ inline int radix_sort_pairs(K* keys, uint32_t* vals, uint64_t n, int bits, void*
     K* tk = ka; ka = kb; kb = tk;
     uint32_t* tv = va; va = vb; vb = tv;
   }
-  if (ka != keys) {
+  if (kres && vres) {
+    *kres = ka;
+    *vres = va;
+  } else if (ka != keys) {
     cudaMemcpyAsync(keys, ka, n * sizeof(K), cudaMemcpyDeviceToDevice, st);
     cudaMemcpyAsync(vals, va, n * 4, cudaMemcpyDeviceToDevice, st);
   }
