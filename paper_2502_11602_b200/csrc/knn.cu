@@ -79,6 +79,12 @@ __device__ __forceinline__ void shell_column_spans(const Tables& t, int64_t i, i
 // Radius-box walk in the per-thread kernel (CMGPU_KNN_R0MULT > 0 at run
 // time): exact, measured slower than the shells on config 3 (k = 8: 10.4 ->
 // 13.4 ms at 1.3 x the expected k-th distance); compiled in only on request.
+#ifndef CM_KNN_TBATCH
+#define CM_KNN_TBATCH 2  // records in flight per thread (per-thread kNN walk)
+#endif
+#ifndef CM_KNN_TMINB
+#define CM_KNN_TMINB 10  // blocks per SM the per-thread kernel is compiled for (k <= 16)
+#endif
 #ifndef CM_KNN_BOX
 #define CM_KNN_BOX 0
 #endif
@@ -559,7 +565,7 @@ struct KnnHeap {
 // whole shells with the stop test after each (fewer registers: measured
 // faster at k = 8 / 16, 8.6 / 12.5 ms against 11.2 / 16.2 ms on config 3).
 template <int FLAVOR, int K, bool BALL = (K > 16)>
-__global__ void __launch_bounds__(kTThreads, (K > 16 ? 4 : 6)) knn_thread_kernel(
+__global__ void __launch_bounds__(kTThreads, (K > 16 ? 4 : CM_KNN_TMINB)) knn_thread_kernel(
     const Tables t, const double* __restrict__ q, uint64_t nq, uint32_t k,
     const uint32_t* __restrict__ list, const uint32_t* __restrict__ n_list, int lmax,
     uint32_t* __restrict__ idx_out, double* __restrict__ d2_out, uint32_t* __restrict__ redo,
@@ -607,15 +613,16 @@ __global__ void __launch_bounds__(kTThreads, (K > 16 ? 4 : 6)) knn_thread_kernel
       // slower: config 3 k = 8 9.6 -> 13.2 ms.)
       auto visit = [&](uint32_t b, uint32_t e, int64_t, int64_t) {
         uint32_t p = b;
-        for (; p + 4 <= e; p += 4) {
-          PointRec pr[4];
+        constexpr int B = CM_KNN_TBATCH;
+        for (; p + B <= e; p += B) {
+          PointRec pr[B];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) pr[u] = load_rec(rec + p + u);
-          double d2[4];
+          for (int u = 0; u < B; ++u) pr[u] = load_rec(rec + p + u);
+          double d2[B];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) d2[u] = sqdist(pr[u].x, pr[u].y, pr[u].z, cx, cy, cz);
+          for (int u = 0; u < B; ++u) d2[u] = sqdist(pr[u].x, pr[u].y, pr[u].z, cx, cy, cz);
 #pragma unroll
-          for (int u = 0; u < 4; ++u) offer(d2[u], pr[u].id);
+          for (int u = 0; u < B; ++u) offer(d2[u], pr[u].id);
         }
         for (; p < e; ++p) {
           const PointRec pr = load_rec(rec + p);
