@@ -165,8 +165,16 @@ def lib():
         "cm_slab_radius_search": ([p, p, u64, i32, dbl, p, ctypes.POINTER(p)], i32),
         "cm_slab_radius_digest": ([p, p, u64, i32, dbl, p, p, p], i32),
     }
+    # CMGPU_ALLOW_MISSING=1: bind what an older library build exports (A/B
+    # measurements against earlier versions); the product binds everything
+    lenient = bool(os.environ.get("CMGPU_ALLOW_MISSING"))
     for name, (args, res) in sig.items():
-        fn = getattr(L, name)
+        try:
+            fn = getattr(L, name)
+        except AttributeError:
+            if lenient:
+                continue
+            raise
         fn.argtypes, fn.restype = args, res
     _LIB = L
     return L

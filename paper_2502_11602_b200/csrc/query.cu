@@ -25,6 +25,7 @@
 // rows into a scratch arena at atomically allocated offsets; a gather copies
 // them into CSR order after the row_ptr scan).
 #include <algorithm>
+#include <type_traits>
 #include <cstdlib>
 
 #include "index.cuh"
@@ -37,8 +38,16 @@ namespace {
 
 using namespace ::cmg::tw;  // tile_walk.cuh
 
-#ifndef CM_PARK
-#define CM_PARK 1    // long-row centres parked in shared memory across the row stores
+#ifndef CM_FILL_MINB
+// blocks per SM the FILL walk is compiled for: 4 gives it 128 registers and
+// no spills (wide FILL at r = 2.5: 41 -> 34 ms per launch; 5 spilled)
+#define CM_FILL_MINB 4
+#endif
+#ifndef CM_CUBE_MINB
+#define CM_CUBE_MINB CM_QTILE_MINB  // blocks per SM for the cube kernel's other passes
+#endif
+#ifndef CM_CUBE_GROUP
+#define CM_CUBE_GROUP 4
 #endif
 constexpr int kQThreads = 128;
 constexpr int kQWarps = kQThreads / 32;
@@ -366,6 +375,14 @@ __device__ __forceinline__ void warp_sort_row_out(const uint32_t* srow, int l, u
     const uint32_t e = r * 32 + lane;
     if (e < len) dst[e] = v[r];
   }
+}
+
+// A read-only global load the compiler cannot merge with an earlier one (so
+// values can be re-read instead of kept live in registers).
+__device__ __forceinline__ double ldg_opaque(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
 }
 
 // Predicated 16-bit shared store (no branch around it).
@@ -788,8 +805,15 @@ __device__ __forceinline__ void wide_tile(const Tables& t, const Range& R, bool 
 }
 
 // Query-tile kernel (see the file comment).
-template <int FLAVOR, int MODE, int CUBE>
-__global__ void __launch_bounds__(kQThreads, CM_QTILE_MINB) radius_tile_kernel(
+// XQ: explicit per-centre queries (a radius per centre, kNN brackets, or a
+// kernel box per centre, cm_kernel_search). The common batch (one radius,
+// centre +- r) is compiled without them: the extra live radius and box
+// pointer cost the FILL walk its register budget (spills: wide FILL 34 ->
+// 41 ms per launch at r = 2.5).
+template <int FLAVOR, int MODE, int CUBE, bool XQ = false>
+__global__ void __launch_bounds__(kQThreads, MODE == MODE_FILL ? CM_FILL_MINB
+                                             : CUBE == 1 ? CM_CUBE_MINB : CM_QTILE_MINB)
+    radius_tile_kernel(
     const Tables t, const double* __restrict__ q, uint64_t nq, double r,
     const uint32_t* __restrict__ perm, const Out o) {
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -828,9 +852,9 @@ __global__ void __launch_bounds__(kQThreads, CM_QTILE_MINB) radius_tile_kernel(
       }
     }
     // the centre's own radius (kNN radius brackets), else the batch's
-    const double rl = (o.rq && active) ? __ldg(o.rq + qi) : r;
+    const double rl = (XQ && o.rq && active) ? __ldg(o.rq + qi) : r;
     // explicit kernel boxes (cm_kernel_search: Aabb boxes, bounded cylinders)
-    const double* qb = (o.qbox && active) ? o.qbox + 6 * (uint64_t)qi : nullptr;
+    const double* qb = (XQ && o.qbox && active) ? o.qbox + 6 * (uint64_t)qi : nullptr;
     Range R{};
     const bool ok = active && clamped_range(t.g, cx, cy, cz, rl, &R, CUBE, qb);
     const uint32_t okmask = __ballot_sync(0xffffffffu, ok);
@@ -1028,12 +1052,16 @@ __global__ void __launch_bounds__(kQThreads, CM_QTILE_MINB) radius_tile_kernel(
       // chunks (k-sorted) outside every lane's z window are skipped whole
       const bool want = need & (sr[len - 1].meta >= kk0) & (sr[0].meta <= kk0 + kspan);
       uint32_t u = __any_sync(0xffffffffu, want) ? 0u : len;
-      for (; u + 8 <= len; u += 8) {
-        SRec v[8];
+      // records per group, all loaded before the first test: 8, or 4 for the
+      // cube, whose six live bounds otherwise push ptxas into keeping the
+      // comparison results in a general register (collect 15.8 -> 18.2 ms)
+      constexpr int G = CUBE == 1 ? CM_CUBE_GROUP : 8;
+      for (; u + G <= len; u += G) {
+        SRec v[G];
 #pragma unroll
-        for (int w = 0; w < 8; ++w) v[w] = sr[u + w];
+        for (int w = 0; w < G; ++w) v[w] = sr[u + w];
 #pragma unroll
-        for (int w = 0; w < 8; ++w) {
+        for (int w = 0; w < G; ++w) {
           const bool in = need & (v[w].meta - kk0 <= kspan);
           const bool hit = in & pred<CUBE>(P, v[w].x, v[w].y, v[w].z);
           if (MODE == MODE_DIGEST && hit) dig += mix64(v[w].id);
@@ -1090,9 +1118,19 @@ __global__ void __launch_bounds__(kQThreads, CM_QTILE_MINB) radius_tile_kernel(
       const bool longrow = cnt > (uint32_t)kLaneRowCap;
       uint32_t* spark = reinterpret_cast<uint32_t*>(stg) + 32;
       double* sc = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(stg) + 256);
-      if (CM_PARK && __any_sync(0xffffffffu, active && longrow)) {
+      if (__any_sync(0xffffffffu, active && longrow)) {
+        // the centre and its radius are loaded again here (opaque loads)
+        // rather than kept in registers through the walk, where they are
+        // dead for the cube: the walk's register pressure decides whether
+        // ptxas keeps the eight records' comparison results in predicates
+        double rx = 0.0, ry = 0.0, rz = 0.0, rr2 = r;
+        if (active) {
+          const double* src = q == nullptr ? &rec[s].x : q + 3 * (uint64_t)qi;
+          rx = ldg_opaque(src), ry = ldg_opaque(src + 1), rz = ldg_opaque(src + 2);
+          if (XQ && o.rq) rr2 = ldg_opaque(o.rq + qi);
+        }
         spark[lane] = qi;
-        sc[lane] = cx, sc[32 + lane] = cy, sc[64 + lane] = cz, sc[96 + lane] = rl;
+        sc[lane] = rx, sc[32 + lane] = ry, sc[64 + lane] = rz, sc[96 + lane] = rr2;
       }
       const uint32_t mine = (active && !longrow) ? cnt : 0u;
       uint64_t dst;
@@ -1186,8 +1224,8 @@ __global__ void __launch_bounds__(kQThreads, CM_QTILE_MINB) radius_tile_kernel(
       // single_query reuses the whole warp region: take every parked centre
       // into registers first (lane l holds centre l)
       uint32_t pq = qi;
-      double px = cx, py = cy, pz = cz, pr = rl;
-      if (CM_PARK && lm) {  // warp-uniform; the loads are branch-free selects
+      double px = 0.0, py = 0.0, pz = 0.0, pr = r;
+      if (lm) {  // warp-uniform; the loads are branch-free selects
         const bool mine = (lm >> lane) & 1u;
         const uint32_t a = spark[lane];
         const double b0 = sc[lane], b1 = sc[32 + lane], b2 = sc[64 + lane], b3 = sc[96 + lane];
@@ -1900,20 +1938,24 @@ cm_status launch_radius(const cm_index* ix, const double* q, uint64_t nq, int ke
     CM_CUDA_TRY(cudaGetLastError());
     return CM_OK;
   };
-  switch (ix->opts.flavor) {
-    case CM_DENSE:
-      return kernel == CM_CUBE       ? run(radius_tile_kernel<CM_DENSE, MODE, 1>)
-             : kernel == CM_CYLINDER ? run(radius_tile_kernel<CM_DENSE, MODE, 2>)
-                                     : run(radius_tile_kernel<CM_DENSE, MODE, 0>);
-    case CM_SPARSE:
-      return kernel == CM_CUBE       ? run(radius_tile_kernel<CM_SPARSE, MODE, 1>)
-             : kernel == CM_CYLINDER ? run(radius_tile_kernel<CM_SPARSE, MODE, 2>)
-                                     : run(radius_tile_kernel<CM_SPARSE, MODE, 0>);
-    default:
-      return kernel == CM_CUBE       ? run(radius_tile_kernel<CM_MIXED, MODE, 1>)
-             : kernel == CM_CYLINDER ? run(radius_tile_kernel<CM_MIXED, MODE, 2>)
-                                     : run(radius_tile_kernel<CM_MIXED, MODE, 0>);
-  }
+  auto pick = [&](auto xq) -> cm_status {
+    constexpr bool XQ = decltype(xq)::value;
+    switch (ix->opts.flavor) {
+      case CM_DENSE:
+        return kernel == CM_CUBE       ? run(radius_tile_kernel<CM_DENSE, MODE, 1, XQ>)
+               : kernel == CM_CYLINDER ? run(radius_tile_kernel<CM_DENSE, MODE, 2, XQ>)
+                                       : run(radius_tile_kernel<CM_DENSE, MODE, 0, XQ>);
+      case CM_SPARSE:
+        return kernel == CM_CUBE       ? run(radius_tile_kernel<CM_SPARSE, MODE, 1, XQ>)
+               : kernel == CM_CYLINDER ? run(radius_tile_kernel<CM_SPARSE, MODE, 2, XQ>)
+                                       : run(radius_tile_kernel<CM_SPARSE, MODE, 0, XQ>);
+      default:
+        return kernel == CM_CUBE       ? run(radius_tile_kernel<CM_MIXED, MODE, 1, XQ>)
+               : kernel == CM_CYLINDER ? run(radius_tile_kernel<CM_MIXED, MODE, 2, XQ>)
+                                       : run(radius_tile_kernel<CM_MIXED, MODE, 0, XQ>);
+    }
+  };
+  return (o.rq || o.qbox) ? pick(std::true_type{}) : pick(std::false_type{});
 }
 
 // Rows longer than a warp buffer (kSortCap), from the one-query-per-warp
