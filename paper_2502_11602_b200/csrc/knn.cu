@@ -564,7 +564,10 @@ struct KnnHeap {
 // BALL: ball completion after the first full block (k > 16); otherwise
 // whole shells with the stop test after each (fewer registers: measured
 // faster at k = 8 / 16, 8.6 / 12.5 ms against 11.2 / 16.2 ms on config 3).
-template <int FLAVOR, int K, bool BALL = (K > 16)>
+#ifndef CM_KNN_TBALL
+#define CM_KNN_TBALL 1  // ball completion in the per-thread kernel for k > 16
+#endif
+template <int FLAVOR, int K, bool BALL = (CM_KNN_TBALL && K > 16)>
 __global__ void __launch_bounds__(kTThreads, (K > 16 ? 4 : CM_KNN_TMINB)) knn_thread_kernel(
     const Tables t, const double* __restrict__ q, uint64_t nq, uint32_t k,
     const uint32_t* __restrict__ list, const uint32_t* __restrict__ n_list, int lmax,
