@@ -55,13 +55,13 @@ def test_no_fma_in_predicate_kernels():
     counts = {}
     for b in sass.split("Function : ")[1:]:
         name = b.split("\n", 1)[0]
-        m = re.search(r"radius_tile_kernelILi(\d)ELi(\d)ELi(\d)E", name)
+        m = re.search(r"radius_tile_kernelILi(\d)ELi(\d)ELi(\d)ELb(\d)E", name)
         if m:
             counts[m.groups()] = b.count("DFMA")
-    assert len(counts) >= 12
-    for (flavor, mode, cube), n in counts.items():
+    assert len(counts) >= 24  # with and without per-centre radii / boxes
+    for (flavor, mode, cube, xq), n in counts.items():
         if cube == "0":
-            assert n == counts[(flavor, mode, "1")], (flavor, mode)
+            assert n == counts[(flavor, mode, "1", xq)], (flavor, mode, xq)
 
 
 def test_status_names_and_default_options():
