@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
+#include <string>
 #include <vector>
 
 #include "index.cuh"
@@ -87,6 +88,9 @@ __device__ __forceinline__ void shell_column_spans(const Tables& t, int64_t i, i
 #endif
 #ifndef CM_KNN_BOX
 #define CM_KNN_BOX 0
+#endif
+#ifndef CM_KNN_PRUNE
+#define CM_KNN_PRUNE 2  // per-thread kernel: 0 whole block, 1 pruned columns, 2 pruned + nearest first
 #endif
 #ifndef CM_KNN_BALL
 #define CM_KNN_BALL 0  // measured slower on config 3 (k = 64: 39.3 -> 47.8 ms): opt-in
@@ -341,6 +345,149 @@ __global__ void __launch_bounds__(kKThreads) knn_warp_kernel(const Tables t,
     __syncwarp();
   }
   (void)lt;
+}
+
+// One warp per centre with the sorted (d², handle) list in REGISTERS (k <= 32):
+// lane l holds the l-th best entry, pads are (inf, 0xffffffff) — the output
+// convention for missing neighbours. The walk is knn_warp_kernel's (lanes
+// look up one column each, candidates flattened 32 per step); a step's
+// accepted candidates enter the list one by one (rank by ballot, shift by
+// shuffle: no shared memory) or, when there are many, sorted and merged
+// through the bitonic half-cleaner (the 32 smallest of two sorted 32-lists
+// are min(A[l], B[31 - l]), a bitonic sequence). Used for the centres the
+// per-thread kernel's first pass cannot finish (sparse neighbourhoods: many
+// span lookups, few candidates), and for 16 < k <= 32.
+#ifndef CM_KNN_SORTMIN
+#define CM_KNN_SORTMIN 12  // accepted candidates per step from which the batch is sorted and merged
+#endif
+template <int FLAVOR>
+__global__ void __launch_bounds__(kKThreads) knn_warp_reg_kernel(
+    const Tables t, const double* __restrict__ q, uint64_t s_begin, uint64_t s_end, uint32_t k,
+    const uint32_t* __restrict__ perm, uint32_t* __restrict__ idx_out, double* __restrict__ d2_out,
+    const uint32_t* __restrict__ n_dev) {
+  if (n_dev) s_end = s_end < (uint64_t)*n_dev ? s_end : (uint64_t)*n_dev;
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const uint64_t W = (uint64_t)gridDim.x * kKWarps;
+  const DevGrid& g = t.g;
+  const int64_t nx = (int64_t)g.nx, ny = (int64_t)g.ny, nzm = (int64_t)g.nz - 1;
+  const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+  for (uint64_t s = s_begin + (uint64_t)blockIdx.x * kKWarps + wib; s < s_end; s += W) {
+    const uint32_t qi = perm ? __ldg(perm + s) : (uint32_t)s;
+    const double cx = __ldg(q + 3 * (uint64_t)qi);
+    const double cy = __ldg(q + 3 * (uint64_t)qi + 1);
+    const double cz = __ldg(q + 3 * (uint64_t)qi + 2);
+    const int64_t ic = (int64_t)axis_index(cx, g.ox, g.sx, g.nx);
+    const int64_t jc = (int64_t)axis_index(cy, g.oy, g.sy, g.ny);
+    const int64_t kc = g.mode3d ? (int64_t)axis_index(cz, g.oz, g.sz, g.nz) : 0;
+    const double eps = 1e-12 * (fabs(cx) + fabs(cy) + fabs(cz) + fabs(g.ox) + fabs(g.oy) +
+                                fabs(g.oz) + g.sx + g.sy + g.sz);
+    double rd = kInf;  // this lane's list entry
+    uint32_t ri = 0xffffffffu;
+    double kd = kInf;  // entry k - 1 (warp-uniform)
+    uint32_t kid = 0xffffffffu;
+    auto walk_cols = [&](uint32_t ncol, auto spans) {
+      for (uint32_t cb = 0; cb < ncol; cb += 32) {
+        const uint32_t c = cb + lane;
+        uint32_t b1 = 0, e1 = 0, b2 = 0, e2 = 0;
+        if (c < ncol) spans(c, &b1, &e1, &b2, &e2);
+        const uint32_t l1 = e1 - b1;
+        const uint32_t len = l1 + (e2 - b2);
+        const uint32_t incl = warp_incl_scan(len);
+        const uint32_t excl = incl - len;
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        for (uint32_t t0 = 0; t0 < total; t0 += 32) {
+          const uint32_t tt = t0 + lane;
+          int Lq = 0;
+#pragma unroll
+          for (int sft = 16; sft > 0; sft >>= 1) {
+            const uint32_t v = __shfl_sync(0xffffffffu, incl, Lq + sft - 1);
+            if (v <= tt) Lq += sft;
+          }
+          const uint32_t xL = __shfl_sync(0xffffffffu, excl, Lq);
+          const uint32_t b1L = __shfl_sync(0xffffffffu, b1, Lq);
+          const uint32_t l1L = __shfl_sync(0xffffffffu, l1, Lq);
+          const uint32_t b2L = __shfl_sync(0xffffffffu, b2, Lq);
+          double d2 = kInf;
+          uint32_t id = 0xffffffffu;
+          bool acc = false;
+          if (tt < total) {
+            const uint32_t o = tt - xL;
+            const uint32_t pos = o < l1L ? b1L + o : b2L + (o - l1L);
+            const PointRec pr = load_rec(t.rec + pos);
+            d2 = sqdist(pr.x, pr.y, pr.z, cx, cy, cz);
+            id = pr.id;
+            acc = pair_less(d2, id, kd, kid);
+          }
+          uint32_t m = __ballot_sync(0xffffffffu, acc);
+          if (!m) continue;
+          if (__popc(m) >= CM_KNN_SORTMIN) {
+            double bd = acc ? d2 : kInf;
+            uint32_t bi = acc ? id : 0xffffffffu;
+            warp_sort_pairs32(bd, bi, lane);
+            const double od = __shfl_sync(0xffffffffu, bd, 31 - lane);
+            const uint32_t oi = __shfl_sync(0xffffffffu, bi, 31 - lane);
+            if (pair_less(od, oi, rd, ri)) rd = od, ri = oi;
+#pragma unroll
+            for (int j = 16; j > 0; j >>= 1) {
+              const double pd = __shfl_xor_sync(0xffffffffu, rd, j);
+              const uint32_t pi = __shfl_xor_sync(0xffffffffu, ri, j);
+              const bool p_less = pair_less(pd, pi, rd, ri);
+              const bool take = ((lane & j) == 0) ? p_less : !p_less;
+              rd = take ? pd : rd;
+              ri = take ? pi : ri;
+            }
+          } else {
+            while (m) {
+              const int src = __ffs(m) - 1;
+              m &= m - 1;
+              const double d = __shfl_sync(0xffffffffu, d2, src);
+              const uint32_t di = __shfl_sync(0xffffffffu, id, src);
+              // rank among the 32 entries: lanes holding smaller entries are a prefix
+              const uint32_t pos = __popc(__ballot_sync(0xffffffffu, pair_less(rd, ri, d, di)));
+              const double ud = __shfl_up_sync(0xffffffffu, rd, 1);
+              const uint32_t ui = __shfl_up_sync(0xffffffffu, ri, 1);
+              if ((uint32_t)lane > pos) rd = ud, ri = ui;
+              if ((uint32_t)lane == pos) rd = d, ri = di;
+            }
+          }
+          kd = __shfl_sync(0xffffffffu, rd, (int)k - 1);
+          kid = __shfl_sync(0xffffffffu, ri, (int)k - 1);
+        }
+      }
+    };
+    for (int64_t L = 1;; ++L) {
+      const int64_t i0 = imax64(0, ic - L), i1 = imin64(nx - 1, ic + L);
+      const int64_t j0 = imax64(0, jc - L), j1 = imin64(ny - 1, jc + L);
+      const uint32_t nj = (uint32_t)(j1 - j0 + 1);
+      const uint32_t ncol = (uint32_t)(i1 - i0 + 1) * nj;
+      walk_cols(ncol, [&](uint32_t c, uint32_t* b1, uint32_t* e1, uint32_t* b2, uint32_t* e2) {
+        const int64_t i = i0 + (int64_t)(c / nj), j = j0 + (int64_t)(c % nj);
+        const bool ring = L == 1 || (i == ic - L) || (i == ic + L) || (j == jc - L) || (j == jc + L);
+        shell_column_spans<FLAVOR>(t, i, j, ring, kc, L, (uint64_t)nzm, b1, e1, b2, e2);
+      });
+      const bool all = i0 == 0 && i1 == nx - 1 && j0 == 0 && j1 == ny - 1 &&
+                       imax64(0, kc - L) == 0 && imin64(nzm, kc + L) == nzm;
+      if (all) break;
+      if (kid != 0xffffffffu) {  // k entries known: the shell walk's stop test
+        double dmin = 1e300;
+        if (i0 > 0) dmin = fmin(dmin, cx - (g.ox + (double)i0 * g.sx));
+        if (i1 < nx - 1) dmin = fmin(dmin, (g.ox + (double)(i1 + 1) * g.sx) - cx);
+        if (j0 > 0) dmin = fmin(dmin, cy - (g.oy + (double)j0 * g.sy));
+        if (j1 < ny - 1) dmin = fmin(dmin, (g.oy + (double)(j1 + 1) * g.sy) - cy);
+        if (g.mode3d) {
+          if (kc - L > 0) dmin = fmin(dmin, cz - (g.oz + (double)(kc - L) * g.sz));
+          if (kc + L < nzm) dmin = fmin(dmin, (g.oz + (double)(kc + L + 1) * g.sz) - cz);
+        }
+        const double dm = dmin - eps;
+        if (dm > 0.0 && kd < dm * dm) break;
+      }
+    }
+    if ((uint32_t)lane < k) {
+      idx_out[(uint64_t)qi * k + lane] = ri;
+      if (d2_out) d2_out[(uint64_t)qi * k + lane] = rd;
+    }
+  }
 }
 
 // kNN query tiles (k <= KMAX, used for k <= kKnnTileMax): 32 cell-sorted
@@ -721,6 +868,56 @@ __global__ void __launch_bounds__(kTThreads, (K > 16 ? 4 : CM_KNN_TMINB)) knn_th
         const int64_t j0 = imax64(0, jc - L), j1 = imin64(ny - 1, jc + L);
         const int64_t nj = j1 - j0 + 1;
         const int64_t ncol = (i1 - i0 + 1) * nj;
+        if (CM_KNN_PRUNE && L == 1) {
+          // The 3 x 3 x 3 block with pruning: once k points are known, a
+          // neighbour column (and each of its three voxels) is skipped when
+          // every point it can hold is farther than the current k-th: the
+          // squared distance from the centre to the column's (voxel's) near
+          // faces, each face distance reduced by the stop test's rounding
+          // margin, strictly exceeds the k-th d². The k-th only shrinks, so
+          // a skipped point can never enter the result: exact.
+          uint32_t b, e;
+          column_span<FLAVOR>(t, (uint64_t)ic, (uint64_t)jc, (uint64_t)imax64(0, kc - 1),
+                              (uint64_t)imin64(nzm, kc + 1), &b, &e);
+          visit(b, e, ic, jc);
+          // lower bounds of |dx| to the columns at ic -/+ 1 (same for y, z)
+          const double fxm = fmax(0.0, (cx - (g.ox + (double)ic * g.sx)) - eps);
+          const double fxp = fmax(0.0, ((g.ox + (double)(ic + 1) * g.sx) - cx) - eps);
+          const double fym = fmax(0.0, (cy - (g.oy + (double)jc * g.sy)) - eps);
+          const double fyp = fmax(0.0, ((g.oy + (double)(jc + 1) * g.sy) - cy) - eps);
+          const double fzm = fmax(0.0, (cz - (g.oz + (double)kc * g.sz)) - eps);
+          const double fzp = fmax(0.0, ((g.oz + (double)(kc + 1) * g.sz) - cz) - eps);
+          // CM_KNN_PRUNE == 2: nearest columns first, relative to each centre
+          // (near x side, near y side, near corner, far sides, far corners)
+          const int nsx = (CM_KNN_PRUNE == 2 && fxp < fxm) ? 1 : -1;
+          const int nsy = (CM_KNN_PRUNE == 2 && fyp < fym) ? 1 : -1;
+#pragma unroll 1
+          for (int c = 0; c < 8; ++c) {
+            int di, dj;
+            if (CM_KNN_PRUNE == 2) {
+              di = ((int)((0x926u >> (2 * c)) & 3u) - 1) * nsx;
+              dj = ((int)((0x2069u >> (2 * c)) & 3u) - 1) * nsy;
+            } else {
+              const int cc = c + (c >= 4);  // 0..8 without the centre (4)
+              di = cc / 3 - 1, dj = cc % 3 - 1;
+            }
+            const int64_t i = ic + di, j = jc + dj;
+            if (i < 0 || i >= nx || j < 0 || j >= ny) continue;
+            int64_t klo = imax64(0, kc - 1), khi = imin64(nzm, kc + 1);
+            if (cnt == k) {
+              const double bx = di == 0 ? 0.0 : (di < 0 ? fxm : fxp);
+              const double by = dj == 0 ? 0.0 : (dj < 0 ? fym : fyp);
+              const double lb2 = bx * bx + by * by;
+              if (kd < lb2) continue;
+              if (g.mode3d) {
+                if (kd < lb2 + fzm * fzm) klo = kc;
+                if (kd < lb2 + fzp * fzp) khi = kc;
+              }
+            }
+            column_span<FLAVOR>(t, (uint64_t)i, (uint64_t)j, (uint64_t)klo, (uint64_t)khi, &b, &e);
+            visit(b, e, i, j);
+          }
+        } else
         for (int64_t c = -1; c < ncol; ++c) {
           int64_t i, j;
           if (c < 0) {
@@ -1235,9 +1432,35 @@ cm_status knn_dev(const cm_index* ix, const double* q, uint64_t nq, uint32_t k,
       CM_CUDA_TRY(cudaGetLastError());
       return CM_OK;
     };
+    // pass 2: the centres pass 1 left (sparse neighbourhoods: several
+    // shells of span lookups for a handful of candidates) go one per WARP
+    // with the list in registers (config 3 k = 8 / 16: the per-thread pass 2
+    // took 3.7 / 6.7 ms for 15 % of the centres); CMGPU_KNN_REDO=thread
+    // keeps the per-thread walk
+    static const bool redo_thread =
+        std::getenv("CMGPU_KNN_REDO") && std::string(std::getenv("CMGPU_KNN_REDO")) == "thread";
+    auto redo_warp = [&](auto kern) -> cm_status {
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kKThreads, 0);
+      per_sm = std::max(per_sm, 1);
+      const uint64_t need = (nq + kKWarps - 1) / kKWarps;
+      const unsigned grid =
+          (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(need, (uint64_t)sm_count() * per_sm));
+      kern<<<grid, kKThreads, 0, st>>>(t, q, 0, nq, k, redo1, idx, d2, nr);
+      ::cmg::note_launch();
+      CM_CUDA_TRY(cudaGetLastError());
+      return CM_OK;
+    };
     auto both = [&](auto kern, int K) -> cm_status {
       const cm_status s1 = pass(kern, K, perm, nullptr, lfirst, redo1, nr);
       if (s1 != CM_OK) return s1;
+      if (!redo_thread && k <= 32) {
+        switch (ix->opts.flavor) {
+          case CM_DENSE: return redo_warp(knn_warp_reg_kernel<CM_DENSE>);
+          case CM_SPARSE: return redo_warp(knn_warp_reg_kernel<CM_SPARSE>);
+          default: return redo_warp(knn_warp_reg_kernel<CM_MIXED>);
+        }
+      }
       return pass(kern, K, redo1, nr, 1 << 30, redo2, nr + 1);
     };
     auto by_k = [&](auto k8, auto k16, auto k32, auto k64) -> cm_status {
@@ -1327,6 +1550,31 @@ cm_status knn_dev(const cm_index* ix, const double* q, uint64_t nq, uint32_t k,
       return ts;
     }
     wperm = redo;
+  }
+  // 16 < k <= 32: one warp per centre with the list in registers
+  static const bool reg32 = !(std::getenv("CMGPU_KNN_REG32") && std::atoi(std::getenv("CMGPU_KNN_REG32")) == 0);
+  if (reg32 && !legacy && !glist && k <= 32) {
+    auto runr = [&](auto kern) -> cm_status {
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kKThreads, 0);
+      per_sm = std::max(per_sm, 1);
+      const uint64_t need = (nq + kKWarps - 1) / kKWarps;
+      const unsigned grid =
+          (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(need, (uint64_t)sm_count() * per_sm));
+      kern<<<grid, kKThreads, 0, st>>>(t, q, 0, nq, k, wperm, idx, d2, n_redo);
+      ::cmg::note_launch();
+      CM_CUDA_TRY(cudaGetLastError());
+      return CM_OK;
+    };
+    cm_status s;
+    switch (ix->opts.flavor) {
+      case CM_DENSE: s = runr(knn_warp_reg_kernel<CM_DENSE>); break;
+      case CM_SPARSE: s = runr(knn_warp_reg_kernel<CM_SPARSE>); break;
+      default: s = runr(knn_warp_reg_kernel<CM_MIXED>);
+    }
+    if (redo) dev_free(redo, st);
+    if (n_redo) dev_free(n_redo, st);
+    return s;
   }
   auto run = [&](auto kern) -> cm_status {
     int per_sm = 0;
