@@ -364,7 +364,10 @@ template <int FLAVOR>
 __global__ void __launch_bounds__(kKThreads) knn_warp_reg_kernel(
     const Tables t, const double* __restrict__ q, uint64_t s_begin, uint64_t s_end, uint32_t k,
     const uint32_t* __restrict__ perm, uint32_t* __restrict__ idx_out, double* __restrict__ d2_out,
-    const uint32_t* __restrict__ n_dev) {
+    const uint32_t* __restrict__ n_dev, int L0) {
+  // L0: the first step visits the whole Chebyshev-L0 block (one span lookup
+  // per column); the pass-2 centres are known to need more than the 3 x 3 x 3
+  // block, so they start at L0 = 2: one round of lookups less
   if (n_dev) s_end = s_end < (uint64_t)*n_dev ? s_end : (uint64_t)*n_dev;
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -456,14 +459,14 @@ __global__ void __launch_bounds__(kKThreads) knn_warp_reg_kernel(
         }
       }
     };
-    for (int64_t L = 1;; ++L) {
+    for (int64_t L = L0;; ++L) {
       const int64_t i0 = imax64(0, ic - L), i1 = imin64(nx - 1, ic + L);
       const int64_t j0 = imax64(0, jc - L), j1 = imin64(ny - 1, jc + L);
       const uint32_t nj = (uint32_t)(j1 - j0 + 1);
       const uint32_t ncol = (uint32_t)(i1 - i0 + 1) * nj;
       walk_cols(ncol, [&](uint32_t c, uint32_t* b1, uint32_t* e1, uint32_t* b2, uint32_t* e2) {
         const int64_t i = i0 + (int64_t)(c / nj), j = j0 + (int64_t)(c % nj);
-        const bool ring = L == 1 || (i == ic - L) || (i == ic + L) || (j == jc - L) || (j == jc + L);
+        const bool ring = L == L0 || (i == ic - L) || (i == ic + L) || (j == jc - L) || (j == jc + L);
         shell_column_spans<FLAVOR>(t, i, j, ring, kc, L, (uint64_t)nzm, b1, e1, b2, e2);
       });
       const bool all = i0 == 0 && i1 == nx - 1 && j0 == 0 && j1 == ny - 1 &&
@@ -1135,6 +1138,180 @@ __device__ __forceinline__ void warp_sort_pairs_blocked(double (&d)[E], uint32_t
   }
 }
 
+// ---- kNN by histogram selection (16 < k <= 64) -----------------------------
+// One warp per centre. For the Chebyshev block L around the centre's voxel
+// (L = 1, 2, ...: one span lookup per column, lanes = columns), D = the
+// squared distance to the nearest unvisited voxel face (the shell walk's stop
+// bound). Pass A walks the block's candidates (32 per step, coalesced) and
+// counts the ones with d² < D in 32 bins uniform in d²; if at least k lie
+// below D, the bin b* that holds the k-th is known, and pass B walks the same
+// spans again and keeps every candidate with bin <= b* (bins are monotone in
+// d², so these are a prefix of the candidates in (d², handle) order that
+// holds the k best; all of them lie below D, so the shell walk's stop test
+// holds and the block's k best are the answer). The kept ones (k .. 128) are
+// sorted once in registers: no per-candidate list maintenance. Centres whose block never holds k points below D within
+// lmax levels, whose bin b* overflows the buffer (heavy ties), or whose
+// block covers the whole grid go to the redo list (shell walk).
+constexpr int kHistCap = 128;
+
+template <int E>
+__device__ __forceinline__ void hist_sort_out(const double* __restrict__ bd,
+                                              const uint32_t* __restrict__ bi, uint32_t m,
+                                              uint32_t k, uint64_t qi, int lane,
+                                              uint32_t* __restrict__ idx_out,
+                                              double* __restrict__ d2_out) {
+  double d[E];
+  uint32_t id[E];
+#pragma unroll
+  for (int r = 0; r < E; ++r) {
+    const uint32_t i = (uint32_t)lane * E + r;
+    d[r] = i < m ? bd[i] : __longlong_as_double(0x7ff0000000000000ll);
+    id[r] = i < m ? bi[i] : 0xffffffffu;
+  }
+  warp_sort_pairs_blocked<E>(d, id, lane);
+#pragma unroll
+  for (int r = 0; r < E; ++r) {
+    const uint32_t i = (uint32_t)lane * E + r;
+    if (i < k) {
+      idx_out[qi * k + i] = id[r];
+      if (d2_out) d2_out[qi * k + i] = d[r];
+    }
+  }
+}
+
+__device__ __forceinline__ int hist_bin(double d2, double scale) {
+  const int b = (int)__dmul_rn(d2, scale);
+  return b > 31 ? 31 : b;
+}
+
+template <int FLAVOR>
+__global__ void __launch_bounds__(kKThreads) knn_hist_kernel(
+    const Tables t, const double* __restrict__ q, uint64_t nq, uint32_t k,
+    const uint32_t* __restrict__ perm, uint32_t* __restrict__ idx_out, double* __restrict__ d2_out,
+    uint32_t* __restrict__ redo, uint32_t* __restrict__ n_redo, int lmax) {
+  __shared__ uint32_t s_hist[kKWarps][32];
+  __shared__ double s_bd[kKWarps][kHistCap];
+  __shared__ uint32_t s_bi[kKWarps][kHistCap];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  uint32_t* hist = s_hist[wib];
+  double* bd = s_bd[wib];
+  uint32_t* bi = s_bi[wib];
+  const uint64_t W = (uint64_t)gridDim.x * kKWarps;
+  const DevGrid& g = t.g;
+  const uint32_t lt = lanemask_lt();
+  const int64_t nx = (int64_t)g.nx, ny = (int64_t)g.ny, nzm = (int64_t)g.nz - 1;
+  for (uint64_t s = (uint64_t)blockIdx.x * kKWarps + wib; s < nq; s += W) {
+    const uint32_t qi = perm ? __ldg(perm + s) : (uint32_t)s;
+    const double cx = __ldg(q + 3 * (uint64_t)qi);
+    const double cy = __ldg(q + 3 * (uint64_t)qi + 1);
+    const double cz = __ldg(q + 3 * (uint64_t)qi + 2);
+    const int64_t ic = (int64_t)axis_index(cx, g.ox, g.sx, g.nx);
+    const int64_t jc = (int64_t)axis_index(cy, g.oy, g.sy, g.ny);
+    const int64_t kc = g.mode3d ? (int64_t)axis_index(cz, g.oz, g.sz, g.nz) : 0;
+    const double eps = 1e-12 * (fabs(cx) + fabs(cy) + fabs(cz) + fabs(g.ox) + fabs(g.oy) +
+                                fabs(g.oz) + g.sx + g.sy + g.sz);
+    bool finished = false;
+    for (int64_t L = 1; L <= (int64_t)lmax; ++L) {
+      const int64_t i0 = imax64(0, ic - L), i1 = imin64(nx - 1, ic + L);
+      const int64_t j0 = imax64(0, jc - L), j1 = imin64(ny - 1, jc + L);
+      const int64_t k0 = imax64(0, kc - L), k1 = imin64(nzm, kc + L);
+      double dmin = 1e300;
+      if (i0 > 0) dmin = fmin(dmin, cx - (g.ox + (double)i0 * g.sx));
+      if (i1 < nx - 1) dmin = fmin(dmin, (g.ox + (double)(i1 + 1) * g.sx) - cx);
+      if (j0 > 0) dmin = fmin(dmin, cy - (g.oy + (double)j0 * g.sy));
+      if (j1 < ny - 1) dmin = fmin(dmin, (g.oy + (double)(j1 + 1) * g.sy) - cy);
+      if (g.mode3d) {
+        if (k0 > 0) dmin = fmin(dmin, cz - (g.oz + (double)k0 * g.sz));
+        if (k1 < nzm) dmin = fmin(dmin, (g.oz + (double)(k1 + 1) * g.sz) - cz);
+      }
+      if (dmin == 1e300) break;  // the block is the whole grid: no bound, shell walk
+      const double dm = dmin - eps;
+      if (!(dm > 0.0)) continue;
+      const double D = dm * dm;
+      const double scale = 32.0 / D;
+      const uint32_t nj = (uint32_t)(j1 - j0 + 1);
+      const uint32_t ncol = (uint32_t)(i1 - i0 + 1) * nj;
+      const bool single = ncol <= 32;
+      uint32_t b = 0, len = 0, incl = 0, total = 0;
+      int bstar = 0;
+      uint32_t m = 0, pos = 0;
+      bool ok = true;
+      hist[lane] = 0;
+      __syncwarp();
+      for (int pass = 0; pass < 2 && ok; ++pass) {
+        for (uint32_t cb = 0; cb < ncol; cb += 32) {
+          if (pass == 0 || !single) {
+            const uint32_t c = cb + lane;
+            uint32_t e = 0;
+            b = 0;
+            if (c < ncol)
+              column_span<FLAVOR>(t, (uint64_t)(i0 + (int64_t)(c / nj)), (uint64_t)(j0 + (int64_t)(c % nj)),
+                                  (uint64_t)k0, (uint64_t)k1, &b, &e);
+            len = e - b;
+            incl = warp_incl_scan(len);
+            total = __shfl_sync(0xffffffffu, incl, 31);
+          }
+          const uint32_t excl = incl - len;
+          for (uint32_t t0 = 0; t0 < total; t0 += 32) {
+            const uint32_t tt = t0 + lane;
+            int Lq = 0;
+#pragma unroll
+            for (int sft = 16; sft > 0; sft >>= 1) {
+              const uint32_t v = __shfl_sync(0xffffffffu, incl, Lq + sft - 1);
+              if (v <= tt) Lq += sft;
+            }
+            const uint32_t xL = __shfl_sync(0xffffffffu, excl, Lq);
+            const uint32_t bL = __shfl_sync(0xffffffffu, b, Lq);
+            double d2 = 0.0;
+            uint32_t id = 0;
+            int bin = 32;
+            if (tt < total) {
+              const PointRec pr = load_rec(t.rec + bL + (tt - xL));
+              d2 = sqdist(pr.x, pr.y, pr.z, cx, cy, cz);
+              id = pr.id;
+              if (d2 < D) bin = hist_bin(d2, scale);
+            }
+            if (pass == 0) {
+              if (bin < 32) atomicAdd(hist + bin, 1u);
+            } else {
+              const bool sel = bin <= bstar;
+              const uint32_t mm = __ballot_sync(0xffffffffu, sel);
+              if (sel) {
+                const uint32_t p = pos + __popc(mm & lt);
+                bd[p] = d2;
+                bi[p] = id;
+              }
+              pos += __popc(mm);
+            }
+          }
+        }
+        __syncwarp();
+        if (pass == 0) {
+          const uint32_t hi = warp_incl_scan(hist[lane]);
+          const uint32_t ge = __ballot_sync(0xffffffffu, hi >= k);
+          if (!ge) {
+            ok = false;  // fewer than k below D: next level
+          } else {
+            bstar = __ffs(ge) - 1;
+            m = __shfl_sync(0xffffffffu, hi, bstar);
+            if (m > (uint32_t)kHistCap) ok = false, L = (int64_t)lmax;  // heavy bin: shell walk
+          }
+        }
+      }
+      if (!ok) continue;
+      CM_DCHECK(pos == m);
+      if (m <= 32) hist_sort_out<1>(bd, bi, m, k, (uint64_t)qi, lane, idx_out, d2_out);
+      else if (m <= 64) hist_sort_out<2>(bd, bi, m, k, (uint64_t)qi, lane, idx_out, d2_out);
+      else hist_sort_out<4>(bd, bi, m, k, (uint64_t)qi, lane, idx_out, d2_out);
+      __syncwarp();
+      finished = true;
+      break;
+    }
+    if (!finished && lane == 0) redo[atomicAdd(n_redo, 1u)] = qi;
+  }
+}
+
 template <int E>
 __device__ __forceinline__ void select_row(const PointRec* __restrict__ rec,
                                            const uint32_t* __restrict__ rec_of,
@@ -1390,10 +1567,11 @@ cm_status knn_dev(const cm_index* ix, const double* q, uint64_t nq, uint32_t k,
   // CMGPU_KNN_BRACKETS for that comparison.
   static const bool brackets = std::getenv("CMGPU_KNN_BRACKETS") != nullptr;
   static const bool legacy = std::getenv("CMGPU_KNN_LEGACY") != nullptr;
-  // (k = 32 / 64 measured slower per thread than one warp per centre: 36.9 /
-  // 109 ms against 25.5 / 39 ms on config 3)
+  // (k = 64 measured slower per thread than one warp per centre: 109 ms
+  // against 39 ms on config 3; k = 32 with the register-list second pass:
+  // 19.0 ms against 20.9 ms for one warp per centre)
   static const uint32_t thread_kmax =
-      std::getenv("CMGPU_KNN_THREAD_KMAX") ? (uint32_t)std::atoi(std::getenv("CMGPU_KNN_THREAD_KMAX")) : 16u;
+      std::getenv("CMGPU_KNN_THREAD_KMAX") ? (uint32_t)std::atoi(std::getenv("CMGPU_KNN_THREAD_KMAX")) : 32u;
   if (!brackets && !legacy && k <= std::min(64u, thread_kmax)) {
     // per-thread kNN: pass 1 up to shell LFIRST, pass 2 (all shells) on the
     // centres pass 1 could not finish
@@ -1446,7 +1624,12 @@ cm_status knn_dev(const cm_index* ix, const double* q, uint64_t nq, uint32_t k,
       const uint64_t need = (nq + kKWarps - 1) / kKWarps;
       const unsigned grid =
           (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(need, (uint64_t)sm_count() * per_sm));
-      kern<<<grid, kKThreads, 0, st>>>(t, q, 0, nq, k, redo1, idx, d2, nr);
+      // first block of pass 2 (config 3, L0 = 1 / 2 / 3: k = 8 6.11 / 5.43 /
+      // 5.84 ms, k = 16 9.35 / 8.63 / 8.34 ms)
+      static const int redo_l0_env =
+          std::getenv("CMGPU_KNN_REDO_L0") ? std::max(1, std::atoi(std::getenv("CMGPU_KNN_REDO_L0"))) : 0;
+      const int redo_l0 = redo_l0_env ? redo_l0_env : (k <= 8 ? 2 : 3);
+      kern<<<grid, kKThreads, 0, st>>>(t, q, 0, nq, k, redo1, idx, d2, nr, redo_l0);
       ::cmg::note_launch();
       CM_CUDA_TRY(cudaGetLastError());
       return CM_OK;
@@ -1551,6 +1734,44 @@ cm_status knn_dev(const cm_index* ix, const double* q, uint64_t nq, uint32_t k,
     }
     wperm = redo;
   }
+  // 16 < k <= 64: histogram selection first; what it leaves goes to the
+  // register-list walk (k <= 32, from block 3) or the shell walk
+  // (config 3: k = 64 38.8 / 35.7 ms with 2 / 6 levels against 39.3 ms for
+  // the shell walk alone; k = 32 20.3 ms, where the per-thread first pass
+  // plus the register-list second pass takes 19.0 ms and is the default)
+  static const int hist_lmax =
+      std::getenv("CMGPU_KNN_HIST") ? std::atoi(std::getenv("CMGPU_KNN_HIST")) : 6;
+  int reg_l0 = 1;
+  if (hist_lmax > 0 && !legacy && !brackets && !glist && !redo && k > 16 && k <= 64) {
+    CM_CUDA_TRY(dev_alloc_t(&redo, nq, st));
+    CM_CUDA_TRY(dev_alloc_t(&n_redo, 1, st));
+    CM_CUDA_TRY(cudaMemsetAsync(n_redo, 0, 4, st));
+    auto runh = [&](auto kern) -> cm_status {
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kKThreads, 0);
+      per_sm = std::max(per_sm, 1);
+      const uint64_t need = (nq + kKWarps - 1) / kKWarps;
+      const unsigned grid =
+          (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(need, (uint64_t)sm_count() * per_sm));
+      kern<<<grid, kKThreads, 0, st>>>(t, q, nq, k, perm, idx, d2, redo, n_redo, hist_lmax);
+      ::cmg::note_launch();
+      CM_CUDA_TRY(cudaGetLastError());
+      return CM_OK;
+    };
+    cm_status hs;
+    switch (ix->opts.flavor) {
+      case CM_DENSE: hs = runh(knn_hist_kernel<CM_DENSE>); break;
+      case CM_SPARSE: hs = runh(knn_hist_kernel<CM_SPARSE>); break;
+      default: hs = runh(knn_hist_kernel<CM_MIXED>);
+    }
+    if (hs != CM_OK) {
+      dev_free(redo, st);
+      dev_free(n_redo, st);
+      return hs;
+    }
+    wperm = redo;
+    reg_l0 = hist_lmax >= 2 ? 3 : 1;
+  }
   // 16 < k <= 32: one warp per centre with the list in registers
   static const bool reg32 = !(std::getenv("CMGPU_KNN_REG32") && std::atoi(std::getenv("CMGPU_KNN_REG32")) == 0);
   if (reg32 && !legacy && !glist && k <= 32) {
@@ -1561,7 +1782,7 @@ cm_status knn_dev(const cm_index* ix, const double* q, uint64_t nq, uint32_t k,
       const uint64_t need = (nq + kKWarps - 1) / kKWarps;
       const unsigned grid =
           (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(need, (uint64_t)sm_count() * per_sm));
-      kern<<<grid, kKThreads, 0, st>>>(t, q, 0, nq, k, wperm, idx, d2, n_redo);
+      kern<<<grid, kKThreads, 0, st>>>(t, q, 0, nq, k, wperm, idx, d2, n_redo, reg_l0);
       ::cmg::note_launch();
       CM_CUDA_TRY(cudaGetLastError());
       return CM_OK;

@@ -142,6 +142,41 @@ def test_knn_radius_brackets_parity():
     assert r.returncode == 0 and "brackets ok" in r.stdout, r.stderr[-2000:]
 
 
+@pytest.mark.parametrize("env", [
+    {},                                                      # defaults: thread pass 1 + register-list pass 2; histogram selection for k > 32
+    {"CMGPU_KNN_THREAD_KMAX": "16"},                         # histogram selection for 16 < k <= 64, register list for its leftovers
+    {"CMGPU_KNN_THREAD_KMAX": "16", "CMGPU_KNN_HIST": "2"},
+    {"CMGPU_KNN_THREAD_KMAX": "16", "CMGPU_KNN_HIST": "0"},  # register-list walk alone for k <= 32, shell walk above
+    {"CMGPU_KNN_REDO": "thread"},                            # per-thread second pass
+    {"CMGPU_KNN_REDO_L0": "1"},
+    {"CMGPU_KNN_REDO_L0": "4"},
+], ids=lambda e: ",".join(f"{k[10:]}={v}" for k, v in e.items()) or "default")
+def test_knn_paths_parity(env):
+    """Every kNN path (pruned per-thread block walk, register-list warp
+    walk, histogram selection, shell walk) returns the oracle's rows: an ALS
+    tile with sparse lifted points (several shells), all flavours, plus an
+    integer lattice with duplicates (distance ties across bin edges, heavy
+    bins) and a cloud smaller than k."""
+    code = ("import numpy as np, sys; sys.path.insert(0, %r)\n"
+            "from paper_2502_11602_b200 import cheesemap as cm, synth\n"
+            "from oracle.oracle import CpuIndex\n"
+            "c = synth.config_cloud(1, scale=0.01); q = synth.config_queries(3, c, count=12000)\n"
+            "rng = np.random.default_rng(7)\n"
+            "lat = rng.integers(0, 12, size=(6000, 3)).astype(np.float64) * 0.5\n"
+            "few = rng.random((20, 3)) * 3.0\n"
+            "far = np.array([[-50.0, 3.0, 1.0], [1e4, 1e4, 1e4], [3.0, 3.0, 500.0]])\n"
+            "for fl in (cm.Flavor.Dense, cm.Flavor.Sparse, cm.Flavor.Mixed):\n"
+            "    for cloud, qs, ks in ((c, q, (5, 8, 16, 17, 24, 32, 33, 48, 64)), (lat, np.vstack([lat[:1500], far]), (8, 16, 32, 64)), (few, np.vstack([few, far]), (8, 32, 64))):\n"
+            "        m = cm.Cheesemap.build(cloud, cm.BuildOptions(flavor=fl)); o = CpuIndex(cloud, flavor=int(fl))\n"
+            "        for k in ks:\n"
+            "            i, d = cm.knn_batch(m, qs, k); oi, od = o.knn(qs, k)\n"
+            "            assert np.array_equal(i, oi) and np.array_equal(d, od), (int(fl), cloud.shape, k)\n"
+            "print('paths ok')\n") % ROOT
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env), capture_output=True,
+                       text=True, timeout=900)
+    assert r.returncode == 0 and "paths ok" in r.stdout, (r.stdout[-500:], r.stderr[-2000:])
+
+
 def test_voxel_lookup_mirror(cloud):
     m = cm.Cheesemap.build(cloud, cm.BuildOptions(flavor=cm.Flavor.Sparse))
     keys, hs = m.export_voxels()
