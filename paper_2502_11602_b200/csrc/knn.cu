@@ -360,8 +360,11 @@ __global__ void __launch_bounds__(kKThreads) knn_warp_kernel(const Tables t,
 #ifndef CM_KNN_SORTMIN
 #define CM_KNN_SORTMIN 12  // accepted candidates per step from which the batch is sorted and merged
 #endif
+#ifndef CM_KNN_REG_MINB
+#define CM_KNN_REG_MINB 8  // 64 registers (an explicit 1 lets ptxas take far more: slower)
+#endif
 template <int FLAVOR>
-__global__ void __launch_bounds__(kKThreads) knn_warp_reg_kernel(
+__global__ void __launch_bounds__(kKThreads, CM_KNN_REG_MINB) knn_warp_reg_kernel(
     const Tables t, const double* __restrict__ q, uint64_t s_begin, uint64_t s_end, uint32_t k,
     const uint32_t* __restrict__ perm, uint32_t* __restrict__ idx_out, double* __restrict__ d2_out,
     const uint32_t* __restrict__ n_dev, int L0) {
@@ -1184,8 +1187,14 @@ __device__ __forceinline__ int hist_bin(double d2, double scale) {
   return b > 31 ? 31 : b;
 }
 
+#ifndef CM_KNN_HIST_SKIP
+#define CM_KNN_HIST_SKIP 1
+#endif
+#ifndef CM_KNN_HIST_MINB
+#define CM_KNN_HIST_MINB 10  // 48 registers, small spill: config 3 k = 64 35.5 -> 33.7 ms
+#endif
 template <int FLAVOR>
-__global__ void __launch_bounds__(kKThreads) knn_hist_kernel(
+__global__ void __launch_bounds__(kKThreads, CM_KNN_HIST_MINB) knn_hist_kernel(
     const Tables t, const double* __restrict__ q, uint64_t nq, uint32_t k,
     const uint32_t* __restrict__ perm, uint32_t* __restrict__ idx_out, double* __restrict__ d2_out,
     uint32_t* __restrict__ redo, uint32_t* __restrict__ n_redo, int lmax) {
@@ -1292,6 +1301,8 @@ __global__ void __launch_bounds__(kKThreads) knn_hist_kernel(
           const uint32_t ge = __ballot_sync(0xffffffffu, hi >= k);
           if (!ge) {
             ok = false;  // fewer than k below D: next level
+            // far fewer than k (sparse neighbourhood): skip a level
+            if (CM_KNN_HIST_SKIP && __shfl_sync(0xffffffffu, hi, 31) * 4u < k && L + 2 <= (int64_t)lmax) ++L;
           } else {
             bstar = __ffs(ge) - 1;
             m = __shfl_sync(0xffffffffu, hi, bstar);
