@@ -35,7 +35,10 @@
  *  - Input/output pointers may be HOST or DEVICE memory (detected with
  *    cudaPointerGetAttributes). Host inputs are copied in, host outputs are
  *    copied back and the call synchronises. With device outputs calls are
- *    ordered on `stream` (a cudaStream_t; NULL = legacy default stream).
+ *    ordered on `stream` (a cudaStream_t; NULL = legacy default stream);
+ *    ordered, not asynchronous: cm_radius_search waits on the host once
+ *    inside the call (the arena cursor is read back to size the CSR), so
+ *    overlap other work from other host threads.
  *  - A built index is immutable and may be queried concurrently from many
  *    host threads / streams (map.hpp:50-52). The index owns device copies of
  *    the points; the caller's cloud need not outlive it.
