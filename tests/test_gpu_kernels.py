@@ -171,6 +171,13 @@ def test_knn_paths_parity(env):
             "        for k in ks:\n"
             "            i, d = cm.knn_batch(m, qs, k); oi, od = o.knn(qs, k)\n"
             "            assert np.array_equal(i, oi) and np.array_equal(d, od), (int(fl), cloud.shape, k)\n"
+            "    # 2D grid mode and anisotropic cells (the z bounds drop out of every prune / stop test)\n"
+            "    for mode in (cm.GridMode.TwoD, cm.GridMode.ThreeD):\n"
+            "        opts = cm.BuildOptions(flavor=fl, mode=mode, cell=cm.CellSize(1.5, 0.7, 0.4))\n"
+            "        m = cm.Cheesemap.build(c, opts); o = CpuIndex(c, flavor=int(fl), mode=int(mode), cell=(1.5, 0.7, 0.4))\n"
+            "        for k in (8, 24, 40, 64):\n"
+            "            i, d = cm.knn_batch(m, q[:3000], k); oi, od = o.knn(q[:3000], k)\n"
+            "            assert np.array_equal(i, oi) and np.array_equal(d, od), (int(fl), int(mode), k)\n"
             "print('paths ok')\n") % ROOT
     r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env), capture_output=True,
                        text=True, timeout=900)
