@@ -278,8 +278,9 @@ uint64_t cm_launch_count(void);
  * in-range candidates (count pass only). out8 has 8 entries. */
 cm_status cm_debug_query_stats(uint64_t* out8, int reset);
 /* The library allocates from a private stream-ordered pool per device.
- * Defaults: nothing reserved, up to 1/8 of HBM kept cached across
- * synchronisations. A process that owns the GPU may keep more cached
+ * Defaults: nothing reserved up front; large requests grow the pool in
+ * blocks of four times the request (CMGPU_POOL_GROW), up to 1/8 of HBM, which
+ * is also what stays cached across synchronisations. A process that owns the GPU may keep more cached
  * (keep_bytes) and reserve a block up front (reserve_bytes), so later calls
  * carve from it instead of mapping fresh memory. */
 cm_status cm_pool_configure(int device, uint64_t keep_bytes, uint64_t reserve_bytes);

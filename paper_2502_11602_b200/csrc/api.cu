@@ -41,8 +41,9 @@ int sm_count() {
 // The library's device memory comes from a PRIVATE stream-ordered pool per
 // device (not the device's default pool), so torch or any other user of the
 // default pool is unaffected by what this pool caches. Defaults are
-// conservative: nothing is reserved up front, and at most 1/8 of HBM stays
-// cached across synchronisations. Serving processes that own the GPU opt in
+// conservative: nothing is reserved up front, the pool grows with demand in
+// large blocks (dev_alloc), and at most 1/8 of HBM stays cached across
+// synchronisations. Serving processes that own the GPU opt in
 // to more with cm_pool_configure (the bench does: a reservation carved into
 // later requests avoids mapping fresh memory inside a call — measured 0.3-12
 // ms per cudaMallocAsync once the pool's chunks fragment) or with
@@ -98,6 +99,39 @@ cudaError_t dev_alloc(void** p, size_t bytes, cudaStream_t st) {
     return pool ? cudaMallocFromPoolAsync(p, bytes == 0 ? 16 : bytes, pool, st)
                 : cudaMallocAsync(p, bytes == 0 ? 16 : bytes, st);
   };
+  // Growth on demand, geometric and in one block: when a large request
+  // exceeds what the pool holds free, the pool first takes one block of
+  // four times the request (at least what it already holds), so this and the
+  // next requests carve from a few large blocks instead of mapping a fresh
+  // one per call. Without it the host-buffer search of config 1 took 79-139
+  // ms per 20M-query call (the pool mapping memory inside the calls: 11.7 GB
+  // reserved, fragmented) against 72 ms with one up-front reservation; with
+  // it the second call onward takes 72 ms (the first one maps the blocks:
+  // 0.3 s once). Factor 2 left it at 80 ms. The pool never grows this way
+  // past its release threshold (it would be trimmed at the next
+  // synchronisation) nor past half of the free memory, and small workloads
+  // (requests under 64 MB) never trigger it. CMGPU_POOL_GROW=f sets the
+  // factor, 0 turns it off.
+  static const bool grow_on = !(std::getenv("CMGPU_POOL_GROW") && std::atof(std::getenv("CMGPU_POOL_GROW")) == 0.0);
+  if (pool && grow_on && bytes >= (64ull << 20)) {
+    uint64_t reserved = 0, used = 0, thr = 0;
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    if (reserved - std::min(reserved, used) < bytes) {
+      size_t fr = 0, tot = 0;
+      cudaMemGetInfo(&fr, &tot);
+      static const double gf = std::getenv("CMGPU_POOL_GROW") ? std::max(1.0, std::atof(std::getenv("CMGPU_POOL_GROW"))) : 4.0;
+      uint64_t grow = std::max<uint64_t>((uint64_t)(gf * (double)bytes), (uint64_t)((double)reserved * gf / 4.0));
+      grow = std::min<uint64_t>(grow, (uint64_t)fr / 2);
+      if (thr > reserved) grow = std::min<uint64_t>(grow, thr - reserved); else grow = 0;
+      if (grow >= bytes) {
+        void* blk = nullptr;
+        if (cudaMallocFromPoolAsync(&blk, grow, pool, st) == cudaSuccess) cudaFreeAsync(blk, st);
+        else cudaGetLastError();
+      }
+    }
+  }
   cudaError_t e = alloc();
   if (e == cudaErrorMemoryAllocation) {
     // the pool keeps freed blocks cached: give them back to the device and

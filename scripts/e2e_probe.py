@@ -44,3 +44,4 @@ for i in range(3):
     t2 = time.perf_counter()
     L.cm_csr_free(csr)
     print(f"device search {(t1-t)*1e3:.1f} ms, download {(t2-t1)*1e3:.1f} ms", flush=True)
+print("pool (reserved, in use) bytes:", _native.pool_bytes(0), flush=True)
