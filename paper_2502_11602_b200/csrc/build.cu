@@ -64,6 +64,74 @@ __global__ void bbox_kernel(const double* __restrict__ xyz, uint64_t n,
   }
 }
 
+// K1, 16-byte loads: the cloud as a flat array of 3n doubles read two at a
+// time. The launch has a multiple of 3 threads, so the two components a
+// thread sees ((2t) mod 3 and the next) stay the same on every stride and
+// each thread keeps just two running (min, max) pairs; four loads in
+// flight per thread, one set of atomics per block.
+__global__ void bbox_flat_kernel(const double2* __restrict__ v2, uint64_t nvec, const double* tail,
+                                 unsigned long long* __restrict__ out) {
+  const uint64_t T = (uint64_t)gridDim.x * blockDim.x;  // T % 3 == 0
+  const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const int c0 = (int)((2 * t) % 3), c1 = (c0 + 1) % 3;
+  const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+  double lo0 = kInf, hi0 = -kInf, lo1 = kInf, hi1 = -kInf;
+  auto take = [&](const double2 v) {
+    lo0 = (v.x < lo0) ? v.x : lo0;
+    hi0 = (hi0 < v.x) ? v.x : hi0;
+    lo1 = (v.y < lo1) ? v.y : lo1;
+    hi1 = (hi1 < v.y) ? v.y : hi1;
+  };
+  uint64_t e = t;
+  for (; e + 3 * T < nvec; e += 4 * T) {
+    const double2 a = v2[e], b = v2[e + T], c = v2[e + 2 * T], d = v2[e + 3 * T];
+    take(a), take(b), take(c), take(d);
+  }
+  for (; e < nvec; e += T) take(v2[e]);
+  double lo[3], hi[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    lo[a] = c0 == a ? lo0 : (c1 == a ? lo1 : kInf);
+    hi[a] = c0 == a ? hi0 : (c1 == a ? hi1 : -kInf);
+  }
+  if (tail && t == 0) {  // 3n odd: the last z
+    const double v = *tail;
+    lo[2] = (v < lo[2]) ? v : lo[2];
+    hi[2] = (hi[2] < v) ? v : hi[2];
+  }
+  unsigned long long olo[3], ohi[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    olo[a] = ord_of(lo[a]);
+    ohi[a] = ord_of(hi[a]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long l2 = __shfl_xor_sync(0xffffffffu, olo[a], o);
+      const unsigned long long h2 = __shfl_xor_sync(0xffffffffu, ohi[a], o);
+      olo[a] = l2 < olo[a] ? l2 : olo[a];
+      ohi[a] = h2 > ohi[a] ? h2 : ohi[a];
+    }
+  }
+  // one set of six atomics per BLOCK (per warp they are 19 K same-address
+  // atomics per axis at 20M points: as long as the reads)
+  __shared__ unsigned long long sred[8][6];
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) sred[w][a] = olo[a], sred[w][3 + a] = ohi[a];
+  }
+  __syncthreads();
+  if (threadIdx.x < 6) {
+    unsigned long long v = sred[0][threadIdx.x];
+    for (int x = 1; x < (int)(blockDim.x >> 5); ++x) {
+      const unsigned long long u = sred[x][threadIdx.x];
+      v = threadIdx.x < 3 ? (u < v ? u : v) : (u > v ? u : v);
+    }
+    if (threadIdx.x < 3) atomicMin(out + threadIdx.x, v);
+    else atomicMax(out + threadIdx.x, v);
+  }
+}
+
 // K2: key = global_index(voxel_of(p)) (grid.cpp:63-72, grid.hpp:65-67).
 template <typename K>
 __global__ void keys_kernel(const double* __restrict__ xyz, uint64_t n, DevGrid g,
@@ -137,36 +205,102 @@ __global__ void gather_kernel(const double* __restrict__ xyz, const K* __restric
       frec[s] = f;
     }
     ids[s] = h;
-    flags[s] = (s == 0 || keys[s - 1] != keys[s]) ? 1u : 0u;
+    if (flags) flags[s] = (s == 0 || keys[s - 1] != keys[s]) ? 1u : 0u;
     }
   }
 }
 
-// Unique voxels: key, first record, z index; per-slice non-empty counts
-// (occupancy_stats, map.cpp:160-165) through a per-block shared-memory
-// histogram when the grid has few slices.
+// Per-slice non-empty voxel counts (occupancy_stats, map.cpp:160-165) go
+// through a per-block shared-memory histogram when the grid has few slices.
 constexpr uint32_t kSliceSmem = 8192;
+
+// Unique voxels in two passes over the sorted keys, no flag / position
+// arrays: (1) voxel runs starting in each tile of 4096 keys, (2) after the
+// scan of the tile counts, every tile ranks its run starts (blocked: 16
+// consecutive keys per thread, one block scan) and writes key, first
+// record, z index and the slice counts. 160 MB of key reads at 20M points
+// where flags + scan + unique moved 560 MB (0.18 -> ms: see DESIGN.md).
+constexpr int kUqThreads = 256;
+constexpr int kUqItems = 16;
+constexpr int kUqTile = kUqThreads * kUqItems;
+
 template <typename K>
-__global__ void unique_kernel(const K* __restrict__ keys, const uint32_t* __restrict__ flags,
-                              const uint32_t* __restrict__ pos, uint64_t n, uint64_t nz,
-                              uint64_t* __restrict__ ukey, uint32_t* __restrict__ ustart,
-                              uint32_t* __restrict__ uk_k, unsigned long long* __restrict__ slice_ne) {
-  extern __shared__ uint32_t hist[];
+__global__ void __launch_bounds__(kUqThreads) unique_count_kernel(const K* __restrict__ keys,
+                                                                  uint64_t n,
+                                                                  uint32_t* __restrict__ tile_cnt) {
+  __shared__ uint32_t wsum[kUqThreads / 32];
+  const uint64_t base = (uint64_t)blockIdx.x * kUqTile;
+  uint32_t c = 0;
+#pragma unroll
+  for (int it = 0; it < kUqItems; ++it) {
+    const uint64_t i = base + (uint64_t)it * kUqThreads + threadIdx.x;
+    if (i < n) c += (i == 0 || keys[i - 1] != keys[i]) ? 1u : 0u;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t tot = 0;
+#pragma unroll
+    for (int w = 0; w < kUqThreads / 32; ++w) tot += wsum[w];
+    tile_cnt[blockIdx.x] = tot;
+  }
+}
+
+template <typename K>
+__global__ void __launch_bounds__(kUqThreads) unique_write_kernel(
+    const K* __restrict__ keys, uint64_t n, const uint32_t* __restrict__ tile_off, uint64_t nz,
+    uint64_t* __restrict__ ukey, uint32_t* __restrict__ ustart, uint32_t* __restrict__ uk_k,
+    unsigned long long* __restrict__ slice_ne) {
+  extern __shared__ uint32_t hist[];  // nz slice counters when they fit, then the warp sums
   const bool local = nz <= kSliceSmem;
+  __shared__ uint32_t wsum[kUqThreads / 32];
   if (local)
     for (uint32_t i = threadIdx.x; i < nz; i += blockDim.x) hist[i] = 0;
+  const uint64_t b0 = (uint64_t)blockIdx.x * kUqTile + (uint64_t)threadIdx.x * kUqItems;
+  K kv[kUqItems];
+  K prev = 0;
+  bool has_prev = false;
+  if (b0 < n && b0 > 0) prev = keys[b0 - 1], has_prev = true;
+  uint32_t fl = 0, c = 0;
+#pragma unroll
+  for (int j = 0; j < kUqItems; ++j) {
+    const uint64_t i = b0 + j;
+    if (i < n) {
+      kv[j] = keys[i];
+      const bool f = !has_prev || kv[j] != prev;
+      fl |= (uint32_t)f << j;
+      c += f;
+      prev = kv[j];
+      has_prev = true;
+    }
+  }
+  // block exclusive scan of the per-thread counts
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t inc = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += u;
+  }
+  if (lane == 31) wsum[w] = inc;
   __syncthreads();
-  for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < n;
-       s += (uint64_t)gridDim.x * blockDim.x) {
-    if (flags[s]) {
-      const uint32_t u = pos[s];
-      const uint64_t key = (uint64_t)keys[s];
+  uint32_t woff = 0;
+#pragma unroll
+  for (int x = 0; x < kUqThreads / 32; ++x) woff += x < w ? wsum[x] : 0u;
+  uint32_t u = __ldg(tile_off + blockIdx.x) + woff + inc - c;
+#pragma unroll
+  for (int j = 0; j < kUqItems; ++j) {
+    if ((fl >> j) & 1u) {
+      const uint64_t key = (uint64_t)kv[j];
       ukey[u] = key;
-      ustart[u] = (uint32_t)s;
+      ustart[u] = (uint32_t)(b0 + j);
       const uint32_t k = (uint32_t)(key % nz);
       if (uk_k) uk_k[u] = k;
       if (local) atomicAdd(hist + k, 1u);
       else atomicAdd(slice_ne + k, 1ull);
+      ++u;
     }
   }
   if (local) {
@@ -308,11 +442,14 @@ cm_status build_typed(const double* xyz, uint64_t n, cudaStream_t st, cm_index* 
   CM_CUDA_TRY(dev_alloc_t(&flags, n, st));
   CM_CUDA_TRY(dev_alloc_t(&pos, n + 1, st));
   CM_CUDA_TRY(dev_alloc_t(&part, scan_part_elems(n), st));
-  gather_kernel<K><<<grid_for(n), 256, 0, st>>>(xyz, skeys, sperm, n, g, ix->rec, ix->frec, ix->ids, flags); ::cmg::note_launch();
+  gather_kernel<K><<<grid_for(n), 256, 0, st>>>(xyz, skeys, sperm, n, g, ix->rec, ix->frec, ix->ids, nullptr); ::cmg::note_launch();
   cudaEventRecord(ev.e[4], st);
-  exclusive_scan<uint32_t, uint32_t>(flags, n, pos, part, 1, st);
+  // voxel runs per tile -> tile offsets (pos[0 .. ntiles], total at the end)
+  const uint64_t ntiles = (n + kUqTile - 1) / kUqTile;
+  unique_count_kernel<K><<<(unsigned)ntiles, kUqThreads, 0, st>>>(skeys, n, flags); ::cmg::note_launch();
+  exclusive_scan<uint32_t, uint32_t>(flags, ntiles, pos, part, 1, st);
   uint32_t U32 = 0;
-  CM_CUDA_TRY(cudaMemcpyAsync(&U32, pos + n, 4, cudaMemcpyDeviceToHost, st));
+  CM_CUDA_TRY(cudaMemcpyAsync(&U32, pos + ntiles, 4, cudaMemcpyDeviceToHost, st));
   CM_CUDA_TRY(cudaStreamSynchronize(st));
   const uint64_t U = U32;
   ix->U = U;
@@ -326,8 +463,9 @@ cm_status build_typed(const double* xyz, uint64_t n, cudaStream_t st, cm_index* 
   const uint32_t n32 = (uint32_t)n;
   CM_CUDA_TRY(cudaMemcpyAsync(ix->ustart + U, &n32, 4, cudaMemcpyHostToDevice, st));
   const size_t hsmem = g.nz <= kSliceSmem ? g.nz * 4 : 0;
-  unique_kernel<K><<<grid_for(n), 256, hsmem, st>>>(skeys, flags, pos, n, g.nz, ix->ukey, ix->ustart,
-                                                 ix->uk_k, slice_ne); ::cmg::note_launch();
+  unique_write_kernel<K><<<(unsigned)ntiles, kUqThreads, hsmem, st>>>(skeys, n, pos, g.nz, ix->ukey,
+                                                                     ix->ustart, ix->uk_k, slice_ne);
+  ::cmg::note_launch();
   ix->slice_ne.assign(g.nz, 0);
   CM_CUDA_TRY(cudaMemcpyAsync(ix->slice_ne.data(), slice_ne, g.nz * 8, cudaMemcpyDeviceToHost, st));
   dev_free(keys, st);
@@ -405,7 +543,16 @@ cm_status bbox_dev(const double* xyz, uint64_t n, cudaStream_t st, double lo[3],
   unsigned long long init[6] = {~0ull, ~0ull, ~0ull, 0ull, 0ull, 0ull};
   CM_CUDA_TRY(cudaMemcpyAsync(bb, init, sizeof(init), cudaMemcpyHostToDevice, st));
   if (n) {
-    bbox_kernel<<<grid_for(n), 256, 0, st>>>(xyz, n, bb); ::cmg::note_launch();
+    if ((reinterpret_cast<uintptr_t>(xyz) & 15u) == 0 && n >= 4096) {
+      const uint64_t nvec = 3 * n / 2;
+      unsigned grid = grid_for(nvec);
+      grid = std::max(3u, grid - grid % 3u);  // a multiple of 3 threads in all
+      bbox_flat_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const double2*>(xyz), nvec,
+                                             (3 * n) & 1 ? xyz + 3 * n - 1 : nullptr, bb);
+    } else {
+      bbox_kernel<<<grid_for(n), 256, 0, st>>>(xyz, n, bb);
+    }
+    ::cmg::note_launch();
     CM_CUDA_TRY(cudaGetLastError());
   }
   unsigned long long hb[6];
