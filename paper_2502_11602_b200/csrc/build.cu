@@ -135,7 +135,7 @@ __global__ void bbox_flat_kernel(const double2* __restrict__ v2, uint64_t nvec, 
 // K2: key = global_index(voxel_of(p)) (grid.cpp:63-72, grid.hpp:65-67).
 template <typename K>
 __global__ void keys_kernel(const double* __restrict__ xyz, uint64_t n, DevGrid g,
-                            K* __restrict__ keys, uint32_t* __restrict__ vals) {
+                            K* __restrict__ keys, uint32_t* __restrict__ vals, uint32_t base = 0) {
   for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n;
        p += (uint64_t)gridDim.x * blockDim.x) {
     const double x = xyz[3 * p], y = xyz[3 * p + 1], z = xyz[3 * p + 2];
@@ -143,7 +143,33 @@ __global__ void keys_kernel(const double* __restrict__ xyz, uint64_t n, DevGrid 
     const uint64_t j = axis_index(y, g.oy, g.sy, g.ny);
     const uint64_t k = g.mode3d ? axis_index(z, g.oz, g.sz, g.nz) : 0;
     keys[p] = (K)(i * (g.ny * g.nz) + j * g.nz + k);
-    vals[p] = (uint32_t)p;
+    vals[p] = base + (uint32_t)p;
+  }
+}
+
+// K2 with 16-byte loads: two consecutive points per thread (48 bytes = three
+// aligned double2 loads), both keys and handles stored as one 8-byte word.
+template <typename K>
+__global__ void keys2_kernel(const double2* __restrict__ v2, uint64_t npairs, DevGrid g,
+                             K* __restrict__ keys, uint32_t* __restrict__ vals) {
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < npairs;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const double2 a = v2[3 * t], b = v2[3 * t + 1], c = v2[3 * t + 2];  // x0 y0 | z0 x1 | y1 z1
+    const uint64_t i0 = axis_index(a.x, g.ox, g.sx, g.nx);
+    const uint64_t j0 = axis_index(a.y, g.oy, g.sy, g.ny);
+    const uint64_t k0 = g.mode3d ? axis_index(b.x, g.oz, g.sz, g.nz) : 0;
+    const uint64_t i1 = axis_index(b.y, g.ox, g.sx, g.nx);
+    const uint64_t j1 = axis_index(c.x, g.oy, g.sy, g.ny);
+    const uint64_t k1 = g.mode3d ? axis_index(c.y, g.oz, g.sz, g.nz) : 0;
+    const K key0 = (K)(i0 * (g.ny * g.nz) + j0 * g.nz + k0);
+    const K key1 = (K)(i1 * (g.ny * g.nz) + j1 * g.nz + k1);
+    if constexpr (sizeof(K) == 4) {
+      reinterpret_cast<uint2*>(keys)[t] = make_uint2((uint32_t)key0, (uint32_t)key1);
+    } else {
+      keys[2 * t] = key0;
+      keys[2 * t + 1] = key1;
+    }
+    reinterpret_cast<uint2*>(vals)[t] = make_uint2((uint32_t)(2 * t), (uint32_t)(2 * t + 1));
   }
 }
 
@@ -423,7 +449,19 @@ cm_status build_typed(const double* xyz, uint64_t n, cudaStream_t st, cm_index* 
   CM_CUDA_TRY(dev_alloc_t(&keys, n, st));
   CM_CUDA_TRY(dev_alloc_t(&perm, n, st));
   CM_CUDA_TRY(dev_alloc(&scratch, radix_scratch_bytes<K>(n), st));
-  keys_kernel<K><<<grid_for(n), 256, 0, st>>>(xyz, n, g, keys, perm); ::cmg::note_launch();
+  if ((reinterpret_cast<uintptr_t>(xyz) & 15u) == 0 && n >= 2) {
+    const uint64_t npairs = n / 2;
+    keys2_kernel<K><<<grid_for(npairs), 256, 0, st>>>(reinterpret_cast<const double2*>(xyz), npairs, g,
+                                                     keys, perm);
+    ::cmg::note_launch();
+    if (n & 1) {  // the last point
+      keys_kernel<K><<<1, 32, 0, st>>>(xyz + 3 * (n - 1), 1, g, keys + (n - 1), perm + (n - 1),
+                                       (uint32_t)(n - 1));
+      ::cmg::note_launch();
+    }
+  } else {
+    keys_kernel<K><<<grid_for(n), 256, 0, st>>>(xyz, n, g, keys, perm); ::cmg::note_launch();
+  }
   cudaEventRecord(ev.e[2], st);
   ix->key_bits = bit_width(ix->V - 1);
   // the sorted pairs stay where the last pass left them (no copy back)
