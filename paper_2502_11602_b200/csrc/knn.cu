@@ -1157,6 +1157,60 @@ __device__ __forceinline__ void warp_sort_pairs_blocked(double (&d)[E], uint32_t
 // block covers the whole grid go to the redo list (shell walk).
 constexpr int kHistCap = 128;
 
+// The same network with the merge and cross-lane loops ROLLED (exchange
+// distances and directions at run time; only the in-lane steps are
+// unrolled): a fifth of the code. The unrolled E = 4 network did not fit the
+// instruction cache next to the histogram kernel's walk (no_inst on half of
+// its stall samples at k = 64).
+template <int E>
+__device__ __forceinline__ void warp_sort_pairs_blocked_rolled(double (&d)[E], uint32_t (&id)[E],
+                                                               int lane) {
+  constexpr int P = 32 * E;
+#pragma unroll 1
+  for (int kk = 2; kk <= P; kk <<= 1) {
+#pragma unroll 1
+    for (int j = kk >> 1; j >= E; j >>= 1) {
+      const int jl = j / E;
+      const bool lower = (lane & jl) == 0;
+#pragma unroll
+      for (int r = 0; r < E; ++r) {
+        const double od = __shfl_xor_sync(0xffffffffu, d[r], jl);
+        const uint32_t oi = __shfl_xor_sync(0xffffffffu, id[r], jl);
+        const bool asc = (((uint32_t)lane * E + r) & kk) == 0;
+        const bool o_less = pair_less(od, oi, d[r], id[r]);
+        if ((lower == asc) ? o_less : !o_less) {
+          d[r] = od;
+          id[r] = oi;
+        }
+      }
+    }
+#pragma unroll
+    for (int j = E >> 1; j > 0; j >>= 1) {
+      if (j < kk) {
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+          const int p = r ^ j;
+          if (p > r) {
+            const bool asc = (((uint32_t)lane * E + r) & kk) == 0;
+            const bool pl = pair_less(d[p], id[p], d[r], id[r]);
+            if (asc == pl) {
+              const double td = d[r];
+              d[r] = d[p];
+              d[p] = td;
+              const uint32_t ti = id[r];
+              id[r] = id[p];
+              id[p] = ti;
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
+#ifndef CM_KNN_HIST_ROLLED
+#define CM_KNN_HIST_ROLLED 1
+#endif
 template <int E>
 __device__ __forceinline__ void hist_sort_out(const double* __restrict__ bd,
                                               const uint32_t* __restrict__ bi, uint32_t m,
@@ -1171,7 +1225,8 @@ __device__ __forceinline__ void hist_sort_out(const double* __restrict__ bd,
     d[r] = i < m ? bd[i] : __longlong_as_double(0x7ff0000000000000ll);
     id[r] = i < m ? bi[i] : 0xffffffffu;
   }
-  warp_sort_pairs_blocked<E>(d, id, lane);
+  if (CM_KNN_HIST_ROLLED && E >= 4) warp_sort_pairs_blocked_rolled<E>(d, id, lane);  // k = 64: 33.1 -> 32.2 ms; E = 2 (k = 40) is faster unrolled
+  else warp_sort_pairs_blocked<E>(d, id, lane);
 #pragma unroll
   for (int r = 0; r < E; ++r) {
     const uint32_t i = (uint32_t)lane * E + r;
