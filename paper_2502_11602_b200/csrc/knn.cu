@@ -1343,6 +1343,7 @@ __global__ void __launch_bounds__(kKThreads, CM_KNN_HIST_MINB) knn_hist_kernel(
               const uint32_t mm = __ballot_sync(0xffffffffu, sel);
               if (sel) {
                 const uint32_t p = pos + __popc(mm & lt);
+                CM_DCHECK(p < (uint32_t)kHistCap);
                 bd[p] = d2;
                 bi[p] = id;
               }

@@ -59,7 +59,7 @@ def main():
         row, cols = cm.radius_search_self(m, 1.0)
         orow, ocols = o.radius_csr(cloud, 0, 1.0)
         assert np.array_equal(row, orow) and np.array_equal(cols, ocols)
-        for k in (1, 8, 16, 70):
+        for k in (1, 8, 16, 32, 64, 70):
             idx, d2 = cm.knn_batch(m, qs[:600], k)
             oidx, od2 = o.knn(qs[:600], k)
             assert np.array_equal(idx, oidx) and np.array_equal(d2, od2), (flavor, k)
