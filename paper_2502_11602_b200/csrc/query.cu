@@ -82,6 +82,12 @@ __host__ __device__ constexpr int row_area_bytes() {
 }
 template <int MODE>
 __host__ __device__ constexpr int warp_smem_bytes() { return row_area_bytes<MODE>() + kStageBytes; }
+#ifndef CM_TILE_SPLIT
+#define CM_TILE_SPLIT 1  // COLLECT: sparse tiles answered in parts (halves, quarters, ...)
+#endif
+#ifndef CM_TILE_SPLIT_MIN
+#define CM_TILE_SPLIT_MIN 4  // parts are not halved below this many lanes
+#endif
 constexpr int kWideMaxCols = 4096;                    // wide tiles: hull column limit
 constexpr int kRowCap = kRowWarpBytes / 4;            // one-query row buffer (u32)
 constexpr int kSortCap = (kRowCap - 512) / 2;         // one-query row sorted in smem
@@ -835,9 +841,20 @@ __global__ void __launch_bounds__(kQThreads, MODE == MODE_FILL ? CM_FILL_MINB
   for (uint64_t tile = (uint64_t)blockIdx.x * kQWarps + wib; tile < ntiles; tile += W) {
     const uint64_t s = tile * 32 + lane;
     const bool active = s < nq;
+    constexpr bool SPLIT = MODE == MODE_COLLECT && CM_TILE_SPLIT;
+    // COLLECT: a tile whose hull exceeds 32 columns (a sparse query set: the
+    // chunks of the host-buffer pipeline, random centre samples) is answered
+    // in PARTS — the lower half of the lanes still open, halved again while
+    // its hull is too wide — each part by the compact tile walk with the
+    // other lanes masked out, instead of one query per warp for all 32
+    // lanes. Every other mode keeps one part (wide tiles cover them).
+    // (The centre and its range are loaded and derived again for every part, so
+    // nothing of them stays live through the walk of the common one-part tile.)
+    for (uint32_t pending = __ballot_sync(0xffffffffu, active), part = 0; pending; pending &= ~part) {
+    part = pending;
     uint32_t qi = 0u;
     double cx = 0.0, cy = 0.0, cz = 0.0;
-    if (active) {
+    if ((pending >> lane) & 1u) {
       if (q == nullptr) {
         // self queries (cm_radius_search_self): centre s of the cell-ordered
         // records, answered into row rec[s].id — the order the key sort
@@ -856,27 +873,44 @@ __global__ void __launch_bounds__(kQThreads, MODE == MODE_FILL ? CM_FILL_MINB
     // explicit kernel boxes (cm_kernel_search: Aabb boxes, bounded cylinders)
     const double* qb = (XQ && o.qbox && active) ? o.qbox + 6 * (uint64_t)qi : nullptr;
     Range R{};
-    const bool ok = active && clamped_range(t.g, cx, cy, cz, rl, &R, CUBE, qb);
-    const uint32_t okmask = __ballot_sync(0xffffffffu, ok);
-    bool use_tile = small_grid && okmask != 0;
+    const bool ok = ((pending >> lane) & 1u) && clamped_range(t.g, cx, cy, cz, rl, &R, CUBE, qb);
+    bool act = active, okp = ok;
+    bool use_tile = false;
     bool wide = false;
     uint32_t I0 = 0, J0 = 0, nj = 0, ncol = 0, total = 0, K0 = 0, K1 = 0;
     uint64_t nc = 0;
     uint32_t b = 0, e = 0;
-    if (use_tile) {
-      I0 = warp_min_u32(ok ? (uint32_t)R.i0 : 0xffffffffu);
-      const uint32_t I1 = warp_max_u32(ok ? (uint32_t)R.i1 : 0u);
-      J0 = warp_min_u32(ok ? (uint32_t)R.j0 : 0xffffffffu);
-      const uint32_t J1 = warp_max_u32(ok ? (uint32_t)R.j1 : 0u);
-      K0 = warp_min_u32(ok ? (uint32_t)R.k0 : 0xffffffffu);
-      K1 = warp_max_u32(ok ? (uint32_t)R.k1 : 0u);
+    uint32_t I1 = 0, J1 = 0;
+    for (;;) {
+      const bool inpart = (part >> lane) & 1u;
+      act = active && inpart;
+      okp = ok && inpart;
+      use_tile = small_grid && __any_sync(0xffffffffu, okp);
+      if (!use_tile) break;
+      I0 = warp_min_u32(okp ? (uint32_t)R.i0 : 0xffffffffu);
+      I1 = warp_max_u32(okp ? (uint32_t)R.i1 : 0u);
+      J0 = warp_min_u32(okp ? (uint32_t)R.j0 : 0xffffffffu);
+      J1 = warp_max_u32(okp ? (uint32_t)R.j1 : 0u);
       nj = J1 - J0 + 1;
       nc = (uint64_t)(I1 - I0 + 1) * nj;
+      if (SPLIT && nc > 32 && __popc(part) > CM_TILE_SPLIT_MIN) {
+        // keep the lower half of the part's lanes: cut at the lane whose
+        // rank within the part is n / 2
+        const uint32_t rank = __popc(part & ((2u << lane) - 1u));
+        const uint32_t cut = __ballot_sync(0xffffffffu, inpart && rank == (uint32_t)__popc(part) / 2u);
+        part &= (2u << (__ffs(cut) - 1)) - 1u;
+        continue;
+      }
+      break;
+    }
+    if (use_tile) {
+      K0 = warp_min_u32(okp ? (uint32_t)R.k0 : 0xffffffffu);
+      K1 = warp_max_u32(okp ? (uint32_t)R.k1 : 0u);
       use_tile = nc <= 32;
       if (!use_tile && !o.no_wide && MODE != MODE_COLLECT && (MODE != MODE_FILL || o.wide_fill) &&
           nc <= (uint64_t)kWideMaxCols) {
         // worth it while the lanes' own columns cover >= 1/8 of the hull on average
-        uint32_t own = ok ? (uint32_t)((R.i1 - R.i0 + 1) * (R.j1 - R.j0 + 1)) : 0u;
+        uint32_t own = okp ? (uint32_t)((R.i1 - R.i0 + 1) * (R.j1 - R.j0 + 1)) : 0u;
 #pragma unroll
         for (int sh = 16; sh > 0; sh >>= 1) own += __shfl_xor_sync(0xffffffffu, own, sh);
         wide = (uint64_t)own * 8 >= nc * 32;
@@ -899,13 +933,13 @@ __global__ void __launch_bounds__(kQThreads, MODE == MODE_FILL ? CM_FILL_MINB
     if (wide) {
       Predicate P;
       P.init(cx, cy, cz, rl, CUBE, qb);
-      wide_tile<FLAVOR, MODE, CUBE>(t, R, ok, active, qi, I0, J0, nj, (uint32_t)nc, K0, K1, P,
+      wide_tile<FLAVOR, MODE, CUBE>(t, R, okp, act, qi, I0, J0, nj, (uint32_t)nc, K0, K1, P,
                                     lane, stg, reinterpret_cast<uint32_t*>(wreg), o);
       __syncwarp();
       continue;
     }
     if (!use_tile) {
-      const uint32_t am = __ballot_sync(0xffffffffu, active);
+      const uint32_t am = __ballot_sync(0xffffffffu, act);
       for (uint32_t lr = am; lr; lr &= lr - 1) {
         const int l = __ffs(lr) - 1;
         const uint32_t ql = __shfl_sync(0xffffffffu, qi, l);
@@ -919,13 +953,13 @@ __global__ void __launch_bounds__(kQThreads, MODE == MODE_FILL ? CM_FILL_MINB
     }
     // this lane's columns within the hull, and its k window
     uint32_t colmask = 0;
-    if (ok) {
+    if (okp) {
       const uint64_t rowbits = ((1ull << ((uint32_t)(R.j1 - R.j0) + 1)) - 1ull) << ((uint32_t)R.j0 - J0);
       for (uint32_t ci = (uint32_t)R.i0 - I0; ci <= (uint32_t)R.i1 - I0; ++ci)
         colmask |= (uint32_t)(rowbits << (ci * nj));
     }
-    const uint32_t kk0 = ok ? (uint32_t)R.k0 : 1u;
-    const uint32_t kspan = ok ? (uint32_t)(R.k1 - R.k0) : 0u;
+    const uint32_t kk0 = okp ? (uint32_t)R.k0 : 1u;
+    const uint32_t kspan = okp ? (uint32_t)(R.k1 - R.k0) : 0u;
     Predicate P;
     P.init(cx, cy, cz, rl, CUBE, qb);
     uint32_t cnt = 0, ntest = 0;
@@ -1102,12 +1136,12 @@ __global__ void __launch_bounds__(kQThreads, MODE == MODE_FILL ? CM_FILL_MINB
 #pragma unroll
       for (int sh = 16; sh > 0; sh >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, sh);
       if (lane == 0) atomicAdd(&g_qstats[3], (unsigned long long)sum);
-      if (active) {
+      if (act) {
         if (o.counts) o.counts[qi] = cnt;
         if (o.tested) o.tested[qi] = ntest;
       }
     } else if (MODE == MODE_DIGEST) {
-      if (active) {
+      if (act) {
         o.counts[qi] = cnt;
         o.digests[qi] = dig;
       }
@@ -1118,13 +1152,13 @@ __global__ void __launch_bounds__(kQThreads, MODE == MODE_FILL ? CM_FILL_MINB
       const bool longrow = cnt > (uint32_t)kLaneRowCap;
       uint32_t* spark = reinterpret_cast<uint32_t*>(stg) + 32;
       double* sc = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(stg) + 256);
-      if (__any_sync(0xffffffffu, active && longrow)) {
+      if (__any_sync(0xffffffffu, act && longrow)) {
         // the centre and its radius are loaded again here (opaque loads)
         // rather than kept in registers through the walk, where they are
         // dead for the cube: the walk's register pressure decides whether
         // ptxas keeps the eight records' comparison results in predicates
         double rx = 0.0, ry = 0.0, rz = 0.0, rr2 = r;
-        if (active) {
+        if (act) {
           const double* src = q == nullptr ? &rec[s].x : q + 3 * (uint64_t)qi;
           rx = ldg_opaque(src), ry = ldg_opaque(src + 1), rz = ldg_opaque(src + 2);
           if (XQ && o.rq) rr2 = ldg_opaque(o.rq + qi);
@@ -1132,13 +1166,13 @@ __global__ void __launch_bounds__(kQThreads, MODE == MODE_FILL ? CM_FILL_MINB
         spark[lane] = qi;
         sc[lane] = rx, sc[32 + lane] = ry, sc[64 + lane] = rz, sc[96 + lane] = rr2;
       }
-      const uint32_t mine = (active && !longrow) ? cnt : 0u;
+      const uint32_t mine = (act && !longrow) ? cnt : 0u;
       uint64_t dst;
       bool write_ok = true;
       if (MODE == MODE_FILL) {
-        dst = active ? __ldg(o.row_ptr + qi) : 0;
+        dst = act ? __ldg(o.row_ptr + qi) : 0;
         // the row the count pass sized must hold exactly this walk's hits
-        CM_DCHECK(!active || longrow || __ldg(o.row_ptr + qi + 1) - dst == (uint64_t)cnt);
+        CM_DCHECK(!act || longrow || __ldg(o.row_ptr + qi + 1) - dst == (uint64_t)cnt);
       } else {
         const uint32_t alloc = mine;
         const uint32_t inc = warp_incl_scan(alloc);
@@ -1152,7 +1186,7 @@ __global__ void __launch_bounds__(kQThreads, MODE == MODE_FILL ? CM_FILL_MINB
         dst = base + (inc - alloc);
         write_ok = base + tot <= o.cap;
         CM_DCHECK(!write_ok || dst + alloc <= o.cap);
-        if (active && !longrow) {
+        if (act && !longrow) {
           o.counts[qi] = cnt;
           o.toff[qi] = dst;
           o.scnt[qi] = cnt;
@@ -1219,7 +1253,7 @@ __global__ void __launch_bounds__(kQThreads, MODE == MODE_FILL ? CM_FILL_MINB
         }
       }
       __syncwarp();
-      const uint32_t lm = __ballot_sync(0xffffffffu, active && longrow);
+      const uint32_t lm = __ballot_sync(0xffffffffu, act && longrow);
       if (lane == 0 && lm) atomicAdd(&g_qstats[7], (unsigned long long)__popc(lm));
       // single_query reuses the whole warp region: take every parked centre
       // into registers first (lane l holds centre l)
@@ -1244,6 +1278,7 @@ __global__ void __launch_bounds__(kQThreads, MODE == MODE_FILL ? CM_FILL_MINB
       }
     }
     __syncwarp();
+    }  // parts
   }
 }
 
