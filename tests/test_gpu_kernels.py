@@ -184,6 +184,25 @@ def test_knn_paths_parity(env):
     assert r.returncode == 0 and "paths ok" in r.stdout, (r.stdout[-500:], r.stderr[-2000:])
 
 
+@pytest.mark.parametrize("stride", [3, 11, 50, 400])
+def test_sparse_query_tiles_split(stride):
+    """Sparse centre sets (a tile's hull exceeds 32 columns) go through the
+    COLLECT kernel's part splitting (halves, quarters, ... of the tile, then
+    one query per warp): the CSR must equal the oracle's for every density,
+    flavour and kernel, and for centres off the cloud."""
+    c = synth.config_cloud(1, scale=0.02)
+    rng = np.random.default_rng(stride)
+    q = np.ascontiguousarray(c[::stride][:20000])
+    q = np.vstack([q, q[:200] + rng.normal(0, 3.0, size=(200, 3)), [[-1e3, 0, 0], [1e6, 1e6, 1e6]]])
+    for fl in (cm.Flavor.Dense, cm.Flavor.Sparse, cm.Flavor.Mixed):
+        m = cm.Cheesemap.build(c, cm.BuildOptions(flavor=fl))
+        o = CpuIndex(c, flavor=int(fl))
+        for kernel, r in ((cm.SPHERE, 1.0), (cm.CUBE, 1.0), (cm.SPHERE, 0.4), (cm.SPHERE, 1.45)):
+            row, cols = cm.radius_search_batch(m, q, r, kernel)
+            orow, ocols = o.radius_csr(q, int(kernel), r)
+            assert np.array_equal(row, orow) and np.array_equal(cols, ocols), (int(fl), int(kernel), r)
+
+
 def test_voxel_lookup_mirror(cloud):
     m = cm.Cheesemap.build(cloud, cm.BuildOptions(flavor=cm.Flavor.Sparse))
     keys, hs = m.export_voxels()
