@@ -185,7 +185,7 @@ def reference_arm(a):
         "e2e": {"value": r["value"], "unit": "queries/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def slab_arm(a):
@@ -283,7 +283,7 @@ def slab_arm(a):
     nnz_all = allred(float(nnz.value), dist.ReduceOp.SUM if world > 1 else None)
     halo_all = allred(float(inf["n_halo"]), dist.ReduceOp.SUM if world > 1 else None)
     if rank == 0:
-        print(json.dumps({
+        emit({
             "metric": f"radius-search queries/sec (cfg{a.config} x-slabs, r={a.radius:g} m)",
             "value": round(n / (t * 1e-3), 1), "unit": "queries/s", "n_gpus": world,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(t, 4),
@@ -300,13 +300,28 @@ def slab_arm(a):
             "build_note": "max over ranks: device-resident share -> ready slab index, bbox "
                           "all-reduce + point exchange included (host->device share copy "
                           "excluded)",
-            "gpu_launches": int(launches), "clocks": clk}), flush=True)
+            "gpu_launches": int(launches), "clocks": clk})
     del slab
     if world > 1:
         dist.destroy_process_group()
 
 
+_JSON_OUT = None
+
+
+def emit(line):
+    """The bench line, to the process's original stdout."""
+    print(json.dumps(line), file=_JSON_OUT or sys.stdout, flush=True)
+
+
 def main():
+    # stdout carries exactly one JSON line: everything else written to file
+    # descriptor 1 (NCCL prints its version banner there when NCCL_DEBUG is
+    # set, as on the GPU boxes) goes to stderr
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     a = parse()
     if a.impl == "reference":
         reference_arm(a)
@@ -636,7 +651,7 @@ def main():
         }
         if any(rsn in BAD_REASONS for rsn in clk.get("reasons", [])):
             line["clocks_warning"] = "throttle reason active during the timed region"
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         dist.destroy_process_group()
 
