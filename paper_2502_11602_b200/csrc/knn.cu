@@ -86,6 +86,9 @@ __device__ __forceinline__ void shell_column_spans(const Tables& t, int64_t i, i
 #ifndef CM_KNN_TMINB
 #define CM_KNN_TMINB 10  // blocks per SM the per-thread kernel is compiled for (k <= 16)
 #endif
+#ifndef CM_KNN_TMINB8
+#define CM_KNN_TMINB8 12  // the same for k <= 8 (12 KB of heaps per block: config 3 k = 8 5.54 -> 5.40 ms)
+#endif
 #ifndef CM_KNN_BOX
 #define CM_KNN_BOX 0
 #endif
@@ -721,7 +724,7 @@ struct KnnHeap {
 #define CM_KNN_TBALL 1  // ball completion in the per-thread kernel for k > 16
 #endif
 template <int FLAVOR, int K, bool BALL = (CM_KNN_TBALL && K > 16)>
-__global__ void __launch_bounds__(kTThreads, (K > 16 ? 4 : CM_KNN_TMINB)) knn_thread_kernel(
+__global__ void __launch_bounds__(kTThreads, (K > 16 ? 4 : K > 8 ? CM_KNN_TMINB : CM_KNN_TMINB8)) knn_thread_kernel(
     const Tables t, const double* __restrict__ q, uint64_t nq, uint32_t k,
     const uint32_t* __restrict__ list, const uint32_t* __restrict__ n_list, int lmax,
     uint32_t* __restrict__ idx_out, double* __restrict__ d2_out, uint32_t* __restrict__ redo,
