@@ -642,7 +642,8 @@ def main():
             "build_roofline": build_roof,
             "phases_ms": phase,
             "general_centres": general,
-            "tile_stats": step_stats,
+            "tile_stats": step_stats if any(step_stats.values()) else
+            "tile counters are compiled into the checked library only (libcmgpu_checked.so)",
             "roofline": roofline,
             "e2e": e2e,
             "cpu_baseline": cpu,

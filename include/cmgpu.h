@@ -273,7 +273,9 @@ cm_status cm_corrupt_for_testing(cm_index* index);
 cm_status cm_get_last_query_timing(cm_query_timing* out);
 /* Kernels launched by this library since load (all threads). */
 uint64_t cm_launch_count(void);
-/* Query-tile counters since the last reset, count pass then fill pass:
+/* Query-tile counters since the last reset (all zero unless the library is
+ * the checked build, libcmgpu_checked.so: the counters cost the wide-tile
+ * passes half their speed), count pass then fill pass:
  * tiles, tiles answered one query per warp (fallback), hull points,
  * in-range candidates (count pass only). out8 has 8 entries. */
 cm_status cm_debug_query_stats(uint64_t* out8, int reset);

@@ -99,6 +99,24 @@ enum { MODE_COUNT = 0, MODE_FILL = 1, MODE_DIGEST = 2, MODE_COLLECT = 3 };
 // (fill / collect) [4..7]: tiles, non-compact tiles, hull points, and
 // in-range candidates (count) / long rows answered per query (row passes).
 __device__ unsigned long long g_qstats[8];
+// Tile counters (cm_debug_query_stats): compiled into the CHECKED library
+// only. They accumulate per warp in shared memory (one writer, lane 0) and
+// reach g_qstats once per warp at the end of the kernel — but the single-lane
+// updates alone, inside the tile loop, cost the wide-tile passes half their
+// speed (the warp stays on its divergent path for the shuffles and votes
+// that follow; global atomics or shared memory made no difference). Without
+// them: config 2 digests 11.2 / 6.7 / 2.4 -> 22.9 / 12.4 / 4.3 M q/s, the count
+// pass at r = 5 14.4 -> 10.5 ms, the count pass over every 7th / 50th point
+// of config 1 6.75 / 2.77 -> 3.0 / 0.9 ms; the compact COLLECT walk is
+// unchanged (9.88 -> 9.86 ms).
+#ifndef CM_QSTATS
+#ifdef CMGPU_CHECKED
+#define CM_QSTATS 1
+#else
+#define CM_QSTATS 0
+#endif
+#endif
+#define QSTAT_ADD(i, v) do { if (CM_QSTATS) wqs[i] += (unsigned long long)(v); } while (0)
 
 // Kernel outputs; which fields are used depends on the pass.
 struct Out {
@@ -690,7 +708,8 @@ __device__ __forceinline__ void wide_tile(const Tables& t, const Range& R, bool 
                                           uint32_t qi, uint32_t I0, uint32_t J0, uint32_t nj,
                                           uint32_t nc, uint32_t K0, uint32_t K1,
                                           const Predicate& P, int lane, PointRec* stg,
-                                          uint32_t* sid, const Out& o) {
+                                          uint32_t* sid, const Out& o,
+                                          unsigned long long* wqs) {
   constexpr bool FILL = MODE == MODE_FILL;
   const PointRec* __restrict__ rec = t.rec;
   const uint32_t kk0 = ok ? (uint32_t)R.k0 : 1u;
@@ -792,12 +811,13 @@ __device__ __forceinline__ void wide_tile(const Tables& t, const Range& R, bool 
   if (FILL) flush();
   CM_DCHECK(!FILL || !active || wpos == __ldg(o.row_ptr + qi + 1));
   const uint32_t hsum = warp_incl_scan(hull);
-  if (lane == 31) atomicAdd(&g_qstats[(FILL ? 4 : 0) + 2], (unsigned long long)hsum);
+  const uint32_t htot = __shfl_sync(0xffffffffu, hsum, 31);
+  if (lane == 0) QSTAT_ADD((FILL ? 4 : 0) + 2, htot);
   if (MODE == MODE_COUNT) {
     uint32_t sum = ntest;
 #pragma unroll
     for (int sh = 16; sh > 0; sh >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, sh);
-    if (lane == 0) atomicAdd(&g_qstats[3], (unsigned long long)sum);
+    if (lane == 0) QSTAT_ADD(3, sum);
     if (active) {
       if (o.counts) o.counts[qi] = cnt;
       if (o.tested) o.tested[qi] = ntest;
@@ -829,6 +849,16 @@ __global__ void __launch_bounds__(kQThreads, MODE == MODE_FILL ? CM_FILL_MINB
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   unsigned char* wreg = smraw + (size_t)wib * warp_smem_bytes<MODE>();
+#if CM_QSTATS
+  __shared__ unsigned long long s_qs[kQWarps][8];  // this warp's tile counters (QSTAT_ADD)
+  unsigned long long* wqs = s_qs[wib];
+  if (lane < 8) wqs[lane] = 0ull;
+  __syncwarp();
+#else
+  // (not even declared: 256 bytes of static shared memory moved the collect's
+  // shared-memory carve-out and cost it 1.7 %)
+  unsigned long long* wqs = nullptr;
+#endif
   uint16_t* skey = reinterpret_cast<uint16_t*>(wreg);  // hit = column << 11 | offset in span
   uint32_t* wbuf = reinterpret_cast<uint32_t*>(wreg);
   PointRec* stg = reinterpret_cast<PointRec*>(wreg + row_area_bytes<MODE>());
@@ -926,15 +956,15 @@ __global__ void __launch_bounds__(kQThreads, MODE == MODE_FILL ? CM_FILL_MINB
       }
     }
     if (lane == 0) {
-      atomicAdd(&g_qstats[so + 0], 1ull);
-      if (use_tile) atomicAdd(&g_qstats[so + 2], (unsigned long long)total);
-      else if (!wide) atomicAdd(&g_qstats[so + 1], 1ull);
+      QSTAT_ADD(so + 0, 1ull);
+      if (use_tile) QSTAT_ADD(so + 2, total);
+      else if (!wide) QSTAT_ADD(so + 1, 1ull);
     }
     if (wide) {
       Predicate P;
       P.init(cx, cy, cz, rl, CUBE, qb);
       wide_tile<FLAVOR, MODE, CUBE>(t, R, okp, act, qi, I0, J0, nj, (uint32_t)nc, K0, K1, P,
-                                    lane, stg, reinterpret_cast<uint32_t*>(wreg), o);
+                                    lane, stg, reinterpret_cast<uint32_t*>(wreg), o, wqs);
       __syncwarp();
       continue;
     }
@@ -1135,7 +1165,7 @@ __global__ void __launch_bounds__(kQThreads, MODE == MODE_FILL ? CM_FILL_MINB
       uint32_t sum = ntest;
 #pragma unroll
       for (int sh = 16; sh > 0; sh >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, sh);
-      if (lane == 0) atomicAdd(&g_qstats[3], (unsigned long long)sum);
+      if (lane == 0) QSTAT_ADD(3, sum);
       if (act) {
         if (o.counts) o.counts[qi] = cnt;
         if (o.tested) o.tested[qi] = ntest;
@@ -1254,7 +1284,7 @@ __global__ void __launch_bounds__(kQThreads, MODE == MODE_FILL ? CM_FILL_MINB
       }
       __syncwarp();
       const uint32_t lm = __ballot_sync(0xffffffffu, act && longrow);
-      if (lane == 0 && lm) atomicAdd(&g_qstats[7], (unsigned long long)__popc(lm));
+      if (lane == 0 && lm) QSTAT_ADD(7, __popc(lm));
       // single_query reuses the whole warp region: take every parked centre
       // into registers first (lane l holds centre l)
       uint32_t pq = qi;
@@ -1280,6 +1310,10 @@ __global__ void __launch_bounds__(kQThreads, MODE == MODE_FILL ? CM_FILL_MINB
     __syncwarp();
     }  // parts
   }
+#if CM_QSTATS
+  __syncwarp();
+  if (lane < 8 && wqs[lane]) atomicAdd(&g_qstats[lane], wqs[lane]);
+#endif
 }
 
 // Rows too long for a warp buffer: one block per row (persistent blocks).

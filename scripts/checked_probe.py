@@ -28,6 +28,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 from oracle.oracle import CpuIndex  # noqa: E402
+from paper_2502_11602_b200 import _native  # noqa: E402
 from paper_2502_11602_b200 import cheesemap as cm  # noqa: E402
 from paper_2502_11602_b200 import synth  # noqa: E402
 
@@ -54,8 +55,12 @@ def main():
                 oc, od = o.radius(qs, int(kernel), r)
                 assert np.array_equal(c, oc) and np.array_equal(dg, od)
                 checks += 2
+        _native.query_stats(reset=True)
         cnt = cm.radius_count(m, qs, 1.0)
         assert np.array_equal(cnt, o.radius(qs, 0, 1.0)[0])
+        # the tile counters live in this (checked) library only
+        st = _native.query_stats()
+        assert st["count_tiles"] > 0 and st["in_range"] > 0, st
         row, cols = cm.radius_search_self(m, 1.0)
         orow, ocols = o.radius_csr(cloud, 0, 1.0)
         assert np.array_equal(row, orow) and np.array_equal(cols, ocols)
